@@ -1,0 +1,195 @@
+/*
+ * tls.h -- C ABI of the B200-native AsyncTLS two-level sparse decode attention
+ * operator (arXiv 2604.07815).  Implemented by libtls.so
+ * (paper_2604_07815_b200/csrc/*.cu, sm_100a).
+ *
+ * Citation key: P:n = line n of PAPER.md (the paper's LaTeX source).
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ * - Every pointer is a caller-owned DEVICE pointer unless noted otherwise.
+ *   The library allocates no device memory and keeps no global state other
+ *   than a thread-local error string.
+ * - Every call validates its host-visible arguments synchronously, then
+ *   enqueues its kernels on `stream` and returns; outputs are valid once the
+ *   stream reaches that point.  No call synchronises the host.
+ * - Results are bitwise deterministic for fixed inputs and configuration
+ *   (no order-nondeterministic float atomics).
+ * - Return value: TLS_OK, or a tls_status describing the first problem found;
+ *   tls_last_error() then returns a human-readable detail string.  Nothing is
+ *   enqueued when a call returns an error detected before launch.
+ * - Pairs: a *pair* (b, g) is one batch element b and one KV head g; every
+ *   pair is an independent unit of work ("for each key-value group").
+ *   Query head h belongs to KV head g = h / G, G = num_q_heads / num_kv_heads.
+ *   MLA: one shared latent KV head (num_kv_heads = 1), G = num_q_heads.
+ *
+ * Tensor layouts (row-major, innermost last; element type = cfg.dtype):
+ *   q        [batch, num_q_heads, d_k]
+ *   k_cache  GQA: [batch, num_kv_heads, max_seq_len, d_k]
+ *            MLA: [batch, max_seq_len, d_k]      (latent ++ rope, d_k = 576)
+ *   v_cache  GQA: [batch, num_kv_heads, max_seq_len, d_v]
+ *            MLA: NULL -- V is the first d_v dims of each k_cache row
+ *   seq_lens [batch] int32, 1 <= seq_lens[b] <= max_seq_len (device memory)
+ */
+#ifndef TLS_H_
+#define TLS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cudaStream_t without the CUDA headers (same underlying type). */
+typedef struct CUstream_st* tls_stream_t;
+
+typedef enum {
+  TLS_OK = 0,
+  TLS_ERR_DIM = 1,         /* inconsistent shapes / widths                       */
+  TLS_ERR_CONFIG = 2,      /* invalid hyper-parameter (B, d_c, k_b, k_t, ...)    */
+  TLS_ERR_INPUT = 3,       /* NULL required pointer, empty batch / selection     */
+  TLS_ERR_WORKSPACE = 4,   /* workspace missing or too small                     */
+  TLS_ERR_UNSUPPORTED = 5, /* valid request outside what the kernels implement   */
+  TLS_ERR_CUDA = 6         /* a CUDA launch failed                               */
+} tls_status;
+
+typedef enum { TLS_BF16 = 0, TLS_FP32 = 1 } tls_dtype;
+
+typedef enum {
+  TLS_GQA = 0, /* grouped-query attention; MHA is G = 1, MQA is num_kv_heads = 1 */
+  TLS_MLA = 1  /* absorbed multi-head latent attention: one shared KV head */
+} tls_layout;
+
+typedef struct {
+  int32_t batch;        /* number of sequences                                   */
+  int32_t num_q_heads;  /* H_q                                                    */
+  int32_t num_kv_heads; /* H_kv (1 for MLA)                                       */
+  int32_t d_k;          /* key / query width (GQA: head dim; MLA: 576)            */
+  int32_t d_v;          /* value width (GQA: = d_k; MLA: 512)                     */
+  int32_t max_seq_len;  /* capacity S of the caches (tokens)                      */
+  int32_t block_size;   /* B, tokens per block (64 in P:397)                */
+  int32_t d_c;          /* token-index channels (32 GQA / 128 MLA)  */
+  int32_t top_blocks;   /* k_b (128 in P:397)                              */
+  int32_t top_tokens;   /* k_t (512 / 1024 / 2048 in P:397)                */
+  float sm_scale;       /* 1/sqrt(d): alpha-tilde logits AND final attention       */
+                        /*                                           */
+  int32_t dtype;        /* tls_dtype of q / caches / block summaries / outputs    */
+  int32_t layout;       /* tls_layout                                             */
+} tls_config;
+
+/*
+ * The hierarchical index of one KV cache (Fig. 2 "construct hierarchical
+ * indices"; built by tls_build_index).  All buffers are caller-owned device
+ * memory; M = ceil(max_seq_len / block_size), Hkv = num_kv_heads.
+ */
+typedef struct {
+  void* block_minmax;      /* [batch, Hkv, M, 2, d_k] dtype: [..,0,:] = k^max_i,
+                              [..,1,:] = k^min_i                        */
+  uint8_t* codes;          /* [batch, Hkv, max_seq_len, d_c/2] INT4 codes of the
+                              channel-projected keys; channel 2i in the
+                              low nibble, 2i+1 in the high nibble of byte i      */
+  float* scale_zero;       /* [batch, Hkv, max_seq_len, 2] fp32 (scale, zero):
+                              k~ = zero + scale * code                            */
+  const int32_t* channels; /* [Hkv, d_c] ascending channel ids C; an
+                              input, produced by tls_calibrate_channels or the
+                              caller's own calibration                            */
+} tls_index;
+
+/*
+ * Channel calibration:
+ *   s_i = (1/G) sum_h max_{D_cal} |q_h[i]| * max_{D_cal} |k[i]|,  C = top-d_c(s)
+ * per KV head, ties -> lower channel id; C is written ascending.
+ *   q_cal          [n_q, num_q_heads, d_k] calibration queries
+ *   k_cal          base of the calibration keys of KV head 0: n_k rows of d_k
+ *                  contiguous elements; KV head g starts k_head_stride
+ *                  ELEMENTS after head g-1 (for a GQA cache slice
+ *                  k_cache[b] pass k_head_stride = max_seq_len * d_k).
+ *   channels_out   [Hkv, d_c] int32 (output)
+ *   channel_scores [Hkv, d_k] fp32, nullable (output; the s_i above)
+ * Errors: TLS_ERR_CONFIG if d_c > d_k; TLS_ERR_INPUT if n_q < 1 or n_k < 1.
+ */
+tls_status tls_calibrate_channels(const tls_config* cfg, const void* q_cal, int32_t n_q,
+                                  const void* k_cal, int32_t n_k, int64_t k_head_stride,
+                                  int32_t* channels_out, float* channel_scores,
+                                  tls_stream_t stream);
+
+/*
+ * Index construction: for every pair and every
+ * block i with i*B < seq_lens[b], and i >= start_token / B:
+ *   k^max_i / k^min_i = channelwise max / min of the block's valid keys;
+ * for every valid token j of those blocks, the INT4 token index:
+ *   x = fp32(k_j[C]); zero = min x; scale = fp32(fp32(max x - zero) / 15);
+ *   code_c = scale > 0 ? clamp(rint(fp32(fp32(x_c - zero) / scale)), 0, 15) : 0
+ * (IEEE fp32, round-to-nearest-even; bit-identical to the oracle).
+ * start_token = 0 builds everything (prefill); start_token > 0 rebuilds only
+ * from block start_token / B on (incremental append of decode tokens).
+ * Entries of blocks / tokens at or beyond seq_lens[b] are left untouched.
+ */
+tls_status tls_build_index(const tls_config* cfg, const void* k_cache, const int32_t* seq_lens,
+                           int32_t start_token, const tls_index* idx, tls_stream_t stream);
+
+/*
+ * Two-level selection for one decode step:
+ *   s_i   = sum_h sum_k max(q_hk k^max_ik, q_hk k^min_ik)
+ *         (computed as Q+ . k^max_i + Q- . k^min_i, Q+- = sum_h max/min(q_h,0),
+ *          the P:110 identity plus linearity of sum_h)
+ *   M_t   = top-k_b blocks (ties -> lower id)
+ *   alpha~_j = (1/G) sum_h softmax_{j in J}(q~_h . k~_j * sm_scale)
+ *          over the candidate tokens J of M_t (or of guide_block_ids)
+ *   S_t   = top-k_t tokens of J by alpha~ (ties -> lower token id)
+ * Outputs (all ascending ids, -1 padded):
+ *   block_ids    [batch, Hkv, top_blocks]  M_t
+ *   token_ids    [batch, Hkv, top_tokens]  S_t
+ *   num_tokens   [batch, Hkv]              |S_t| = min(k_t, |J|)
+ *   token_scores [batch, Hkv, top_tokens]  nullable; ln(alpha~_j) of S_t
+ * guide_block_ids: NULL -> candidates are this step's M_t (synchronous form,
+ *   P:137); else [batch, Hkv, top_blocks] ascending, -1 padded: candidates are
+ *   those blocks (one-step-lag form S_t = TokenSelect(q_t, M_{t-1})).
+ * workspace: >= tls_workspace_bytes(cfg, 0) bytes of device memory, 256-B
+ *   aligned, not shared with a concurrently running call.
+ */
+tls_status tls_select(const tls_config* cfg, const void* q, const int32_t* seq_lens,
+                      const tls_index* idx, const int32_t* guide_block_ids, int32_t* block_ids,
+                      int32_t* token_ids, int32_t* num_tokens, float* token_scores,
+                      void* workspace, size_t workspace_bytes, tls_stream_t stream);
+
+/*
+ * Sparse attention over the selected tokens:
+ *   o^(h) = softmax_{j in S}(q^(h) . k_j * sm_scale) V_S,  lse^(h) = ln sum_j exp(.)
+ * with full-dimensional K, V.  token_ids / num_tokens as written by tls_select
+ * (ids must lie in [0, seq_lens[b]); entries past num_tokens are ignored).
+ *   out [batch, num_q_heads, d_v] dtype;  lse [batch, num_q_heads] fp32, nullable.
+ * Errors: TLS_ERR_INPUT if top_tokens < 1.  A pair with num_tokens == 0 gets
+ * out = 0 and lse = -inf.
+ */
+tls_status tls_sparse_attend(const tls_config* cfg, const void* q, const void* k_cache,
+                             const void* v_cache, const int32_t* token_ids,
+                             const int32_t* num_tokens, void* out, float* lse, void* workspace,
+                             size_t workspace_bytes, tls_stream_t stream);
+
+/* tls_select followed by tls_sparse_attend on the same stream (one decode step
+ * of the operator).  workspace >= tls_workspace_bytes(cfg, 2). */
+tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
+                      const void* v_cache, const int32_t* seq_lens, const tls_index* idx,
+                      const int32_t* guide_block_ids, int32_t* block_ids, int32_t* token_ids,
+                      int32_t* num_tokens, float* token_scores, void* out, float* lse,
+                      void* workspace, size_t workspace_bytes, tls_stream_t stream);
+
+/* Workspace bytes needed by: which = 0 tls_select, 1 tls_sparse_attend,
+ * 2 tls_decode.  Returns 0 for an invalid configuration. */
+size_t tls_workspace_bytes(const tls_config* cfg, int32_t which);
+
+/* Number of kernel launches one call enqueues (which as above; 3 =
+ * tls_build_index, 4 = tls_calibrate_channels), for launch accounting. */
+int32_t tls_launch_count(const tls_config* cfg, int32_t which);
+
+const char* tls_status_string(tls_status status);
+const char* tls_last_error(void); /* thread-local detail of the last error */
+const char* tls_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TLS_H_ */
