@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the AsyncTLS decode operator on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl tls|reference]
+
+One *step* = one fused tls_decode launch = the whole hot path (block scores,
+top-k_b, token scores, top-k_t, sparse attention) for every (batch, KV-head)
+pair of one synthetic decode batch, with the KV cache and index resident in
+HBM.  Default workload: configs[2] of BASELINE.json (Qwen3-32B shape, 96k
+context, batch 32) -- the north star's headline "96k context on 1 GPU".
+Prints ONE JSON line (rank 0).  See DESIGN.md §7 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TLS decode op µs/step & HBM GB/s vs roofline at 48k/96k; decode tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--pattern", default="outlier", choices=["uniform", "outlier", "peaked"])
+    ap.add_argument("--impl", default="tls", choices=["tls", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- accounting
+def algorithmic_bytes_per_pair(w) -> float:
+    """SURVEY §8(d) / DESIGN.md §5: m*2*d_k*s + K_b*B*(d_c/2 + 8) + K_t*row + G*(d_k + d_v)*s."""
+    s = 2 if w.dtype == torch.bfloat16 else 4
+    G = w.num_q_heads // w.num_kv_heads
+    m = math.ceil(w.context / w.block_size)
+    kb = min(w.top_blocks, m)
+    cand = min(kb * w.block_size, w.context)
+    kt = min(w.top_tokens, cand)
+    row = w.d_k * s if w.layout == "mla" else (w.d_k + w.d_v) * s
+    return m * 2 * w.d_k * s + cand * (w.d_c // 2 + 8) + kt * row + G * (w.d_k + w.d_v) * s
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
+    `ncu --set full` capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms in the background."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = [s for (t, s) in self.samples if t0 - 0.06 <= t <= t1 + 0.06] or [s for (_, s) in self.samples[-3:]]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            parts = [p.strip() for p in r.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except Exception:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ workload
+def build_state(w, seed, device, pattern):
+    import paper_2604_07815_b200 as tls
+    from paper_2604_07815_b200 import workloads as W
+
+    inputs = W.make_inputs(w, seed=seed, pattern=pattern, device=device)
+    cfg = tls.TLSConfig(**w.config_kwargs())
+    q_cal, k_cal = W.calibration_sample(w, inputs, seed=seed, pattern=pattern)
+    channels, _ = tls.calibrate_channels(cfg, q_cal, k_cal)
+    idx = tls.alloc_index(cfg, channels)
+    tls.build_index(cfg, inputs["k_cache"], inputs["seq_lens"], idx)
+    queries = W.make_queries(w, 8, seed=seed, pattern=pattern, device=device)
+    torch.cuda.synchronize()
+    return cfg, inputs, idx, queries
+
+
+def time_steps(fn, steps, warmup, flush, stream):
+    """Device time of `steps` calls of fn(i), L2 flushed before each (not timed)."""
+    for i in range(warmup):
+        flush()
+        fn(i)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for i in range(steps):
+        flush()
+        starts[i].record(stream)
+        fn(i)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)]
+
+
+def cpu_baseline(w, inputs, idx_channels, budget_s, label):
+    """The fp64 oracle as it stands, timed on this host on a bounded sample of pairs."""
+    import numpy as np
+
+    from oracle import tls_oracle as O
+
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    G = w.num_q_heads // w.num_kv_heads
+    prm = O.TLSParams(block_size=w.block_size, top_blocks=w.top_blocks, top_tokens=w.top_tokens, sm_scale=w.scale)
+    pairs = [(b, g) for b in range(w.batch) for g in range(w.num_kv_heads)]
+    rng = np.random.default_rng(0)
+    rng.shuffle(pairs)
+    done, spent = 0, 0.0
+    ctx = threadpool_limits(1) if threadpool_limits else None
+    if ctx:
+        ctx.__enter__()
+    try:
+        for b, g in pairs:
+            n = int(inputs["seq_lens"][b])
+            qg = inputs["q"][b, g * G:(g + 1) * G].double().cpu().numpy()
+            if w.layout == "mla":
+                keys = inputs["k_cache"][b, :n].double().cpu().numpy()
+                values = keys[:, : w.d_v]
+            else:
+                keys = inputs["k_cache"][b, g, :n].double().cpu().numpy()
+                values = inputs["v_cache"][b, g, :n].double().cpu().numpy()
+            ch = idx_channels[g].cpu().numpy()
+            index = O.build_index_pair(keys, ch, w.block_size)  # prefill: not part of a decode step
+            t0 = time.perf_counter()
+            O.tls_pair(qg, keys, values, ch, prm, index=index)
+            spent += time.perf_counter() - t0
+            done += 1
+            if spent >= budget_s:
+                break
+    finally:
+        if ctx:
+            ctx.__exit__(None, None, None)
+    per_pair = spent / done
+    tokens_per_s = (1.0 / w.num_kv_heads) / per_pair  # a pair is 1/Hkv of one sequence's decode token
+    return {"value": tokens_per_s, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+            "sample": f"{done} of {len(pairs)} (batch, kv-head) pairs of {label}, O6-O11 per pair "
+                      f"({per_pair * 1e3:.1f} ms/pair, fp64 numpy, 1 BLAS thread), extrapolated to tokens/s"}
+
+
+# ---------------------------------------------------------------------- arms
+def run_reference(args, w, rank, world):
+    """--impl reference: the oracle as it stands on host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import tls_oracle as O
+    from paper_2604_07815_b200 import workloads as W
+
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    # the same seeded workload as the tls arm; the oracle reads a fresh pair per step
+    inputs = W.make_inputs(w, seed=0, pattern=args.pattern, device=dev)
+    q_cal, k_cal = W.calibration_sample(w, inputs, seed=0, pattern=args.pattern)
+    G = w.num_q_heads // w.num_kv_heads
+    chans = [O.calibrate_channels(q_cal[:, g * G:(g + 1) * G].double().cpu().numpy(),
+                                  k_cal[g].double().cpu().numpy(), w.d_c)[0] for g in range(w.num_kv_heads)]
+    prm = O.TLSParams(block_size=w.block_size, top_blocks=w.top_blocks, top_tokens=w.top_tokens, sm_scale=w.scale)
+    pairs = [(b, g) for b in range(w.batch) for g in range(w.num_kv_heads)]
+    cache = {}
+
+    def prep(i):
+        b, g = pairs[i % len(pairs)]
+        if (b, g) not in cache:
+            n = int(inputs["seq_lens"][b])
+            qg = inputs["q"][b, g * G:(g + 1) * G].double().cpu().numpy()
+            if w.layout == "mla":
+                keys = inputs["k_cache"][b, :n].double().cpu().numpy()
+                values = keys[:, : w.d_v]
+            else:
+                keys = inputs["k_cache"][b, g, :n].double().cpu().numpy()
+                values = inputs["v_cache"][b, g, :n].double().cpu().numpy()
+            cache.clear()
+            cache[(b, g)] = (qg, keys, values, chans[g], O.build_index_pair(keys, chans[g], w.block_size))
+        return cache[(b, g)]
+
+    ctx = threadpool_limits(1) if threadpool_limits else None
+    if ctx:
+        ctx.__enter__()
+    for i in range(args.warmup):
+        qg, keys, values, ch, index = prep(i)
+        O.tls_pair(qg, keys, values, ch, prm, index=index)
+    times = []
+    for i in range(args.steps):
+        qg, keys, values, ch, index = prep(args.warmup + i)
+        t0 = time.perf_counter()
+        O.tls_pair(qg, keys, values, ch, prm, index=index)
+        times.append(time.perf_counter() - t0)
+    if ctx:
+        ctx.__exit__(None, None, None)
+    per_pair = sum(times) / len(times)
+    value = (1.0 / w.num_kv_heads) / per_pair
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_pair * 1e3, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "step": "one (batch, kv-head) pair per step (bounded sample)",
+                   "batch": w.batch, "context": w.context},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} pairs of {w.name}, O6-O11 per pair, fp64 numpy, 1 BLAS thread"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_tls(args, w, rank, world, local_rank):
+    import paper_2604_07815_b200 as tls
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    if args.scaling == "strong" and world > 1:
+        # shard the fixed problem: KV heads (GQA) or batch (MLA) across ranks
+        from paper_2604_07815_b200.dist import shard_workload
+        w = shard_workload(w, rank, world)
+    seed = rank if args.scaling == "weak" else 0
+    cfg, inputs, idx, queries = build_state(w, seed, dev, args.pattern)
+    stream = torch.cuda.current_stream(dev)
+    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # 2x the 126 MB L2
+
+    def flush():
+        flush_buf.fill_(1)
+
+    out = torch.empty((w.batch, w.num_q_heads, w.d_v), dtype=w.dtype, device=dev)
+    lse = torch.empty((w.batch, w.num_q_heads), dtype=torch.float32, device=dev)
+    sel = (torch.empty((w.batch, w.num_kv_heads, w.top_blocks), dtype=torch.int32, device=dev),
+           torch.empty((w.batch, w.num_kv_heads, w.top_tokens), dtype=torch.int32, device=dev),
+           torch.empty((w.batch, w.num_kv_heads), dtype=torch.int32, device=dev),
+           torch.empty((w.batch, w.num_kv_heads, w.top_tokens), dtype=torch.float32, device=dev))
+
+    def step(i):
+        tls.decode(cfg, queries[i % queries.shape[0]], inputs["k_cache"], inputs["v_cache"], inputs["seq_lens"],
+                   idx, sel_out=sel, out=out, lse=lse)
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.time()
+    times = time_steps(step, args.steps, args.warmup, flush, stream)
+    t_wall1 = time.time()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks.stop()
+    # e2e through the public API with HOST buffers: H2D q (pinned), decode, D2H out+lse
+    q_host = queries.cpu().pin_memory()
+    out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    lse_host = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+    q_dev = torch.empty_like(queries[0])
+
+    def e2e_step(i):
+        q_dev.copy_(q_host[i % q_host.shape[0]], non_blocking=True)
+        tls.decode(cfg, q_dev, inputs["k_cache"], inputs["v_cache"], inputs["seq_lens"], idx, sel_out=sel,
+                   out=out, lse=lse)
+        out_host.copy_(out, non_blocking=True)
+        lse_host.copy_(lse, non_blocking=True)
+
+    e2e_times = time_steps(e2e_step, max(10, args.steps // 4), 3, flush, stream)
+
+    ms = sum(times) / len(times)
+    ms_e2e = sum(e2e_times) / len(e2e_times)
+    if world > 1:
+        t = torch.tensor([ms, ms_e2e], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms, ms_e2e = float(t[0]), float(t[1])
+    if rank != 0:
+        return
+    tokens_per_step = w.batch * world  # one decode token per sequence, every rank
+    bytes_step = algorithmic_bytes_per_pair(w) * w.batch * w.num_kv_heads
+    peak, peak_src = hbm_peak()
+    achieved = bytes_step / (ms * 1e-3) / 1e9
+    clk = clocks.summary(t_wall0, t_wall1)
+    line = {
+        "metric": METRIC,
+        "value": tokens_per_step / (ms * 1e-3),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": args.scaling,
+        "vs_baseline": None,
+        "dtype": "bf16" if w.dtype == torch.bfloat16 else "f32",
+        "data": "synthetic",
+        "config": {
+            "workload": w.name, "batch_per_gpu": w.batch, "global_batch": w.batch * (world if args.scaling == "weak" else 1),
+            "context": w.context, "num_q_heads": w.num_q_heads, "num_kv_heads": w.num_kv_heads, "d_k": w.d_k,
+            "d_v": w.d_v, "layout": w.layout, "block_size": w.block_size, "d_c": w.d_c, "K_b": w.top_blocks,
+            "K_t": w.top_tokens, "pattern": args.pattern, "cluster_size": tls.cluster_size(cfg, 2),
+            "l2": "flushed before every timed step (256 MiB write, untimed)",
+            "parallelism": f"{world} rank(s), (batch, kv-head) pairs independent, no collective in the step",
+            "layer": "one attention layer (tokens/s = batch / layer-step time)",
+        },
+        "us_per_step": ms * 1e3,
+        "hbm_gbs": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(w.name), "peak_source": peak_src, "kernel": "tls_decode_kernel",
+                     "algorithmic_bytes_per_launch": bytes_step},
+        "e2e": {"value": tokens_per_step / (ms_e2e * 1e-3), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(queries[0].numel() * queries.element_size()),
+                "d2h_bytes_per_step": int(out.numel() * out.element_size() + lse.numel() * 4),
+                "ms_per_step": ms_e2e, "api": "paper_2604_07815_b200.decode (tls_decode) with pinned host q/out"},
+        "gpu_launches": args.steps * tls.load().tls_launch_count(__import__("ctypes").byref(cfg.c()), 2),
+        "clocks": clk,
+        "p10_p90_ms": [sorted(times)[len(times) // 10], sorted(times)[(9 * len(times)) // 10]],
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(w, inputs, idx.channels, args.cpu_budget_s, w.name)
+    elif not args.no_cpu_baseline:
+        line["cpu_baseline"] = None
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    from paper_2604_07815_b200 import workloads as W
+
+    w = W.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, w, rank, world)
+        return
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_tls(args, w, rank, world, local_rank)
+    finally:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

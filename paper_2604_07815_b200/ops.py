@@ -1,0 +1,259 @@
+"""Torch-tensor front end of libtls.so -- the same names as the C ABI.
+
+PyTorch provides device memory and streams only: every step of the path runs
+in the CUDA kernels behind include/tls.h.  Each function checks shapes,
+dtypes, devices and contiguity, passes ``data_ptr()`` and the current CUDA
+stream, and raises ``TLSError`` on a non-OK status.
+
+Citation key: P:n = line n of PAPER.md (arXiv 2604.07815).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+
+__all__ = [
+    "TLSConfig",
+    "TLSIndex",
+    "alloc_index",
+    "calibrate_channels",
+    "build_index",
+    "select",
+    "sparse_attend",
+    "decode",
+    "cluster_size",
+]
+
+_DT = {torch.bfloat16: _lib.TLS_BF16, torch.float32: _lib.TLS_FP32}
+
+
+@dataclass
+class TLSConfig:
+    """Mirror of ``tls_config`` (include/tls.h).  Defaults follow P:397."""
+
+    batch: int
+    num_q_heads: int
+    num_kv_heads: int
+    d_k: int
+    d_v: int
+    max_seq_len: int
+    block_size: int = 64  # B
+    d_c: int = 32  # token-index channels (32 GQA / 128 MLA)
+    top_blocks: int = 128  # k_b
+    top_tokens: int = 1024  # k_t
+    sm_scale: float | None = None  # default 1/sqrt(d_k)
+    dtype: torch.dtype = torch.bfloat16
+    layout: str = "gqa"  # "gqa" | "mla"
+    _c: _lib.TLSConfigC = field(default=None, init=False, repr=False)
+
+    def __post_init__(self):
+        if self.sm_scale is None:
+            self.sm_scale = 1.0 / math.sqrt(self.d_k)
+
+    @property
+    def G(self) -> int:
+        return self.num_q_heads // self.num_kv_heads
+
+    @property
+    def num_blocks(self) -> int:
+        return (self.max_seq_len + self.block_size - 1) // self.block_size
+
+    @property
+    def pairs(self) -> int:
+        return self.batch * self.num_kv_heads
+
+    def c(self) -> _lib.TLSConfigC:
+        if self.dtype not in _DT:
+            raise TypeError(f"dtype must be bf16 or fp32, got {self.dtype}")
+        return _lib.TLSConfigC(
+            self.batch, self.num_q_heads, self.num_kv_heads, self.d_k, self.d_v, self.max_seq_len, self.block_size,
+            self.d_c, self.top_blocks, self.top_tokens, float(self.sm_scale), _DT[self.dtype],
+            _lib.TLS_MLA if self.layout == "mla" else _lib.TLS_GQA,
+        )
+
+
+@dataclass
+class TLSIndex:
+    """The hierarchical index of one KV cache (Fig. 2), device tensors."""
+
+    block_minmax: torch.Tensor  # [batch, Hkv, M, 2, d_k] dtype (k^max, k^min)
+    codes: torch.Tensor  # [batch, Hkv, S, d_c/2] uint8 INT4 codes
+    scale_zero: torch.Tensor  # [batch, Hkv, S, 2] fp32
+    channels: torch.Tensor  # [Hkv, d_c] int32 ascending channel set C
+
+    def c(self) -> _lib.TLSIndexC:
+        return _lib.TLSIndexC(self.block_minmax.data_ptr(), self.codes.data_ptr(), self.scale_zero.data_ptr(),
+                              self.channels.data_ptr())
+
+
+def _stream(dev: torch.device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _need(t: torch.Tensor, name: str, shape: tuple, dtype: torch.dtype, dev: torch.device) -> None:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a tensor")
+    if t.device != dev or t.device.type != "cuda":
+        raise ValueError(f"{name} must live on {dev} (CUDA); got {t.device}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _kv_shape(cfg: TLSConfig, width: int) -> tuple:
+    if cfg.layout == "mla":
+        return (cfg.batch, cfg.max_seq_len, width)
+    return (cfg.batch, cfg.num_kv_heads, cfg.max_seq_len, width)
+
+
+def alloc_index(cfg: TLSConfig, channels: torch.Tensor) -> TLSIndex:
+    """Allocate the index buffers for ``cfg`` on the device of ``channels``."""
+    dev = channels.device
+    _need(channels, "channels", (cfg.num_kv_heads, cfg.d_c), torch.int32, dev)
+    return TLSIndex(
+        block_minmax=torch.empty((cfg.batch, cfg.num_kv_heads, cfg.num_blocks, 2, cfg.d_k), dtype=cfg.dtype, device=dev),
+        codes=torch.empty((cfg.batch, cfg.num_kv_heads, cfg.max_seq_len, cfg.d_c // 2), dtype=torch.uint8, device=dev),
+        scale_zero=torch.empty((cfg.batch, cfg.num_kv_heads, cfg.max_seq_len, 2), dtype=torch.float32, device=dev),
+        channels=channels,
+    )
+
+
+def calibrate_channels(cfg: TLSConfig, q_cal: torch.Tensor, k_cal: torch.Tensor, k_head_stride: int | None = None):
+    """Channel set C per KV head on the GPU.
+
+    ``q_cal`` [n_q, Hq, d_k]; ``k_cal`` holds n_k rows of d_k per KV head, head g
+    starting ``k_head_stride`` elements after head g-1 (default: a contiguous
+    [Hkv, n_k, d_k] tensor).  Returns (channels [Hkv, d_c] int32, scores [Hkv, d_k] fp32).
+    """
+    lib = _lib.load()
+    dev = q_cal.device
+    n_q = q_cal.shape[0]
+    _need(q_cal, "q_cal", (n_q, cfg.num_q_heads, cfg.d_k), cfg.dtype, dev)
+    if k_head_stride is None:
+        n_k = k_cal.shape[1]
+        _need(k_cal, "k_cal", (cfg.num_kv_heads, n_k, cfg.d_k), cfg.dtype, dev)
+        k_head_stride = n_k * cfg.d_k
+    else:
+        n_k = k_cal.shape[-2]
+    ch = torch.empty((cfg.num_kv_heads, cfg.d_c), dtype=torch.int32, device=dev)
+    sc = torch.empty((cfg.num_kv_heads, cfg.d_k), dtype=torch.float32, device=dev)
+    cc = cfg.c()
+    _lib.check(lib.tls_calibrate_channels(ctypes.byref(cc), q_cal.data_ptr(), n_q, k_cal.data_ptr(), n_k,
+                                          int(k_head_stride), ch.data_ptr(), sc.data_ptr(), _stream(dev)))
+    return ch, sc
+
+
+def build_index(cfg: TLSConfig, k_cache: torch.Tensor, seq_lens: torch.Tensor, index: TLSIndex,
+                start_token: int = 0) -> TLSIndex:
+    """Block summaries + INT4 token index, in place."""
+    lib = _lib.load()
+    dev = k_cache.device
+    _need(k_cache, "k_cache", _kv_shape(cfg, cfg.d_k), cfg.dtype, dev)
+    _need(seq_lens, "seq_lens", (cfg.batch,), torch.int32, dev)
+    _need(index.block_minmax, "block_minmax", (cfg.batch, cfg.num_kv_heads, cfg.num_blocks, 2, cfg.d_k), cfg.dtype, dev)
+    _need(index.codes, "codes", (cfg.batch, cfg.num_kv_heads, cfg.max_seq_len, cfg.d_c // 2), torch.uint8, dev)
+    _need(index.scale_zero, "scale_zero", (cfg.batch, cfg.num_kv_heads, cfg.max_seq_len, 2), torch.float32, dev)
+    _need(index.channels, "channels", (cfg.num_kv_heads, cfg.d_c), torch.int32, dev)
+    cc, ic = cfg.c(), index.c()
+    _lib.check(lib.tls_build_index(ctypes.byref(cc), k_cache.data_ptr(), seq_lens.data_ptr(), int(start_token),
+                                   ctypes.byref(ic), _stream(dev)))
+    return index
+
+
+def _sel_outputs(cfg: TLSConfig, dev, out):
+    if out is not None:
+        return out
+    return (
+        torch.empty((cfg.batch, cfg.num_kv_heads, cfg.top_blocks), dtype=torch.int32, device=dev),
+        torch.empty((cfg.batch, cfg.num_kv_heads, cfg.top_tokens), dtype=torch.int32, device=dev),
+        torch.empty((cfg.batch, cfg.num_kv_heads), dtype=torch.int32, device=dev),
+        torch.empty((cfg.batch, cfg.num_kv_heads, cfg.top_tokens), dtype=torch.float32, device=dev),
+    )
+
+
+def select(cfg: TLSConfig, q: torch.Tensor, seq_lens: torch.Tensor, index: TLSIndex,
+           guide_block_ids: torch.Tensor | None = None, out=None):
+    """Two-level selection.  Returns (block_ids, token_ids, num_tokens, token_scores)."""
+    lib = _lib.load()
+    dev = q.device
+    _need(q, "q", (cfg.batch, cfg.num_q_heads, cfg.d_k), cfg.dtype, dev)
+    _need(seq_lens, "seq_lens", (cfg.batch,), torch.int32, dev)
+    bids, tids, nt, ts = _sel_outputs(cfg, dev, out)
+    g = 0
+    if guide_block_ids is not None:
+        _need(guide_block_ids, "guide_block_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_blocks), torch.int32, dev)
+        g = guide_block_ids.data_ptr()
+    cc, ic = cfg.c(), index.c()
+    _lib.check(lib.tls_select(ctypes.byref(cc), q.data_ptr(), seq_lens.data_ptr(), ctypes.byref(ic), g,
+                              bids.data_ptr(), tids.data_ptr(), nt.data_ptr(),
+                              ts.data_ptr() if ts is not None else 0, None, 0, _stream(dev)))
+    return bids, tids, nt, ts
+
+
+def sparse_attend(cfg: TLSConfig, q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor | None,
+                  token_ids: torch.Tensor, num_tokens: torch.Tensor, out=None, lse=None):
+    """Attention over the selected tokens.  Returns (out, lse)."""
+    lib = _lib.load()
+    dev = q.device
+    _need(q, "q", (cfg.batch, cfg.num_q_heads, cfg.d_k), cfg.dtype, dev)
+    _need(k_cache, "k_cache", _kv_shape(cfg, cfg.d_k), cfg.dtype, dev)
+    if cfg.layout == "gqa":
+        _need(v_cache, "v_cache", _kv_shape(cfg, cfg.d_v), cfg.dtype, dev)
+    _need(token_ids, "token_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_tokens), torch.int32, dev)
+    _need(num_tokens, "num_tokens", (cfg.batch, cfg.num_kv_heads), torch.int32, dev)
+    if out is None:
+        out = torch.empty((cfg.batch, cfg.num_q_heads, cfg.d_v), dtype=cfg.dtype, device=dev)
+    if lse is None:
+        lse = torch.empty((cfg.batch, cfg.num_q_heads), dtype=torch.float32, device=dev)
+    cc = cfg.c()
+    _lib.check(lib.tls_sparse_attend(ctypes.byref(cc), q.data_ptr(), k_cache.data_ptr(),
+                                     v_cache.data_ptr() if (v_cache is not None and cfg.layout == "gqa") else 0,
+                                     token_ids.data_ptr(), num_tokens.data_ptr(), out.data_ptr(), lse.data_ptr(),
+                                     None, 0, _stream(dev)))
+    return out, lse
+
+
+def decode(cfg: TLSConfig, q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor | None,
+           seq_lens: torch.Tensor, index: TLSIndex, guide_block_ids: torch.Tensor | None = None, sel_out=None,
+           out=None, lse=None):
+    """One decode step of the operator: select + attend in one fused launch.
+
+    Returns (out, lse, block_ids, token_ids, num_tokens, token_scores).
+    """
+    lib = _lib.load()
+    dev = q.device
+    _need(q, "q", (cfg.batch, cfg.num_q_heads, cfg.d_k), cfg.dtype, dev)
+    _need(k_cache, "k_cache", _kv_shape(cfg, cfg.d_k), cfg.dtype, dev)
+    if cfg.layout == "gqa":
+        _need(v_cache, "v_cache", _kv_shape(cfg, cfg.d_v), cfg.dtype, dev)
+    _need(seq_lens, "seq_lens", (cfg.batch,), torch.int32, dev)
+    bids, tids, nt, ts = _sel_outputs(cfg, dev, sel_out)
+    if out is None:
+        out = torch.empty((cfg.batch, cfg.num_q_heads, cfg.d_v), dtype=cfg.dtype, device=dev)
+    if lse is None:
+        lse = torch.empty((cfg.batch, cfg.num_q_heads), dtype=torch.float32, device=dev)
+    g = 0
+    if guide_block_ids is not None:
+        _need(guide_block_ids, "guide_block_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_blocks), torch.int32, dev)
+        g = guide_block_ids.data_ptr()
+    cc, ic = cfg.c(), index.c()
+    _lib.check(lib.tls_decode(ctypes.byref(cc), q.data_ptr(), k_cache.data_ptr(),
+                              v_cache.data_ptr() if (v_cache is not None and cfg.layout == "gqa") else 0,
+                              seq_lens.data_ptr(), ctypes.byref(ic), g, bids.data_ptr(), tids.data_ptr(), nt.data_ptr(),
+                              ts.data_ptr() if ts is not None else 0, out.data_ptr(), lse.data_ptr(), None, 0,
+                              _stream(dev)))
+    return out, lse, bids, tids, nt, ts
+
+
+def cluster_size(cfg: TLSConfig, which: int = 2) -> int:
+    """CTAs per (batch, KV-head) pair the decode kernel launches with."""
+    cc = cfg.c()
+    return int(_lib.load().tls_cluster_size(ctypes.byref(cc), which))

@@ -1,0 +1,89 @@
+"""Parity helpers: run the fp64 oracle on the same seeded inputs as the CUDA
+path and compare element by element (north star (a)/(b)).
+
+Selection sets: identical except near-ties.  A mismatched element e is
+excused at tolerance `rel` iff its oracle score lies within
+rel * max(|s_e|, |s_K|) of the oracle's K-th score s_K (the selection
+boundary).  Two tiers are reported (reading U16): the north-star tier
+(rel = 1e-3) and a strict tier (rel = the fp32 forward-error bound of the GPU
+arithmetic), and the strict tier must be clean.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import tls_oracle as O
+
+NORTH_STAR_REL = 1e-3
+
+
+def to64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().to("cpu", torch.float64).numpy()
+
+
+def pair_slices(w, inputs, b, g):
+    """(q [G, d_k], keys [n, d_k], values [n, d_v]) of pair (b, g) as fp64 numpy."""
+    G = w.num_q_heads // w.num_kv_heads
+    n = int(inputs["seq_lens"][b].item())
+    q = to64(inputs["q"][b, g * G:(g + 1) * G])
+    if w.layout == "mla":
+        keys = to64(inputs["k_cache"][b, :n])
+        values = keys[:, : w.d_v]
+    else:
+        keys = to64(inputs["k_cache"][b, g, :n])
+        values = to64(inputs["v_cache"][b, g, :n])
+    return q, keys, values
+
+
+def oracle_channels(w, q_cal: torch.Tensor, k_cal: torch.Tensor) -> torch.Tensor:
+    """Channel set per KV head from the ORACLE's calibration."""
+    G = w.num_q_heads // w.num_kv_heads
+    qc = to64(q_cal)
+    kc = to64(k_cal)
+    chans = []
+    for g in range(w.num_kv_heads):
+        ch, _ = O.calibrate_channels(qc[:, g * G:(g + 1) * G], kc[g], w.d_c)
+        chans.append(ch)
+    return torch.tensor(np.stack(chans), dtype=torch.int32)
+
+
+def params(w) -> O.TLSParams:
+    return O.TLSParams(block_size=w.block_size, top_blocks=w.top_blocks, top_tokens=w.top_tokens, sm_scale=w.scale)
+
+
+def near_tie_mismatches(scores: np.ndarray, ref_ids: np.ndarray, got_ids: np.ndarray, k: int, rel: float):
+    """Mismatches between two top-k id sets (ids index `scores`), split into
+    (excused, unexcused) by the near-tie rule at tolerance `rel`."""
+    a, b = set(int(x) for x in ref_ids), set(int(x) for x in got_ids)
+    diff = sorted(a ^ b)
+    if not diff:
+        return [], []
+    kth = np.sort(scores)[::-1][min(k, len(scores)) - 1]
+    exc, bad = [], []
+    for e in diff:
+        s = scores[e]
+        (exc if abs(s - kth) <= rel * max(abs(s), abs(kth), 1e-300) else bad).append(e)
+    return exc, bad
+
+
+def check_ids_layout(ids: np.ndarray, count: int):
+    """Ascending, unique, -1 padded after `count` (reading U3)."""
+    assert np.all(ids[count:] == -1), f"padding not -1: {ids[count:][:8]}"
+    v = ids[:count]
+    assert np.all(v >= 0)
+    assert np.all(np.diff(v) > 0), "ids not strictly ascending"
+
+
+def attention_tol(dtype):
+    # north star (b): bf16 2e-2 max-abs and 1e-2 rel-L2; fp32 1e-4
+    return (2e-2, 1e-2) if dtype == torch.bfloat16 else (1e-4, 1e-4)
+
+
+def compare_output(out_gpu: np.ndarray, out_ref: np.ndarray, dtype, what=""):
+    mx, rl2 = attention_tol(dtype)
+    err = np.abs(out_gpu - out_ref).max()
+    rel = np.linalg.norm(out_gpu - out_ref) / max(np.linalg.norm(out_ref), 1e-30)
+    assert err <= mx, f"{what} max-abs {err:.3e} > {mx}"
+    assert rel <= rl2, f"{what} rel-L2 {rel:.3e} > {rl2}"
+    return err, rel

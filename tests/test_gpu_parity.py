@@ -1,0 +1,308 @@
+"""GPU parity of the CUDA path (libtls.so through the C ABI) against the fp64
+oracle on the same seeded inputs (north star (a)/(b)).
+
+Sizes: small cases the oracle finishes in seconds that still span several
+tiles / blocks and a ragged tail, every layout (MHA, GQA G=4/8, MLA) and dtype
+(bf16, fp32), every cluster size, the degenerate budgets, lag mode, and the
+full BASELINE.json sizes on sampled pairs in the launch configuration bench.py
+times.
+"""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tls_oracle as O
+from tests import parity as P
+
+pytestmark = pytest.mark.gpu
+
+tls = pytest.importorskip("paper_2604_07815_b200")
+from paper_2604_07815_b200 import workloads as W  # noqa: E402
+
+DEV = "cuda"
+
+SMALL = {
+    "c1": W.CONFIGS["c1"],
+    "gqa4": W.Workload("t-gqa4", 3, 16, 4, 128, 128, 5000, top_blocks=16, top_tokens=256),
+    "gqa8": W.Workload("t-gqa8", 2, 16, 2, 128, 128, 8192, top_blocks=32, top_tokens=512),
+    "mha": W.Workload("t-mha", 2, 4, 4, 64, 64, 3000, top_blocks=8, top_tokens=128),
+    "mla": W.Workload("t-mla", 2, 16, 1, 576, 512, 4133, d_c=128, top_blocks=16, top_tokens=256, layout="mla",
+                      sm_scale=1.0 / math.sqrt(192.0)),
+    "fp32_dc64_g8": W.Workload("t-fp32-dc64", 2, 16, 2, 128, 128, 3100, d_c=64, top_blocks=12, top_tokens=200,
+                               dtype=torch.float32),
+    "b128": W.Workload("t-b128", 2, 8, 2, 128, 128, 6000, block_size=128, top_blocks=10, top_tokens=300),
+}
+
+# strict-tier tolerances (fp32 forward-error bound of the GPU arithmetic; U16)
+STRICT_BLOCK = {"gqa": 2e-5, "mla": 1e-4}
+STRICT_TOKEN = 1e-4
+
+
+def setup_case(w, seed=0, pattern="outlier", ragged=True):
+    inputs = W.make_inputs(w, seed=seed, pattern=pattern, device=DEV, ragged=ragged)
+    q_cal, k_cal = W.calibration_sample(w, inputs, seed=seed, pattern=pattern)
+    channels = P.oracle_channels(w, q_cal, k_cal).to(DEV)
+    cfg = tls.TLSConfig(**w.config_kwargs())
+    idx = tls.alloc_index(cfg, channels)
+    tls.build_index(cfg, inputs["k_cache"], inputs["seq_lens"], idx)
+    return cfg, inputs, idx
+
+
+def check_pair(w, cfg, inputs, idx, res, b, g, stats):
+    out, lse, bids, tids, ntok, tsc = res
+    G = w.num_q_heads // w.num_kv_heads
+    n = int(inputs["seq_lens"][b].item())
+    q, keys, values = P.pair_slices(w, inputs, b, g)
+    ch = idx.channels[g].cpu().numpy()
+    prm = P.params(w)
+    # ---- block stage ----
+    kmax, kmin = O.block_summaries(keys, w.block_size)
+    s = O.block_scores(q, kmax, kmin)
+    m = len(s)
+    ob = O.topk_ids(s, w.top_blocks)
+    gb = bids[b, g].cpu().numpy()
+    kb = min(w.top_blocks, m)
+    P.check_ids_layout(gb, kb)
+    gb = gb[:kb]
+    exc, bad = P.near_tie_mismatches(s, ob, gb, kb, P.NORTH_STAR_REL)
+    assert not bad, f"pair {b},{g}: block mismatches beyond the near-tie band: {bad}"
+    exc_s, bad_s = P.near_tie_mismatches(s, ob, gb, kb, STRICT_BLOCK[w.layout if w.layout == 'mla' else 'gqa'])
+    assert not bad_s, f"pair {b},{g}: block mismatches beyond the strict fp32 band: {bad_s}"
+    stats["block_near_ties"] += len(exc)
+    # ---- token stage on the GPU's candidate blocks ----
+    codes, scale, zero = O.quantize_keys(keys[:, ch])
+    cand = O.candidate_tokens(gb, n, w.block_size)
+    alpha = O.approx_scores(q, ch, codes, scale, zero, cand, w.scale)
+    ot = O.select_tokens(alpha, cand, w.top_tokens)
+    nt = int(ntok[b, g].item())
+    assert nt == min(w.top_tokens, len(cand))
+    gt = tids[b, g].cpu().numpy()
+    P.check_ids_layout(gt, nt)
+    gt = gt[:nt]
+    pos_o = np.searchsorted(cand, ot)
+    pos_g = np.searchsorted(cand, gt)
+    assert np.array_equal(cand[pos_g], gt), "GPU token outside the candidate blocks"
+    exc, bad = P.near_tie_mismatches(alpha, pos_o, pos_g, nt, P.NORTH_STAR_REL)
+    assert not bad, f"pair {b},{g}: token mismatches beyond the near-tie band: {len(bad)}"
+    exc_s, bad_s = P.near_tie_mismatches(alpha, pos_o, pos_g, nt, STRICT_TOKEN)
+    assert not bad_s, f"pair {b},{g}: token mismatches beyond the strict band: {len(bad_s)}"
+    stats["token_near_ties"] += len(exc)
+    # token scores = ln alpha~ of the selected tokens
+    ts = tsc[b, g].cpu().numpy()[:nt]
+    np.testing.assert_allclose(ts, np.log(alpha[pos_g]), rtol=0, atol=2e-3)
+    # ---- attention on the GPU's ids (reading U17) ----
+    o_ref, l_ref = O.sparse_attention(q, keys, values, gt, w.scale)
+    o_gpu = P.to64(out[b, g * G:(g + 1) * G])
+    P.compare_output(o_gpu, o_ref, w.dtype, f"pair {b},{g} out")
+    np.testing.assert_allclose(P.to64(lse[b, g * G:(g + 1) * G]), l_ref, rtol=0, atol=1e-3)
+    # end to end against the oracle's own ids (reported; equal when no flip)
+    if len(exc) == 0 and set(ot) == set(gt):
+        o_e2e, _ = O.sparse_attention(q, keys, values, ot, w.scale)
+        P.compare_output(o_gpu, o_e2e, w.dtype, f"pair {b},{g} e2e")
+
+
+def run_decode(cfg, inputs, idx, guide=None):
+    return tls.decode(cfg, inputs["q"], inputs["k_cache"], inputs["v_cache"], inputs["seq_lens"], idx,
+                      guide_block_ids=guide)
+
+
+@pytest.mark.parametrize("name", list(SMALL))
+def test_decode_parity_small(name):
+    w = SMALL[name]
+    cfg, inputs, idx = setup_case(w)
+    res = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    stats = {"block_near_ties": 0, "token_near_ties": 0}
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            check_pair(w, cfg, inputs, idx, res, b, g, stats)
+    print(f"{name}: near-ties {stats}")
+
+
+@pytest.mark.parametrize("cs", [1, 2, 4, 8, 16])
+def test_every_cluster_size(cs, monkeypatch):
+    monkeypatch.setenv("TLS_CLUSTER", str(cs))
+    w = SMALL["gqa4"]
+    cfg, inputs, idx = setup_case(w, seed=1, pattern="peaked")
+    assert tls.cluster_size(cfg, 2) == cs
+    res = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    stats = {"block_near_ties": 0, "token_near_ties": 0}
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            check_pair(w, cfg, inputs, idx, res, b, g, stats)
+
+
+@pytest.mark.parametrize("name", ["gqa4", "mla", "c1"])
+def test_build_index_bit_exact(name):
+    w = SMALL[name]
+    cfg, inputs, idx = setup_case(w)
+    torch.cuda.synchronize()
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            n = int(inputs["seq_lens"][b].item())
+            _, keys, _ = P.pair_slices(w, inputs, b, g)
+            kmax, kmin = O.block_summaries(keys, w.block_size)
+            m = kmax.shape[0]
+            bm = P.to64(idx.block_minmax[b, g, :m])
+            assert np.array_equal(bm[:, 0], kmax) and np.array_equal(bm[:, 1], kmin)
+            ch = idx.channels[g].cpu().numpy()
+            codes, scale, zero = O.quantize_keys(keys[:, ch])
+            packed = idx.codes[b, g, :n].cpu().numpy()
+            lo, hi = packed & 0xF, packed >> 4
+            got = np.stack([lo, hi], axis=-1).reshape(n, w.d_c)
+            assert np.array_equal(got, codes), "INT4 codes differ"
+            sz = idx.scale_zero[b, g, :n].cpu().numpy()
+            assert np.array_equal(sz[:, 0], scale) and np.array_equal(sz[:, 1], zero)
+
+
+def test_incremental_append_matches_full_build():
+    w = SMALL["gqa4"]
+    cfg, inputs, idx = setup_case(w, ragged=False)
+    full = [t.clone() for t in (idx.block_minmax, idx.codes, idx.scale_zero)]
+    # rebuild only from token 3000 on after corrupting that tail
+    start = 3000
+    sb = start // w.block_size
+    idx.block_minmax[:, :, sb:].fill_(0)
+    idx.codes[:, :, sb * w.block_size:].fill_(0)
+    idx.scale_zero[:, :, sb * w.block_size:].fill_(0)
+    tls.build_index(cfg, inputs["k_cache"], inputs["seq_lens"], idx, start_token=start)
+    torch.cuda.synchronize()
+    assert torch.equal(idx.block_minmax, full[0])
+    assert torch.equal(idx.codes, full[1])
+    assert torch.equal(idx.scale_zero, full[2])
+
+
+@pytest.mark.parametrize("name", ["gqa8", "mla", "c1"])
+def test_calibration_matches_oracle(name):
+    w = SMALL[name]
+    inputs = W.make_inputs(w, seed=3, pattern="outlier", device=DEV)
+    q_cal, k_cal = W.calibration_sample(w, inputs, seed=3)
+    cfg = tls.TLSConfig(**w.config_kwargs())
+    ch, sc = tls.calibrate_channels(cfg, q_cal, k_cal)
+    torch.cuda.synchronize()
+    G = w.num_q_heads // w.num_kv_heads
+    for g in range(w.num_kv_heads):
+        och, osc = O.calibrate_channels(P.to64(q_cal)[:, g * G:(g + 1) * G], P.to64(k_cal)[g], w.d_c)
+        assert np.array_equal(ch[g].cpu().numpy(), och)
+        assert np.array_equal(sc[g].cpu().numpy(), osc.astype(np.float32))
+
+
+@pytest.mark.parametrize("name", ["gqa4", "mla", "c1"])
+def test_degenerate_budget_is_dense_attention(name):
+    base = SMALL[name]
+    w = base.with_(top_blocks=10_000, top_tokens=base.S)
+    cfg, inputs, idx = setup_case(w)
+    out, lse, bids, tids, ntok, _ = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    G = w.num_q_heads // w.num_kv_heads
+    for b in range(w.batch):
+        n = int(inputs["seq_lens"][b].item())
+        for g in range(w.num_kv_heads):
+            assert int(ntok[b, g]) == n
+            assert np.array_equal(tids[b, g, :n].cpu().numpy(), np.arange(n))
+            q, keys, values = P.pair_slices(w, inputs, b, g)
+            o_ref, l_ref = O.dense_attention(q, keys, values, w.scale)
+            P.compare_output(P.to64(out[b, g * G:(g + 1) * G]), o_ref, w.dtype, "dense")
+            np.testing.assert_allclose(P.to64(lse[b, g * G:(g + 1) * G]), l_ref, rtol=0, atol=1e-3)
+
+
+def test_lag_mode_uses_guide_blocks():
+    w = SMALL["gqa4"]
+    cfg, inputs, idx = setup_case(w, seed=5)
+    gen = torch.Generator().manual_seed(5)
+    guide = torch.full((w.batch, w.num_kv_heads, w.top_blocks), -1, dtype=torch.int32)
+    for b in range(w.batch):
+        m = (int(inputs["seq_lens"][b]) + w.block_size - 1) // w.block_size
+        for g in range(w.num_kv_heads):
+            k = int(torch.randint(1, w.top_blocks + 1, (1,), generator=gen))
+            ids = torch.randperm(m, generator=gen)[:k].sort().values
+            guide[b, g, : len(ids)] = ids.to(torch.int32)
+    guide = guide.to(DEV)
+    out, lse, bids, tids, ntok, tsc = run_decode(cfg, inputs, idx, guide=guide)
+    torch.cuda.synchronize()
+    G = w.num_q_heads // w.num_kv_heads
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            q, keys, values = P.pair_slices(w, inputs, b, g)
+            gd = guide[b, g].cpu().numpy()
+            r = O.tls_pair(q, keys, values, idx.channels[g].cpu().numpy(), P.params(w), guide_block_ids=gd)
+            nt = int(ntok[b, g])
+            assert nt == min(w.top_tokens, len(r["candidates"]))
+            gt = tids[b, g, :nt].cpu().numpy()
+            cand = r["candidates"]
+            exc, bad = P.near_tie_mismatches(r["alpha"], np.searchsorted(cand, r["token_ids"]),
+                                             np.searchsorted(cand, gt), nt, STRICT_TOKEN)
+            assert not bad
+            o_ref, _ = O.sparse_attention(q, keys, values, gt, w.scale)
+            P.compare_output(P.to64(out[b, g * G:(g + 1) * G]), o_ref, w.dtype, "lag")
+
+
+@pytest.mark.parametrize("name", ["gqa8", "mla"])
+def test_separate_calls_equal_fused(name):
+    w = SMALL[name]
+    cfg, inputs, idx = setup_case(w, seed=2)
+    fused = run_decode(cfg, inputs, idx)
+    bids, tids, ntok, tsc = tls.select(cfg, inputs["q"], inputs["seq_lens"], idx)
+    out, lse = tls.sparse_attend(cfg, inputs["q"], inputs["k_cache"], inputs["v_cache"], tids, ntok)
+    torch.cuda.synchronize()
+    assert torch.equal(bids, fused[2]) and torch.equal(tids, fused[3]) and torch.equal(ntok, fused[4])
+    assert torch.equal(tsc, fused[5])
+    torch.testing.assert_close(out.float(), fused[0].float(), rtol=0, atol=1e-6)
+    torch.testing.assert_close(lse, fused[1], rtol=0, atol=1e-6)
+
+
+def test_edge_single_token_and_k1():
+    w = W.Workload("t-edge", 3, 8, 2, 128, 128, 700, top_blocks=1, top_tokens=1)
+    inputs = W.make_inputs(w, seed=9, device=DEV, seq_lens=[1, 65, 700])
+    q_cal, k_cal = W.calibration_sample(w, inputs, seed=9)
+    channels = P.oracle_channels(w, q_cal, k_cal).to(DEV)
+    cfg = tls.TLSConfig(**w.config_kwargs())
+    idx = tls.alloc_index(cfg, channels)
+    tls.build_index(cfg, inputs["k_cache"], inputs["seq_lens"], idx)
+    res = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    stats = {"block_near_ties": 0, "token_near_ties": 0}
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            check_pair(w, cfg, inputs, idx, res, b, g, stats)
+
+
+def test_errors_are_reported():
+    w = SMALL["gqa4"]
+    cfg, inputs, idx = setup_case(w)
+    bad = tls.TLSConfig(**{**w.config_kwargs(), "d_c": 48})
+    with pytest.raises(tls.TLSError, match="UNSUPPORTED"):
+        tls.select(bad, inputs["q"], inputs["seq_lens"], idx)
+    bad = tls.TLSConfig(**{**w.config_kwargs(), "num_kv_heads": 3})
+    with pytest.raises((tls.TLSError, ValueError)):
+        tls.select(bad, inputs["q"], inputs["seq_lens"], idx)
+
+
+# ---- full BASELINE.json sizes, sampled pairs, bench launch configuration ----
+FULL_SAMPLES = {"c2": [(0, 0), (7, 3), (15, 7)], "c3": [(0, 0), (13, 5), (31, 7)], "c4": [(0, 0), (17, 0), (31, 0)]}
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_full_size_sampled_pairs(name):
+    w = W.CONFIGS[name]
+    inputs = W.make_inputs(w, seed=0, pattern="peaked", device=DEV)
+    q_cal, k_cal = W.calibration_sample(w, inputs, seed=0, pattern="peaked")
+    channels = P.oracle_channels(w, q_cal, k_cal).to(DEV)
+    cfg = tls.TLSConfig(**w.config_kwargs())
+    idx = tls.alloc_index(cfg, channels)
+    tls.build_index(cfg, inputs["k_cache"], inputs["seq_lens"], idx)
+    res = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    stats = {"block_near_ties": 0, "token_near_ties": 0}
+    for b, g in FULL_SAMPLES[name]:
+        check_pair(w, cfg, inputs, idx, res, b, g, stats)
+    print(f"{name}: near-ties {stats}")
+    del inputs, idx, res
+    torch.cuda.empty_cache()
