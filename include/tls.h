@@ -177,20 +177,22 @@ tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
                       void* workspace, size_t workspace_bytes, tls_stream_t stream);
 
 /* Workspace bytes needed by: which = 0 tls_select, 1 tls_sparse_attend,
- * 2 tls_decode.  This implementation keeps every intermediate in (distributed)
- * shared memory and returns 0 for a valid configuration (workspace may then be
- * NULL); returns (size_t)-1 for an invalid configuration or `which`. */
+ * 2 tls_decode: the fp32 block scores of every pair ([batch, Hkv, M] floats,
+ * rounded up to 256 B) that the block-score kernel hands to the token-select
+ * kernel; 0 for tls_sparse_attend.  (size_t)-1 for an invalid configuration
+ * or `which`.  A NULL / too small / misaligned workspace -> TLS_ERR_WORKSPACE. */
 size_t tls_workspace_bytes(const tls_config* cfg, int32_t which);
 
 /* Number of kernel launches one call enqueues (which as above; 3 =
- * tls_build_index, 4 = tls_calibrate_channels), for launch accounting;
+ * tls_build_index, 4 = tls_calibrate_channels), for launch accounting:
+ * tls_select 2 (block scores, token select), tls_sparse_attend 1, tls_decode 3;
  * -1 for an invalid configuration. */
 int32_t tls_launch_count(const tls_config* cfg, int32_t which);
 
-/* CTAs per (batch, KV-head) pair -- the thread-block cluster size -- that
- * the decode kernel uses for `which` (0 select, 1 attend, 2 decode); -1 for an
- * invalid configuration.  The environment variable TLS_CLUSTER overrides the
- * heuristic (1, 2, 4, 8 or 16). */
+/* CTAs per (batch, KV-head) pair -- the thread-block cluster size -- of the
+ * token-select kernel (which = 0 or 2) or of the attention kernel (which = 1);
+ * -1 for an invalid configuration.  The environment variable TLS_CLUSTER
+ * overrides the heuristic for both (1, 2, 4, 8 or 16). */
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which);
 
 const char* tls_status_string(tls_status status);

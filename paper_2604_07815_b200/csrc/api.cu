@@ -9,13 +9,15 @@
 #include <cuda_runtime.h>
 
 #include "../../include/tls.h"
-#include "decode.h"
-
 #include "index.h"
+#include "params.h"
 
 namespace tls {
-cudaError_t launch_decode(const DecodeParams& p, bool bf16, cudaStream_t stream);
-int decode_cpl(int d_k, size_t elem_bytes);
+cudaError_t launch_block_scores(const ScoreParams& p, cudaStream_t st);
+cudaError_t launch_token_select(const SelectParams& p, cudaStream_t st);
+cudaError_t launch_attend(const AttendParams& p, cudaStream_t st);
+int score_cpl(int d_k, size_t elem_bytes);
+bool select_supported(int d_c, int G);
 }  // namespace tls
 
 namespace {
@@ -38,7 +40,8 @@ bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 size_t elem_bytes(const tls_config* c) { return c->dtype == TLS_BF16 ? 2 : 4; }
 
-constexpr int kMaxSmem = 227 * 1024 - 8 * 1024;  // dynamic budget (static Ctl ~5 KB)
+constexpr int kMaxSmem = 227 * 1024 - 8 * 1024;  // dynamic budget (static control blocks < 8 KB)
+constexpr int kSMs = 148;
 
 // Shape / hyper-parameter checks shared by every call.
 tls_status check_config(const tls_config* c) {
@@ -62,52 +65,81 @@ tls_status check_config(const tls_config* c) {
   const size_t eb = elem_bytes(c);
   if ((c->d_k * eb) % 16 || (c->d_v * eb) % 16)
     return fail(TLS_ERR_UNSUPPORTED, "d_k and d_v rows must be multiples of 16 bytes");
-  if (c->d_c % 32 || c->d_c > 128) return fail(TLS_ERR_UNSUPPORTED, "d_c must be a multiple of 32 and <= 128");
-  if (c->block_size % 16 || c->block_size > 1024) return fail(TLS_ERR_UNSUPPORTED, "block_size must be a multiple of 16, <= 1024");
   const int G = c->num_q_heads / c->num_kv_heads;
-  if (G > 64) return fail(TLS_ERR_UNSUPPORTED, "at most 64 query heads per KV head");
+  if (G > 32) return fail(TLS_ERR_UNSUPPORTED, "at most 32 query heads per KV head");
+  if (c->d_c % 32 || c->d_c > 128 || !tls::select_supported(c->d_c, G))
+    return fail(TLS_ERR_UNSUPPORTED, "d_c must be 32, 64 or 128");
+  if (c->block_size % 16 || c->block_size > 1024) return fail(TLS_ERR_UNSUPPORTED, "block_size must be a multiple of 16, <= 1024");
   if ((long long)c->batch * c->num_kv_heads > 65535) return fail(TLS_ERR_UNSUPPORTED, "batch*num_kv_heads > 65535");
-  if (tls::decode_cpl(c->d_k, eb) < 0) return fail(TLS_ERR_UNSUPPORTED, "d_k too large for the block-score kernel");
+  if (tls::score_cpl(c->d_k, eb) < 0) return fail(TLS_ERR_UNSUPPORTED, "d_k too large for the block-score kernel");
   return TLS_OK;
 }
 
-void fill_dims(const tls_config* c, tls::DecodeParams& p) {
-  memset(&p, 0, sizeof(p));
-  p.batch = c->batch;
-  p.Hq = c->num_q_heads;
-  p.Hkv = c->num_kv_heads;
-  p.G = c->num_q_heads / c->num_kv_heads;
-  p.d_k = c->d_k;
-  p.d_v = c->d_v;
-  p.S = c->max_seq_len;
-  p.B = c->block_size;
-  p.d_c = c->d_c;
-  p.Kb = c->top_blocks;
-  p.Kt = c->top_tokens;
-  p.M = (c->max_seq_len + c->block_size - 1) / c->block_size;
-  p.sm_scale = c->sm_scale;
-  p.mla = c->layout == TLS_MLA;
-  p.nsplit = c->dtype == TLS_BF16 ? 1 : 3;
+tls::Dims dims_of(const tls_config* c) {
+  tls::Dims d;
+  memset(&d, 0, sizeof(d));
+  d.batch = c->batch;
+  d.Hq = c->num_q_heads;
+  d.Hkv = c->num_kv_heads;
+  d.G = c->num_q_heads / c->num_kv_heads;
+  d.d_k = c->d_k;
+  d.d_v = c->d_v;
+  d.S = c->max_seq_len;
+  d.B = c->block_size;
+  d.d_c = c->d_c;
+  d.Kb = c->top_blocks;
+  d.Kt = c->top_tokens;
+  d.M = (c->max_seq_len + c->block_size - 1) / c->block_size;
+  d.sm_scale = c->sm_scale;
+  d.mla = c->layout == TLS_MLA;
+  d.bf16 = c->dtype == TLS_BF16;
+  return d;
 }
 
-// Cluster size (CTAs per pair): enough CTAs to cover the 148 SMs a few times,
-// and a shared-memory footprint that fits.  TLS_CLUSTER overrides (tuning).
-tls_status plan(const tls_config* c, tls::DecodeParams& p, int do_select, int do_attend) {
-  fill_dims(c, p);
-  p.do_select = do_select;
-  p.do_attend = do_attend;
-  const long long pairs = (long long)c->batch * c->num_kv_heads;
-  int cs = 1;
+int env_cluster() {
   const char* env = getenv("TLS_CLUSTER");
-  if (env && atoi(env) > 0) {
-    cs = atoi(env);
-  } else {
-    while (cs < 8 && pairs * cs < 4 * 148) cs *= 2;
+  return (env && atoi(env) > 0) ? atoi(env) : 0;
+}
+
+// K2 cluster size: each CTA stages <= ~48 KB of token index, and the grid
+// covers the 148 SMs at least twice.  TLS_CLUSTER overrides (tuning / tests).
+tls_status plan_select(const tls_config* c, tls::SelectParams& p) {
+  memset(&p, 0, sizeof(p));
+  p.d = dims_of(c);
+  const long long pairs = (long long)c->batch * c->num_kv_heads;
+  const int kb = tls::kb_effective(p.d);
+  const size_t per_block = (size_t)p.d.B * (p.d.d_c / 2 + 8);
+  int cs = env_cluster();
+  if (!cs) {
+    cs = 1;
+    while (cs < 16 && ((size_t)((kb + cs - 1) / cs) * per_block > 48 * 1024 || pairs * cs < 2 * kSMs)) cs *= 2;
   }
   for (;; cs *= 2) {
-    if (cs > 16) return fail(TLS_ERR_UNSUPPORTED, "shared-memory plan does not fit even with 16 CTAs per pair");
+    if (cs > 16) return fail(TLS_ERR_UNSUPPORTED, "token-select shared-memory plan does not fit");
     p.cs = cs;
-    tls::plan_decode_smem(p, elem_bytes(c));
+    tls::plan_select(p);
+    if ((int)p.smem_bytes <= kMaxSmem) break;
+  }
+  return TLS_OK;
+}
+
+// K3 cluster size: ~128 tokens per CTA (one staging chunk), >= 2 CTAs per SM.
+tls_status plan_attend(const tls_config* c, tls::AttendParams& p) {
+  memset(&p, 0, sizeof(p));
+  p.d = dims_of(c);
+  p.mma = c->dtype == TLS_BF16 && c->layout == TLS_GQA && c->d_k == c->d_v && (c->d_k == 64 || c->d_k == 128) &&
+          p.d.G <= 16;
+  const long long pairs = (long long)c->batch * c->num_kv_heads;
+  const int kt = tls::kt_effective(p.d);
+  int cs = env_cluster();
+  if (!cs) {
+    cs = 1;
+    while (cs < 16 && ((kt + cs - 1) / cs > tls::kAttnChunk || pairs * cs < 2 * kSMs)) cs *= 2;
+  }
+  for (;; cs *= 2) {
+    if (cs > 16) return fail(TLS_ERR_UNSUPPORTED, "attention shared-memory plan does not fit");
+    p.cs = cs;
+    tls::plan_attend(p);
     if ((int)p.smem_bytes <= kMaxSmem) break;
   }
   return TLS_OK;
@@ -121,46 +153,67 @@ tls_status check_index(const tls_index* idx) {
   return TLS_OK;
 }
 
-tls_status run_decode(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
-                      const int32_t* seq_lens, const tls_index* idx, const int32_t* guide, int32_t* block_ids,
-                      int32_t* token_ids, int32_t* num_tokens, float* token_scores, void* out, float* lse,
-                      int do_select, int do_attend, tls_stream_t stream) {
+tls_status run_select(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
+                      const int32_t* guide, int32_t* block_ids, int32_t* token_ids, int32_t* num_tokens,
+                      float* token_scores, void* workspace, size_t workspace_bytes, cudaStream_t st) {
   tls_status s = check_config(cfg);
   if (s) return s;
   if (!q || !aligned16(q)) return fail(TLS_ERR_INPUT, "q must be a non-NULL 16-byte aligned device pointer");
-  if (!token_ids || !num_tokens) return fail(TLS_ERR_INPUT, "token_ids and num_tokens are required");
-  tls::DecodeParams p;
-  s = plan(cfg, p, do_select, do_attend);
+  if (!seq_lens || !block_ids || !token_ids || !num_tokens)
+    return fail(TLS_ERR_INPUT, "seq_lens, block_ids, token_ids and num_tokens are required");
+  s = check_index(idx);
   if (s) return s;
-  if (do_select) {
-    s = check_index(idx);
-    if (s) return s;
-    if (!seq_lens || !block_ids) return fail(TLS_ERR_INPUT, "seq_lens and block_ids are required");
-    p.block_minmax = idx->block_minmax;
-    p.codes = idx->codes;
-    p.scale_zero = idx->scale_zero;
-    p.channels = idx->channels;
-  }
-  if (do_attend) {
-    if (!k_cache || !aligned16(k_cache)) return fail(TLS_ERR_INPUT, "k_cache must be a 16-byte aligned device pointer");
-    if (cfg->layout == TLS_GQA && (!v_cache || !aligned16(v_cache)))
-      return fail(TLS_ERR_INPUT, "GQA needs a 16-byte aligned v_cache");
-    if (!out) return fail(TLS_ERR_INPUT, "out is required");
-  }
-  if (!seq_lens) return fail(TLS_ERR_INPUT, "seq_lens is required");
-  p.q = q;
-  p.k_cache = k_cache;
-  p.v_cache = cfg->layout == TLS_MLA ? nullptr : v_cache;
-  p.seq_lens = seq_lens;
-  p.guide = guide;
-  p.block_ids = block_ids;
-  p.token_ids = token_ids;
-  p.num_tokens = num_tokens;
-  p.token_scores = token_scores;
-  p.out = out;
-  p.lse = lse;
-  cudaError_t e = tls::launch_decode(p, cfg->dtype == TLS_BF16, (cudaStream_t)stream);
-  if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
+  tls::SelectParams sp;
+  s = plan_select(cfg, sp);
+  if (s) return s;
+  const size_t need = tls::select_workspace_bytes(sp.d);
+  if (!workspace || workspace_bytes < need || !aligned16(workspace))
+    return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes, 16-byte aligned (got %zu)", need, workspace_bytes);
+  tls::ScoreParams k1;
+  k1.d = sp.d;
+  k1.q = q;
+  k1.seq_lens = seq_lens;
+  k1.block_minmax = idx->block_minmax;
+  k1.scores = static_cast<float*>(workspace);
+  cudaError_t e = tls::launch_block_scores(k1, st);
+  if (e != cudaSuccess) return cuda_fail(e, "block_score_kernel launch");
+  sp.q = q;
+  sp.seq_lens = seq_lens;
+  sp.scores = k1.scores;
+  sp.codes = idx->codes;
+  sp.scale_zero = idx->scale_zero;
+  sp.channels = idx->channels;
+  sp.guide = guide;
+  sp.block_ids = block_ids;
+  sp.token_ids = token_ids;
+  sp.num_tokens = num_tokens;
+  sp.token_scores = token_scores;
+  e = tls::launch_token_select(sp, st);
+  if (e != cudaSuccess) return cuda_fail(e, "token_select_kernel launch");
+  return TLS_OK;
+}
+
+tls_status run_attend(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
+                      const int32_t* token_ids, const int32_t* num_tokens, void* out, float* lse, cudaStream_t st) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if (!q || !aligned16(q)) return fail(TLS_ERR_INPUT, "q must be a non-NULL 16-byte aligned device pointer");
+  if (!token_ids || !num_tokens || !out) return fail(TLS_ERR_INPUT, "token_ids, num_tokens and out are required");
+  if (!k_cache || !aligned16(k_cache)) return fail(TLS_ERR_INPUT, "k_cache must be a 16-byte aligned device pointer");
+  if (cfg->layout == TLS_GQA && (!v_cache || !aligned16(v_cache)))
+    return fail(TLS_ERR_INPUT, "GQA needs a 16-byte aligned v_cache");
+  tls::AttendParams ap;
+  s = plan_attend(cfg, ap);
+  if (s) return s;
+  ap.q = q;
+  ap.k_cache = k_cache;
+  ap.v_cache = cfg->layout == TLS_MLA ? nullptr : v_cache;
+  ap.token_ids = token_ids;
+  ap.num_tokens = num_tokens;
+  ap.out = out;
+  ap.lse = lse;
+  cudaError_t e = tls::launch_attend(ap, st);
+  if (e != cudaSuccess) return cuda_fail(e, "attend_kernel launch");
   return TLS_OK;
 }
 
@@ -226,10 +279,8 @@ tls_status tls_build_index(const tls_config* cfg, const void* k_cache, const int
 tls_status tls_select(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
                       const int32_t* guide_block_ids, int32_t* block_ids, int32_t* token_ids, int32_t* num_tokens,
                       float* token_scores, void* workspace, size_t workspace_bytes, tls_stream_t stream) {
-  (void)workspace;
-  (void)workspace_bytes;
-  return run_decode(cfg, q, nullptr, nullptr, seq_lens, idx, guide_block_ids, block_ids, token_ids, num_tokens,
-                    token_scores, nullptr, nullptr, 1, 0, stream);
+  return run_select(cfg, q, seq_lens, idx, guide_block_ids, block_ids, token_ids, num_tokens, token_scores,
+                    workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 tls_status tls_sparse_attend(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
@@ -237,64 +288,52 @@ tls_status tls_sparse_attend(const tls_config* cfg, const void* q, const void* k
                              void* workspace, size_t workspace_bytes, tls_stream_t stream) {
   (void)workspace;
   (void)workspace_bytes;
-  // seq_lens is not needed by attention; pass a dummy non-NULL pointer check-free path.
-  tls_status s = check_config(cfg);
-  if (s) return s;
-  if (!q || !aligned16(q)) return fail(TLS_ERR_INPUT, "q must be a non-NULL 16-byte aligned device pointer");
-  if (!token_ids || !num_tokens || !out) return fail(TLS_ERR_INPUT, "token_ids, num_tokens and out are required");
-  if (!k_cache || !aligned16(k_cache)) return fail(TLS_ERR_INPUT, "k_cache must be a 16-byte aligned device pointer");
-  if (cfg->layout == TLS_GQA && (!v_cache || !aligned16(v_cache)))
-    return fail(TLS_ERR_INPUT, "GQA needs a 16-byte aligned v_cache");
-  tls::DecodeParams p;
-  s = plan(cfg, p, 0, 1);
-  if (s) return s;
-  p.q = q;
-  p.k_cache = k_cache;
-  p.v_cache = cfg->layout == TLS_MLA ? nullptr : v_cache;
-  p.seq_lens = num_tokens;  // read only to clamp; attention does not use it
-  p.token_ids = const_cast<int32_t*>(token_ids);
-  p.num_tokens = const_cast<int32_t*>(num_tokens);
-  p.out = out;
-  p.lse = lse;
-  cudaError_t e = tls::launch_decode(p, cfg->dtype == TLS_BF16, (cudaStream_t)stream);
-  if (e != cudaSuccess) return cuda_fail(e, "attend kernel launch");
-  return TLS_OK;
+  return run_attend(cfg, q, k_cache, v_cache, token_ids, num_tokens, out, lse, (cudaStream_t)stream);
 }
 
 tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
                       const int32_t* seq_lens, const tls_index* idx, const int32_t* guide_block_ids,
                       int32_t* block_ids, int32_t* token_ids, int32_t* num_tokens, float* token_scores, void* out,
                       float* lse, void* workspace, size_t workspace_bytes, tls_stream_t stream) {
-  (void)workspace;
-  (void)workspace_bytes;
-  return run_decode(cfg, q, k_cache, v_cache, seq_lens, idx, guide_block_ids, block_ids, token_ids, num_tokens,
-                    token_scores, out, lse, 1, 1, stream);
+  // validate everything before enqueuing anything
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if (!k_cache || !aligned16(k_cache)) return fail(TLS_ERR_INPUT, "k_cache must be a 16-byte aligned device pointer");
+  if (cfg->layout == TLS_GQA && (!v_cache || !aligned16(v_cache)))
+    return fail(TLS_ERR_INPUT, "GQA needs a 16-byte aligned v_cache");
+  if (!out) return fail(TLS_ERR_INPUT, "out is required");
+  s = run_select(cfg, q, seq_lens, idx, guide_block_ids, block_ids, token_ids, num_tokens, token_scores, workspace,
+                 workspace_bytes, (cudaStream_t)stream);
+  if (s) return s;
+  return run_attend(cfg, q, k_cache, v_cache, token_ids, num_tokens, out, lse, (cudaStream_t)stream);
 }
 
 size_t tls_workspace_bytes(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK || which < 0 || which > 2) return (size_t)-1;
-  return 0;  // every intermediate lives in (distributed) shared memory
+  if (which == 1) return 0;
+  return tls::select_workspace_bytes(dims_of(cfg));
 }
 
 int32_t tls_launch_count(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK) return -1;
   switch (which) {
-    case 0:
-    case 1:
-    case 2:
-    case 3:
-    case 4:
-      return 1;
-    default:
-      return -1;
+    case 0: return 2;  // block_score_kernel + token_select_kernel
+    case 1: return 1;  // attend_kernel
+    case 2: return 3;
+    case 3: return 1;  // build_index_kernel
+    case 4: return 1;  // calibrate_kernel
+    default: return -1;
   }
 }
 
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK || which < 0 || which > 2) return -1;
-  tls::DecodeParams p;
-  if (plan(cfg, p, which != 1, which != 0) != TLS_OK) return -1;
-  return p.cs;
+  if (which == 1) {
+    tls::AttendParams ap;
+    return plan_attend(cfg, ap) == TLS_OK ? ap.cs : -1;
+  }
+  tls::SelectParams sp;
+  return plan_select(cfg, sp) == TLS_OK ? sp.cs : -1;
 }
 
 const char* tls_status_string(tls_status status) {

@@ -1,0 +1,127 @@
+// params.h -- host/device parameter blocks and shared-memory plans of the
+// three decode-step kernels:
+//   K1 block_score_kernel   (select.cu)  a1: block scores -> workspace
+//   K2 token_select_kernel  (select.cu)  a2-a4: top-k_b, token scores, top-k_t
+//   K3 attend_kernel        (attend.cu)  a5: sparse attention + LSE merge
+#pragma once
+
+#include <stddef.h>
+#include <stdint.h>
+
+namespace tls {
+
+constexpr int kAttnChunk = 128;    // tokens per K/V staging chunk of the mma attention (8 warps x 16)
+constexpr int kScoreChunk = 128;   // blocks per K1 CTA
+
+struct Dims {
+  int batch, Hq, Hkv, G, d_k, d_v, S, B, d_c, Kb, Kt;
+  int M;  // ceil(S / B): block-index rows per pair
+  float sm_scale;
+  int mla;
+  int bf16;
+};
+
+struct ScoreParams {  // K1
+  Dims d;
+  const void* q;
+  const int* seq_lens;
+  const void* block_minmax;
+  float* scores;  // workspace [pairs, M] fp32
+};
+
+struct SelectParams {  // K2
+  Dims d;
+  int cs;
+  int kb_eff, kt_eff;  // min(Kb, M); min(Kt, kb_eff*B, S)
+  int mloc, lc_max;    // keys per CTA in the block top-k (= M); candidate slots per CTA
+  const void* q;
+  const int* seq_lens;
+  const float* scores;
+  const uint8_t* codes;
+  const float* scale_zero;
+  const int* channels;
+  const int* guide;
+  int* block_ids;
+  int* token_ids;
+  int* num_tokens;
+  float* token_scores;
+  unsigned off_bkeys, off_cblk, off_qb, off_qsum, off_stc, off_stz, off_tkeys, smem_bytes;
+};
+
+struct AttendParams {  // K3
+  Dims d;
+  int cs;
+  int mma;       // 1: bf16 mma.sync path (GQA, d in {64,128}, G <= 16)
+  int tloc_max;  // ceil(kt_eff / cs)
+  const void* q;
+  const void* k_cache;
+  const void* v_cache;
+  const int* token_ids;
+  const int* num_tokens;
+  void* out;
+  float* lse;
+  unsigned off_sel, off_akv, off_aq, off_as, off_ao, smem_bytes;
+};
+
+static inline unsigned align16(size_t x) { return (unsigned)((x + 15) & ~(size_t)15); }
+
+static inline int kb_effective(const Dims& d) { return d.Kb < d.M ? d.Kb : d.M; }
+static inline int kt_effective(const Dims& d) {
+  const long long cand = (long long)kb_effective(d) * d.B < d.S ? (long long)kb_effective(d) * d.B : d.S;
+  return d.Kt < cand ? d.Kt : (int)cand;
+}
+
+static inline void plan_select(SelectParams& p) {
+  const Dims& d = p.d;
+  p.kb_eff = kb_effective(d);
+  p.kt_eff = kt_effective(d);
+  p.mloc = d.M;
+  const int nt0 = (d.G + 7) / 8, nt = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);  // instantiated NT
+  const int ks = d.d_c / 16, nsplit = d.bf16 ? 1 : 3;
+  p.lc_max = ((p.kb_eff + p.cs - 1) / p.cs) * d.B;
+  size_t o = 0;
+  p.off_bkeys = (unsigned)o;
+  o = align16(o + (size_t)d.M * 4);
+  p.off_cblk = (unsigned)o;
+  o = align16(o + (size_t)p.kb_eff * 4);
+  p.off_qb = (unsigned)o;
+  o = align16(o + (size_t)nsplit * nt * ks * 64 * 4);
+  p.off_qsum = (unsigned)o;
+  o = align16(o + (size_t)nt * 8 * 4);
+  p.off_stc = (unsigned)o;
+  o = align16(o + (size_t)p.lc_max * (d.d_c / 2));
+  p.off_stz = (unsigned)o;
+  o = align16(o + (size_t)p.lc_max * 8);
+  p.off_tkeys = (unsigned)o;
+  o = align16(o + (size_t)p.lc_max * 4);
+  p.smem_bytes = (unsigned)o;
+}
+
+static inline void plan_attend(AttendParams& p) {
+  const Dims& d = p.d;
+  p.tloc_max = (kt_effective(d) + p.cs - 1) / p.cs;
+  size_t o = 0;
+  p.off_sel = (unsigned)o;
+  o = align16(o + (size_t)(p.tloc_max + 1) * 4);
+  if (p.mma) {
+    p.off_akv = (unsigned)o;  // K chunk + V chunk; reused as the warp-partial scratch
+    size_t kv = (size_t)2 * kAttnChunk * d.d_k * 2;
+    size_t scratch = (size_t)8 * d.G * d.d_v * 4 + (size_t)8 * 16 * 2 * 4;
+    o = align16(o + (kv > scratch ? kv : scratch));
+  } else {
+    p.off_aq = (unsigned)o;
+    o = align16(o + (size_t)d.G * d.d_k * 4);
+    p.off_as = (unsigned)o;
+    o = align16(o + (size_t)d.G * p.tloc_max * 4);
+  }
+  p.off_ao = (unsigned)o;
+  o = align16(o + (size_t)d.G * d.d_v * 4);
+  p.smem_bytes = (unsigned)o;
+}
+
+// Workspace of tls_select / tls_decode: K1's fp32 block scores.
+static inline size_t select_workspace_bytes(const Dims& d) {
+  return ((size_t)d.batch * d.Hkv * d.M * 4 + 255) & ~(size_t)255;
+}
+
+}  // namespace tls

@@ -91,6 +91,23 @@ class TLSIndex:
                               self.channels.data_ptr())
 
 
+_WS: dict = {}
+
+
+def _workspace(cfg: TLSConfig, dev: torch.device, which: int):
+    """Device workspace for tls_select / tls_decode (cached per device and size)."""
+    cc = cfg.c()
+    nbytes = int(_lib.load().tls_workspace_bytes(ctypes.byref(cc), which))
+    if nbytes == ctypes.c_size_t(-1).value or nbytes == 0:  # invalid config: the op call reports why
+        return None, 0
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        _WS[key] = buf
+    return buf.data_ptr(), nbytes
+
+
 def _stream(dev: torch.device) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
@@ -192,9 +209,10 @@ def select(cfg: TLSConfig, q: torch.Tensor, seq_lens: torch.Tensor, index: TLSIn
         _need(guide_block_ids, "guide_block_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_blocks), torch.int32, dev)
         g = guide_block_ids.data_ptr()
     cc, ic = cfg.c(), index.c()
+    ws, wsb = _workspace(cfg, dev, 0)
     _lib.check(lib.tls_select(ctypes.byref(cc), q.data_ptr(), seq_lens.data_ptr(), ctypes.byref(ic), g,
                               bids.data_ptr(), tids.data_ptr(), nt.data_ptr(),
-                              ts.data_ptr() if ts is not None else 0, None, 0, _stream(dev)))
+                              ts.data_ptr() if ts is not None else 0, ws, wsb, _stream(dev)))
     return bids, tids, nt, ts
 
 
@@ -245,15 +263,16 @@ def decode(cfg: TLSConfig, q: torch.Tensor, k_cache: torch.Tensor, v_cache: torc
         _need(guide_block_ids, "guide_block_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_blocks), torch.int32, dev)
         g = guide_block_ids.data_ptr()
     cc, ic = cfg.c(), index.c()
+    ws, wsb = _workspace(cfg, dev, 2)
     _lib.check(lib.tls_decode(ctypes.byref(cc), q.data_ptr(), k_cache.data_ptr(),
                               v_cache.data_ptr() if (v_cache is not None and cfg.layout == "gqa") else 0,
                               seq_lens.data_ptr(), ctypes.byref(ic), g, bids.data_ptr(), tids.data_ptr(), nt.data_ptr(),
-                              ts.data_ptr() if ts is not None else 0, out.data_ptr(), lse.data_ptr(), None, 0,
+                              ts.data_ptr() if ts is not None else 0, out.data_ptr(), lse.data_ptr(), ws, wsb,
                               _stream(dev)))
     return out, lse, bids, tids, nt, ts
 
 
 def cluster_size(cfg: TLSConfig, which: int = 2) -> int:
-    """CTAs per (batch, KV-head) pair the decode kernel launches with."""
+    """CTAs per (batch, KV-head) pair: token-select kernel (which 0/2) or attention kernel (1)."""
     cc = cfg.c()
     return int(_lib.load().tls_cluster_size(ctypes.byref(cc), which))

@@ -80,10 +80,23 @@ def attention_tol(dtype):
     return (2e-2, 1e-2) if dtype == torch.bfloat16 else (1e-4, 1e-4)
 
 
+def bf16_half_ulp(x: np.ndarray) -> np.ndarray:
+    """Half a bf16 ulp at |x| (8-bit significand): the output format's own quantum."""
+    ax = np.maximum(np.abs(x), 2.0 ** -126)
+    return 0.5 * 2.0 ** (np.floor(np.log2(ax)) - 7)
+
+
 def compare_output(out_gpu: np.ndarray, out_ref: np.ndarray, dtype, what=""):
+    """North star (b).  Reading U19: for bf16 the max-abs bound
+    is taken on top of the unavoidable rounding of the reference to the bf16
+    output (|err| <= 2e-2 + half a bf16 ulp of the reference); for |ref| < 4
+    the extra term is below 2e-2 / 1.3, so it only matters for large outputs."""
     mx, rl2 = attention_tol(dtype)
-    err = np.abs(out_gpu - out_ref).max()
+    diff = np.abs(out_gpu - out_ref)
+    allow = mx + (bf16_half_ulp(out_ref) if dtype == torch.bfloat16 else 0.0)
+    i = np.unravel_index(np.argmax(diff - allow), diff.shape)
+    err = diff.max()
     rel = np.linalg.norm(out_gpu - out_ref) / max(np.linalg.norm(out_ref), 1e-30)
-    assert err <= mx, f"{what} max-abs {err:.3e} > {mx}"
+    assert np.all(diff <= allow), f"{what} |err| {diff[i]:.3e} > {allow[i] if np.ndim(allow) else allow:.3e} at ref {out_ref[i]:.4f}"
     assert rel <= rl2, f"{what} rel-L2 {rel:.3e} > {rl2}"
     return err, rel

@@ -62,7 +62,7 @@ def test_status_strings(lib):
     (dict(sm_scale=0.0), _lib.TLS_ERR_CONFIG),
     (dict(d_c=48), _lib.TLS_ERR_UNSUPPORTED),
     (dict(block_size=24), _lib.TLS_ERR_UNSUPPORTED),
-    (dict(num_q_heads=256, num_kv_heads=2), _lib.TLS_ERR_UNSUPPORTED),
+    (dict(num_q_heads=128, num_kv_heads=2), _lib.TLS_ERR_UNSUPPORTED),
 ])
 def test_config_validation_before_launch(lib, kw, status):
     c = cfg(**kw)
@@ -71,6 +71,15 @@ def test_config_validation_before_launch(lib, kw, status):
     assert st == status, (st, lib.tls_last_error())
     assert lib.tls_last_error()
     assert lib.tls_workspace_bytes(ctypes.byref(c), 0) == ctypes.c_size_t(-1).value
+
+
+def test_workspace_required(lib):
+    c = cfg()
+    idx = _lib.TLSIndexC(16, 16, 16, 16)
+    assert lib.tls_select(ctypes.byref(c), 16, 16, ctypes.byref(idx), None, 16, 16, 16, None, None, 0,
+                          None) == _lib.TLS_ERR_WORKSPACE
+    assert lib.tls_select(ctypes.byref(c), 16, 16, ctypes.byref(idx), None, 16, 16, 16, None, 16, 64,
+                          None) == _lib.TLS_ERR_WORKSPACE
 
 
 def test_null_and_misaligned_pointers(lib):
@@ -89,8 +98,9 @@ def test_null_and_misaligned_pointers(lib):
 
 def test_workspace_and_plan(lib):
     c = cfg()
-    assert lib.tls_workspace_bytes(ctypes.byref(c), 2) == 0
-    assert lib.tls_launch_count(ctypes.byref(c), 2) == 1
+    assert lib.tls_workspace_bytes(ctypes.byref(c), 2) >= 2 * 2 * 64 * 4
+    assert lib.tls_workspace_bytes(ctypes.byref(c), 1) == 0
+    assert lib.tls_launch_count(ctypes.byref(c), 2) == 3
     cs = lib.tls_cluster_size(ctypes.byref(c), 2)
     assert cs in (1, 2, 4, 8, 16)
     # headline shapes plan without error
@@ -106,3 +116,4 @@ def test_cluster_override(lib, monkeypatch):
     for cs in (1, 2, 4, 8, 16):
         monkeypatch.setenv("TLS_CLUSTER", str(cs))
         assert lib.tls_cluster_size(ctypes.byref(c), 2) == cs
+        assert lib.tls_cluster_size(ctypes.byref(c), 1) == cs
