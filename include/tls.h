@@ -130,6 +130,17 @@ tls_status tls_build_index(const tls_config* cfg, const void* k_cache, const int
                            int32_t start_token, const tls_index* idx, tls_stream_t stream);
 
 /*
+ * Block scores alone (step a1, P:99 via the P:104-118 GEMM identity):
+ *   scores[b, g, i] = sum_h sum_c max(q_hc k^max_ic, q_hc k^min_ic)   (fp32)
+ * for every block i < ceil(seq_lens[b] / B); entries at or beyond that are
+ * left untouched.  scores: [batch, Hkv, ceil(max_seq_len / B)] fp32 device
+ * memory.  This is the first kernel of tls_select (also usable on its own,
+ * e.g. for block-only Quest-style selection).
+ */
+tls_status tls_block_scores(const tls_config* cfg, const void* q, const int32_t* seq_lens,
+                            const void* block_minmax, float* scores, tls_stream_t stream);
+
+/*
  * Two-level selection for one decode step:
  *   s_i   = sum_h sum_k max(q_hk k^max_ik, q_hk k^min_ik)
  *         (computed as Q+ . k^max_i + Q- . k^min_i, Q+- = sum_h max/min(q_h,0),
@@ -176,11 +187,13 @@ tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
                       int32_t* num_tokens, float* token_scores, void* out, float* lse,
                       void* workspace, size_t workspace_bytes, tls_stream_t stream);
 
-/* Workspace bytes needed by: which = 0 tls_select, 1 tls_sparse_attend,
- * 2 tls_decode: the fp32 block scores of every pair ([batch, Hkv, M] floats,
- * rounded up to 256 B) that the block-score kernel hands to the token-select
- * kernel; 0 for tls_sparse_attend.  (size_t)-1 for an invalid configuration
- * or `which`.  A NULL / too small / misaligned workspace -> TLS_ERR_WORKSPACE. */
+/* Workspace bytes needed by: which = 0 tls_select (the fp32 block scores of
+ * every pair, [batch, Hkv, M] floats, handed from the block-score kernel to the
+ * token-select kernel), 1 tls_sparse_attend (the per-CTA partial (max, sum, o)
+ * of the split-K attention, [batch, Hkv, cs, G, d_v + 2] floats), 2 tls_decode
+ * (the sum; select part first).  Sizes are rounded up to 256 B; the contents
+ * need no initialisation.  (size_t)-1 for an invalid configuration or `which`.
+ * A NULL / too small / misaligned workspace -> TLS_ERR_WORKSPACE. */
 size_t tls_workspace_bytes(const tls_config* cfg, int32_t which);
 
 /* Number of kernel launches one call enqueues (which as above; 3 =
@@ -198,6 +211,12 @@ int32_t tls_cluster_size(const tls_config* cfg, int32_t which);
 const char* tls_status_string(tls_status status);
 const char* tls_last_error(void); /* thread-local detail of the last error */
 const char* tls_version(void);
+
+/* Diagnostics only: when device_buffer is non-NULL, the token-select kernel
+ * launched by this thread writes 8 %globaltimer stamps (ns) per CTA at its
+ * phase boundaries into device_buffer[(pair * cs + rank) * 8 + i].  NULL
+ * (the default) turns it off.  Not part of the measured path. */
+void tls_debug_phase_timing(unsigned long long* device_buffer);
 
 #ifdef __cplusplus
 }

@@ -8,6 +8,7 @@ from .ops import (  # noqa: F401
     TLSConfig,
     TLSIndex,
     alloc_index,
+    block_scores,
     build_index,
     calibrate_channels,
     cluster_size,

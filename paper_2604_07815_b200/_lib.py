@@ -20,6 +20,7 @@ TLS_GQA, TLS_MLA = 0, 1
 EXPORTS = (
     "tls_calibrate_channels",
     "tls_build_index",
+    "tls_block_scores",
     "tls_select",
     "tls_sparse_attend",
     "tls_decode",
@@ -29,6 +30,7 @@ EXPORTS = (
     "tls_status_string",
     "tls_last_error",
     "tls_version",
+    "tls_debug_phase_timing",
 )
 
 
@@ -90,6 +92,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     sig = {
         "tls_calibrate_channels": (_I32, [_PCFG, _P, _I32, _P, _I32, ctypes.c_int64, _P, _P, _P]),
         "tls_build_index": (_I32, [_PCFG, _P, _P, _I32, _PIDX, _P]),
+        "tls_block_scores": (_I32, [_PCFG, _P, _P, _P, _P, _P]),
         "tls_select": (_I32, [_PCFG, _P, _P, _PIDX, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_sparse_attend": (_I32, [_PCFG, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_decode": (_I32, [_PCFG, _P, _P, _P, _P, _PIDX, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
@@ -99,6 +102,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "tls_status_string": (ctypes.c_char_p, [_I32]),
         "tls_last_error": (ctypes.c_char_p, []),
         "tls_version": (ctypes.c_char_p, []),
+        "tls_debug_phase_timing": (None, [_P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -23,6 +23,7 @@ bool select_supported(int d_c, int G);
 namespace {
 
 thread_local char g_err[512] = "";
+thread_local unsigned long long* g_dbg = nullptr;  // diagnostics only (tls_debug_phase_timing)
 
 tls_status fail(tls_status s, const char* fmt, ...) {
   va_list ap;
@@ -69,7 +70,8 @@ tls_status check_config(const tls_config* c) {
   if (G > 32) return fail(TLS_ERR_UNSUPPORTED, "at most 32 query heads per KV head");
   if (c->d_c % 32 || c->d_c > 128 || !tls::select_supported(c->d_c, G))
     return fail(TLS_ERR_UNSUPPORTED, "d_c must be 32, 64 or 128");
-  if (c->block_size % 16 || c->block_size > 1024) return fail(TLS_ERR_UNSUPPORTED, "block_size must be a multiple of 16, <= 1024");
+  if (c->block_size < 16 || c->block_size > 1024 || (c->block_size & (c->block_size - 1)))
+    return fail(TLS_ERR_UNSUPPORTED, "block_size must be a power of two in [16, 1024]");
   if ((long long)c->batch * c->num_kv_heads > 65535) return fail(TLS_ERR_UNSUPPORTED, "batch*num_kv_heads > 65535");
   if (tls::score_cpl(c->d_k, eb) < 0) return fail(TLS_ERR_UNSUPPORTED, "d_k too large for the block-score kernel");
   return TLS_OK;
@@ -93,6 +95,8 @@ tls::Dims dims_of(const tls_config* c) {
   d.sm_scale = c->sm_scale;
   d.mla = c->layout == TLS_MLA;
   d.bf16 = c->dtype == TLS_BF16;
+  d.log2B = 0;
+  while ((1 << d.log2B) < c->block_size) ++d.log2B;
   return d;
 }
 
@@ -129,12 +133,13 @@ tls_status plan_attend(const tls_config* c, tls::AttendParams& p) {
   p.d = dims_of(c);
   p.mma = c->dtype == TLS_BF16 && c->layout == TLS_GQA && c->d_k == c->d_v && (c->d_k == 64 || c->d_k == 128) &&
           p.d.G <= 16;
+  if (c->dtype == TLS_BF16 && c->layout == TLS_MLA && c->d_k == 576 && c->d_v == 512 && p.d.G <= 32) p.mma = 2;
   const long long pairs = (long long)c->batch * c->num_kv_heads;
   const int kt = tls::kt_effective(p.d);
   int cs = env_cluster();
-  if (!cs) {
+  if (!cs) {  // one CTA per pair once the pairs cover the SMs; else split the tokens
     cs = 1;
-    while (cs < 16 && ((kt + cs - 1) / cs > tls::kAttnChunk || pairs * cs < 2 * kSMs)) cs *= 2;
+    while (cs < 16 && pairs * cs < kSMs && (kt + 2 * cs - 1) / (2 * cs) >= 64) cs *= 2;
   }
   for (;; cs *= 2) {
     if (cs > 16) return fail(TLS_ERR_UNSUPPORTED, "attention shared-memory plan does not fit");
@@ -171,6 +176,8 @@ tls_status run_select(const tls_config* cfg, const void* q, const int32_t* seq_l
     return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes, 16-byte aligned (got %zu)", need, workspace_bytes);
   tls::ScoreParams k1;
   k1.d = sp.d;
+  k1.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
+  if (k1.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
   k1.q = q;
   k1.seq_lens = seq_lens;
   k1.block_minmax = idx->block_minmax;
@@ -188,13 +195,15 @@ tls_status run_select(const tls_config* cfg, const void* q, const int32_t* seq_l
   sp.token_ids = token_ids;
   sp.num_tokens = num_tokens;
   sp.token_scores = token_scores;
+  sp.dbg = g_dbg;
   e = tls::launch_token_select(sp, st);
   if (e != cudaSuccess) return cuda_fail(e, "token_select_kernel launch");
   return TLS_OK;
 }
 
 tls_status run_attend(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
-                      const int32_t* token_ids, const int32_t* num_tokens, void* out, float* lse, cudaStream_t st) {
+                      const int32_t* token_ids, const int32_t* num_tokens, void* out, float* lse, void* workspace,
+                      size_t workspace_bytes, cudaStream_t st) {
   tls_status s = check_config(cfg);
   if (s) return s;
   if (!q || !aligned16(q)) return fail(TLS_ERR_INPUT, "q must be a non-NULL 16-byte aligned device pointer");
@@ -205,6 +214,10 @@ tls_status run_attend(const tls_config* cfg, const void* q, const void* k_cache,
   tls::AttendParams ap;
   s = plan_attend(cfg, ap);
   if (s) return s;
+  const size_t need = tls::attend_workspace_bytes(ap.d, ap.cs);
+  if (!workspace || workspace_bytes < need || !aligned16(workspace))
+    return fail(TLS_ERR_WORKSPACE, "attention workspace must be >= %zu bytes, 16-byte aligned (got %zu)", need,
+                workspace_bytes);
   ap.q = q;
   ap.k_cache = k_cache;
   ap.v_cache = cfg->layout == TLS_MLA ? nullptr : v_cache;
@@ -212,9 +225,19 @@ tls_status run_attend(const tls_config* cfg, const void* q, const void* k_cache,
   ap.num_tokens = num_tokens;
   ap.out = out;
   ap.lse = lse;
+  const size_t pairs = (size_t)cfg->batch * cfg->num_kv_heads;
+  ap.part_o = static_cast<float*>(workspace);
+  ap.part_ml = reinterpret_cast<float*>(static_cast<char*>(workspace) +
+                                        ((pairs * ap.cs * ap.d.G * ap.d.d_v * 4 + 255) & ~(size_t)255));
   cudaError_t e = tls::launch_attend(ap, st);
   if (e != cudaSuccess) return cuda_fail(e, "attend_kernel launch");
   return TLS_OK;
+}
+
+size_t attend_ws(const tls_config* cfg) {
+  tls::AttendParams ap;
+  if (plan_attend(cfg, ap) != TLS_OK) return (size_t)-1;
+  return tls::attend_workspace_bytes(ap.d, ap.cs);
 }
 
 }  // namespace
@@ -276,6 +299,26 @@ tls_status tls_build_index(const tls_config* cfg, const void* k_cache, const int
   return TLS_OK;
 }
 
+tls_status tls_block_scores(const tls_config* cfg, const void* q, const int32_t* seq_lens,
+                            const void* block_minmax, float* scores, tls_stream_t stream) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if (!q || !aligned16(q)) return fail(TLS_ERR_INPUT, "q must be a non-NULL 16-byte aligned device pointer");
+  if (!seq_lens || !block_minmax || !scores || !aligned16(block_minmax))
+    return fail(TLS_ERR_INPUT, "seq_lens, block_minmax (16-byte aligned) and scores are required");
+  tls::ScoreParams k1;
+  k1.d = dims_of(cfg);
+  k1.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
+  if (k1.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
+  k1.q = q;
+  k1.seq_lens = seq_lens;
+  k1.block_minmax = block_minmax;
+  k1.scores = scores;
+  cudaError_t e = tls::launch_block_scores(k1, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "block_score_kernel launch");
+  return TLS_OK;
+}
+
 tls_status tls_select(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
                       const int32_t* guide_block_ids, int32_t* block_ids, int32_t* token_ids, int32_t* num_tokens,
                       float* token_scores, void* workspace, size_t workspace_bytes, tls_stream_t stream) {
@@ -286,9 +329,8 @@ tls_status tls_select(const tls_config* cfg, const void* q, const int32_t* seq_l
 tls_status tls_sparse_attend(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
                              const int32_t* token_ids, const int32_t* num_tokens, void* out, float* lse,
                              void* workspace, size_t workspace_bytes, tls_stream_t stream) {
-  (void)workspace;
-  (void)workspace_bytes;
-  return run_attend(cfg, q, k_cache, v_cache, token_ids, num_tokens, out, lse, (cudaStream_t)stream);
+  return run_attend(cfg, q, k_cache, v_cache, token_ids, num_tokens, out, lse, workspace, workspace_bytes,
+                    (cudaStream_t)stream);
 }
 
 tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
@@ -302,16 +344,25 @@ tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
   if (cfg->layout == TLS_GQA && (!v_cache || !aligned16(v_cache)))
     return fail(TLS_ERR_INPUT, "GQA needs a 16-byte aligned v_cache");
   if (!out) return fail(TLS_ERR_INPUT, "out is required");
+  const size_t wsel = tls::select_workspace_bytes(dims_of(cfg));
+  const size_t watt = attend_ws(cfg);
+  if (watt == (size_t)-1) return fail(TLS_ERR_UNSUPPORTED, "attention plan does not fit");
+  if (!workspace || workspace_bytes < wsel + watt || !aligned16(workspace))
+    return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes, 16-byte aligned (got %zu)", wsel + watt,
+                workspace_bytes);
   s = run_select(cfg, q, seq_lens, idx, guide_block_ids, block_ids, token_ids, num_tokens, token_scores, workspace,
-                 workspace_bytes, (cudaStream_t)stream);
+                 wsel, (cudaStream_t)stream);
   if (s) return s;
-  return run_attend(cfg, q, k_cache, v_cache, token_ids, num_tokens, out, lse, (cudaStream_t)stream);
+  return run_attend(cfg, q, k_cache, v_cache, token_ids, num_tokens, out, lse, static_cast<char*>(workspace) + wsel,
+                    watt, (cudaStream_t)stream);
 }
 
 size_t tls_workspace_bytes(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK || which < 0 || which > 2) return (size_t)-1;
-  if (which == 1) return 0;
-  return tls::select_workspace_bytes(dims_of(cfg));
+  const size_t wsel = tls::select_workspace_bytes(dims_of(cfg));
+  const size_t watt = attend_ws(cfg);
+  if (watt == (size_t)-1) return (size_t)-1;
+  return which == 0 ? wsel : (which == 1 ? watt : wsel + watt);
 }
 
 int32_t tls_launch_count(const tls_config* cfg, int32_t which) {
@@ -350,6 +401,8 @@ const char* tls_status_string(tls_status status) {
 }
 
 const char* tls_last_error(void) { return g_err; }
+
+void tls_debug_phase_timing(unsigned long long* device_buffer) { g_dbg = device_buffer; }
 
 const char* tls_version(void) { return "tls-b200 0.1 (sm_100a)"; }
 

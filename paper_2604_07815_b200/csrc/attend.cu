@@ -1,8 +1,8 @@
 // attend.cu -- sparse attention over the selected tokens
 // for sm_100a: K3 attend_kernel, one thread-block cluster of cs CTAs per
 // (batch, KV-head) pair, each CTA a 1/cs slice of the pair's k_t tokens
-// (split-K flash decoding), partials merged over DSMEM with the LSE identity
-// (T10).  bf16 GQA with head dim 64/128 runs on tensor cores (mma.sync);
+// (split-K flash decoding); the cs partials go to an L2-resident workspace,
+// one cluster barrier, then every CTA merges a slice with the LSE identity (T10).  bf16 GQA with head dim 64/128 runs on tensor cores (mma.sync);
 // MLA and fp32 run the generic CUDA-core path (NEXT: tcgen05 for MLA).
 #include <math_constants.h>
 
@@ -13,10 +13,6 @@
 
 namespace tls {
 
-struct AttCtl {
-  float am[64], al[64];  // per-head partial max / sum, log2 units (read remotely)
-};
-
 // --------------------------------------------------------------------------
 // Phase E (generic CUDA-core path): partial attention of this CTA over its
 // tokens sel[0..tloc) for the G heads of the pair, log2 domain.
@@ -24,7 +20,7 @@ struct AttCtl {
 // --------------------------------------------------------------------------
 template <typename T>
 __device__ void phase_attend_generic(const AttendParams& p, int pair, int b, int g, const int* sel, int tloc,
-                                     float* aq, float* as, float* ao, AttCtl& ctl) {
+                                     float* aq, float* as, float* po, float* pml) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * p.d.Hq + (size_t)g * p.d.G) * p.d.d_k;
   for (int i = tid; i < p.d.G * p.d.d_k; i += kThreads) aq[i] = to_f32<T>(qg[i]);
@@ -49,14 +45,14 @@ __device__ void phase_attend_generic(const AttendParams& p, int pair, int b, int
     mx = warp_max(mx);
     float l = 0.f;
     for (int t = lane; t < tloc; t += 32) {
-      const float e = exp2f(as[h * p.tloc_max + t] - mx);
+      const float e = fexp2(as[h * p.tloc_max + t] - mx);
       as[h * p.tloc_max + t] = e;
       l += e;
     }
     l = warp_sum(l);
     if (lane == 0) {
-      ctl.am[h] = mx;
-      ctl.al[h] = l;
+      pml[2 * h] = mx;
+      pml[2 * h + 1] = l;
     }
   }
   __syncthreads();
@@ -64,7 +60,7 @@ __device__ void phase_attend_generic(const AttendParams& p, int pair, int b, int
     const int h = idx / p.d.d_v, c = idx - h * p.d.d_v;
     float acc = 0.f;
     for (int t = 0; t < tloc; ++t) acc = fmaf(as[h * p.tloc_max + t], to_f32<T>(vb[(size_t)sel[t] * vstride + c]), acc);
-    ao[idx] = acc;
+    po[idx] = acc;
   }
 }
 
@@ -79,17 +75,32 @@ __device__ void phase_attend_generic(const AttendParams& p, int pair, int b, int
 // --------------------------------------------------------------------------
 template <int D>
 __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, const int* sel, int tloc,
-                                 uint8_t* kvbuf, float* ao, AttCtl& ctl) {
+                                 uint8_t* kvbuf, float* po, float* pml) {
   constexpr int TC = kAttnChunk;
   constexpr int CPR = D / 8;  // 16-byte chunks per row
   constexpr int KS = D / 16;  // k-steps of QK^T
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = lane >> 2, c2 = 2 * (lane & 3);
-  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(kvbuf);
-  __nv_bfloat16* sV = sK + TC * D;
+  __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(kvbuf);  // [2 stages][K TC*D | V TC*D]
   const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + ((size_t)b * p.d.Hq + (size_t)g * p.d.G) * D;
   const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.d.S * D;
   const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(p.v_cache) + (size_t)pair * p.d.S * D;
+  const int nchunks = (tloc + TC - 1) / TC;
+  auto load_chunk = [&](int c, int stage) {
+    __nv_bfloat16* sK = sbuf + (size_t)stage * 2 * TC * D;
+    __nv_bfloat16* sV = sK + TC * D;
+    const int nt = min(TC, tloc - c * TC);
+    for (int i = tid; i < TC * CPR; i += kThreads) {
+      const int row = i / CPR, ch = i - row * CPR;
+      const bool ok = row < nt;
+      const int tok = ok ? sel[c * TC + row] : 0;
+      const int dst = row * D + ((ch ^ (row & 7)) << 3);
+      cp_async16(sK + dst, kb + (size_t)tok * D + ch * 8, ok);
+      cp_async16(sV + dst, vb + (size_t)tok * D + ch * 8, ok);
+    }
+    cp_async_commit();
+  };
+  if (nchunks > 0) load_chunk(0, 0);
   // Q as the A operand (rows = heads; rows >= G are zero)
   uint32_t qa[KS][4];
 #pragma unroll
@@ -106,20 +117,17 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
 #pragma unroll
   for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
 
-  for (int c0 = 0; c0 < tloc; c0 += TC) {
-    const int nt = min(TC, tloc - c0);
-    __syncthreads();  // previous chunk consumed
-    for (int i = tid; i < TC * CPR; i += kThreads) {
-      const int row = i / CPR, ch = i - row * CPR;
-      const bool ok = row < nt;
-      const int tok = ok ? sel[c0 + row] : 0;
-      const int dst = row * D + ((ch ^ (row & 7)) << 3);
-      cp_async16(sK + dst, kb + (size_t)tok * D + ch * 8, ok);
-      cp_async16(sV + dst, vb + (size_t)tok * D + ch * 8, ok);
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      load_chunk(c + 1, (c + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
+    __syncthreads();  // chunk c landed for every thread's copies
+    const __nv_bfloat16* sK = sbuf + (size_t)(c & 1) * 2 * TC * D;
+    const __nv_bfloat16* sV = sK + TC * D;
+    const int nt = min(TC, tloc - c * TC);
     const int tb = warp * 16;
     if (tb < nt) {
       float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -146,14 +154,14 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
       x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 1));
       x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 2));
       const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);  // finite: token tb is valid
-      const float a0 = exp2f(m0 - n0), a1 = exp2f(m1 - n1);
+      const float a0 = fexp2(m0 - n0), a1 = fexp2(m1 - n1);
       float pr[2][4];
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        pr[j][0] = exp2f(s[j][0] - n0);
-        pr[j][1] = exp2f(s[j][1] - n0);
-        pr[j][2] = exp2f(s[j][2] - n1);
-        pr[j][3] = exp2f(s[j][3] - n1);
+        pr[j][0] = fexp2(s[j][0] - n0);
+        pr[j][1] = fexp2(s[j][1] - n0);
+        pr[j][2] = fexp2(s[j][2] - n1);
+        pr[j][3] = fexp2(s[j][3] - n1);
       }
       float r0s = pr[0][0] + pr[0][1] + pr[1][0] + pr[1][1];
       float r1s = pr[0][2] + pr[0][3] + pr[1][2] + pr[1][3];
@@ -187,11 +195,12 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
         mma_bf16_16816(o[2 * jj + 1], pa, bv[2], bv[3]);
       }
     }
+    __syncthreads();  // stage (c & 1) consumed before it is refilled
   }
-  // ---- merge the 8 warp partials (the staging buffer becomes scratch) ----
-  __syncthreads();
-  float* wo = reinterpret_cast<float*>(kvbuf);  // [warp][G][D]
-  float* wml = wo + kWarps * p.d.G * D;           // [warp][16][2]
+  // ---- merge the 8 warp partials (the staging buffers become scratch) ----
+  constexpr int WS = D + 4;  // padded row stride of the warp partials
+  float* wo = reinterpret_cast<float*>(kvbuf);  // [warp][G][WS]
+  float* wml = wo + kWarps * p.d.G * WS;        // [warp][16][2]
   if ((lane & 3) == 0) {
     wml[(warp * 16 + r) * 2] = m0;
     wml[(warp * 16 + r) * 2 + 1] = l0;
@@ -201,67 +210,73 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
 #pragma unroll
   for (int j = 0; j < D / 8; ++j) {
     const int d = j * 8 + c2;
-    if (r < p.d.G) {
-      wo[(warp * p.d.G + r) * D + d] = o[j][0];
-      wo[(warp * p.d.G + r) * D + d + 1] = o[j][1];
-    }
-    if (r + 8 < p.d.G) {
-      wo[(warp * p.d.G + r + 8) * D + d] = o[j][2];
-      wo[(warp * p.d.G + r + 8) * D + d + 1] = o[j][3];
-    }
+    if (r < p.d.G) *reinterpret_cast<float2*>(wo + (warp * p.d.G + r) * WS + d) = make_float2(o[j][0], o[j][1]);
+    if (r + 8 < p.d.G)
+      *reinterpret_cast<float2*>(wo + (warp * p.d.G + r + 8) * WS + d) = make_float2(o[j][2], o[j][3]);
   }
   __syncthreads();
+  const bool direct = p.cs == 1;  // one CTA per pair: normalise and write the output here
+  __nv_bfloat16* outg =
+      reinterpret_cast<__nv_bfloat16*>(p.out) + ((size_t)b * p.d.Hq + (size_t)g * p.d.G) * p.d.d_v;
   for (int idx = tid; idx < p.d.G * D; idx += kThreads) {
-    const int h = idx / D;
+    const int h = idx / D, dcol = idx - h * D;
     float M = -CUDART_INF_F;
     for (int w = 0; w < kWarps; ++w) M = fmaxf(M, wml[(w * 16 + h) * 2]);
     float L = 0.f, acc = 0.f;
     if (M != -CUDART_INF_F) {
       for (int w = 0; w < kWarps; ++w) {
         const float mw = wml[(w * 16 + h) * 2];
-        const float sc = mw == -CUDART_INF_F ? 0.f : exp2f(mw - M);
+        const float sc = mw == -CUDART_INF_F ? 0.f : fexp2(mw - M);
         L = fmaf(wml[(w * 16 + h) * 2 + 1], sc, L);
-        acc = fmaf(wo[(w * p.d.G + h) * D + (idx - h * D)], sc, acc);
+        acc = fmaf(wo[(w * p.d.G + h) * WS + dcol], sc, acc);
       }
     }
-    ao[idx] = acc;
-    if (idx - h * D == 0) {
-      ctl.am[h] = M;
-      ctl.al[h] = L;
+    if (direct) {
+      outg[idx] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+      if (dcol == 0 && p.lse != nullptr)
+        p.lse[(size_t)b * p.d.Hq + (size_t)g * p.d.G + h] = L > 0.f ? (M + flog2(L)) * kLn2 : -CUDART_INF_F;
+    } else {
+      po[idx] = acc;
+      if (dcol == 0) {
+        pml[2 * h] = M;
+        pml[2 * h + 1] = L;
+      }
     }
   }
 }
 
-// Merge the cs partials of the pair (flash-decoding LSE merge, T10) and write
-// out / lse.  CTA `rank` writes a 1/cs slice of the G*d_v outputs.
+// Merge the cs CTA partials of the pair (flash-decoding LSE merge, T10) from
+// the L2-resident workspace and write out / lse; CTA `rank` writes a 1/cs
+// slice of the G*d_v outputs.
 template <typename T>
-__device__ void phase_merge(const AttendParams& p, int b, int g, unsigned rank, const float* ao, AttCtl& ctl) {
-  const int tid = threadIdx.x;
+__device__ void phase_merge(const AttendParams& p, int pair, int b, int g, unsigned rank) {
   const int tot = p.d.G * p.d.d_v;
   const int lo = (int)((long long)tot * rank / p.cs), hi = (int)((long long)tot * (rank + 1) / p.cs);
+  const float* po = p.part_o + (size_t)pair * p.cs * tot;
+  const float* pml = p.part_ml + (size_t)pair * p.cs * p.d.G * 2;
   T* outg = reinterpret_cast<T*>(p.out) + ((size_t)b * p.d.Hq + (size_t)g * p.d.G) * p.d.d_v;
-  for (int idx = lo + tid; idx < hi; idx += kThreads) {
+  for (int idx = lo + (int)threadIdx.x; idx < hi; idx += kThreads) {
     const int h = idx / p.d.d_v, c = idx - h * p.d.d_v;
     float M = -CUDART_INF_F;
-    for (int rr = 0; rr < p.cs; ++rr) M = fmaxf(M, *dsmem(&ctl.am[h], rr));
+    for (int rr = 0; rr < p.cs; ++rr) M = fmaxf(M, __ldcg(pml + (rr * p.d.G + h) * 2));
     float L = 0.f, o = 0.f;
     if (M != -CUDART_INF_F) {
       for (int rr = 0; rr < p.cs; ++rr) {
-        const float w = exp2f(*dsmem(&ctl.am[h], rr) - M);
-        L = fmaf(*dsmem(&ctl.al[h], rr), w, L);
-        o = fmaf(*dsmem(&ao[idx], rr), w, o);
+        const float mr = __ldcg(pml + (rr * p.d.G + h) * 2);
+        const float w = mr == -CUDART_INF_F ? 0.f : fexp2(mr - M);
+        L = fmaf(__ldcg(pml + (rr * p.d.G + h) * 2 + 1), w, L);
+        o = fmaf(__ldcg(po + (size_t)rr * tot + idx), w, o);
       }
     }
     outg[idx] = from_f32<T>(L > 0.f ? o / L : 0.f);
     if (c == 0 && p.lse != nullptr)
-      p.lse[(size_t)b * p.d.Hq + (size_t)g * p.d.G + h] = L > 0.f ? (M + log2f(L)) * kLn2 : -CUDART_INF_F;
+      p.lse[(size_t)b * p.d.Hq + (size_t)g * p.d.G + h] = L > 0.f ? (M + flog2(L)) * kLn2 : -CUDART_INF_F;
   }
 }
 
 template <typename T, bool MMA, int D>
 __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_constant__ AttendParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ AttCtl ctl;
   const int tid = threadIdx.x;
   const unsigned rank = blockIdx.x;
   const int cs = p.cs;
@@ -274,16 +289,213 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_consta
   const int* ids = p.token_ids + (size_t)pair * p.d.Kt;
   for (int i = tid; i < tloc; i += kThreads) sel[i] = ids[t0 + i];
   __syncthreads();
-  float* ao = reinterpret_cast<float*>(smem + p.off_ao);
+  const int tot = p.d.G * p.d.d_v;
+  float* po = p.part_o + ((size_t)pair * cs + rank) * tot;
+  float* pml = p.part_ml + ((size_t)pair * cs + rank) * p.d.G * 2;
   if constexpr (MMA) {
-    phase_attend_mma<D>(p, pair, b, g, sel, tloc, smem + p.off_akv, ao, ctl);
+    phase_attend_mma<D>(p, pair, b, g, sel, tloc, smem + p.off_akv, po, pml);
   } else {
     phase_attend_generic<T>(p, pair, b, g, sel, tloc, reinterpret_cast<float*>(smem + p.off_aq),
-                            reinterpret_cast<float*>(smem + p.off_as), ao, ctl);
+                            reinterpret_cast<float*>(smem + p.off_as), po, pml);
   }
-  cluster_sync_all();
-  phase_merge<T>(p, b, g, rank, ao, ctl);
-  cluster_sync_all();  // no CTA leaves while its smem may still be read remotely
+  if (MMA && cs == 1) return;  // the mma path wrote the output directly
+  if (cs > 1) cluster_sync_all();  // release/acquire at cluster scope: partials visible in L2
+  __syncthreads();
+  phase_merge<T>(p, pair, b, g, rank);
+}
+
+// --------------------------------------------------------------------------
+// MLA tensor-core path (one shared latent KV head; V = the first d_v
+// dims of each cached row).  Per CTA: the G <= 32 query heads (MT m-tiles of
+// 16) against 32-token chunks of latent rows gathered with cp.async into
+// XOR-swizzled smem, double-buffered.  S = Q K^T: warp w computes head-tile
+// w/4, tokens 8*(w%4)..+8 over the DK/16 k-steps (Q and K fragments via
+// ldmatrix).  Online softmax per head in smem (P stored as bf16).  O += P V:
+// warp w owns output dims [64w, 64w + 64) (V^T fragments via ldmatrix.trans).
+// --------------------------------------------------------------------------
+constexpr int kMlaChunk = 32;
+
+template <int DK, int DV, int MT>
+__global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_constant__ AttendParams p) {
+  static_assert(DV == 64 * kWarps, "each warp owns 64 output dims");
+  constexpr int TC = kMlaChunk;
+  constexpr int CPR = DK / 8;       // 16-byte chunks per latent row
+  constexpr int KS = DK / 16;       // k-steps of QK^T
+  constexpr int PST = TC + 8;       // P row stride (bf16): 80 B, conflict-free ldmatrix
+  constexpr int SST = TC + 4;       // S row stride (fp32)
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned rank = blockIdx.x;
+  const int cs = p.cs;
+  const int pair = blockIdx.y;
+  const int b = pair;  // MLA: one KV head
+  const int G = p.d.G;
+  const int K = min(min(max(p.num_tokens[pair], 0), p.d.Kt), p.tloc_max * cs);
+  const int t0 = (int)((long long)K * rank / cs), t1 = (int)((long long)K * (rank + 1) / cs);
+  const int tloc = t1 - t0;
+  int* sel = reinterpret_cast<int*>(smem + p.off_sel);
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem + p.off_akv);
+  __nv_bfloat16* sKV = sQ + MT * 16 * DK;           // 2 buffers of TC rows
+  float* sS = reinterpret_cast<float*>(sKV + 2 * TC * DK);
+  __nv_bfloat16* sP = reinterpret_cast<__nv_bfloat16*>(sS + MT * 16 * SST);
+  float* sAlpha = reinterpret_cast<float*>(sP + MT * 16 * PST);
+  float* sM = sAlpha + MT * 16;
+  float* sL = sM + MT * 16;
+  const int* ids = p.token_ids + (size_t)pair * p.d.Kt;
+  for (int i = tid; i < tloc; i += kThreads) sel[i] = ids[t0 + i];
+  const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + (size_t)b * p.d.Hq * DK;
+  for (int i = tid; i < MT * 16 * CPR; i += kThreads) {
+    const int row = i / CPR, ch = i - row * CPR;
+    cp_async16(sQ + row * DK + ((ch ^ (row & 7)) << 3), qg + (size_t)(row < G ? row : 0) * DK + ch * 8, row < G);
+  }
+  cp_async_commit();
+  if (tid < MT * 16) {
+    sM[tid] = -CUDART_INF_F;
+    sL[tid] = 0.f;
+  }
+  __syncthreads();  // sel visible
+  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.d.S * DK;
+  auto load_chunk = [&](int c, int buf) {
+    __nv_bfloat16* dst = sKV + buf * TC * DK;
+    for (int i = tid; i < TC * CPR; i += kThreads) {
+      const int row = i / CPR, ch = i - row * CPR;
+      const int t = c * TC + row;
+      const bool ok = t < tloc;
+      cp_async16(dst + row * DK + ((ch ^ (row & 7)) << 3), kb + (size_t)(ok ? sel[t] : 0) * DK + ch * 8, ok);
+    }
+    cp_async_commit();
+  };
+  const int nchunks = (tloc + TC - 1) / TC;
+  if (nchunks > 0) load_chunk(0, 0);
+  const float sm2 = p.d.sm_scale * kLog2e;
+  float o[MT][8][4];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[mt][j][0] = o[mt][j][1] = o[mt][j][2] = o[mt][j][3] = 0.f;
+  const int r = lane >> 2, c2 = 2 * (lane & 3);
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nchunks) {
+      load_chunk(c + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const __nv_bfloat16* sK = sKV + buf * TC * DK;
+    // ---- S = Q K^T (log2 units) ----
+    {
+      const int mt = warp >> 2, nb = (warp & 3) * 8;
+      if (mt < MT) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+        for (int kk = 0; kk < KS; ++kk) {
+          uint32_t a[4], bk[4];
+          const int qrow = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, qch = kk * 2 + (lane >> 4);
+          ldsm_x4(a, sQ + qrow * DK + ((qch ^ (qrow & 7)) << 3));
+          const int krow = nb + (lane & 7), kch = kk * 2 + ((lane >> 3) & 1);
+          ldsm_x4(bk, sK + krow * DK + ((kch ^ (krow & 7)) << 3));  // lanes 16-31 duplicate 0-15
+          mma_bf16_16816(acc, a, bk[0], bk[1]);
+        }
+        const int tk = nb + c2;
+        const bool v0 = c * TC + tk < tloc, v1 = c * TC + tk + 1 < tloc;
+        sS[(mt * 16 + r) * SST + tk] = v0 ? acc[0] * sm2 : -CUDART_INF_F;
+        sS[(mt * 16 + r) * SST + tk + 1] = v1 ? acc[1] * sm2 : -CUDART_INF_F;
+        sS[(mt * 16 + r + 8) * SST + tk] = v0 ? acc[2] * sm2 : -CUDART_INF_F;
+        sS[(mt * 16 + r + 8) * SST + tk + 1] = v1 ? acc[3] * sm2 : -CUDART_INF_F;
+      }
+    }
+    __syncthreads();
+    // ---- online softmax: 8 threads per head, 4 tokens each ----
+    {
+      const int h = tid >> 3, tq = (tid & 7) * 4;
+      if (h < MT * 16) {
+        float x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = sS[h * SST + tq + i];
+        float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        const float mo = sM[h];
+        const float mn = fmaxf(mo, mx);  // finite: every chunk has >= 1 valid token
+        float ps = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float e = fexp2(x[i] - mn);
+          ps += e;
+          sP[h * PST + tq + i] = __float2bfloat16_rn(e);
+        }
+        ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+        ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+        ps += __shfl_xor_sync(0xffffffffu, ps, 4);
+        __syncwarp();
+        if ((tid & 7) == 0) {
+          const float al = fexp2(mo - mn);
+          sAlpha[h] = al;
+          sL[h] = sL[h] * al + ps;
+          sM[h] = mn;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- O = O * alpha + P V  (warp owns dims [64w, 64w+64)) ----
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const float a0 = sAlpha[mt * 16 + r], a1 = sAlpha[mt * 16 + r + 8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        o[mt][j][0] *= a0;
+        o[mt][j][1] *= a0;
+        o[mt][j][2] *= a1;
+        o[mt][j][3] *= a1;
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < TC / 16; ++kk) {
+      uint32_t pa[MT][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int prow = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int pcol = kk * 16 + (lane >> 4) * 8;
+        ldsm_x4(pa[mt], sP + prow * PST + pcol);
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int vrow = kk * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
+        const int vch = (warp * 64 + jj * 16) / 8 + (lane >> 4);
+        uint32_t bv[4];
+        ldsm_x4_trans(bv, sK + vrow * DK + ((vch ^ (vrow & 7)) << 3));
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          mma_bf16_16816(o[mt][2 * jj], pa[mt], bv[0], bv[1]);
+          mma_bf16_16816(o[mt][2 * jj + 1], pa[mt], bv[2], bv[3]);
+        }
+      }
+    }
+    __syncthreads();  // buffer `buf` and sS / sP free for the next chunk
+  }
+  // ---- this CTA's partial (unnormalised o, max, sum) -> workspace ----
+  const int tot = G * DV;
+  float* po = p.part_o + ((size_t)pair * cs + rank) * tot;
+  float* pml = p.part_ml + ((size_t)pair * cs + rank) * G * 2;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int dcol = warp * 64 + j * 8 + c2;
+      const int h0 = mt * 16 + r, h1 = h0 + 8;
+      if (h0 < G) *reinterpret_cast<float2*>(po + (size_t)h0 * DV + dcol) = make_float2(o[mt][j][0], o[mt][j][1]);
+      if (h1 < G) *reinterpret_cast<float2*>(po + (size_t)h1 * DV + dcol) = make_float2(o[mt][j][2], o[mt][j][3]);
+    }
+  if (tid < G) {
+    pml[2 * tid] = nchunks > 0 ? sM[tid] : -CUDART_INF_F;
+    pml[2 * tid + 1] = nchunks > 0 ? sL[tid] : 0.f;
+  }
+  if (cs > 1) cluster_sync_all();
+  __syncthreads();
+  phase_merge<__nv_bfloat16>(p, pair, b, 0, rank);
 }
 
 template <typename T, bool MMA, int D>
@@ -312,7 +524,32 @@ static cudaError_t launch_k3(const AttendParams& p, cudaStream_t st) {
   return cudaLaunchKernelEx(&lc, kern, p);
 }
 
+template <int MT>
+static cudaError_t launch_mla(const AttendParams& p, cudaStream_t st) {
+  auto kern = attend_mla_kernel<576, 512, MT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  if (e != cudaSuccess) return e;
+  if (p.cs > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)p.cs, (unsigned)(p.d.batch * p.d.Hkv), 1);
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.dynamicSmemBytes = p.smem_bytes;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)p.cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, kern, p);
+}
+
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t st) {
+  if (p.mma == 2) return p.d.G <= 16 ? launch_mla<1>(p, st) : launch_mla<2>(p, st);
   if (p.d.bf16) {
     if (p.mma) return p.d.d_k == 128 ? launch_k3<__nv_bfloat16, true, 128>(p, st)
                                      : launch_k3<__nv_bfloat16, true, 64>(p, st);

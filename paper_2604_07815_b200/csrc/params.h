@@ -11,7 +11,8 @@
 namespace tls {
 
 constexpr int kAttnChunk = 128;    // tokens per K/V staging chunk of the mma attention (8 warps x 16)
-constexpr int kScoreChunk = 128;   // blocks per K1 CTA
+constexpr int kMlaChunkTokens = 32;  // latent rows per staging chunk of the MLA attention (double-buffered)
+constexpr int kScoreTileBytes = 32 * 1024;  // K1: bytes of block summaries per CTA (TMA tile)
 
 struct Dims {
   int batch, Hq, Hkv, G, d_k, d_v, S, B, d_c, Kb, Kt;
@@ -19,10 +20,12 @@ struct Dims {
   float sm_scale;
   int mla;
   int bf16;
+  int log2B;  // block_size is a power of two
 };
 
 struct ScoreParams {  // K1
   Dims d;
+  int tb;  // blocks per CTA: the tile of summaries is <= kScoreTileBytes
   const void* q;
   const int* seq_lens;
   const void* block_minmax;
@@ -45,13 +48,14 @@ struct SelectParams {  // K2
   int* token_ids;
   int* num_tokens;
   float* token_scores;
-  unsigned off_bkeys, off_cblk, off_qb, off_qsum, off_stc, off_stz, off_tkeys, smem_bytes;
+  unsigned long long* dbg;  // diagnostics: per-CTA phase timestamps (NULL = off)
+  unsigned off_bkeys, off_cblk, off_qb, off_qsum, off_qc, off_stc, off_stz, off_tkeys, smem_bytes;
 };
 
 struct AttendParams {  // K3
   Dims d;
   int cs;
-  int mma;       // 1: bf16 mma.sync path (GQA, d in {64,128}, G <= 16)
+  int mma;       // 1: bf16 mma.sync GQA path (d in {64,128}, G <= 16); 2: bf16 mma.sync MLA path (576/512)
   int tloc_max;  // ceil(kt_eff / cs)
   const void* q;
   const void* k_cache;
@@ -60,7 +64,9 @@ struct AttendParams {  // K3
   const int* num_tokens;
   void* out;
   float* lse;
-  unsigned off_sel, off_akv, off_aq, off_as, off_ao, smem_bytes;
+  float* part_o;   // workspace [pairs, cs, G, d_v] fp32 partial outputs
+  float* part_ml;  // workspace [pairs, cs, G, 2] fp32 partial (max, sum), log2 units
+  unsigned off_sel, off_akv, off_aq, off_as, smem_bytes;
 };
 
 static inline unsigned align16(size_t x) { return (unsigned)((x + 15) & ~(size_t)15); }
@@ -88,6 +94,9 @@ static inline void plan_select(SelectParams& p) {
   o = align16(o + (size_t)nsplit * nt * ks * 64 * 4);
   p.off_qsum = (unsigned)o;
   o = align16(o + (size_t)nt * 8 * 4);
+  p.off_qc = (unsigned)o;
+  o = align16(o + (size_t)nt * 8 * d.d_c * 4);
+  o = (o + 127) & ~(size_t)127;
   p.off_stc = (unsigned)o;
   o = align16(o + (size_t)p.lc_max * (d.d_c / 2));
   p.off_stz = (unsigned)o;
@@ -103,10 +112,18 @@ static inline void plan_attend(AttendParams& p) {
   size_t o = 0;
   p.off_sel = (unsigned)o;
   o = align16(o + (size_t)(p.tloc_max + 1) * 4);
-  if (p.mma) {
-    p.off_akv = (unsigned)o;  // K chunk + V chunk; reused as the warp-partial scratch
-    size_t kv = (size_t)2 * kAttnChunk * d.d_k * 2;
-    size_t scratch = (size_t)8 * d.G * d.d_v * 4 + (size_t)8 * 16 * 2 * 4;
+  if (p.mma == 2) {  // MLA tensor-core path: Q, 2 latent-row chunks, S, P, alpha/m/l
+    const int mt16 = d.G <= 16 ? 16 : 32;
+    o = (o + 127) & ~(size_t)127;
+    p.off_akv = (unsigned)o;
+    o += (size_t)mt16 * d.d_k * 2 + (size_t)2 * kMlaChunkTokens * d.d_k * 2;
+    o += (size_t)mt16 * (kMlaChunkTokens + 4) * 4 + (size_t)mt16 * (kMlaChunkTokens + 8) * 2 + (size_t)3 * mt16 * 4;
+    o = align16(o);
+  } else if (p.mma) {
+    o = (o + 127) & ~(size_t)127;
+    p.off_akv = (unsigned)o;  // 2 stages x (K chunk + V chunk); reused as the warp-partial scratch
+    size_t kv = (size_t)2 * 2 * kAttnChunk * d.d_k * 2;
+    size_t scratch = (size_t)8 * d.G * (d.d_v + 4) * 4 + (size_t)8 * 16 * 2 * 4;
     o = align16(o + (kv > scratch ? kv : scratch));
   } else {
     p.off_aq = (unsigned)o;
@@ -114,14 +131,19 @@ static inline void plan_attend(AttendParams& p) {
     p.off_as = (unsigned)o;
     o = align16(o + (size_t)d.G * p.tloc_max * 4);
   }
-  p.off_ao = (unsigned)o;
-  o = align16(o + (size_t)d.G * d.d_v * 4);
   p.smem_bytes = (unsigned)o;
 }
 
-// Workspace of tls_select / tls_decode: K1's fp32 block scores.
+// Workspace of tls_select: K1's fp32 block scores.
 static inline size_t select_workspace_bytes(const Dims& d) {
   return ((size_t)d.batch * d.Hkv * d.M * 4 + 255) & ~(size_t)255;
+}
+// Workspace of tls_sparse_attend with cluster size cs: the CTA partials.
+static inline size_t attend_workspace_bytes(const Dims& d, int cs) {
+  const size_t pairs = (size_t)d.batch * d.Hkv;
+  const size_t o = (pairs * cs * d.G * d.d_v * 4 + 255) & ~(size_t)255;
+  const size_t ml = (pairs * cs * d.G * 2 * 4 + 255) & ~(size_t)255;
+  return o + ml;
 }
 
 }  // namespace tls

@@ -19,24 +19,45 @@
 namespace tls {
 
 // ============================================================== K1: a1
-// grid (ceil(M / kScoreChunk), pairs); a CTA scores blocks [i0, i0 + 128) of
-// one pair.  QQ = [Q+ | Q-] (2*d_k fp32); a block's summary row is
-// [k^max | k^min], so s_i = QQ . row_i.  Each warp keeps U blocks (U*CPL
-// 16-byte loads per lane) in flight.
+// grid (ceil(m_max / tb), pairs).  A CTA scores blocks [i0, i0 + tb) of one
+// pair: one thread streams the tile of block summaries (tb rows of
+// [k^max | k^min], contiguous, <= 32 KB) into shared memory with TMA bulk
+// copies in kSub sub-chunks, each completing on its own mbarrier; the warps
+// score a sub-chunk as soon as it lands.  QQ = [Q+ | Q-] (2*d_k fp32), so
+// s_i = QQ . row_i: 1 flop per byte, HBM-bound.
+constexpr int kSub = 4;
+
 template <typename T, int CPL>
 __global__ void __launch_bounds__(kThreads) block_score_kernel(const __grid_constant__ ScoreParams p) {
   constexpr int EPC = 16 / sizeof(T);
-  constexpr int U = CPL == 1 ? 8 : (CPL == 2 ? 4 : 2);
-  __shared__ float QQ[2 * 32 * CPL * EPC];
+  extern __shared__ __align__(128) uint8_t tile[];
+  __shared__ float QQ[32 * CPL * EPC];
+  __shared__ __align__(8) uint64_t bars[kSub];
   const Dims& d = p.d;
   const int pair = blockIdx.y;
   const int b = pair / d.Hkv, g = pair - b * d.Hkv;
   const int n = min(max(p.seq_lens[b], 0), d.S);
   const int m = (n + d.B - 1) / d.B;  // reading U1
-  const int i0 = blockIdx.x * kScoreChunk;
+  const int i0 = blockIdx.x * p.tb;
   if (i0 >= m) return;
-  const int i1 = min(i0 + kScoreChunk, m);
+  const int nb = min(p.tb, m - i0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rowbytes = 2 * d.d_k * (int)sizeof(T);
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(p.block_minmax) + ((size_t)pair * d.M + i0) * rowbytes;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kSub; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+#pragma unroll
+    for (int s = 0; s < kSub; ++s) {
+      const int s0 = nb * s / kSub, s1 = nb * (s + 1) / kSub;
+      if (s1 > s0) {
+        mbar_arrive_expect_tx(&bars[s], (uint32_t)((s1 - s0) * rowbytes));
+        tma_bulk_g2s(tile + (size_t)s0 * rowbytes, src + (size_t)s0 * rowbytes, (uint32_t)((s1 - s0) * rowbytes),
+                     &bars[s]);
+      }
+    }
+  }
   const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
   for (int c = tid; c < d.d_k; c += kThreads) {
     float qp = 0.f, qn = 0.f;
@@ -48,8 +69,8 @@ __global__ void __launch_bounds__(kThreads) block_score_kernel(const __grid_cons
     QQ[c] = qp;
     QQ[d.d_k + c] = qn;
   }
-  __syncthreads();
-  const int nchunk = 2 * d.d_k / EPC;
+  __syncthreads();  // QQ ready, barriers initialised
+  const int nchunk = rowbytes / 16;
   float qreg[CPL][EPC];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
@@ -57,38 +78,27 @@ __global__ void __launch_bounds__(kThreads) block_score_kernel(const __grid_cons
 #pragma unroll
     for (int e = 0; e < EPC; ++e) qreg[c][e] = ch < nchunk ? QQ[ch * EPC + e] : 0.f;
   }
-  const T* bm = reinterpret_cast<const T*>(p.block_minmax) + (size_t)pair * d.M * 2 * d.d_k;
-  float* out = p.scores + (size_t)pair * d.M;
-  for (int i = i0 + warp * U; i < i1; i += kWarps * U) {
-    uint4 v[U][CPL];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
+  float* out = p.scores + (size_t)pair * d.M + i0;
+#pragma unroll 1
+  for (int s = 0; s < kSub; ++s) {
+    const int s0 = nb * s / kSub, s1 = nb * (s + 1) / kSub;
+    if (s1 <= s0) continue;
+    mbar_wait(&bars[s], 0);
+    for (int i = s0 + warp; i < s1; i += kWarps) {
+      const uint4* row = reinterpret_cast<const uint4*>(tile + (size_t)i * rowbytes);
+      float acc = 0.f;
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         const int ch = lane + 32 * c;
-        v[u][c] = (i + u < i1 && ch < nchunk) ? ldg_stream16(bm + (size_t)(i + u) * 2 * d.d_k + (size_t)ch * EPC)
-                                               : make_uint4(0u, 0u, 0u, 0u);
+        if (ch < nchunk) {
+          float f[EPC];
+          unpack16<T>(row[ch], f);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) acc = fmaf(qreg[c][e], f[e], acc);
+        }
       }
-    float acc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      acc[u] = 0.f;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        float f[EPC];
-        unpack16<T>(v[u][c], f);
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) acc[u] = fmaf(qreg[c][e], f[e], acc[u]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc[u] = warp_sum(acc[u]);
-    if (lane < U && i + lane < i1) {
-      float mine = acc[0];
-#pragma unroll
-      for (int u = 1; u < U; ++u)
-        if (lane == u) mine = acc[u];
-      out[i + lane] = mine;
+      acc = warp_sum(acc);
+      if (lane == 0) out[i] = acc;
     }
   }
 }
@@ -116,37 +126,48 @@ __device__ __forceinline__ float split_piece(float x, int sp) {
 __device__ __forceinline__ void stat_merge(float& m, float& s, float om, float os) {
   const float nm = fmaxf(m, om);
   if (nm == -CUDART_INF_F) return;
-  s = (m == -CUDART_INF_F ? 0.f : s * exp2f(m - nm)) + (om == -CUDART_INF_F ? 0.f : os * exp2f(om - nm));
+  s = (m == -CUDART_INF_F ? 0.f : s * fexp2(m - nm)) + (om == -CUDART_INF_F ? 0.f : os * fexp2(om - nm));
   m = nm;
 }
 
-// Stage codes + (scale, zero) of candidate blocks cblk[c0 .. c0+nbl) in smem.
+// Stage codes + (scale, zero) of candidate blocks cblk[c0 .. c0+nbl) in smem:
+// one TMA bulk copy per block for the codes (B*d_c/2 contiguous bytes) and one
+// for (scale, zero) (B*8 bytes) on one mbarrier; 8-byte cp.async for a
+// (scale, zero) run that is not 16-byte aligned (odd max_seq_len).
 __device__ void stage_token_index(const SelectParams& p, int pair, const int* cblk, int c0, int nbl, uint8_t* stc,
-                                  float2* stz) {
+                                  float2* stz, uint64_t* bar) {
   const Dims& d = p.d;
   const int rowbytes = d.d_c / 2;
-  const int cpb = d.B * rowbytes / 16;  // 16-byte pieces of codes per block
-  const int per = cpb + d.B;            // + one 8-byte (scale, zero) per token
   const uint8_t* cbase = p.codes + (size_t)pair * d.S * rowbytes;
   const float2* zbase = reinterpret_cast<const float2*>(p.scale_zero) + (size_t)pair * d.S;
-  const size_t cend = (size_t)d.S * rowbytes;
-  for (int i = threadIdx.x; i < nbl * per; i += kThreads) {
-    const int kb = i / per;
-    const int r = i - kb * per;
-    const int blk = cblk[c0 + kb];
-    if (r < cpb) {
-      const size_t off = (size_t)blk * d.B * rowbytes + (size_t)r * 16;
-      const bool ok = off + 16 <= cend;
-      cp_async16(stc + (size_t)kb * d.B * rowbytes + (size_t)r * 16, cbase + (ok ? off : 0), ok);
-    } else {
-      const int t = blk * d.B + (r - cpb);
-      const bool ok = t < d.S;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(stz + kb * d.B + (r - cpb))),
-                   "l"(zbase + (ok ? t : 0)), "r"(ok ? 8 : 0));
+  const bool zal = (((size_t)pair * d.S) & 1) == 0;
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    uint32_t total = 0;
+    for (int kb = 0; kb < nbl; ++kb) {
+      const int rows = min(d.B, d.S - cblk[c0 + kb] * d.B);
+      total += rows * rowbytes + ((zal && !(rows & 1)) ? rows * 8 : 0);
     }
+    if (tid == 0) mbar_arrive_expect_tx(bar, total);
+    __syncwarp();
+    for (int kb = tid; kb < nbl; kb += 32) {
+      const int blk = cblk[c0 + kb];
+      const int rows = min(d.B, d.S - blk * d.B);
+      tma_bulk_g2s(stc + (size_t)kb * d.B * rowbytes, cbase + (size_t)blk * d.B * rowbytes, rows * rowbytes, bar);
+      if (zal && !(rows & 1)) tma_bulk_g2s(stz + kb * d.B, zbase + (size_t)blk * d.B, rows * 8, bar);
+    }
+  }
+  for (int kb = 0; kb < nbl; ++kb) {  // rare fallback: unaligned (scale, zero) runs
+    const int blk = cblk[c0 + kb];
+    const int rows = min(d.B, d.S - blk * d.B);
+    if (zal && !(rows & 1)) continue;
+    for (int r = tid; r < rows; r += kThreads)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(stz + kb * d.B + r)),
+                   "l"(zbase + (size_t)blk * d.B + r));
   }
   cp_async_commit();
   cp_async_wait<0>();
+  mbar_wait(bar, 0);
   __syncthreads();
 }
 
@@ -199,8 +220,9 @@ __device__ __forceinline__ void token_tile_mma(const uint8_t* stc, const uint2* 
 
 template <typename T, int KS, int NT, int NSPLIT>
 __global__ void __launch_bounds__(kThreads, 2) token_select_kernel(const __grid_constant__ SelectParams p) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   __shared__ SelCtl ctl;
+  __shared__ __align__(8) uint64_t stage_bar;
   const Dims& d = p.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q4 = lane & 3, r0 = lane >> 2;
   const unsigned rank = blockIdx.x;  // cluster = the cs CTAs of blockIdx.y
@@ -208,48 +230,54 @@ __global__ void __launch_bounds__(kThreads, 2) token_select_kernel(const __grid_
   const int pair = blockIdx.y;
   const int b = pair / d.Hkv, g = pair - b * d.Hkv;
   const int n = min(max(p.seq_lens[b], 0), d.S);
-  const int m = (n + d.B - 1) / d.B;
+  const int m = (n + d.B - 1) >> d.log2B;
   uint32_t* bkeys = reinterpret_cast<uint32_t*>(smem + p.off_bkeys);
   int* cblk = reinterpret_cast<int*>(smem + p.off_cblk);
   uint32_t* qb = reinterpret_cast<uint32_t*>(smem + p.off_qb);
   float* qsum = reinterpret_cast<float*>(smem + p.off_qsum);
+  float* qc = reinterpret_cast<float*>(smem + p.off_qc);
   uint8_t* stc = smem + p.off_stc;
   float2* stz = reinterpret_cast<float2*>(smem + p.off_stz);
   uint32_t* tkeys = reinterpret_cast<uint32_t*>(smem + p.off_tkeys);
+  unsigned long long* dbg = p.dbg ? p.dbg + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 : nullptr;
+#define TLS_STAMP(i) \
+  if (dbg && tid == 0) dbg[i] = gtimer();
+  TLS_STAMP(0)
+  if (tid == 0) {
+    mbar_init(&stage_bar, 1);
+    mbar_fence_init();
+  }
+  // ---- channel-projected query q~_h[c] = q_h[C_c], gathered once ----
   const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
   const int* chan = p.channels + (size_t)g * d.d_c;
-
-  // ---- query fragments for the token contraction, and sum_c q_h[C_c] ----
+  constexpr int DC = KS * 16;
+  for (int i = tid; i < NT * 8 * DC; i += kThreads) {
+    const int h = i / DC, c = i - h * DC;
+    qc[i] = h < d.G ? to_f32<T>(qg[(size_t)h * d.d_k + chan[c]]) : 0.f;
+  }
+  // ---- a2 input: keys of the m block scores (K1's output, L2-resident) ----
+  const float* sc = p.scores + (size_t)pair * d.M;
+  for (int i = tid; i < m; i += kThreads) bkeys[i] = f2key(sc[i]);
+  __syncthreads();
+  // B fragments of the token contraction (MMA K order = channel permutation,
+  // thread q4 owns code words q4*WPT..; see token_tile_mma), and sum_c q~_h[c]
   constexpr int WPT = KS / 2;
   for (int idx = tid; idx < NSPLIT * NT * KS * 32; idx += kThreads) {
     const int ln = idx & 31, rest = idx >> 5;
     const int s = rest % KS, nt = (rest / KS) % NT, sp = rest / (KS * NT);
-    const int hh = nt * 8 + (ln >> 2);
-    const int wi = (ln & 3) * WPT + (s >> 1);
-    const int cb = 8 * wi + 2 * (s & 1);
-    float x[4] = {0.f, 0.f, 0.f, 0.f};
-    if (hh < d.G) {
-      const T* qh = qg + (size_t)hh * d.d_k;
-      x[0] = to_f32<T>(qh[chan[cb]]);
-      x[1] = to_f32<T>(qh[chan[cb + 4]]);
-      x[2] = to_f32<T>(qh[chan[cb + 1]]);
-      x[3] = to_f32<T>(qh[chan[cb + 5]]);
-    }
-    qb[2 * idx] = pack_bf16x2(split_piece(x[0], sp), split_piece(x[1], sp));
-    qb[2 * idx + 1] = pack_bf16x2(split_piece(x[2], sp), split_piece(x[3], sp));
+    const float* qh = qc + (nt * 8 + (ln >> 2)) * DC;
+    const int cb = 8 * ((ln & 3) * WPT + (s >> 1)) + 2 * (s & 1);
+    qb[2 * idx] = pack_bf16x2(split_piece(qh[cb], sp), split_piece(qh[cb + 4], sp));
+    qb[2 * idx + 1] = pack_bf16x2(split_piece(qh[cb + 1], sp), split_piece(qh[cb + 5], sp));
   }
-  for (int h = tid; h < NT * 8; h += kThreads) {
+  if (tid < NT * 8) {
     float s = 0.f;
-    if (h < d.G)
-      for (int c = 0; c < d.d_c; ++c) s += to_f32<T>(qg[(size_t)h * d.d_k + chan[c]]);
-    qsum[h] = s;
+    for (int c = 0; c < DC; ++c) s += qc[tid * DC + c];
+    qsum[tid] = s;
   }
-  // ---- a2: M_t = top-k_b of the block scores (K1's output, L2-resident) ----
-  // Every CTA of the cluster selects redundantly from identical data, so the
-  // candidate list needs no exchange.
-  const float* sc = p.scores + (size_t)pair * d.M;
-  for (int i = tid; i < m; i += kThreads) bkeys[i] = f2key(sc[i]);
-  __syncthreads();
+  TLS_STAMP(1)
+  // ---- a2: M_t = top-k_b blocks.  Every CTA of the cluster selects
+  // redundantly from identical data, so the candidate list needs no exchange.
   const bool sync_mode = p.guide == nullptr;
   {
     const TopK t = radix_topk<false>(bkeys, m, min(d.Kb, m), d.Kb >= m, 1, 0, ctl.tk);
@@ -282,17 +310,26 @@ __global__ void __launch_bounds__(kThreads, 2) token_select_kernel(const __grid_
   const int kc = ctl.kc;
   const int cb0 = (int)((long long)kc * rank / cs), cb1 = (int)((long long)kc * (rank + 1) / cs);
   const int nbl = cb1 - cb0;
-  const int lc = nbl * d.B;
-  const int ntiles = lc / 16;
-  stage_token_index(p, pair, cblk, cb0, nbl, stc, stz);
+  const int lc = nbl << d.log2B;
+  const int tshift = d.log2B - 4;  // 16-token tiles per block = 2^tshift
+  const int ntiles = lc >> 4;
+  TLS_STAMP(2)
+  stage_token_index(p, pair, cblk, cb0, nbl, stc, stz, &stage_bar);
+  TLS_STAMP(3)
   if (tid == 0) {
     int nv = 0;
-    for (int k = cb0; k < cb1; ++k) nv += min(d.B, n - cblk[k] * d.B);
+    for (int k = cb0; k < cb1; ++k) nv += min(d.B, n - (cblk[k] << d.log2B));
     ctl.nvalid = nv;
   }
   const float sm2 = d.sm_scale * kLog2e;
+  // per-thread head constants: L = zero * (sm2*qsum_h) + scale * (sm2 * acc)
+  float sq[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) sq[nt][e] = sm2 * qsum[nt * 8 + 2 * q4 + e];
   const uint2* qb2 = reinterpret_cast<const uint2*>(qb);
-  {  // pass 1: online per-head (max, sum) of L_hj = sm2*(zero*qsum_h + scale*(q~_h . code_j))
+  {  // pass 1: online per-head (max, sum)
     float rm[NT][2], rs[NT][2];
 #pragma unroll
     for (int i = 0; i < NT; ++i) rm[i][0] = rm[i][1] = -CUDART_INF_F, rs[i][0] = rs[i][1] = 0.f;
@@ -300,21 +337,20 @@ __global__ void __launch_bounds__(kThreads, 2) token_select_kernel(const __grid_
       float acc[NT][4];
       token_tile_mma<KS, NT, NSPLIT>(stc, qb2, tile, acc);
       const int j0 = tile * 16 + r0;
-      const int kb = j0 / d.B;
-      const int tok0 = cblk[cb0 + kb] * d.B + (j0 - kb * d.B);
+      const int tok0 = (cblk[cb0 + (tile >> tshift)] << d.log2B) + ((tile & ((1 << tshift) - 1)) << 4) + r0;
       const bool v0 = tok0 < n, v1 = tok0 + 8 < n;
       const float2 z0 = stz[j0], z1 = stz[j0 + 8];
+      const float s0 = sm2 * z0.x, s1 = sm2 * z1.x;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const float qs = qsum[nt * 8 + 2 * q4 + e];
-          const float l0 = v0 ? sm2 * fmaf(z0.y, qs, z0.x * acc[nt][e]) : -CUDART_INF_F;
-          const float l1 = v1 ? sm2 * fmaf(z1.y, qs, z1.x * acc[nt][2 + e]) : -CUDART_INF_F;
+          const float l0 = v0 ? fmaf(s0, acc[nt][e], z0.y * sq[nt][e]) : -CUDART_INF_F;
+          const float l1 = v1 ? fmaf(s1, acc[nt][2 + e], z1.y * sq[nt][e]) : -CUDART_INF_F;
           const float mt = fmaxf(l0, l1);
           if (mt != -CUDART_INF_F) {
             const float nm = fmaxf(rm[nt][e], mt);
-            rs[nt][e] = rs[nt][e] * exp2f(rm[nt][e] - nm) + exp2f(l0 - nm) + exp2f(l1 - nm);
+            rs[nt][e] = rs[nt][e] * fexp2(rm[nt][e] - nm) + fexp2(l0 - nm) + fexp2(l1 - nm);
             rm[nt][e] = nm;
           }
         }
@@ -346,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 2) token_select_kernel(const __grid_
       ctl.hz[tid] = ss;
     }
   }
+  TLS_STAMP(4)
   cluster_sync_all();
   if (tid < d.G) {  // the cs CTAs' (max, sum) merged in rank order: lz_h = M_h + log2 Z_h
     float hm[kMaxCluster], hz[kMaxCluster];
@@ -357,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 2) token_select_kernel(const __grid_
     float M = -CUDART_INF_F, Z = 0.f;
 #pragma unroll
     for (int rr = 0; rr < kMaxCluster; ++rr) stat_merge(M, Z, hm[rr], hz[rr]);
-    ctl.hlz[tid] = M + log2f(Z);
+    ctl.hlz[tid] = M + flog2(Z);
   }
   if (tid == 32) {
     int nv[kMaxCluster];
@@ -370,54 +407,59 @@ __global__ void __launch_bounds__(kThreads, 2) token_select_kernel(const __grid_
   }
   __syncthreads();
   // pass 2: ranking key log2 alpha~_j + log2 G = log2 sum_h exp2(L_hj - lz_h)  (reading U15)
-  for (int tile = warp; tile < ntiles; tile += kWarps) {
-    float acc[NT][4];
-    token_tile_mma<KS, NT, NSPLIT>(stc, qb2, tile, acc);
-    const int j0 = tile * 16 + r0;
-    const int kb = j0 / d.B;
-    const int tok0 = cblk[cb0 + kb] * d.B + (j0 - kb * d.B);
-    const bool v0 = tok0 < n, v1 = tok0 + 8 < n;
-    const float2 z0 = stz[j0], z1 = stz[j0 + 8];
-    float t0[NT][2], t1[NT][2];
-    float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+  {
+    float lz[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int h = nt * 8 + 2 * q4 + e;
-        if (h < d.G) {
-          const float qs = qsum[h], lz = ctl.hlz[h];
-          t0[nt][e] = sm2 * fmaf(z0.y, qs, z0.x * acc[nt][e]) - lz;
-          t1[nt][e] = sm2 * fmaf(z1.y, qs, z1.x * acc[nt][2 + e]) - lz;
-        } else {
-          t0[nt][e] = t1[nt][e] = -CUDART_INF_F;
+        lz[nt][e] = h < d.G ? ctl.hlz[h] : CUDART_INF_F;  // padded heads contribute exp2(-inf) = 0
+      }
+    for (int tile = warp; tile < ntiles; tile += kWarps) {
+      float acc[NT][4];
+      token_tile_mma<KS, NT, NSPLIT>(stc, qb2, tile, acc);
+      const int j0 = tile * 16 + r0;
+      const int tok0 = (cblk[cb0 + (tile >> tshift)] << d.log2B) + ((tile & ((1 << tshift) - 1)) << 4) + r0;
+      const bool v0 = tok0 < n, v1 = tok0 + 8 < n;
+      const float2 z0 = stz[j0], z1 = stz[j0 + 8];
+      const float s0 = sm2 * z0.x, s1 = sm2 * z1.x;
+      float t0[NT][2], t1[NT][2];
+      float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          t0[nt][e] = fmaf(s0, acc[nt][e], fmaf(z0.y, sq[nt][e], -lz[nt][e]));
+          t1[nt][e] = fmaf(s1, acc[nt][2 + e], fmaf(z1.y, sq[nt][e], -lz[nt][e]));
+          mx0 = fmaxf(mx0, t0[nt][e]);
+          mx1 = fmaxf(mx1, t1[nt][e]);
         }
-        mx0 = fmaxf(mx0, t0[nt][e]);
-        mx1 = fmaxf(mx1, t1[nt][e]);
-      }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    float s0 = 0.f, s1 = 0.f;
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      float e0 = 0.f, e1 = 0.f;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        s0 += exp2f(t0[nt][e] - mx0);
-        s1 += exp2f(t1[nt][e] - mx1);
+        for (int e = 0; e < 2; ++e) {
+          e0 += fexp2(t0[nt][e] - mx0);
+          e1 += fexp2(t1[nt][e] - mx1);
+        }
+      e0 += __shfl_xor_sync(0xffffffffu, e0, 1);
+      e0 += __shfl_xor_sync(0xffffffffu, e0, 2);
+      e1 += __shfl_xor_sync(0xffffffffu, e1, 1);
+      e1 += __shfl_xor_sync(0xffffffffu, e1, 2);
+      if (q4 == 0) {
+        tkeys[j0] = v0 ? f2key(mx0 + flog2(e0)) : 0u;
+        tkeys[j0 + 8] = v1 ? f2key(mx1 + flog2(e1)) : 0u;
       }
-    s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
-    s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
-    if (q4 == 0) {
-      tkeys[j0] = v0 ? f2key(mx0 + log2f(s0)) : 0u;
-      tkeys[j0 + 8] = v1 ? f2key(mx1 + log2f(s1)) : 0u;
     }
   }
   __syncthreads();
 
+  TLS_STAMP(5)
   // ---- a4: S_t = top-k_t tokens over the cluster ----
   {
     const int jtot = ctl.jtot;
@@ -427,8 +469,7 @@ __global__ void __launch_bounds__(kThreads, 2) token_select_kernel(const __grid_
     float* sout = p.token_scores ? p.token_scores + (size_t)pair * d.Kt : nullptr;
     const float lnG = logf((float)d.G);
     topk_emit(tkeys, lc, t, ctl.tk, [&](int i, int pos) {
-      const int kb = i / d.B;
-      tout[pos] = cblk[cb0 + kb] * d.B + (i - kb * d.B);
+      tout[pos] = (cblk[cb0 + (i >> d.log2B)] << d.log2B) + (i & (d.B - 1));
       if (sout) sout[pos] = key2f(tkeys[i]) * kLn2 - lnG;
     });
     if (rank == 0) {
@@ -439,7 +480,10 @@ __global__ void __launch_bounds__(kThreads, 2) token_select_kernel(const __grid_
       if (tid == 0) p.num_tokens[pair] = K;
     }
   }
+  TLS_STAMP(6)
   cluster_sync_all();  // no CTA leaves while its smem may still be read remotely
+  TLS_STAMP(7)
+#undef TLS_STAMP
 }
 
 // ============================================================== launchers
@@ -453,8 +497,14 @@ int score_cpl(int d_k, size_t elem_bytes) {
 
 template <typename T, int CPL>
 static cudaError_t launch_k1(const ScoreParams& p, cudaStream_t st) {
-  dim3 grid((unsigned)((p.d.M + kScoreChunk - 1) / kScoreChunk), (unsigned)(p.d.batch * p.d.Hkv), 1);
-  block_score_kernel<T, CPL><<<grid, kThreads, 0, st>>>(p);
+  auto kern = block_score_kernel<T, CPL>;
+  const int smem = p.tb * 2 * p.d.d_k * (int)sizeof(T);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((p.d.M + p.tb - 1) / p.tb), (unsigned)(p.d.batch * p.d.Hkv), 1);
+  kern<<<grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();
 }
 

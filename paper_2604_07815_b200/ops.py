@@ -23,6 +23,7 @@ __all__ = [
     "alloc_index",
     "calibrate_channels",
     "build_index",
+    "block_scores",
     "select",
     "sparse_attend",
     "decode",
@@ -185,6 +186,20 @@ def build_index(cfg: TLSConfig, k_cache: torch.Tensor, seq_lens: torch.Tensor, i
     return index
 
 
+def block_scores(cfg: TLSConfig, q: torch.Tensor, seq_lens: torch.Tensor, index: TLSIndex, out=None):
+    """Block scores s_i of every pair, fp32 [batch, Hkv, M]."""
+    lib = _lib.load()
+    dev = q.device
+    _need(q, "q", (cfg.batch, cfg.num_q_heads, cfg.d_k), cfg.dtype, dev)
+    _need(seq_lens, "seq_lens", (cfg.batch,), torch.int32, dev)
+    if out is None:
+        out = torch.empty((cfg.batch, cfg.num_kv_heads, cfg.num_blocks), dtype=torch.float32, device=dev)
+    cc = cfg.c()
+    _lib.check(lib.tls_block_scores(ctypes.byref(cc), q.data_ptr(), seq_lens.data_ptr(), index.block_minmax.data_ptr(),
+                                    out.data_ptr(), _stream(dev)))
+    return out
+
+
 def _sel_outputs(cfg: TLSConfig, dev, out):
     if out is not None:
         return out
@@ -232,10 +247,11 @@ def sparse_attend(cfg: TLSConfig, q: torch.Tensor, k_cache: torch.Tensor, v_cach
     if lse is None:
         lse = torch.empty((cfg.batch, cfg.num_q_heads), dtype=torch.float32, device=dev)
     cc = cfg.c()
+    ws, wsb = _workspace(cfg, dev, 1)
     _lib.check(lib.tls_sparse_attend(ctypes.byref(cc), q.data_ptr(), k_cache.data_ptr(),
                                      v_cache.data_ptr() if (v_cache is not None and cfg.layout == "gqa") else 0,
                                      token_ids.data_ptr(), num_tokens.data_ptr(), out.data_ptr(), lse.data_ptr(),
-                                     None, 0, _stream(dev)))
+                                     ws, wsb, _stream(dev)))
     return out, lse
 
 

@@ -306,3 +306,21 @@ def test_full_size_sampled_pairs(name):
     print(f"{name}: near-ties {stats}")
     del inputs, idx, res
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["gqa4", "mla", "c1"])
+def test_block_scores_match_direct_form(name):
+    """tls_block_scores vs the oracle's direct Quest form O3, fp32 bound."""
+    w = SMALL[name]
+    cfg, inputs, idx = setup_case(w, seed=6)
+    sc = tls.block_scores(cfg, inputs["q"], inputs["seq_lens"], idx)
+    torch.cuda.synchronize()
+    G = w.num_q_heads // w.num_kv_heads
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            q, keys, _ = P.pair_slices(w, inputs, b, g)
+            kmax, kmin = O.block_summaries(keys, w.block_size)
+            ref = O.block_scores(q, kmax, kmin)
+            got = sc[b, g, : len(ref)].double().cpu().numpy()
+            bound = 2e-6 * (np.abs(q).sum() * np.maximum(np.abs(kmax), np.abs(kmin)).max(axis=1) + 1.0)
+            assert np.all(np.abs(got - ref) <= bound)
