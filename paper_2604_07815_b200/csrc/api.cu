@@ -105,25 +105,23 @@ int env_cluster() {
   return (env && atoi(env) > 0) ? atoi(env) : 0;
 }
 
-// K2 cluster size: each CTA stages <= ~48 KB of token index, and the grid
-// covers the 148 SMs at least twice.  TLS_CLUSTER overrides (tuning / tests).
+// K2 cluster size: one CTA per pair once the pairs cover the SMs (no cluster
+// synchronisation at all); otherwise split a pair's candidate blocks over cs
+// CTAs so the grid covers the SMs.  TLS_CLUSTER overrides (tuning / tests).
 tls_status plan_select(const tls_config* c, tls::SelectParams& p) {
   memset(&p, 0, sizeof(p));
   p.d = dims_of(c);
   const long long pairs = (long long)c->batch * c->num_kv_heads;
   const int kb = tls::kb_effective(p.d);
-  const size_t per_block = (size_t)p.d.B * (p.d.d_c / 2 + 8);
   int cs = env_cluster();
   if (!cs) {
     cs = 1;
-    while (cs < 16 && ((size_t)((kb + cs - 1) / cs) * per_block > 48 * 1024 || pairs * cs < 2 * kSMs)) cs *= 2;
+    while (cs < 16 && pairs * cs < kSMs && kb / (2 * cs) >= 4) cs *= 2;
   }
-  for (;; cs *= 2) {
-    if (cs > 16) return fail(TLS_ERR_UNSUPPORTED, "token-select shared-memory plan does not fit");
-    p.cs = cs;
-    tls::plan_select(p);
-    if ((int)p.smem_bytes <= kMaxSmem) break;
-  }
+  if (cs > 16) return fail(TLS_ERR_UNSUPPORTED, "cluster size > 16");
+  p.cs = cs;
+  tls::plan_select(p);
+  if ((int)p.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "token-select shared-memory plan does not fit");
   return TLS_OK;
 }
 

@@ -76,9 +76,9 @@ __device__ void phase_attend_generic(const AttendParams& p, int pair, int b, int
 template <int D>
 __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, const int* sel, int tloc,
                                  uint8_t* kvbuf, float* po, float* pml) {
-  constexpr int TC = kAttnChunk;
-  constexpr int CPR = D / 8;  // 16-byte chunks per row
-  constexpr int KS = D / 16;  // k-steps of QK^T
+  constexpr int TC = kAttnChunk;  // 64 tokens per stage: 8 warps x 8 tokens
+  constexpr int CPR = D / 8;      // 16-byte chunks per row
+  constexpr int KS = D / 16;      // k-steps of QK^T
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = lane >> 2, c2 = 2 * (lane & 3);
   __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(kvbuf);  // [2 stages][K TC*D | V TC*D]
@@ -90,7 +90,9 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
     __nv_bfloat16* sK = sbuf + (size_t)stage * 2 * TC * D;
     __nv_bfloat16* sV = sK + TC * D;
     const int nt = min(TC, tloc - c * TC);
-    for (int i = tid; i < TC * CPR; i += kThreads) {
+#pragma unroll
+    for (int it = 0; it < (TC * CPR) / kThreads; ++it) {
+      const int i = tid + it * kThreads;
       const int row = i / CPR, ch = i - row * CPR;
       const bool ok = row < nt;
       const int tok = ok ? sel[c * TC + row] : 0;
@@ -128,43 +130,33 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
     const __nv_bfloat16* sK = sbuf + (size_t)(c & 1) * 2 * TC * D;
     const __nv_bfloat16* sV = sK + TC * D;
     const int nt = min(TC, tloc - c * TC);
-    const int tb = warp * 16;
+    const int tb = warp * 8;
     if (tb < nt) {
-      float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      // S (16 head rows x 8 tokens) = Q K^T
+      float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int kk = 0; kk < KS; ++kk) {
-        const int row = tb + ((lane >> 4) << 3) + (lane & 7);
-        const int ch = kk * 2 + ((lane >> 3) & 1);
+      for (int kk = 0; kk < KS; kk += 2) {
+        const int row = tb + (lane & 7);
+        const int ch = kk * 2 + (lane >> 3);  // 4 matrices: k-steps kk (b0, b1) and kk+1 (b0, b1)
         uint32_t bk[4];
         ldsm_x4(bk, sK + row * D + ((ch ^ (row & 7)) << 3));
-        mma_bf16_16816(s[0], qa[kk], bk[0], bk[1]);
-        mma_bf16_16816(s[1], qa[kk], bk[2], bk[3]);
+        mma_bf16_16816(s, qa[kk], bk[0], bk[1]);
+        mma_bf16_16816(s, qa[kk + 1], bk[2], bk[3]);
       }
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int t = tb + j * 8 + c2 + (e & 1);
-          s[j][e] = t < nt ? s[j][e] * sm2 : -CUDART_INF_F;
-        }
-      float x0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
-      float x1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+      for (int e = 0; e < 4; ++e) {
+        const int t = tb + c2 + (e & 1);
+        s[e] = t < nt ? s[e] * sm2 : -CUDART_INF_F;
+      }
+      float x0 = fmaxf(s[0], s[1]), x1 = fmaxf(s[2], s[3]);
       x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, 1));
       x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, 2));
       x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 1));
       x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 2));
       const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);  // finite: token tb is valid
       const float a0 = fexp2(m0 - n0), a1 = fexp2(m1 - n1);
-      float pr[2][4];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        pr[j][0] = fexp2(s[j][0] - n0);
-        pr[j][1] = fexp2(s[j][1] - n0);
-        pr[j][2] = fexp2(s[j][2] - n1);
-        pr[j][3] = fexp2(s[j][3] - n1);
-      }
-      float r0s = pr[0][0] + pr[0][1] + pr[1][0] + pr[1][1];
-      float r1s = pr[0][2] + pr[0][3] + pr[1][2] + pr[1][3];
+      const float p0 = fexp2(s[0] - n0), p1 = fexp2(s[1] - n0), p2 = fexp2(s[2] - n1), p3 = fexp2(s[3] - n1);
+      float r0s = p0 + p1, r1s = p2 + p3;
       r0s += __shfl_xor_sync(0xffffffffu, r0s, 1);
       r0s += __shfl_xor_sync(0xffffffffu, r0s, 2);
       r1s += __shfl_xor_sync(0xffffffffu, r1s, 1);
@@ -180,19 +172,22 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
         o[j][2] *= a1;
         o[j][3] *= a1;
       }
+      // P (16 x 16, tokens 8..15 of the k-step zero) x V (8 tokens of this warp)
       uint32_t pa[4];
-      pa[0] = pack_bf16x2(pr[0][0], pr[0][1]);
-      pa[1] = pack_bf16x2(pr[0][2], pr[0][3]);
-      pa[2] = pack_bf16x2(pr[1][0], pr[1][1]);
-      pa[3] = pack_bf16x2(pr[1][2], pr[1][3]);
+      pa[0] = pack_bf16x2(p0, p1);
+      pa[1] = pack_bf16x2(p2, p3);
+      pa[2] = 0u;
+      pa[3] = 0u;
 #pragma unroll
-      for (int jj = 0; jj < D / 16; ++jj) {
-        const int row = tb + ((lane >> 3) & 1) * 8 + (lane & 7);
-        const int ch = jj * 2 + (lane >> 4);
+      for (int jj = 0; jj < D / 32; ++jj) {
+        const int row = tb + (lane & 7);
+        const int ch = jj * 4 + (lane >> 3);  // dims 32jj + 8*(lane>>3): 4 n-tiles
         uint32_t bv[4];
         ldsm_x4_trans(bv, sV + row * D + ((ch ^ (row & 7)) << 3));
-        mma_bf16_16816(o[2 * jj], pa, bv[0], bv[1]);
-        mma_bf16_16816(o[2 * jj + 1], pa, bv[2], bv[3]);
+        mma_bf16_16816(o[4 * jj + 0], pa, bv[0], 0u);
+        mma_bf16_16816(o[4 * jj + 1], pa, bv[1], 0u);
+        mma_bf16_16816(o[4 * jj + 2], pa, bv[2], 0u);
+        mma_bf16_16816(o[4 * jj + 3], pa, bv[3], 0u);
       }
     }
     __syncthreads();  // stage (c & 1) consumed before it is refilled

@@ -246,3 +246,35 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 }  // namespace tls
+
+namespace tls {
+// (a & b) | c in one LOP3 (b, c in registers).
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+// Unpack one 32-bit word of 8 INT4 codes n0..n7 into 4 bf16x2 registers
+// (n_s, n_{s+4}), s = 0..3, each an exact integer 0..15 (see nib2bf16).
+__device__ __forceinline__ void unpack_nibbles8(uint32_t w, uint32_t (&out)[4]) {
+  const uint32_t mask = 0x000f000fu, magic = 0x43004300u;
+  const __nv_bfloat162 m128 = __halves2bfloat162(__ushort_as_bfloat16(0x4300), __ushort_as_bfloat16(0x4300));
+  uint32_t x[4];
+  x[0] = lop3_and_or(w, mask, magic);
+  x[1] = lop3_and_or(w >> 4, mask, magic);
+  x[2] = lop3_and_or(w >> 8, mask, magic);
+  x[3] = lop3_and_or(w >> 12, mask, magic);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 v = __hsub2(*reinterpret_cast<__nv_bfloat162*>(&x[i]), m128);
+    out[i] = *reinterpret_cast<uint32_t*>(&v);
+  }
+}
+}  // namespace tls
+
+namespace tls {
+// TMA bulk prefetch of [src, src + bytes) into L2 (no shared memory, no wait).
+__device__ __forceinline__ void tma_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+}  // namespace tls

@@ -10,7 +10,7 @@
 
 namespace tls {
 
-constexpr int kAttnChunk = 128;    // tokens per K/V staging chunk of the mma attention (8 warps x 16)
+constexpr int kAttnChunk = 64;     // tokens per K/V staging stage of the GQA mma attention (8 warps x 8)
 constexpr int kMlaChunkTokens = 32;  // latent rows per staging chunk of the MLA attention (double-buffered)
 constexpr int kScoreTileBytes = 32 * 1024;  // K1: bytes of block summaries per CTA (TMA tile)
 
@@ -25,7 +25,7 @@ struct Dims {
 
 struct ScoreParams {  // K1
   Dims d;
-  int tb;  // blocks per CTA: the tile of summaries is <= kScoreTileBytes
+  int tb;  // block-summary rows per CTA (<= kScoreTileBytes)
   const void* q;
   const int* seq_lens;
   const void* block_minmax;
@@ -36,7 +36,8 @@ struct SelectParams {  // K2
   Dims d;
   int cs;
   int kb_eff, kt_eff;  // min(Kb, M); min(Kt, kb_eff*B, S)
-  int mloc, lc_max;    // keys per CTA in the block top-k (= M); candidate slots per CTA
+  int rb;              // candidate blocks per ring stage
+  int ring_stage_bytes;
   const void* q;
   const int* seq_lens;
   const float* scores;
@@ -49,7 +50,7 @@ struct SelectParams {  // K2
   int* num_tokens;
   float* token_scores;
   unsigned long long* dbg;  // diagnostics: per-CTA phase timestamps (NULL = off)
-  unsigned off_bkeys, off_cblk, off_qb, off_qsum, off_qc, off_stc, off_stz, off_tkeys, smem_bytes;
+  unsigned off_bkeys, off_cblk, off_qb, off_qsum, off_qc, off_ring, off_tkeys, smem_bytes;
 };
 
 struct AttendParams {  // K3
@@ -81,10 +82,12 @@ static inline void plan_select(SelectParams& p) {
   const Dims& d = p.d;
   p.kb_eff = kb_effective(d);
   p.kt_eff = kt_effective(d);
-  p.mloc = d.M;
   const int nt0 = (d.G + 7) / 8, nt = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);  // instantiated NT
   const int ks = d.d_c / 16, nsplit = d.bf16 ? 1 : 3;
-  p.lc_max = ((p.kb_eff + p.cs - 1) / p.cs) * d.B;
+  const int per_block = d.B * (d.d_c / 2 + 8);
+  p.rb = (16 * 1024) / per_block;  // ~16 KB per ring stage
+  if (p.rb < 1) p.rb = 1;
+  p.ring_stage_bytes = (int)align16((size_t)p.rb * per_block);
   size_t o = 0;
   p.off_bkeys = (unsigned)o;
   o = align16(o + (size_t)d.M * 4);
@@ -97,12 +100,10 @@ static inline void plan_select(SelectParams& p) {
   p.off_qc = (unsigned)o;
   o = align16(o + (size_t)nt * 8 * d.d_c * 4);
   o = (o + 127) & ~(size_t)127;
-  p.off_stc = (unsigned)o;
-  o = align16(o + (size_t)p.lc_max * (d.d_c / 2));
-  p.off_stz = (unsigned)o;
-  o = align16(o + (size_t)p.lc_max * 8);
-  p.off_tkeys = (unsigned)o;
-  o = align16(o + (size_t)p.lc_max * 4);
+  p.off_ring = (unsigned)o;
+  o = align16(o + (size_t)3 * p.ring_stage_bytes);
+  p.off_tkeys = (unsigned)o;  // keys of ALL candidate slots of the pair (rank 0 selects)
+  o = align16(o + (size_t)p.kb_eff * d.B * 4);
   p.smem_bytes = (unsigned)o;
 }
 

@@ -21,8 +21,10 @@ for it in range(3):
 torch.cuda.synchronize()
 lib.tls_debug_phase_timing(None)
 t = buf.cpu().double()
+if cs > 1:
+    t = t.view(-1, cs, 8)[:, 0, :]  # rank 0 runs every phase
 t0 = t[:, 0].min()
-names = ["gather q/keys", "block top-k", "stage index", "stats pass", "merge+keys", "top-k_t+emit", "final sync"]
+names = ["q gather + block top-k", "stats pass (ring)", "stats merge", "keys pass (ring)", "key exchange", "top-k_t + emit", "-"]
 d = (t[:, 1:] - t[:, :-1]) / 1e3
 print(f"{name}: cs={cs} ctas={t.shape[0]} kernel span {(t[:, 7].max() - t0) / 1e3:.1f} us; "
       f"CTA lifetime median {((t[:, 7] - t[:, 0]) / 1e3).median():.1f} us")
