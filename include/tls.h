@@ -187,13 +187,15 @@ tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
                       int32_t* num_tokens, float* token_scores, void* out, float* lse,
                       void* workspace, size_t workspace_bytes, tls_stream_t stream);
 
-/* Workspace bytes needed by: which = 0 tls_select (the fp32 block scores of
- * every pair, [batch, Hkv, M] floats, handed from the block-score kernel to the
- * token-select kernel), 1 tls_sparse_attend (the per-CTA partial (max, sum, o)
- * of the split-K attention, [batch, Hkv, cs, G, d_v + 2] floats), 2 tls_decode
- * (the sum; select part first).  Sizes are rounded up to 256 B; the contents
- * need no initialisation.  (size_t)-1 for an invalid configuration or `which`.
- * A NULL / too small / misaligned workspace -> TLS_ERR_WORKSPACE. */
+/* Workspace bytes needed by: which = 0 tls_select, 1 tls_sparse_attend,
+ * 2 tls_decode.  The select part holds the fp32 block scores of every pair,
+ * per-chunk softmax statistics, the ranking key of every candidate token and a
+ * per-pair key histogram; the attention part the
+ * per-CTA partial (max, sum, o) of the split-K attention.  Sizes are rounded
+ * up to 256 B.  No initialisation is needed (every word is written before it
+ * is read within a call).  Do not share one workspace between calls that may
+ * run concurrently.  (size_t)-1 for an invalid configuration or
+ * `which`.  A NULL / too small / misaligned workspace -> TLS_ERR_WORKSPACE. */
 size_t tls_workspace_bytes(const tls_config* cfg, int32_t which);
 
 /* Number of kernel launches one call enqueues (which as above; 3 =
@@ -212,11 +214,6 @@ const char* tls_status_string(tls_status status);
 const char* tls_last_error(void); /* thread-local detail of the last error */
 const char* tls_version(void);
 
-/* Diagnostics only: when device_buffer is non-NULL, the token-select kernel
- * launched by this thread writes 8 %globaltimer stamps (ns) per CTA at its
- * phase boundaries into device_buffer[(pair * cs + rank) * 8 + i].  NULL
- * (the default) turns it off.  Not part of the measured path. */
-void tls_debug_phase_timing(unsigned long long* device_buffer);
 
 #ifdef __cplusplus
 }

@@ -30,7 +30,6 @@ EXPORTS = (
     "tls_status_string",
     "tls_last_error",
     "tls_version",
-    "tls_debug_phase_timing",
 )
 
 
@@ -102,7 +101,6 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "tls_status_string": (ctypes.c_char_p, [_I32]),
         "tls_last_error": (ctypes.c_char_p, []),
         "tls_version": (ctypes.c_char_p, []),
-        "tls_debug_phase_timing": (None, [_P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -11,10 +11,12 @@
 #include "../../include/tls.h"
 #include "index.h"
 #include "params.h"
+#include "fasttopk.cuh"
 
 namespace tls {
 cudaError_t launch_block_scores(const ScoreParams& p, cudaStream_t st);
-cudaError_t launch_token_select(const SelectParams& p, cudaStream_t st);
+cudaError_t launch_token_cluster(const SelectParams& p, cudaStream_t st);
+cudaError_t launch_block_topk(const ScoreParams& p, cudaStream_t st);
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t st);
 int score_cpl(int d_k, size_t elem_bytes);
 bool select_supported(int d_c, int G);
@@ -23,7 +25,6 @@ bool select_supported(int d_c, int G);
 namespace {
 
 thread_local char g_err[512] = "";
-thread_local unsigned long long* g_dbg = nullptr;  // diagnostics only (tls_debug_phase_timing)
 
 tls_status fail(tls_status s, const char* fmt, ...) {
   va_list ap;
@@ -97,6 +98,7 @@ tls::Dims dims_of(const tls_config* c) {
   d.bf16 = c->dtype == TLS_BF16;
   d.log2B = 0;
   while ((1 << d.log2B) < c->block_size) ++d.log2B;
+  d.Ms = (d.M + 3) & ~3;
   return d;
 }
 
@@ -105,44 +107,36 @@ int env_cluster() {
   return (env && atoi(env) > 0) ? atoi(env) : 0;
 }
 
-// K2 cluster size: one CTA per pair once the pairs cover the SMs (no cluster
-// synchronisation at all); otherwise split a pair's candidate blocks over cs
-// CTAs so the grid covers the SMs.  TLS_CLUSTER overrides (tuning / tests).
 tls_status plan_select(const tls_config* c, tls::SelectParams& p) {
   memset(&p, 0, sizeof(p));
   p.d = dims_of(c);
-  const long long pairs = (long long)c->batch * c->num_kv_heads;
-  const int kb = tls::kb_effective(p.d);
-  int cs = env_cluster();
-  if (!cs) {
-    cs = 1;
-    while (cs < 16 && pairs * cs < kSMs && kb / (2 * cs) >= 4) cs *= 2;
-  }
-  if (cs > 16) return fail(TLS_ERR_UNSUPPORTED, "cluster size > 16");
-  p.cs = cs;
   tls::plan_select(p);
-  if ((int)p.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "token-select shared-memory plan does not fit");
+  if ((int)p.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "token-kernel shared-memory plan does not fit");
   return TLS_OK;
 }
 
-// K3 cluster size: ~128 tokens per CTA (one staging chunk), >= 2 CTAs per SM.
-tls_status plan_attend(const tls_config* c, tls::AttendParams& p) {
+// K3 cluster size: one CTA per pair once the pairs cover the SMs; else split
+// the pair's tokens.  TLS_CLUSTER overrides (tuning / tests).
+tls_status plan_attend(const tls_config* c, tls::AttendParams& p, int select, int attend) {
   memset(&p, 0, sizeof(p));
   p.d = dims_of(c);
+  p.select = select;
+  p.attend = attend;
   p.mma = c->dtype == TLS_BF16 && c->layout == TLS_GQA && c->d_k == c->d_v && (c->d_k == 64 || c->d_k == 128) &&
           p.d.G <= 16;
   if (c->dtype == TLS_BF16 && c->layout == TLS_MLA && c->d_k == 576 && c->d_v == 512 && p.d.G <= 32) p.mma = 2;
   const long long pairs = (long long)c->batch * c->num_kv_heads;
   const int kt = tls::kt_effective(p.d);
   int cs = env_cluster();
-  if (!cs) {  // one CTA per pair once the pairs cover the SMs; else split the tokens
+  if (!attend) cs = 1;  // selection only: one CTA per pair
+  if (!cs) {
     cs = 1;
     while (cs < 16 && pairs * cs < kSMs && (kt + 2 * cs - 1) / (2 * cs) >= 64) cs *= 2;
   }
   for (;; cs *= 2) {
     if (cs > 16) return fail(TLS_ERR_UNSUPPORTED, "attention shared-memory plan does not fit");
     p.cs = cs;
-    tls::plan_attend(p);
+    tls::plan_attend(p, sizeof(tls::FastTopKCtl));
     if ((int)p.smem_bytes <= kMaxSmem) break;
   }
   return TLS_OK;
@@ -156,9 +150,12 @@ tls_status check_index(const tls_index* idx) {
   return TLS_OK;
 }
 
-tls_status run_select(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
-                      const int32_t* guide, int32_t* block_ids, int32_t* token_ids, int32_t* num_tokens,
-                      float* token_scores, void* workspace, size_t workspace_bytes, cudaStream_t st) {
+// Enqueue the decode-step kernels: K1 block scores, K2 (two passes), then K3
+// (top-k_t prologue + attention when do_attend; selection only otherwise).
+tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
+                    const int32_t* seq_lens, const tls_index* idx, const int32_t* guide, int32_t* block_ids,
+                    int32_t* token_ids, int32_t* num_tokens, float* token_scores, void* out, float* lse,
+                    void* workspace, size_t workspace_bytes, int do_attend, cudaStream_t st) {
   tls_status s = check_config(cfg);
   if (s) return s;
   if (!q || !aligned16(q)) return fail(TLS_ERR_INPUT, "q must be a non-NULL 16-byte aligned device pointer");
@@ -166,12 +163,24 @@ tls_status run_select(const tls_config* cfg, const void* q, const int32_t* seq_l
     return fail(TLS_ERR_INPUT, "seq_lens, block_ids, token_ids and num_tokens are required");
   s = check_index(idx);
   if (s) return s;
+  if (do_attend) {
+    if (!k_cache || !aligned16(k_cache)) return fail(TLS_ERR_INPUT, "k_cache must be a 16-byte aligned device pointer");
+    if (cfg->layout == TLS_GQA && (!v_cache || !aligned16(v_cache)))
+      return fail(TLS_ERR_INPUT, "GQA needs a 16-byte aligned v_cache");
+    if (!out) return fail(TLS_ERR_INPUT, "out is required");
+  }
   tls::SelectParams sp;
   s = plan_select(cfg, sp);
   if (s) return s;
-  const size_t need = tls::select_workspace_bytes(sp.d);
-  if (!workspace || workspace_bytes < need || !aligned16(workspace))
-    return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes, 16-byte aligned (got %zu)", need, workspace_bytes);
+  tls::AttendParams ap;
+  s = plan_attend(cfg, ap, 1, do_attend);
+  if (s) return s;
+  const tls::SelectWs w = tls::select_workspace(sp.d);
+  const size_t watt = do_attend ? tls::attend_workspace_bytes(ap.d, ap.cs) : 0;
+  if (!workspace || workspace_bytes < w.total + watt || !aligned16(workspace))
+    return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes, 16-byte aligned (got %zu)", w.total + watt,
+                workspace_bytes);
+  char* ws = static_cast<char*>(workspace);
   tls::ScoreParams k1;
   k1.d = sp.d;
   k1.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
@@ -179,9 +188,17 @@ tls_status run_select(const tls_config* cfg, const void* q, const int32_t* seq_l
   k1.q = q;
   k1.seq_lens = seq_lens;
   k1.block_minmax = idx->block_minmax;
-  k1.scores = static_cast<float*>(workspace);
+  k1.scores = reinterpret_cast<float*>(ws + w.scores);
+  k1.kb_eff = sp.kb_eff;
+  k1.sstride = sp.d.Ms;
+  k1.done = nullptr;
+  k1.khist = reinterpret_cast<uint32_t*>(ws + w.khist);
+  k1.guide = guide;
+  k1.block_ids = block_ids;
   cudaError_t e = tls::launch_block_scores(k1, st);
   if (e != cudaSuccess) return cuda_fail(e, "block_score_kernel launch");
+  e = tls::launch_block_topk(k1, st);
+  if (e != cudaSuccess) return cuda_fail(e, "block_topk_kernel launch");
   sp.q = q;
   sp.seq_lens = seq_lens;
   sp.scores = k1.scores;
@@ -190,12 +207,28 @@ tls_status run_select(const tls_config* cfg, const void* q, const int32_t* seq_l
   sp.channels = idx->channels;
   sp.guide = guide;
   sp.block_ids = block_ids;
-  sp.token_ids = token_ids;
-  sp.num_tokens = num_tokens;
-  sp.token_scores = token_scores;
-  sp.dbg = g_dbg;
-  e = tls::launch_token_select(sp, st);
-  if (e != cudaSuccess) return cuda_fail(e, "token_select_kernel launch");
+  sp.stats = reinterpret_cast<float*>(ws + w.stats);
+  sp.keys = reinterpret_cast<uint32_t*>(ws + w.keys);
+  sp.khist = k1.khist;
+  e = tls::launch_token_cluster(sp, st);
+  if (e != cudaSuccess) return cuda_fail(e, "token_cluster_kernel launch");
+  ap.q = q;
+  ap.k_cache = k_cache;
+  ap.v_cache = cfg->layout == TLS_MLA ? nullptr : v_cache;
+  ap.seq_lens = seq_lens;
+  ap.cand = guide ? guide : block_ids;
+  ap.keys = sp.keys;
+  ap.khist = sp.khist;
+  ap.token_ids = token_ids;
+  ap.num_tokens = num_tokens;
+  ap.token_scores = token_scores;
+  ap.out = out;
+  ap.lse = lse;
+  const size_t pairs = (size_t)cfg->batch * cfg->num_kv_heads;
+  ap.part_o = reinterpret_cast<float*>(ws + w.total);
+  ap.part_ml = reinterpret_cast<float*>(ws + w.total + tls::a256(pairs * ap.cs * ap.d.G * ap.d.d_v * 4));
+  e = tls::launch_attend(ap, st);
+  if (e != cudaSuccess) return cuda_fail(e, "attend_kernel launch");
   return TLS_OK;
 }
 
@@ -210,7 +243,7 @@ tls_status run_attend(const tls_config* cfg, const void* q, const void* k_cache,
   if (cfg->layout == TLS_GQA && (!v_cache || !aligned16(v_cache)))
     return fail(TLS_ERR_INPUT, "GQA needs a 16-byte aligned v_cache");
   tls::AttendParams ap;
-  s = plan_attend(cfg, ap);
+  s = plan_attend(cfg, ap, 0, 1);
   if (s) return s;
   const size_t need = tls::attend_workspace_bytes(ap.d, ap.cs);
   if (!workspace || workspace_bytes < need || !aligned16(workspace))
@@ -219,22 +252,22 @@ tls_status run_attend(const tls_config* cfg, const void* q, const void* k_cache,
   ap.q = q;
   ap.k_cache = k_cache;
   ap.v_cache = cfg->layout == TLS_MLA ? nullptr : v_cache;
-  ap.token_ids = token_ids;
-  ap.num_tokens = num_tokens;
+  ap.token_ids = const_cast<int32_t*>(token_ids);
+  ap.num_tokens = const_cast<int32_t*>(num_tokens);
   ap.out = out;
   ap.lse = lse;
   const size_t pairs = (size_t)cfg->batch * cfg->num_kv_heads;
   ap.part_o = static_cast<float*>(workspace);
   ap.part_ml = reinterpret_cast<float*>(static_cast<char*>(workspace) +
-                                        ((pairs * ap.cs * ap.d.G * ap.d.d_v * 4 + 255) & ~(size_t)255));
+                                        tls::a256(pairs * ap.cs * ap.d.G * ap.d.d_v * 4));
   cudaError_t e = tls::launch_attend(ap, st);
   if (e != cudaSuccess) return cuda_fail(e, "attend_kernel launch");
   return TLS_OK;
 }
 
-size_t attend_ws(const tls_config* cfg) {
+size_t attend_ws(const tls_config* cfg, int select) {
   tls::AttendParams ap;
-  if (plan_attend(cfg, ap) != TLS_OK) return (size_t)-1;
+  if (plan_attend(cfg, ap, select, 1) != TLS_OK) return (size_t)-1;
   return tls::attend_workspace_bytes(ap.d, ap.cs);
 }
 
@@ -308,10 +341,15 @@ tls_status tls_block_scores(const tls_config* cfg, const void* q, const int32_t*
   k1.d = dims_of(cfg);
   k1.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
   if (k1.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
+  k1.sstride = k1.d.M;
   k1.q = q;
   k1.seq_lens = seq_lens;
   k1.block_minmax = block_minmax;
   k1.scores = scores;
+  k1.done = nullptr;  // scores only: no ticket, no top-k_b, no histogram
+  k1.khist = nullptr;
+  k1.guide = nullptr;
+  k1.block_ids = nullptr;
   cudaError_t e = tls::launch_block_scores(k1, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "block_score_kernel launch");
   return TLS_OK;
@@ -320,8 +358,8 @@ tls_status tls_block_scores(const tls_config* cfg, const void* q, const int32_t*
 tls_status tls_select(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
                       const int32_t* guide_block_ids, int32_t* block_ids, int32_t* token_ids, int32_t* num_tokens,
                       float* token_scores, void* workspace, size_t workspace_bytes, tls_stream_t stream) {
-  return run_select(cfg, q, seq_lens, idx, guide_block_ids, block_ids, token_ids, num_tokens, token_scores,
-                    workspace, workspace_bytes, (cudaStream_t)stream);
+  return run_step(cfg, q, nullptr, nullptr, seq_lens, idx, guide_block_ids, block_ids, token_ids, num_tokens,
+                  token_scores, nullptr, nullptr, workspace, workspace_bytes, 0, (cudaStream_t)stream);
 }
 
 tls_status tls_sparse_attend(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
@@ -335,40 +373,25 @@ tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
                       const int32_t* seq_lens, const tls_index* idx, const int32_t* guide_block_ids,
                       int32_t* block_ids, int32_t* token_ids, int32_t* num_tokens, float* token_scores, void* out,
                       float* lse, void* workspace, size_t workspace_bytes, tls_stream_t stream) {
-  // validate everything before enqueuing anything
-  tls_status s = check_config(cfg);
-  if (s) return s;
-  if (!k_cache || !aligned16(k_cache)) return fail(TLS_ERR_INPUT, "k_cache must be a 16-byte aligned device pointer");
-  if (cfg->layout == TLS_GQA && (!v_cache || !aligned16(v_cache)))
-    return fail(TLS_ERR_INPUT, "GQA needs a 16-byte aligned v_cache");
-  if (!out) return fail(TLS_ERR_INPUT, "out is required");
-  const size_t wsel = tls::select_workspace_bytes(dims_of(cfg));
-  const size_t watt = attend_ws(cfg);
-  if (watt == (size_t)-1) return fail(TLS_ERR_UNSUPPORTED, "attention plan does not fit");
-  if (!workspace || workspace_bytes < wsel + watt || !aligned16(workspace))
-    return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes, 16-byte aligned (got %zu)", wsel + watt,
-                workspace_bytes);
-  s = run_select(cfg, q, seq_lens, idx, guide_block_ids, block_ids, token_ids, num_tokens, token_scores, workspace,
-                 wsel, (cudaStream_t)stream);
-  if (s) return s;
-  return run_attend(cfg, q, k_cache, v_cache, token_ids, num_tokens, out, lse, static_cast<char*>(workspace) + wsel,
-                    watt, (cudaStream_t)stream);
+  return run_step(cfg, q, k_cache, v_cache, seq_lens, idx, guide_block_ids, block_ids, token_ids, num_tokens,
+                  token_scores, out, lse, workspace, workspace_bytes, 1, (cudaStream_t)stream);
 }
 
 size_t tls_workspace_bytes(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK || which < 0 || which > 2) return (size_t)-1;
   const size_t wsel = tls::select_workspace_bytes(dims_of(cfg));
-  const size_t watt = attend_ws(cfg);
+  if (which == 0) return wsel;
+  const size_t watt = attend_ws(cfg, which == 2);
   if (watt == (size_t)-1) return (size_t)-1;
-  return which == 0 ? wsel : (which == 1 ? watt : wsel + watt);
+  return which == 1 ? watt : wsel + watt;
 }
 
 int32_t tls_launch_count(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK) return -1;
   switch (which) {
-    case 0: return 2;  // block_score_kernel + token_select_kernel
+    case 0: return 4;  // block_score, block_topk, token_cluster, attend_kernel (selection prologue only)
     case 1: return 1;  // attend_kernel
-    case 2: return 3;
+    case 2: return 4;  // the same four; the last one also attends
     case 3: return 1;  // build_index_kernel
     case 4: return 1;  // calibrate_kernel
     default: return -1;
@@ -377,12 +400,8 @@ int32_t tls_launch_count(const tls_config* cfg, int32_t which) {
 
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK || which < 0 || which > 2) return -1;
-  if (which == 1) {
-    tls::AttendParams ap;
-    return plan_attend(cfg, ap) == TLS_OK ? ap.cs : -1;
-  }
-  tls::SelectParams sp;
-  return plan_select(cfg, sp) == TLS_OK ? sp.cs : -1;
+  tls::AttendParams ap;
+  return plan_attend(cfg, ap, which != 1, which != 0) == TLS_OK ? ap.cs : -1;
 }
 
 const char* tls_status_string(tls_status status) {
@@ -399,8 +418,6 @@ const char* tls_status_string(tls_status status) {
 }
 
 const char* tls_last_error(void) { return g_err; }
-
-void tls_debug_phase_timing(unsigned long long* device_buffer) { g_dbg = device_buffer; }
 
 const char* tls_version(void) { return "tls-b200 0.1 (sm_100a)"; }
 

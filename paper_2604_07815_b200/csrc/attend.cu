@@ -9,9 +9,172 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "fasttopk.cuh"
 #include "params.h"
+#include "topk.cuh"
 
 namespace tls {
+
+// --------------------------------------------------------------------------
+// a4 prologue: S_t = top-k_t tokens from the ranking keys the
+// token kernels left in the workspace, ties -> lower token id (U2).  Every CTA
+// of the pair's cluster selects redundantly from identical keys; rank 0
+// writes token_ids / token_scores / num_tokens, and each CTA keeps its own
+// slice [t0, t1) of the selected ids in `sel`.  Returns K = |S_t|.
+// --------------------------------------------------------------------------
+static __device__ int select_tokens_prologue(const AttendParams& p, int pair, int b, unsigned rank, uint8_t* smem, int* sel,
+                                             TopKCtl& tk) {
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cs = p.cs;
+  const int n = min(max(p.seq_lens[b], 0), d.S);
+  const int m = (n + d.B - 1) >> d.log2B;
+  int* cblk = reinterpret_cast<int*>(smem + p.off_cblk);
+  uint32_t* skeys = reinterpret_cast<uint32_t*>(smem + p.off_skeys);
+  uint32_t* scratch = skeys + p.kb_eff * d.B;
+  uint32_t* shist = scratch + 2048;
+  FastTopKCtl& fk = *reinterpret_cast<FastTopKCtl*>(smem + p.off_fk);
+  __shared__ int s_kc, s_bsel, s_above, s_jtot;
+  // candidate blocks in the order the token kernels used (valid entries, in order)
+  const int* cand = p.cand + (size_t)pair * d.Kb;
+  {
+    const int per = (d.Kb + kThreads - 1) / kThreads;
+    const int lo = min(tid * per, d.Kb), hi = min(lo + per, d.Kb);
+    int cnt = 0;
+    for (int i = lo; i < hi; ++i) cnt += (cand[i] >= 0 && cand[i] < m);
+    int total;
+    int pos = block_exclusive_scan(cnt, tk.scan, &total);
+    for (int i = lo; i < hi; ++i)
+      if (cand[i] >= 0 && cand[i] < m && pos < p.kb_eff) cblk[pos++] = cand[i];
+    if (tid == 0) s_kc = min(total, p.kb_eff);
+  }
+  // keys of every candidate slot and the key histogram: two TMA bulk copies
+  __shared__ __align__(8) uint64_t kbar;
+  __syncthreads();
+  const int nslots = s_kc << d.log2B;
+  if (tid == 0) {
+    mbar_init(&kbar, 1);
+    mbar_fence_init();
+    mbar_arrive_expect_tx(&kbar, (uint32_t)(nslots * 4 + kKeyBins * 4));
+    tma_bulk_g2s(shist, p.khist + (size_t)pair * kKeyBins, kKeyBins * 4, &kbar);
+    if (nslots > 0) tma_bulk_g2s(skeys, p.keys + (size_t)pair * p.kb_eff * d.B, (uint32_t)(nslots * 4), &kbar);
+  }
+  __syncthreads();
+  mbar_wait(&kbar, 0);
+  // boundary bin of the histogram (bins ascend as keys descend): 4 bins per thread
+  int c4[4], sum = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    c4[j] = (int)shist[4 * tid + j];
+    sum += c4[j];
+  }
+  int jtot;
+  const int excl = block_exclusive_scan(sum, tk.scan, &jtot);  // jtot = number of valid candidates
+  const int K = min(d.Kt, jtot);
+  if (tid == 0) {
+    s_bsel = -1;
+    s_jtot = jtot;
+  }
+  __syncthreads();
+  if (K < jtot && excl < K && K <= excl + sum) {
+    int above = excl;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (above + c4[j] >= K) {
+        s_bsel = 4 * tid + j;
+        s_above = above;
+        break;
+      }
+      above += c4[j];
+    }
+  }
+  __syncthreads();
+  TopK t;
+  t.offset = 0;
+  t.total = K;
+  const int bsel = s_bsel;
+  bool need_full = false;
+  if (K >= jtot) {
+    t.thr = 0;  // take every valid candidate
+    t.eq_mode = false;
+    t.take_eq = 0;
+  } else {
+    // gather the keys of the boundary bin; the kr-th largest of them is the threshold
+    const int kr = K - s_above;
+    if (tid == 0) fk.bcount = 0;
+    __syncthreads();
+    for (int base = warp * 32; base < nslots; base += kThreads) {
+      const int i = base + lane;
+      const uint32_t k = i < nslots ? skeys[i] : 0u;
+      const bool in = k != 0u && key_bin(key2f(k)) == bsel;
+      const unsigned bal = __ballot_sync(0xffffffffu, in);
+      int off = 0;
+      if (lane == 0 && bal) off = atomicAdd(&fk.bcount, __popc(bal));
+      off = __shfl_sync(0xffffffffu, off, 0);
+      const int dst = off + __popc(bal & ((1u << lane) - 1u));
+      if (in && dst < 2048) scratch[dst] = k;
+    }
+    __syncthreads();
+    const int nbk = fk.bcount;
+    if (nbk <= 2048) {
+      uint32_t lo = 0xffffffffu, hi = 0u;
+      for (int i = tid; i < nbk; i += kThreads) {
+        lo = min(lo, scratch[i]);
+        hi = max(hi, scratch[i]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      if (lane == 0) {
+        fk.red_min[warp] = lo;
+        fk.red_max[warp] = hi;
+      }
+      __syncthreads();
+      lo = 0xffffffffu;
+      hi = 0u;
+      for (int w = 0; w < kWarps; ++w) {
+        lo = min(lo, fk.red_min[w]);
+        hi = max(hi, fk.red_max[w]);
+      }
+      __syncthreads();
+      range_select(scratch, nbk, lo, hi, kr, fk, tk);
+      const uint32_t thr = fk.thr;
+      int gt = 0;
+      for (int i = tid; i < nbk; i += kThreads) gt += scratch[i] > thr;
+      int dummy = 0;
+      block_sum2(gt, dummy, fk);
+      t.thr = thr;
+      t.eq_mode = true;
+      t.take_eq = kr - gt;
+    } else {
+      need_full = true;
+    }
+  }
+  if (need_full) t = fast_topk(skeys, nslots, K, false, fk, tk, scratch);
+  const int t0 = (int)((long long)K * rank / cs), t1 = (int)((long long)K * (rank + 1) / cs);
+  int* tout = p.token_ids + (size_t)pair * d.Kt;
+  float* sout = p.token_scores ? p.token_scores + (size_t)pair * d.Kt : nullptr;
+  const float lnG = logf((float)d.G);
+  topk_emit(skeys, nslots, t, tk, [&](int i, int pos) {
+    const int tok = (cblk[i >> d.log2B] << d.log2B) + (i & (d.B - 1));
+    if (rank == 0) {
+      tout[pos] = tok;
+      if (sout) sout[pos] = key2f(skeys[i]) * kLn2 - lnG;
+    }
+    if (pos >= t0 && pos < t1) sel[pos - t0] = tok;
+  });
+  if (rank == 0) {
+    for (int pos = K + tid; pos < d.Kt; pos += kThreads) {
+      tout[pos] = -1;
+      if (sout) sout[pos] = -CUDART_INF_F;
+    }
+    if (tid == 0) p.num_tokens[pair] = K;
+  }
+  __syncthreads();
+  return K;
+}
 
 // --------------------------------------------------------------------------
 // Phase E (generic CUDA-core path): partial attention of this CTA over its
@@ -271,19 +434,28 @@ __device__ void phase_merge(const AttendParams& p, int pair, int b, int g, unsig
 
 template <typename T, bool MMA, int D>
 __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_constant__ AttendParams p) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ TopKCtl tk;
   const int tid = threadIdx.x;
   const unsigned rank = blockIdx.x;
   const int cs = p.cs;
   const int pair = blockIdx.y;
   const int b = pair / p.d.Hkv, g = pair - b * p.d.Hkv;
-  const int K = min(min(max(p.num_tokens[pair], 0), p.d.Kt), p.tloc_max * cs);
+  int* sel = reinterpret_cast<int*>(smem + p.off_sel);
+  int K;
+  if (p.select) {
+    K = select_tokens_prologue(p, pair, b, rank, smem, sel, tk);
+    if (!p.attend) return;
+  } else {
+    K = min(min(max(p.num_tokens[pair], 0), p.d.Kt), p.tloc_max * cs);
+  }
   const int t0 = (int)((long long)K * rank / cs), t1 = (int)((long long)K * (rank + 1) / cs);
   const int tloc = t1 - t0;
-  int* sel = reinterpret_cast<int*>(smem + p.off_sel);
-  const int* ids = p.token_ids + (size_t)pair * p.d.Kt;
-  for (int i = tid; i < tloc; i += kThreads) sel[i] = ids[t0 + i];
-  __syncthreads();
+  if (!p.select) {
+    const int* ids = p.token_ids + (size_t)pair * p.d.Kt;
+    for (int i = tid; i < tloc; i += kThreads) sel[i] = ids[t0 + i];
+    __syncthreads();
+  }
   const int tot = p.d.G * p.d.d_v;
   float* po = p.part_o + ((size_t)pair * cs + rank) * tot;
   float* pml = p.part_ml + ((size_t)pair * cs + rank) * p.d.G * 2;
@@ -325,10 +497,15 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
   const int pair = blockIdx.y;
   const int b = pair;  // MLA: one KV head
   const int G = p.d.G;
-  const int K = min(min(max(p.num_tokens[pair], 0), p.d.Kt), p.tloc_max * cs);
-  const int t0 = (int)((long long)K * rank / cs), t1 = (int)((long long)K * (rank + 1) / cs);
-  const int tloc = t1 - t0;
   int* sel = reinterpret_cast<int*>(smem + p.off_sel);
+  __shared__ TopKCtl tk;
+  int K;
+  if (p.select) {
+    K = select_tokens_prologue(p, pair, b, rank, smem, sel, tk);
+    if (!p.attend) return;
+  } else {
+    K = min(min(max(p.num_tokens[pair], 0), p.d.Kt), p.tloc_max * cs);
+  }
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem + p.off_akv);
   __nv_bfloat16* sKV = sQ + MT * 16 * DK;           // 2 buffers of TC rows
   float* sS = reinterpret_cast<float*>(sKV + 2 * TC * DK);
@@ -336,8 +513,12 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
   float* sAlpha = reinterpret_cast<float*>(sP + MT * 16 * PST);
   float* sM = sAlpha + MT * 16;
   float* sL = sM + MT * 16;
-  const int* ids = p.token_ids + (size_t)pair * p.d.Kt;
-  for (int i = tid; i < tloc; i += kThreads) sel[i] = ids[t0 + i];
+  const int t0 = (int)((long long)K * rank / cs), t1 = (int)((long long)K * (rank + 1) / cs);
+  const int tloc = t1 - t0;
+  if (!p.select) {
+    const int* ids = p.token_ids + (size_t)pair * p.d.Kt;
+    for (int i = tid; i < tloc; i += kThreads) sel[i] = ids[t0 + i];
+  }
   const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + (size_t)b * p.d.Hq * DK;
   for (int i = tid; i < MT * 16 * CPR; i += kThreads) {
     const int row = i / CPR, ch = i - row * CPR;
@@ -544,6 +725,10 @@ static cudaError_t launch_mla(const AttendParams& p, cudaStream_t st) {
 }
 
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t st) {
+  if (!p.attend) {  // selection only: any instantiation runs just the prologue
+    if (p.d.bf16) return launch_k3<__nv_bfloat16, false, 0>(p, st);
+    return launch_k3<float, false, 0>(p, st);
+  }
   if (p.mma == 2) return p.d.G <= 16 ? launch_mla<1>(p, st) : launch_mla<2>(p, st);
   if (p.d.bf16) {
     if (p.mma) return p.d.d_k == 128 ? launch_k3<__nv_bfloat16, true, 128>(p, st)

@@ -278,3 +278,13 @@ __device__ __forceinline__ void tma_prefetch_l2(const void* src, uint32_t bytes)
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 }  // namespace tls
+
+namespace tls {
+// Fixed binning of a ranking key f = log2 alpha~ + log2 G <= log2 G < 6:
+// bin 0 holds the largest keys; bins are 1/16 log2 unit wide; monotone
+// non-increasing in f (the same fp32 ops everywhere it is evaluated).
+__device__ __forceinline__ int key_bin(float f) {
+  const float x = (6.0f - f) * 16.0f;
+  return x < 0.f ? 0 : (x >= 1023.f ? 1023 : (int)x);
+}
+}  // namespace tls

@@ -21,53 +21,69 @@ struct Dims {
   int mla;
   int bf16;
   int log2B;  // block_size is a power of two
+  int Ms;     // score row stride (floats): M rounded up to a multiple of 4 (16-byte rows)
 };
 
-struct ScoreParams {  // K1
+constexpr int kKeyBins = 1024;      // fixed binning of the ranking keys: 1/16 log2 unit below kKeyTop
+constexpr float kKeyTop = 6.0f;     // > log2(32) >= every key (key = log2 alpha~ + log2 G <= log2 G)
+
+struct ScoreParams {  // K1 (+ the pair's top-k_b in its last CTA)
   Dims d;
   int tb;  // block-summary rows per CTA (<= kScoreTileBytes)
+  int sstride;  // scores row stride (floats): Ms inside tls_select / tls_decode, M for tls_block_scores
+  int kb_eff;
   const void* q;
   const int* seq_lens;
   const void* block_minmax;
-  float* scores;  // workspace [pairs, M] fp32
+  float* scores;       // workspace [pairs, M] fp32
+  int* done;           // unused (NULL)
+  uint32_t* khist;     // workspace [pairs, kKeyBins] key histogram, zeroed here for K2 pass 2
+  const int* guide;    // lag mode: the pair's candidates are the guide (M_t is still reported)
+  int* block_ids;      // [pairs, Kb] out: M_t ascending, -1 padded
 };
 
-struct SelectParams {  // K2
+struct SelectParams {  // K2 (token_chunk_kernel, both passes)
   Dims d;
-  int cs;
   int kb_eff, kt_eff;  // min(Kb, M); min(Kt, kb_eff*B, S)
-  int rb;              // candidate blocks per ring stage
-  int ring_stage_bytes;
+  int cb;              // candidate blocks per chunk CTA
+  int nch;             // chunks per pair = ceil(kb_eff / cb)
   const void* q;
   const int* seq_lens;
-  const float* scores;
+  const float* scores;  // workspace [pairs, M] (K1)
   const uint8_t* codes;
   const float* scale_zero;
   const int* channels;
   const int* guide;
   int* block_ids;
-  int* token_ids;
-  int* num_tokens;
-  float* token_scores;
-  unsigned long long* dbg;  // diagnostics: per-CTA phase timestamps (NULL = off)
-  unsigned off_bkeys, off_cblk, off_qb, off_qsum, off_qc, off_ring, off_tkeys, smem_bytes;
+  float* stats;    // workspace [pairs, nch, 32, 2] per-chunk per-head (max, sum), log2 units
+  uint32_t* keys;  // workspace [pairs, kb_eff * B] ranking keys (0 = past the end)
+  uint32_t* khist; // workspace [pairs, kKeyBins] histogram of the keys (PASS 2 adds)
+  unsigned off_cblk, off_qb, off_qsum, off_qc, off_stage, smem_bytes;
 };
 
-struct AttendParams {  // K3
+struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally with the a4 prologue
   Dims d;
   int cs;
   int mma;       // 1: bf16 mma.sync GQA path (d in {64,128}, G <= 16); 2: bf16 mma.sync MLA path (576/512)
   int tloc_max;  // ceil(kt_eff / cs)
+  int select;    // 1: first select S_t = top-k_t from the keys (a4); 0: read token_ids / num_tokens
+  int attend;    // 1: attention (a5); 0: selection only (tls_select)
+  int kb_eff;
   const void* q;
   const void* k_cache;
   const void* v_cache;
-  const int* token_ids;
-  const int* num_tokens;
+  const int* seq_lens;  // select only
+  const int* cand;      // select only: candidate blocks (block_ids, or the lag-mode guide)
+  const uint32_t* keys;  // select only: workspace keys [pairs, kb_eff*B]
+  const uint32_t* khist; // select only: workspace key histogram [pairs, kKeyBins]
+  int* token_ids;
+  int* num_tokens;
+  float* token_scores;
   void* out;
   float* lse;
   float* part_o;   // workspace [pairs, cs, G, d_v] fp32 partial outputs
   float* part_ml;  // workspace [pairs, cs, G, 2] fp32 partial (max, sum), log2 units
-  unsigned off_sel, off_akv, off_aq, off_as, smem_bytes;
+  unsigned off_sel, off_cblk, off_union, off_skeys, off_fk, off_akv, off_aq, off_as, smem_bytes;
 };
 
 static inline unsigned align16(size_t x) { return (unsigned)((x + 15) & ~(size_t)15); }
@@ -85,12 +101,13 @@ static inline void plan_select(SelectParams& p) {
   const int nt0 = (d.G + 7) / 8, nt = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);  // instantiated NT
   const int ks = d.d_c / 16, nsplit = d.bf16 ? 1 : 3;
   const int per_block = d.B * (d.d_c / 2 + 8);
-  p.rb = (16 * 1024) / per_block;  // ~16 KB per ring stage
-  if (p.rb < 1) p.rb = 1;
-  p.ring_stage_bytes = (int)align16((size_t)p.rb * per_block);
+  // a pair's candidate blocks split over a cluster of nch <= 8 CTAs, ~24 KB (or more) of index each
+  p.cb = (24 * 1024) / per_block;
+  if (p.cb < 1) p.cb = 1;
+  if (p.cb * 8 < p.kb_eff) p.cb = (p.kb_eff + 7) / 8;
+  if (p.cb > p.kb_eff) p.cb = p.kb_eff;
+  p.nch = (p.kb_eff + p.cb - 1) / p.cb;
   size_t o = 0;
-  p.off_bkeys = (unsigned)o;
-  o = align16(o + (size_t)d.M * 4);
   p.off_cblk = (unsigned)o;
   o = align16(o + (size_t)p.kb_eff * 4);
   p.off_qb = (unsigned)o;
@@ -100,45 +117,77 @@ static inline void plan_select(SelectParams& p) {
   p.off_qc = (unsigned)o;
   o = align16(o + (size_t)nt * 8 * d.d_c * 4);
   o = (o + 127) & ~(size_t)127;
-  p.off_ring = (unsigned)o;
-  o = align16(o + (size_t)3 * p.ring_stage_bytes);
-  p.off_tkeys = (unsigned)o;  // keys of ALL candidate slots of the pair (rank 0 selects)
-  o = align16(o + (size_t)p.kb_eff * d.B * 4);
+  p.off_stage = (unsigned)o;  // staged index; in PASS 1 first the block keys + top-k scratch
+  const size_t stage = (size_t)p.cb * per_block;
+  const size_t sel = (size_t)((d.M + 31) & ~31) * 4 + 2048 * 4;
+  o = align16(o + (stage > sel ? stage : sel));
   p.smem_bytes = (unsigned)o;
 }
 
-static inline void plan_attend(AttendParams& p) {
+static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
   const Dims& d = p.d;
+  p.kb_eff = kb_effective(d);
   p.tloc_max = (kt_effective(d) + p.cs - 1) / p.cs;
   size_t o = 0;
   p.off_sel = (unsigned)o;
   o = align16(o + (size_t)(p.tloc_max + 1) * 4);
-  if (p.mma == 2) {  // MLA tensor-core path: Q, 2 latent-row chunks, S, P, alpha/m/l
-    const int mt16 = d.G <= 16 ? 16 : 32;
-    o = (o + 127) & ~(size_t)127;
-    p.off_akv = (unsigned)o;
-    o += (size_t)mt16 * d.d_k * 2 + (size_t)2 * kMlaChunkTokens * d.d_k * 2;
-    o += (size_t)mt16 * (kMlaChunkTokens + 4) * 4 + (size_t)mt16 * (kMlaChunkTokens + 8) * 2 + (size_t)3 * mt16 * 4;
-    o = align16(o);
-  } else if (p.mma) {
-    o = (o + 127) & ~(size_t)127;
-    p.off_akv = (unsigned)o;  // 2 stages x (K chunk + V chunk); reused as the warp-partial scratch
-    size_t kv = (size_t)2 * 2 * kAttnChunk * d.d_k * 2;
-    size_t scratch = (size_t)8 * d.G * (d.d_v + 4) * 4 + (size_t)8 * 16 * 2 * 4;
-    o = align16(o + (kv > scratch ? kv : scratch));
-  } else {
-    p.off_aq = (unsigned)o;
-    o = align16(o + (size_t)d.G * d.d_k * 4);
-    p.off_as = (unsigned)o;
-    o = align16(o + (size_t)d.G * p.tloc_max * 4);
+  p.off_cblk = (unsigned)o;
+  o = align16(o + (size_t)p.kb_eff * 4);
+  o = (o + 127) & ~(size_t)127;
+  p.off_union = (unsigned)o;
+  size_t sel_end = o, att_end = o;
+  if (p.select) {  // keys of every candidate slot + bracket scratch + top-k control block
+    size_t s2 = o;
+    p.off_skeys = (unsigned)s2;
+    s2 = align16(s2 + (size_t)p.kb_eff * d.B * 4 + 2048 * 4 + kKeyBins * 4);
+    p.off_fk = (unsigned)s2;
+    s2 = align16(s2 + fastctl_bytes);
+    sel_end = s2;
   }
-  p.smem_bytes = (unsigned)o;
+  if (p.attend) {
+    size_t s2 = o;
+    if (p.mma == 2) {  // MLA tensor-core path: Q, 2 latent-row chunks, S, P, alpha/m/l
+      const int mt16 = d.G <= 16 ? 16 : 32;
+      p.off_akv = (unsigned)s2;
+      s2 += (size_t)mt16 * d.d_k * 2 + (size_t)2 * kMlaChunkTokens * d.d_k * 2;
+      s2 += (size_t)mt16 * (kMlaChunkTokens + 4) * 4 + (size_t)mt16 * (kMlaChunkTokens + 8) * 2 + (size_t)3 * mt16 * 4;
+      s2 = align16(s2);
+    } else if (p.mma) {
+      p.off_akv = (unsigned)s2;  // 2 stages x (K chunk + V chunk); reused as the warp-partial scratch
+      size_t kv = (size_t)2 * 2 * kAttnChunk * d.d_k * 2;
+      size_t scratch = (size_t)8 * d.G * (d.d_v + 4) * 4 + (size_t)8 * 16 * 2 * 4;
+      s2 = align16(s2 + (kv > scratch ? kv : scratch));
+    } else {
+      p.off_aq = (unsigned)s2;
+      s2 = align16(s2 + (size_t)d.G * d.d_k * 4);
+      p.off_as = (unsigned)s2;
+      s2 = align16(s2 + (size_t)d.G * p.tloc_max * 4);
+    }
+    att_end = s2;
+  }
+  p.smem_bytes = (unsigned)(sel_end > att_end ? sel_end : att_end);
 }
 
-// Workspace of tls_select: K1's fp32 block scores.
-static inline size_t select_workspace_bytes(const Dims& d) {
-  return ((size_t)d.batch * d.Hkv * d.M * 4 + 255) & ~(size_t)255;
+static inline size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+// Workspace of tls_select: K1's fp32 block scores | chunk statistics | keys.
+struct SelectWs {
+  size_t scores, stats, keys, khist, done, total;
+};
+static inline SelectWs select_workspace(const Dims& d) {
+  SelectWs w;
+  SelectParams p;
+  p.d = d;
+  plan_select(p);
+  const size_t pairs = (size_t)d.batch * d.Hkv;
+  w.scores = 0;
+  w.stats = a256(pairs * d.Ms * 4);
+  w.keys = w.stats + a256(pairs * p.nch * 32 * 2 * 4);
+  w.khist = w.keys + a256(pairs * (size_t)p.kb_eff * d.B * 4);
+  w.done = w.khist + a256(pairs * kKeyBins * 4);
+  w.total = w.done + a256(pairs * 4);
+  return w;
 }
+static inline size_t select_workspace_bytes(const Dims& d) { return select_workspace(d).total; }
 // Workspace of tls_sparse_attend with cluster size cs: the CTA partials.
 static inline size_t attend_workspace_bytes(const Dims& d, int cs) {
   const size_t pairs = (size_t)d.batch * d.Hkv;

@@ -101,7 +101,7 @@ def test_workspace_and_plan(lib):
     assert lib.tls_workspace_bytes(ctypes.byref(c), 2) >= 2 * 2 * 64 * 4
     assert lib.tls_workspace_bytes(ctypes.byref(c), 1) > 0
     assert lib.tls_workspace_bytes(ctypes.byref(c), 2) == lib.tls_workspace_bytes(ctypes.byref(c), 0) + lib.tls_workspace_bytes(ctypes.byref(c), 1)
-    assert lib.tls_launch_count(ctypes.byref(c), 2) == 3
+    assert lib.tls_launch_count(ctypes.byref(c), 2) == 4
     cs = lib.tls_cluster_size(ctypes.byref(c), 2)
     assert cs in (1, 2, 4, 8, 16)
     # headline shapes plan without error

@@ -26,7 +26,9 @@ for cs in (args.cs.split(",") if args.cs else [""]):
     flush = lambda: flush_buf.fill_(1)  # noqa: E731
     st = torch.cuda.current_stream()
     sel = tls.select(cfg, queries[0], inputs["seq_lens"], idx)
+    sc_out = torch.empty((w.batch, w.num_kv_heads, cfg.num_blocks), dtype=torch.float32, device=dev)
     fns = {
+        "scores": lambda i: tls.block_scores(cfg, queries[i % 8], inputs["seq_lens"], idx, out=sc_out),
         "select": lambda i: tls.select(cfg, queries[i % 8], inputs["seq_lens"], idx, out=sel),
         "attend": lambda i: tls.sparse_attend(cfg, queries[i % 8], inputs["k_cache"], inputs["v_cache"], sel[1], sel[2]),
         "decode": lambda i: tls.decode(cfg, queries[i % 8], inputs["k_cache"], inputs["v_cache"], inputs["seq_lens"], idx),
