@@ -3,7 +3,7 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl tls|reference]
 
-One *step* = one fused tls_decode launch = the whole hot path (block scores,
+One *step* = one tls_decode call (4 launches) = the whole hot path (block scores,
 top-k_b, token scores, top-k_t, sparse attention) for every (batch, KV-head)
 pair of one synthetic decode batch, with the KV cache and index resident in
 HBM.  Default workload: configs[2] of BASELINE.json (Qwen3-32B shape, 96k
@@ -57,6 +57,25 @@ def algorithmic_bytes_per_pair(w) -> float:
     return m * 2 * w.d_k * s + cand * (w.d_c // 2 + 8) + kt * row + G * (w.d_k + w.d_v) * s
 
 
+def kernel_bytes_per_pair(w) -> dict:
+    """Algorithmic bytes per (batch, kv-head) pair of each launch of the step
+    (the terms of algorithmic_bytes_per_pair split by the kernel that moves
+    them; q is read by every kernel that uses it; intermediates -- scores,
+    ids, token keys -- are excluded as in SURVEY §8(d))."""
+    s = 2 if w.dtype == torch.bfloat16 else 4
+    G = w.num_q_heads // w.num_kv_heads
+    m = math.ceil(w.context / w.block_size)
+    kb = min(w.top_blocks, m)
+    cand = min(kb * w.block_size, w.context)
+    kt = min(w.top_tokens, cand)
+    row = w.d_k * s if w.layout == "mla" else (w.d_k + w.d_v) * s
+    q = G * w.d_k * s
+    return {"block_score_kernel": m * 2 * w.d_k * s + q,  # a1: block summaries
+            "block_topk_kernel": 0.0,  # a2: scores -> ids, intermediates only
+            "token_cluster_kernel": cand * (w.d_c // 2 + 8) + q,  # a3: INT4 codes + scale/zero
+            "attend_kernel": kt * row + q + G * w.d_v * s}  # a4+a5: selected rows, o
+
+
 def hbm_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -66,12 +85,12 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
-    `ncu --set full` capture (profiles/traffic.json), or None."""
+def ncu_traffic(workload: str, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed `ncu --set full` capture (profiles/traffic.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(workload)
+            return json.load(f).get(workload, {}).get(kernel)
     except Exception:
         return None
 
@@ -144,12 +163,14 @@ def build_state(w, seed, device, pattern):
     return cfg, inputs, idx, queries
 
 
-def time_steps(fn, steps, warmup, flush, stream):
+def time_steps(fn, steps, warmup, flush, stream, on_timed_start=None):
     """Device time of `steps` calls of fn(i), L2 flushed before each (not timed)."""
     for i in range(warmup):
         flush()
         fn(i)
     torch.cuda.synchronize()
+    if on_timed_start:
+        on_timed_start()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     for i in range(steps):
@@ -312,7 +333,11 @@ def run_tls(args, w, rank, world, local_rank):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t_wall0 = time.time()
-    times = time_steps(step, args.steps, args.warmup, flush, stream)
+    # live per-kernel durations: library events around each launch, on the launch stream
+    tls.timing_enable(args.steps + args.warmup)
+    times = time_steps(step, args.steps, args.warmup, flush, stream, on_timed_start=tls.timing_read)
+    kern_ms, kern_calls = tls.timing_read()
+    tls.timing_enable(0)
     t_wall1 = time.time()
     if world > 1:
         torch.distributed.barrier()
@@ -334,10 +359,12 @@ def run_tls(args, w, rank, world, local_rank):
 
     ms = sum(times) / len(times)
     ms_e2e = sum(e2e_times) / len(e2e_times)
+    kavg = [kern_ms[k] / max(1, kern_calls) for k in tls.KERNELS]
     if world > 1:
-        t = torch.tensor([ms, ms_e2e], device=dev)
+        t = torch.tensor([ms, ms_e2e] + kavg, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms, ms_e2e = float(t[0]), float(t[1])
+        kavg = [float(x) for x in t[2:]]
     if rank != 0:
         return
     tokens_per_step = w.batch * world  # one decode token per sequence, every rank
@@ -345,6 +372,14 @@ def run_tls(args, w, rank, world, local_rank):
     peak, peak_src = hbm_peak()
     achieved = bytes_step / (ms * 1e-3) / 1e9
     clk = clocks.summary(t_wall0, t_wall1)
+    pairs = w.batch * w.num_kv_heads
+    kbytes = kernel_bytes_per_pair(w)
+    kernels = {k: {"avg_us": kavg[i] * 1e3, "share": kavg[i] / ms,
+                   "algorithmic_bytes_per_launch": kbytes[k] * pairs,
+                   "gbs": kbytes[k] * pairs / (kavg[i] * 1e-3) / 1e9 if kavg[i] > 0 else None}
+               for i, k in enumerate(tls.KERNELS)}
+    dom = max(tls.KERNELS, key=lambda k: kernels[k]["avg_us"])
+    dom_ach = kernels[dom]["gbs"]
     line = {
         "metric": METRIC,
         "value": tokens_per_step / (ms * 1e-3),
@@ -369,9 +404,14 @@ def run_tls(args, w, rank, world, local_rank):
         },
         "us_per_step": ms * 1e3,
         "hbm_gbs": achieved,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(w.name), "peak_source": peak_src, "kernel": "tls_decode_kernel",
-                     "algorithmic_bytes_per_launch": bytes_step},
+        "roofline": {"bound": "hbm", "achieved": dom_ach, "peak": peak, "unit": "GB/s", "frac": dom_ach / peak,
+                     "traffic": ncu_traffic(w.name, dom), "peak_source": peak_src, "kernel": dom,
+                     "algorithmic_bytes_per_launch": kernels[dom]["algorithmic_bytes_per_launch"],
+                     "avg_launch_us": kernels[dom]["avg_us"],
+                     "timing": f"CUDA events around each launch on its stream, {kern_calls} timed steps"},
+        "step_roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                          "algorithmic_bytes_per_step": bytes_step},
+        "kernels": kernels,
         "e2e": {"value": tokens_per_step / (ms_e2e * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(queries[0].numel() * queries.element_size()),
                 "d2h_bytes_per_step": int(out.numel() * out.element_size() + lse.numel() * 4),

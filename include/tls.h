@@ -200,7 +200,8 @@ size_t tls_workspace_bytes(const tls_config* cfg, int32_t which);
 
 /* Number of kernel launches one call enqueues (which as above; 3 =
  * tls_build_index, 4 = tls_calibrate_channels), for launch accounting:
- * tls_select 2 (block scores, token select), tls_sparse_attend 1, tls_decode 3;
+ * tls_select 4 (block scores, block top-k, token scores, token top-k),
+ * tls_sparse_attend 1, tls_decode 4 (the last one also attends);
  * -1 for an invalid configuration. */
 int32_t tls_launch_count(const tls_config* cfg, int32_t which);
 
@@ -209,6 +210,24 @@ int32_t tls_launch_count(const tls_config* cfg, int32_t which);
  * -1 for an invalid configuration.  The environment variable TLS_CLUSTER
  * overrides the heuristic for both (1, 2, 4, 8 or 16). */
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which);
+
+/* Live per-kernel device timing (diagnostics; used by bench.py for the
+ * roofline of the dominant kernel).  While enabled, every tls_select /
+ * tls_decode call records library-owned CUDA events on its stream before and
+ * after each of its four launches (no extra synchronisation; events sit
+ * between launches that are already stream-ordered).  Slots: 0 =
+ * block_score_kernel (K1), 1 = block_topk_kernel (K1b), 2 =
+ * token_cluster_kernel (K2), 3 = attend kernel (K3: token top-k [+ sparse
+ * attention]).
+ *   tls_timing_enable(n): n > 0 enables and pre-creates events for n calls
+ *     (more are created on demand), clearing previous records; n == 0
+ *     disables and frees the events.
+ *   tls_timing_read(ms_sum[4], calls): synchronises the recorded events,
+ *     writes the summed milliseconds per slot and the number of calls
+ *     recorded, and clears the records (enable state unchanged).
+ * Process-global, not thread-safe: enable/read from one host thread. */
+tls_status tls_timing_enable(int32_t n_calls);
+tls_status tls_timing_read(double* ms_sum, int64_t* calls);
 
 const char* tls_status_string(tls_status status);
 const char* tls_last_error(void); /* thread-local detail of the last error */

@@ -15,6 +15,9 @@ from .ops import (  # noqa: F401
     decode,
     select,
     sparse_attend,
+    KERNELS,
+    timing_enable,
+    timing_read,
 )
 from ._lib import TLSError, load  # noqa: F401
 

@@ -6,6 +6,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <vector>
+
 #include <cuda_runtime.h>
 
 #include "../../include/tls.h"
@@ -102,6 +104,14 @@ tls::Dims dims_of(const tls_config* c) {
   return d;
 }
 
+// Diagnostics only: TLS_DEBUG_BUF=<hex device address> makes K2 and K3 write
+// per-CTA %globaltimer stamps there (K2 at [pair*8+chunk]*8, K3 at 65536*8 +
+// pair*8).  Unset in normal use.
+unsigned long long* env_debug_buf() {
+  const char* e = getenv("TLS_DEBUG_BUF");
+  return e ? reinterpret_cast<unsigned long long*>(strtoull(e, nullptr, 16)) : nullptr;
+}
+
 int env_cluster() {
   const char* env = getenv("TLS_CLUSTER");
   return (env && atoi(env) > 0) ? atoi(env) : 0;
@@ -110,6 +120,8 @@ int env_cluster() {
 tls_status plan_select(const tls_config* c, tls::SelectParams& p) {
   memset(&p, 0, sizeof(p));
   p.d = dims_of(c);
+  const char* cbe = getenv("TLS_CHUNK_BLOCKS");
+  p.cb_override = cbe ? atoi(cbe) : 0;
   tls::plan_select(p);
   if ((int)p.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "token-kernel shared-memory plan does not fit");
   return TLS_OK;
@@ -149,6 +161,27 @@ tls_status check_index(const tls_index* idx) {
     return fail(TLS_ERR_INPUT, "index buffers must be 16-byte aligned");
   return TLS_OK;
 }
+
+// ---- live per-kernel timing (tls_timing_enable / tls_timing_read) ----
+struct KernelTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // 5 per recorded call
+  size_t used = 0;              // events recorded so far
+  cudaEvent_t next() {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      ev.push_back(e);
+    }
+    return ev[used++];
+  }
+  void mark(cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e = next();
+    if (e) cudaEventRecord(e, st);
+  }
+};
+KernelTimer g_timer;
 
 // Enqueue the decode-step kernels: K1 block scores, K2 (two passes), then K3
 // (top-k_t prologue + attention when do_attend; selection only otherwise).
@@ -195,10 +228,14 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
   k1.khist = reinterpret_cast<uint32_t*>(ws + w.khist);
   k1.guide = guide;
   k1.block_ids = block_ids;
+  if (g_timer.on && g_timer.used % 5 != 0) g_timer.used -= g_timer.used % 5;  // drop a partial record
+  g_timer.mark(st);
   cudaError_t e = tls::launch_block_scores(k1, st);
   if (e != cudaSuccess) return cuda_fail(e, "block_score_kernel launch");
+  g_timer.mark(st);
   e = tls::launch_block_topk(k1, st);
   if (e != cudaSuccess) return cuda_fail(e, "block_topk_kernel launch");
+  g_timer.mark(st);
   sp.q = q;
   sp.seq_lens = seq_lens;
   sp.scores = k1.scores;
@@ -207,11 +244,12 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
   sp.channels = idx->channels;
   sp.guide = guide;
   sp.block_ids = block_ids;
-  sp.stats = reinterpret_cast<float*>(ws + w.stats);
   sp.keys = reinterpret_cast<uint32_t*>(ws + w.keys);
   sp.khist = k1.khist;
+  sp.dbg = env_debug_buf();
   e = tls::launch_token_cluster(sp, st);
   if (e != cudaSuccess) return cuda_fail(e, "token_cluster_kernel launch");
+  g_timer.mark(st);
   ap.q = q;
   ap.k_cache = k_cache;
   ap.v_cache = cfg->layout == TLS_MLA ? nullptr : v_cache;
@@ -219,6 +257,7 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
   ap.cand = guide ? guide : block_ids;
   ap.keys = sp.keys;
   ap.khist = sp.khist;
+  ap.dbg = sp.dbg ? sp.dbg + 65536 * 8 : nullptr;
   ap.token_ids = token_ids;
   ap.num_tokens = num_tokens;
   ap.token_scores = token_scores;
@@ -229,6 +268,7 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
   ap.part_ml = reinterpret_cast<float*>(ws + w.total + tls::a256(pairs * ap.cs * ap.d.G * ap.d.d_v * 4));
   e = tls::launch_attend(ap, st);
   if (e != cudaSuccess) return cuda_fail(e, "attend_kernel launch");
+  g_timer.mark(st);
   return TLS_OK;
 }
 
@@ -402,6 +442,46 @@ int32_t tls_cluster_size(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK || which < 0 || which > 2) return -1;
   tls::AttendParams ap;
   return plan_attend(cfg, ap, which != 1, which != 0) == TLS_OK ? ap.cs : -1;
+}
+
+tls_status tls_timing_enable(int32_t n_calls) {
+  if (n_calls < 0) return fail(TLS_ERR_INPUT, "n_calls must be >= 0");
+  g_timer.used = 0;
+  if (n_calls == 0) {
+    cudaDeviceSynchronize();
+    for (cudaEvent_t e : g_timer.ev) cudaEventDestroy(e);
+    g_timer.ev.clear();
+    g_timer.on = false;
+    return TLS_OK;
+  }
+  while (g_timer.ev.size() < (size_t)n_calls * 5) {
+    cudaEvent_t e;
+    cudaError_t err = cudaEventCreate(&e);
+    if (err != cudaSuccess) return cuda_fail(err, "cudaEventCreate");
+    g_timer.ev.push_back(e);
+  }
+  g_timer.on = true;
+  return TLS_OK;
+}
+
+tls_status tls_timing_read(double* ms_sum, int64_t* calls) {
+  if (!ms_sum || !calls) return fail(TLS_ERR_INPUT, "ms_sum and calls are required");
+  const size_t n = g_timer.used / 5;
+  for (int k = 0; k < 4; ++k) ms_sum[k] = 0.0;
+  for (size_t c = 0; c < n; ++c) {
+    for (int k = 0; k < 4; ++k) {
+      cudaEvent_t a = g_timer.ev[c * 5 + k], b = g_timer.ev[c * 5 + k + 1];
+      cudaError_t err = cudaEventSynchronize(b);
+      if (err != cudaSuccess) return cuda_fail(err, "cudaEventSynchronize");
+      float ms = 0.f;
+      err = cudaEventElapsedTime(&ms, a, b);
+      if (err != cudaSuccess) return cuda_fail(err, "cudaEventElapsedTime");
+      ms_sum[k] += ms;
+    }
+  }
+  *calls = (int64_t)n;
+  g_timer.used = 0;
+  return TLS_OK;
 }
 
 const char* tls_status_string(tls_status status) {

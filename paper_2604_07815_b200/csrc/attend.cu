@@ -35,6 +35,10 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
   uint32_t* shist = scratch + 2048;
   FastTopKCtl& fk = *reinterpret_cast<FastTopKCtl*>(smem + p.off_fk);
   __shared__ int s_kc, s_bsel, s_above, s_jtot;
+  unsigned long long* dbg = (p.dbg && rank == 0) ? p.dbg + (size_t)pair * 8 : nullptr;
+#define TLS_STAMP(i) \
+  if (dbg && tid == 0) dbg[i] = gtimer();
+  TLS_STAMP(0)
   // candidate blocks in the order the token kernels used (valid entries, in order)
   const int* cand = p.cand + (size_t)pair * d.Kb;
   {
@@ -61,6 +65,7 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
   }
   __syncthreads();
   mbar_wait(&kbar, 0);
+  TLS_STAMP(1)
   // boundary bin of the histogram (bins ascend as keys descend): 4 bins per thread
   int c4[4], sum = 0;
 #pragma unroll
@@ -89,82 +94,134 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
     }
   }
   __syncthreads();
+  TLS_STAMP(2)
   TopK t;
   t.offset = 0;
   t.total = K;
   const int bsel = s_bsel;
   bool need_full = false;
+  // per-warp segment counts for the one-pass emit (segments as in topk_emit)
+  __shared__ int wgt[kWarps], weq[kWarps];
+  const int seg = (((nslots + kWarps - 1) / kWarps) + 127) & ~127;  // as in topk_emit_counted
+  const int s0 = min(warp * seg, nslots), s1 = min(s0 + seg, nslots);
   if (K >= jtot) {
     t.thr = 0;  // take every valid candidate
     t.eq_mode = false;
     t.take_eq = 0;
+    int c = 0;
+    for (int base = s0; base < s1; base += 32) {
+      const int i = base + lane;
+      c += __popc(__ballot_sync(0xffffffffu, i < s1 && skeys[i] != 0u));
+    }
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (lane == 0) {
+      wgt[warp] = c;
+      weq[warp] = 0;
+    }
+    __syncthreads();
   } else {
-    // gather the keys of the boundary bin; the kr-th largest of them is the threshold
+    // One pass over the keys: count keys in bins above the boundary per warp
+    // segment, and gather the boundary bin's keys (with their segment).
     const int kr = K - s_above;
     if (tid == 0) fk.bcount = 0;
     __syncthreads();
-    for (int base = warp * 32; base < nslots; base += kThreads) {
-      const int i = base + lane;
-      const uint32_t k = i < nslots ? skeys[i] : 0u;
-      const bool in = k != 0u && key_bin(key2f(k)) == bsel;
-      const unsigned bal = __ballot_sync(0xffffffffu, in);
-      int off = 0;
-      if (lane == 0 && bal) off = atomicAdd(&fk.bcount, __popc(bal));
-      off = __shfl_sync(0xffffffffu, off, 0);
-      const int dst = off + __popc(bal & ((1u << lane) - 1u));
-      if (in && dst < 2048) scratch[dst] = k;
+    int above_w = 0;
+    for (int base = s0; base < s1; base += 128) {  // four independent 32-key groups per step
+      uint32_t k[4];
+      unsigned bal[4];
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + 32 * u + lane;
+        k[u] = i < s1 ? skeys[i] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int bn = k[u] != 0u ? key_bin(key2f(k[u])) : kKeyBins;
+        above_w += __popc(__ballot_sync(0xffffffffu, bn < bsel));
+        bal[u] = __ballot_sync(0xffffffffu, bn == bsel);
+        cnt += __popc(bal[u]);
+      }
+      if (cnt) {
+        int off = 0;
+        if (lane == 0) off = atomicAdd(&fk.bcount, cnt);
+        off = __shfl_sync(0xffffffffu, off, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int dst = off + __popc(bal[u] & ((1u << lane) - 1u));
+          if (((bal[u] >> lane) & 1u) && dst < 1024) {
+            scratch[dst] = k[u];
+            scratch[1024 + dst] = (uint32_t)warp;
+          }
+          off += __popc(bal[u]);
+        }
+      }
     }
     __syncthreads();
     const int nbk = fk.bcount;
-    if (nbk <= 2048) {
-      uint32_t lo = 0xffffffffu, hi = 0u;
+    if (nbk <= 1024) {
+      // exact threshold by rank: the kr-th largest boundary key
+      if (tid == 0) fk.thr = 0u;
+      __syncthreads();
       for (int i = tid; i < nbk; i += kThreads) {
-        lo = min(lo, scratch[i]);
-        hi = max(hi, scratch[i]);
+        const uint32_t v = scratch[i];
+        int gtc = 0, eqc = 0;
+        for (int j = 0; j < nbk; ++j) {
+          const uint32_t o = scratch[j];
+          gtc += o > v;
+          eqc += o == v;
+        }
+        if (gtc < kr && gtc + eqc >= kr) fk.thr = v;  // every writer writes the same value
+      }
+      __syncthreads();
+      const uint32_t thr = fk.thr;
+      // per-warp counts: keys above the boundary bin + boundary keys > thr / == thr
+      int gb = 0, eb = 0;
+      for (int i = lane; i < nbk; i += 32) {
+        if ((int)scratch[1024 + i] == warp) {
+          gb += scratch[i] > thr;
+          eb += scratch[i] == thr;
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        gb += __shfl_xor_sync(0xffffffffu, gb, o);
+        eb += __shfl_xor_sync(0xffffffffu, eb, o);
       }
       if (lane == 0) {
-        fk.red_min[warp] = lo;
-        fk.red_max[warp] = hi;
+        wgt[warp] = above_w + gb;
+        weq[warp] = eb;
       }
       __syncthreads();
-      lo = 0xffffffffu;
-      hi = 0u;
-      for (int w = 0; w < kWarps; ++w) {
-        lo = min(lo, fk.red_min[w]);
-        hi = max(hi, fk.red_max[w]);
-      }
-      __syncthreads();
-      range_select(scratch, nbk, lo, hi, kr, fk, tk);
-      const uint32_t thr = fk.thr;
-      int gt = 0;
-      for (int i = tid; i < nbk; i += kThreads) gt += scratch[i] > thr;
-      int dummy = 0;
-      block_sum2(gt, dummy, fk);
+      int gtot = 0;
+      for (int w = 0; w < kWarps; ++w) gtot += wgt[w];
       t.thr = thr;
       t.eq_mode = true;
-      t.take_eq = kr - gt;
+      t.take_eq = K - gtot;
     } else {
       need_full = true;
     }
   }
-  if (need_full) t = fast_topk(skeys, nslots, K, false, fk, tk, scratch);
+  if (need_full) {  // rare: an oversized boundary bin -> generic select and two-pass emit
+    t = fast_topk(skeys, nslots, K, false, fk, tk, scratch);
+  }
+  TLS_STAMP(3)
   const int t0 = (int)((long long)K * rank / cs), t1 = (int)((long long)K * (rank + 1) / cs);
   int* tout = p.token_ids + (size_t)pair * d.Kt;
   float* sout = p.token_scores ? p.token_scores + (size_t)pair * d.Kt : nullptr;
   const float lnG = logf((float)d.G);
-  topk_emit(skeys, nslots, t, tk, [&](int i, int pos) {
+  auto put = [&](int i, int pos) {
     const int tok = (cblk[i >> d.log2B] << d.log2B) + (i & (d.B - 1));
     if (rank == 0) {
       tout[pos] = tok;
       if (sout) sout[pos] = key2f(skeys[i]) * kLn2 - lnG;
     }
     if (pos >= t0 && pos < t1) sel[pos - t0] = tok;
-  });
+  };
+  if (need_full)
+    topk_emit(skeys, nslots, t, tk, put);
+  else
+    topk_emit_counted(skeys, nslots, t, wgt, weq, put);
   if (rank == 0) {
     for (int pos = K + tid; pos < d.Kt; pos += kThreads) {
       tout[pos] = -1;
@@ -173,6 +230,8 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
     if (tid == 0) p.num_tokens[pair] = K;
   }
   __syncthreads();
+  TLS_STAMP(4)
+#undef TLS_STAMP
   return K;
 }
 
@@ -465,6 +524,7 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_consta
     phase_attend_generic<T>(p, pair, b, g, sel, tloc, reinterpret_cast<float*>(smem + p.off_aq),
                             reinterpret_cast<float*>(smem + p.off_as), po, pml);
   }
+  if (p.dbg && rank == 0 && tid == 0) p.dbg[(size_t)pair * 8 + 5] = gtimer();
   if (MMA && cs == 1) return;  // the mma path wrote the output directly
   if (cs > 1) cluster_sync_all();  // release/acquire at cluster scope: partials visible in L2
   __syncthreads();

@@ -211,7 +211,24 @@ __device__ inline TopK fast_topk(const uint32_t* keys, int n, int K, bool take_a
       }
       __syncthreads();
       const int nb = c.bcount;
-      range_select(scratch, nb, loT, hiT, K - cgt, c, tk);
+      const int kr = K - cgt;
+      if (nb <= 1024) {  // exact threshold by rank: the kr-th largest bracketed key
+        if (tid == 0) c.thr = 0u;
+        __syncthreads();
+        for (int i = tid; i < nb; i += kThreads) {
+          const uint32_t v = scratch[i];
+          int gtc = 0, eqc = 0;
+          for (int j = 0; j < nb; ++j) {
+            const uint32_t o = scratch[j];
+            gtc += o > v;
+            eqc += o == v;
+          }
+          if (gtc < kr && gtc + eqc >= kr) c.thr = v;  // all writers write the same value
+        }
+        __syncthreads();
+      } else {
+        range_select(scratch, nb, loT, hiT, kr, c, tk);
+      }
       thr = c.thr;
       done = true;
     }

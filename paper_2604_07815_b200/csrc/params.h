@@ -42,10 +42,12 @@ struct ScoreParams {  // K1 (+ the pair's top-k_b in its last CTA)
   int* block_ids;      // [pairs, Kb] out: M_t ascending, -1 padded
 };
 
-struct SelectParams {  // K2 (token_chunk_kernel, both passes)
+struct SelectParams {  // K2 (token_reg_kernel, or token_cluster_kernel when a chunk exceeds the registers)
   Dims d;
   int kb_eff, kt_eff;  // min(Kb, M); min(Kt, kb_eff*B, S)
   int cb;              // candidate blocks per chunk CTA
+  int tpw;             // > 0: token_reg_kernel with tpw 16-token tiles per warp; 0: token_cluster_kernel
+  int cb_override;     // tuning: env TLS_CHUNK_BLOCKS (0 = heuristic)
   int nch;             // chunks per pair = ceil(kb_eff / cb)
   const void* q;
   const int* seq_lens;
@@ -55,10 +57,11 @@ struct SelectParams {  // K2 (token_chunk_kernel, both passes)
   const int* channels;
   const int* guide;
   int* block_ids;
-  float* stats;    // workspace [pairs, nch, 32, 2] per-chunk per-head (max, sum), log2 units
   uint32_t* keys;  // workspace [pairs, kb_eff * B] ranking keys (0 = past the end)
   uint32_t* khist; // workspace [pairs, kKeyBins] histogram of the keys (PASS 2 adds)
-  unsigned off_cblk, off_qb, off_qsum, off_qc, off_stage, smem_bytes;
+  unsigned long long* dbg;  // diagnostics only (env TLS_DEBUG_BUF): per-CTA phase stamps
+  int qtma;  // 1: the q rows of the pair arrive by TMA into smem (off_qrows)
+  unsigned off_cblk, off_qb, off_qsum, off_qc, off_qrows, off_stage, smem_bytes;
 };
 
 struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally with the a4 prologue
@@ -83,6 +86,7 @@ struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally wit
   float* lse;
   float* part_o;   // workspace [pairs, cs, G, d_v] fp32 partial outputs
   float* part_ml;  // workspace [pairs, cs, G, 2] fp32 partial (max, sum), log2 units
+  unsigned long long* dbg;  // diagnostics only (env TLS_DEBUG_BUF): per-CTA phase stamps
   unsigned off_sel, off_cblk, off_union, off_skeys, off_fk, off_akv, off_aq, off_as, smem_bytes;
 };
 
@@ -105,6 +109,15 @@ static inline void plan_select(SelectParams& p) {
   p.cb = (24 * 1024) / per_block;
   if (p.cb < 1) p.cb = 1;
   if (p.cb * 8 < p.kb_eff) p.cb = (p.kb_eff + 7) / 8;
+  // register-resident K2: a CTA holds at most 8 warps x tpw tiles x 16 tokens, in a cluster of <= 16
+  p.tpw = 8 / nt;
+  const int cb_reg = (8 * p.tpw * 16) / d.B;  // 8 warps (kThreads = 256)
+  if (cb_reg >= 1 && (p.kb_eff + cb_reg - 1) / cb_reg <= 16) {
+    if (p.cb > cb_reg) p.cb = cb_reg;
+  } else {
+    p.tpw = 0;
+  }
+  if (p.cb_override > 0 && (p.tpw == 0 || p.cb_override <= cb_reg)) p.cb = p.cb_override;  // tuning
   if (p.cb > p.kb_eff) p.cb = p.kb_eff;
   p.nch = (p.kb_eff + p.cb - 1) / p.cb;
   size_t o = 0;
@@ -116,11 +129,13 @@ static inline void plan_select(SelectParams& p) {
   o = align16(o + (size_t)nt * 8 * 4);
   p.off_qc = (unsigned)o;
   o = align16(o + (size_t)nt * 8 * d.d_c * 4);
+  const size_t qbytes = (size_t)d.G * d.d_k * (d.bf16 ? 2 : 4);
+  p.qtma = qbytes <= 16 * 1024;
+  p.off_qrows = (unsigned)o;
+  if (p.qtma) o = align16(o + qbytes + (size_t)d.d_c * 4);
   o = (o + 127) & ~(size_t)127;
-  p.off_stage = (unsigned)o;  // staged index; in PASS 1 first the block keys + top-k scratch
-  const size_t stage = (size_t)p.cb * per_block;
-  const size_t sel = (size_t)((d.M + 31) & ~31) * 4 + 2048 * 4;
-  o = align16(o + (stage > sel ? stage : sel));
+  p.off_stage = (unsigned)o;  // staged candidate index
+  o = align16(o + (size_t)p.cb * per_block);
   p.smem_bytes = (unsigned)o;
 }
 
@@ -175,16 +190,14 @@ struct SelectWs {
 };
 static inline SelectWs select_workspace(const Dims& d) {
   SelectWs w;
-  SelectParams p;
-  p.d = d;
-  plan_select(p);
   const size_t pairs = (size_t)d.batch * d.Hkv;
+  const size_t kb = (size_t)kb_effective(d);
   w.scores = 0;
   w.stats = a256(pairs * d.Ms * 4);
-  w.keys = w.stats + a256(pairs * p.nch * 32 * 2 * 4);
-  w.khist = w.keys + a256(pairs * (size_t)p.kb_eff * d.B * 4);
+  w.keys = w.stats;
+  w.khist = w.keys + a256(pairs * kb * d.B * 4);
   w.done = w.khist + a256(pairs * kKeyBins * 4);
-  w.total = w.done + a256(pairs * 4);
+  w.total = w.done;
   return w;
 }
 static inline size_t select_workspace_bytes(const Dims& d) { return select_workspace(d).total; }

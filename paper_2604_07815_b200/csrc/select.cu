@@ -77,6 +77,33 @@ __global__ void __launch_bounds__(kThreads, 4) block_score_kernel(const __grid_c
   __syncthreads();  // QQ ready, barriers initialised
   const int nchunk = rowbytes / 16;
   float* out = p.scores + (size_t)pair * p.sstride + i0;
+  if constexpr (CPL > 1) {  // wide rows (fp32, MLA): one row per warp step, rows w, w+8, ...
+    float qreg[CPL][EPC];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int ch = lane + 32 * c;
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) qreg[c][e] = ch < nchunk ? QQ[ch * EPC + e] : 0.f;
+    }
+    for (int r = warp; r < nb; r += kWarps) {
+      mbar_wait(&bars[r >> 3], 0);
+      const uint4* row = reinterpret_cast<const uint4*>(tile + (size_t)r * rowbytes);
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int ch = lane + 32 * c;
+        if (ch < nchunk) {
+          float f[EPC];
+          unpack16<T>(row[ch], f);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) acc = fmaf(qreg[c][e], f[e], acc);
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) out[r] = acc;
+    }
+    return;
+  }
   for (int gq = warp; gq < ngrp; gq += kWarps) {
     float qreg[CPL][EPC];
 #pragma unroll
@@ -266,6 +293,10 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
   const Dims& d = p.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q4 = lane & 3, r0 = lane >> 2;
   const int chunk = blockIdx.x, pair = blockIdx.y;
+  unsigned long long* dbg = p.dbg ? p.dbg + ((size_t)pair * 8 + chunk) * 8 : nullptr;
+#define TLS_STAMP(i) \
+  if (dbg && tid == 0) dbg[i] = gtimer();
+  TLS_STAMP(0)
   for (int i = tid; i < kKeyBins; i += kThreads) lhist[i] = 0u;
   const int b = pair / d.Hkv, g = pair - b * d.Hkv;
   const int n = min(max(p.seq_lens[b], 0), d.S);
@@ -276,11 +307,22 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
   float* qc = reinterpret_cast<float*>(smem + p.off_qc);
   uint8_t* stc = smem + p.off_stage;
   float2* stz = reinterpret_cast<float2*>(smem + p.off_stage + (size_t)p.cb * d.B * (d.d_c / 2));
+  __shared__ __align__(8) uint64_t qbar;
+  const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
+  T* qrows = reinterpret_cast<T*>(smem + p.off_qrows);
+  int* chan_s = reinterpret_cast<int*>(smem + p.off_qrows + (size_t)d.G * d.d_k * sizeof(T));
   if (tid == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&qbar, 1);
     mbar_fence_init();
+    if (p.qtma) {  // the pair's q rows and channel ids: two TMA bulk copies
+      const uint32_t qb_ = (uint32_t)(d.G * d.d_k * sizeof(T)), cb_ = (uint32_t)(d.d_c * 4);
+      mbar_arrive_expect_tx(&qbar, qb_ + cb_);
+      tma_bulk_g2s(qrows, qg, qb_, &qbar);
+      tma_bulk_g2s(chan_s, p.channels + (size_t)g * d.d_c, cb_, &qbar);
+    }
   }
-  if (tid < KS * 16) ctl.chan[tid] = p.channels[(size_t)g * d.d_c + tid];
+  if (!p.qtma && tid < KS * 16) ctl.chan[tid] = p.channels[(size_t)g * d.d_c + tid];
   const int* cand = p.guide ? p.guide + (size_t)pair * d.Kb : p.block_ids + (size_t)pair * d.Kb;
   // ---- candidate blocks (ascending): M_t from K1 (block_ids) or the lag-mode guide ----
   {
@@ -318,10 +360,17 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
   }
   // ---- channel-projected query q~, its B fragments and sum ----
   constexpr int DC = KS * 16;
-  const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
-  for (int i = tid; i < NT * 8 * DC; i += kThreads) {
-    const int h = i / DC, c = i - h * DC;
-    qc[i] = h < d.G ? to_f32<T>(qg[(size_t)h * d.d_k + ctl.chan[c]]) : 0.f;
+  if (p.qtma) {
+    mbar_wait(&qbar, 0);
+    for (int i = tid; i < NT * 8 * DC; i += kThreads) {
+      const int h = i / DC, c = i - h * DC;
+      qc[i] = h < d.G ? to_f32<T>(qrows[(size_t)h * d.d_k + chan_s[c]]) : 0.f;
+    }
+  } else {
+    for (int i = tid; i < NT * 8 * DC; i += kThreads) {
+      const int h = i / DC, c = i - h * DC;
+      qc[i] = h < d.G ? to_f32<T>(qg[(size_t)h * d.d_k + ctl.chan[c]]) : 0.f;
+    }
   }
   __syncthreads();
   constexpr int WPT = KS / 2;
@@ -339,7 +388,9 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
     qsum[tid] = s;
   }
   __syncthreads();
+  TLS_STAMP(1)
   if (nbl > 0) mbar_wait(&bar, 0);
+  TLS_STAMP(2)
   const float sm2 = d.sm_scale * kLog2e;
   float sq[NT][2];
 #pragma unroll
@@ -354,28 +405,35 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
     float rm[NT][2], rs[NT][2];
 #pragma unroll
     for (int i = 0; i < NT; ++i) rm[i][0] = rm[i][1] = -CUDART_INF_F, rs[i][0] = rs[i][1] = 0.f;
-    for (int tile = warp; tile < ntiles; tile += kWarps) {
-      float acc[NT][4];
-      token_tile_mma<KS, NT, NSPLIT>(stc + (size_t)tile * 16 * rowbytes, qb2, acc);
-      const int blk = cblk[cb0 + (tile >> tshift)];
-      const int tok0 = (blk << d.log2B) + ((tile & ((1 << tshift) - 1)) << 4) + r0;
-      const bool v0 = tok0 < n, v1 = tok0 + 8 < n;
-      const float2 z0 = zal ? stz[tile * 16 + r0] : (v0 ? __ldg(zglob + tok0) : make_float2(0.f, 0.f));
-      const float2 z1 = zal ? stz[tile * 16 + r0 + 8] : (v1 ? __ldg(zglob + tok0 + 8) : make_float2(0.f, 0.f));
-      const float s0 = sm2 * z0.x, s1 = sm2 * z1.x;
+    for (int tp = warp * 2; tp < ntiles; tp += kWarps * 2) {  // two independent tiles per step
+      float acc[2][NT][4];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+      for (int u = 0; u < 2; ++u)
+        if (tp + u < ntiles) token_tile_mma<KS, NT, NSPLIT>(stc + (size_t)(tp + u) * 16 * rowbytes, qb2, acc[u]);
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const float l0 = v0 ? fmaf(s0, acc[nt][e], z0.y * sq[nt][e]) : -CUDART_INF_F;
-          const float l1 = v1 ? fmaf(s1, acc[nt][2 + e], z1.y * sq[nt][e]) : -CUDART_INF_F;
-          const float mt = fmaxf(l0, l1);
-          if (mt > rm[nt][e]) {  // rescale only when the running max grows
-            rs[nt][e] *= fexp2(rm[nt][e] - mt);
-            rm[nt][e] = mt;
+      for (int u = 0; u < 2; ++u) {
+        const int tile = tp + u;
+        if (tile >= ntiles) break;
+        const int blk = cblk[cb0 + (tile >> tshift)];
+        const int tok0 = (blk << d.log2B) + ((tile & ((1 << tshift) - 1)) << 4) + r0;
+        const bool v0 = tok0 < n, v1 = tok0 + 8 < n;
+        const float2 z0 = zal ? stz[tile * 16 + r0] : (v0 ? __ldg(zglob + tok0) : make_float2(0.f, 0.f));
+        const float2 z1 = zal ? stz[tile * 16 + r0 + 8] : (v1 ? __ldg(zglob + tok0 + 8) : make_float2(0.f, 0.f));
+        const float s0 = sm2 * z0.x, s1 = sm2 * z1.x;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float l0 = v0 ? fmaf(s0, acc[u][nt][e], z0.y * sq[nt][e]) : -CUDART_INF_F;
+            const float l1 = v1 ? fmaf(s1, acc[u][nt][2 + e], z1.y * sq[nt][e]) : -CUDART_INF_F;
+            const float mt = fmaxf(l0, l1);
+            if (mt > rm[nt][e]) {  // rescale only when the running max grows
+              rs[nt][e] *= fexp2(rm[nt][e] - mt);
+              rm[nt][e] = mt;
+            }
+            if (mt != -CUDART_INF_F) rs[nt][e] += fexp2(l0 - rm[nt][e]) + fexp2(l1 - rm[nt][e]);
           }
-          if (mt != -CUDART_INF_F) rs[nt][e] += fexp2(l0 - rm[nt][e]) + fexp2(l1 - rm[nt][e]);
-        }
+      }
     }
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -405,7 +463,9 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
     }
   }
   // ---- merge the nch chunks' statistics of the pair through DSMEM, in chunk order ----
+  TLS_STAMP(3)
   cluster_sync_all();
+  TLS_STAMP(4)
   if (tid < d.G) {
     float M = -CUDART_INF_F, Z = 0.f;
     for (int rr = 0; rr < (int)gridDim.x; ++rr) stat_merge(M, Z, *dsmem(&s_hm[tid], rr), *dsmem(&s_hz[tid], rr));
@@ -423,49 +483,66 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
         lz[nt][e] = h < d.G ? ctl.hlz[h] : CUDART_INF_F;  // padded heads: exp2(-inf) = 0
       }
     uint32_t* kout = p.keys + (size_t)pair * p.kb_eff * d.B + ((size_t)cb0 << d.log2B);
-    for (int tile = warp; tile < ntiles; tile += kWarps) {
-      float acc[NT][4];
-      token_tile_mma<KS, NT, NSPLIT>(stc + (size_t)tile * 16 * rowbytes, qb2, acc);
-      const int blk = cblk[cb0 + (tile >> tshift)];
-      const int tok0 = (blk << d.log2B) + ((tile & ((1 << tshift) - 1)) << 4) + r0;
-      const bool v0 = tok0 < n, v1 = tok0 + 8 < n;
-      const float2 z0 = zal ? stz[tile * 16 + r0] : (v0 ? __ldg(zglob + tok0) : make_float2(0.f, 0.f));
-      const float2 z1 = zal ? stz[tile * 16 + r0 + 8] : (v1 ? __ldg(zglob + tok0 + 8) : make_float2(0.f, 0.f));
-      const float s0 = sm2 * z0.x, s1 = sm2 * z1.x;
-      float t0[NT][2], t1[NT][2];
-      float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+    for (int tp = warp * 2; tp < ntiles; tp += kWarps * 2) {  // two independent tiles per step
+      float acc[2][NT][4];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+      for (int u = 0; u < 2; ++u)
+        if (tp + u < ntiles) token_tile_mma<KS, NT, NSPLIT>(stc + (size_t)(tp + u) * 16 * rowbytes, qb2, acc[u]);
+      float mx[2][2], es[2][2];
+      bool vv[2][2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          t0[nt][e] = fmaf(s0, acc[nt][e], fmaf(z0.y, sq[nt][e], -lz[nt][e]));
-          t1[nt][e] = fmaf(s1, acc[nt][2 + e], fmaf(z1.y, sq[nt][e], -lz[nt][e]));
-          mx0 = fmaxf(mx0, t0[nt][e]);
-          mx1 = fmaxf(mx1, t1[nt][e]);
+      for (int u = 0; u < 2; ++u) {
+        const int tile = min(tp + u, ntiles - 1);
+        const int blk = cblk[cb0 + (tile >> tshift)];
+        const int tok0 = (blk << d.log2B) + ((tile & ((1 << tshift) - 1)) << 4) + r0;
+        vv[u][0] = tp + u < ntiles && tok0 < n;
+        vv[u][1] = tp + u < ntiles && tok0 + 8 < n;
+        const float2 z0 = zal ? stz[tile * 16 + r0] : (vv[u][0] ? __ldg(zglob + tok0) : make_float2(0.f, 0.f));
+        const float2 z1 = zal ? stz[tile * 16 + r0 + 8] : (vv[u][1] ? __ldg(zglob + tok0 + 8) : make_float2(0.f, 0.f));
+        const float s0 = sm2 * z0.x, s1 = sm2 * z1.x;
+        float t0[NT][2], t1[NT][2];
+        float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            t0[nt][e] = fmaf(s0, acc[u][nt][e], fmaf(z0.y, sq[nt][e], -lz[nt][e]));
+            t1[nt][e] = fmaf(s1, acc[u][nt][2 + e], fmaf(z1.y, sq[nt][e], -lz[nt][e]));
+            m0 = fmaxf(m0, t0[nt][e]);
+            m1 = fmaxf(m1, t1[nt][e]);
+          }
+        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
+        m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+        m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
+        float e0 = 0.f, e1 = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            e0 += fexp2(t0[nt][e] - m0);
+            e1 += fexp2(t1[nt][e] - m1);
+          }
+        e0 += __shfl_xor_sync(0xffffffffu, e0, 1);
+        e0 += __shfl_xor_sync(0xffffffffu, e0, 2);
+        e1 += __shfl_xor_sync(0xffffffffu, e1, 1);
+        e1 += __shfl_xor_sync(0xffffffffu, e1, 2);
+        mx[u][0] = m0;
+        mx[u][1] = m1;
+        es[u][0] = e0;
+        es[u][1] = e1;
+      }
+      // lane q4 = 0 finishes row r0, lane q4 = 1 row r0 + 8 (of both tiles)
+      if (q4 < 2) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (tp + u >= ntiles) break;
+          const int j = (tp + u) * 16 + r0 + 8 * q4;
+          const bool v = q4 == 0 ? vv[u][0] : vv[u][1];
+          const float kf = (q4 == 0 ? mx[u][0] : mx[u][1]) + flog2(q4 == 0 ? es[u][0] : es[u][1]);
+          kout[j] = v ? f2key(kf) : 0u;
+          if (v) atomicAdd(&lhist[key_bin(kf)], 1u);
         }
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-      float e0 = 0.f, e1 = 0.f;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          e0 += fexp2(t0[nt][e] - mx0);
-          e1 += fexp2(t1[nt][e] - mx1);
-        }
-      e0 += __shfl_xor_sync(0xffffffffu, e0, 1);
-      e0 += __shfl_xor_sync(0xffffffffu, e0, 2);
-      e1 += __shfl_xor_sync(0xffffffffu, e1, 1);
-      e1 += __shfl_xor_sync(0xffffffffu, e1, 2);
-      if (q4 == 0) {
-        const int j0 = tile * 16 + r0;
-        const float k0 = mx0 + flog2(e0), k1 = mx1 + flog2(e1);
-        kout[j0] = v0 ? f2key(k0) : 0u;
-        kout[j0 + 8] = v1 ? f2key(k1) : 0u;
-        if (v0) atomicAdd(&lhist[key_bin(k0)], 1u);
-        if (v1) atomicAdd(&lhist[key_bin(k1)], 1u);
       }
     }
     __syncthreads();
@@ -473,7 +550,305 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
     for (int i = tid; i < kKeyBins; i += kThreads)
       if (lhist[i]) atomicAdd(&gh[i], lhist[i]);
   }
+  TLS_STAMP(5)
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");  // keep smem alive for remote readers
+  TLS_STAMP(6)
+#undef TLS_STAMP
+}
+
+// ----------------------------------------------------------------------------
+// K2, register-resident form (used whenever a CTA's tiles fit: <= TPW 16-token
+// tiles per warp, TPW = 8 / NT).  Same arithmetic contract as
+// token_cluster_kernel, one tensor-core pass instead of two:
+//   pass 1: L_hj for every staged tile (token_tile_mma, once); per-warp head
+//           max m_h^w; E_hj = exp2(L_hj - m_h^w) kept in registers; per-warp
+//           sums -> CTA -> cluster (DSMEM, chunk order) -> lz_h = M_h + log2 Z_h.
+//   pass 2: sum_h exp2(L_hj - lz_h) = sum_h E_hj * c_h^w with the per-(warp,
+//           head) factor c_h^w = exp2(m_h^w - lz_h) (scaled by 2^kKeyOff so
+//           that alpha~ down to ~2^-126 per head stays representable), reduced
+//           over the four lanes that hold a token's heads with a transposed
+//           butterfly (3 shuffles per 4 tokens); every lane emits one key.
+// Reading U20: a head's term below 2^-126 of the warp's largest
+// term for that head flushes to 0 (fp32 range); only tokens with alpha~ below
+// ~2^-126 are affected.
+constexpr float kKeyOff = 64.f;
+
+template <typename T, int KS, int NT, int NSPLIT, int TPW>
+__global__ void __launch_bounds__(kThreads, 3) token_reg_kernel(const __grid_constant__ SelectParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ SelCtl ctl;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t qbar;
+  __shared__ uint32_t lhist[kKeyBins];
+  __shared__ float s_hm[32], s_hz[32];
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q4 = lane & 3, r0 = lane >> 2;
+  const int chunk = blockIdx.x, pair = blockIdx.y;
+  unsigned long long* dbg = p.dbg && chunk < 8 ? p.dbg + ((size_t)pair * 8 + chunk) * 8 : nullptr;
+#define TLS_STAMP(i) \
+  if (dbg && tid == 0) dbg[i] = gtimer();
+  TLS_STAMP(0)
+  for (int i = tid; i < kKeyBins; i += kThreads) lhist[i] = 0u;
+  const int b = pair / d.Hkv, g = pair - b * d.Hkv;
+  const int n = min(max(p.seq_lens[b], 0), d.S);
+  const int m = (n + d.B - 1) >> d.log2B;
+  int* cblk = reinterpret_cast<int*>(smem + p.off_cblk);
+  uint32_t* qb = reinterpret_cast<uint32_t*>(smem + p.off_qb);
+  float* qsum = reinterpret_cast<float*>(smem + p.off_qsum);
+  float* qc = reinterpret_cast<float*>(smem + p.off_qc);
+  uint8_t* stc = smem + p.off_stage;
+  float2* stz = reinterpret_cast<float2*>(smem + p.off_stage + (size_t)p.cb * d.B * (d.d_c / 2));
+  const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
+  T* qrows = reinterpret_cast<T*>(smem + p.off_qrows);
+  int* chan_s = reinterpret_cast<int*>(smem + p.off_qrows + (size_t)d.G * d.d_k * sizeof(T));
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&qbar, 1);
+    mbar_fence_init();
+    if (p.qtma) {
+      const uint32_t qb_ = (uint32_t)(d.G * d.d_k * sizeof(T)), cb_ = (uint32_t)(d.d_c * 4);
+      mbar_arrive_expect_tx(&qbar, qb_ + cb_);
+      tma_bulk_g2s(qrows, qg, qb_, &qbar);
+      tma_bulk_g2s(chan_s, p.channels + (size_t)g * d.d_c, cb_, &qbar);
+    }
+  }
+  __syncthreads();  // mbarriers initialised before any wait / copy issue
+  if (!p.qtma && tid < KS * 16) ctl.chan[tid] = p.channels[(size_t)g * d.d_c + tid];
+  const int rowbytes = d.d_c / 2;
+  const uint8_t* cbase = p.codes + (size_t)pair * d.S * rowbytes;
+  const float2* zbase = reinterpret_cast<const float2*>(p.scale_zero) + (size_t)pair * d.S;
+  const bool zal = (((size_t)pair * d.S) & 1) == 0;
+  const int cb0 = chunk * p.cb;
+  int nbl;
+  if (p.guide == nullptr) {
+    // K1b's M_t is already compact: min(kb_eff, m) ascending valid ids, -1 padded.
+    // Warp 0 reads this chunk's ids and issues the TMA copies straight away.
+    const int kc = min(p.kb_eff, m);
+    nbl = max(0, min(p.cb, kc - cb0));
+    if (warp == 0 && nbl > 0) {
+      const int* cand = p.block_ids + (size_t)pair * d.Kb + cb0;
+      uint32_t bytes = 0;
+      for (int k = lane; k < nbl; k += 32) {
+        const int blk = cand[k];
+        cblk[cb0 + k] = blk;
+        const int rows = min(d.B, d.S - blk * d.B);
+        bytes += rows * rowbytes + (zal ? rows * 8 : 0);
+      }
+      bytes = warp_sum_u32(bytes);
+      if (lane == 0) mbar_arrive_expect_tx(&bar, bytes);
+      __syncwarp();
+      for (int k = lane; k < nbl; k += 32) {
+        const int blk = cblk[cb0 + k];
+        const int rows = min(d.B, d.S - blk * d.B);
+        tma_bulk_g2s(stc + (size_t)k * d.B * rowbytes, cbase + (size_t)blk * d.B * rowbytes, rows * rowbytes, &bar);
+        if (zal) tma_bulk_g2s(stz + k * d.B, zbase + (size_t)blk * d.B, rows * 8, &bar);
+      }
+    }
+  } else {  // lag mode: the guide may hold ids past this step's m or -1: compact it first
+    const int* cand = p.guide + (size_t)pair * d.Kb;
+    const int per = (d.Kb + kThreads - 1) / kThreads;
+    const int lo = min(tid * per, d.Kb), hi = min(lo + per, d.Kb);
+    int cnt = 0;
+    for (int i = lo; i < hi; ++i) cnt += (cand[i] >= 0 && cand[i] < m);
+    int total;
+    int pos = block_exclusive_scan(cnt, ctl.tk.scan, &total);
+    for (int i = lo; i < hi; ++i)
+      if (cand[i] >= 0 && cand[i] < m && pos < p.kb_eff) cblk[pos++] = cand[i];
+    __syncthreads();
+    const int kc = min(total, p.kb_eff);
+    nbl = max(0, min(p.cb, kc - cb0));
+    if (warp == 0 && nbl > 0) {
+      uint32_t bytes = 0;
+      for (int k = lane; k < nbl; k += 32) {
+        const int rows = min(d.B, d.S - cblk[cb0 + k] * d.B);
+        bytes += rows * rowbytes + (zal ? rows * 8 : 0);
+      }
+      bytes = warp_sum_u32(bytes);
+      if (lane == 0) mbar_arrive_expect_tx(&bar, bytes);
+      __syncwarp();
+      for (int k = lane; k < nbl; k += 32) {
+        const int blk = cblk[cb0 + k];
+        const int rows = min(d.B, d.S - blk * d.B);
+        tma_bulk_g2s(stc + (size_t)k * d.B * rowbytes, cbase + (size_t)blk * d.B * rowbytes, rows * rowbytes, &bar);
+        if (zal) tma_bulk_g2s(stz + k * d.B, zbase + (size_t)blk * d.B, rows * 8, &bar);
+      }
+    }
+  }
+  // channel-projected query q~, its B fragments and sum
+  constexpr int DC = KS * 16;
+  if (p.qtma) {
+    mbar_wait(&qbar, 0);
+    for (int i = tid; i < NT * 8 * DC; i += kThreads) {
+      const int h = i / DC, c = i - h * DC;
+      qc[i] = h < d.G ? to_f32<T>(qrows[(size_t)h * d.d_k + chan_s[c]]) : 0.f;
+    }
+  } else {
+    for (int i = tid; i < NT * 8 * DC; i += kThreads) {
+      const int h = i / DC, c = i - h * DC;
+      qc[i] = h < d.G ? to_f32<T>(qg[(size_t)h * d.d_k + ctl.chan[c]]) : 0.f;
+    }
+  }
+  __syncthreads();
+  constexpr int WPT = KS / 2;
+  for (int idx = tid; idx < NSPLIT * NT * KS * 32; idx += kThreads) {
+    const int ln = idx & 31, rest = idx >> 5;
+    const int s = rest % KS, nt = (rest / KS) % NT, sp = rest / (KS * NT);
+    const float* qh = qc + (nt * 8 + (ln >> 2)) * DC;
+    const int cb = 8 * ((ln & 3) * WPT + (s >> 1)) + 2 * (s & 1);
+    qb[2 * idx] = pack_bf16x2(split_piece(qh[cb], sp), split_piece(qh[cb + 4], sp));
+    qb[2 * idx + 1] = pack_bf16x2(split_piece(qh[cb + 1], sp), split_piece(qh[cb + 5], sp));
+  }
+  if (tid < NT * 8) {
+    float s = 0.f;
+    for (int c = 0; c < DC; ++c) s += qc[tid * DC + c];
+    qsum[tid] = s;
+  }
+  __syncthreads();
+  TLS_STAMP(1)
+  if (nbl > 0) mbar_wait(&bar, 0);
+  TLS_STAMP(2)
+  const float sm2 = d.sm_scale * kLog2e;
+  float sq[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) sq[nt][e] = sm2 * qsum[nt * 8 + 2 * q4 + e];
+  const uint2* qb2 = reinterpret_cast<const uint2*>(qb);
+  const int tshift = d.log2B - 4;
+  const int ntiles = nbl << tshift;
+  // ---- pass 1: logits of every tile (tile = warp + t * kWarps), per-warp head max ----
+  float ev[TPW][NT][4];
+  float hm[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) hm[nt][0] = hm[nt][1] = -CUDART_INF_F;
+#pragma unroll
+  for (int t = 0; t < TPW; ++t) {
+    const int tile = warp + t * kWarps;
+    if (tile < ntiles) {
+      float acc[NT][4];
+      token_tile_mma<KS, NT, NSPLIT>(stc + (size_t)tile * 16 * rowbytes, qb2, acc);
+      const int blk = cblk[cb0 + (tile >> tshift)];
+      const int tok0 = (blk << d.log2B) + ((tile & ((1 << tshift) - 1)) << 4) + r0;
+      const bool v0 = tok0 < n, v1 = tok0 + 8 < n;
+      const float2 z0 = zal ? stz[tile * 16 + r0] : (v0 ? __ldg(zbase + tok0) : make_float2(0.f, 0.f));
+      const float2 z1 = zal ? stz[tile * 16 + r0 + 8] : (v1 ? __ldg(zbase + tok0 + 8) : make_float2(0.f, 0.f));
+      const float s0 = sm2 * z0.x, s1 = sm2 * z1.x;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          ev[t][nt][e] = v0 ? fmaf(s0, acc[nt][e], z0.y * sq[nt][e]) : -CUDART_INF_F;
+          ev[t][nt][2 + e] = v1 ? fmaf(s1, acc[nt][2 + e], z1.y * sq[nt][e]) : -CUDART_INF_F;
+          hm[nt][e] = fmaxf(hm[nt][e], fmaxf(ev[t][nt][e], ev[t][nt][2 + e]));
+        }
+    } else {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ev[t][nt][e] = -CUDART_INF_F;
+    }
+  }
+  float hs[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) hm[nt][e] = fmaxf(hm[nt][e], __shfl_xor_sync(0xffffffffu, hm[nt][e], o));
+      const float mref = hm[nt][e] == -CUDART_INF_F ? 0.f : hm[nt][e];
+      float s = 0.f;
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) {
+        ev[t][nt][e] = fexp2(ev[t][nt][e] - mref);
+        ev[t][nt][2 + e] = fexp2(ev[t][nt][2 + e] - mref);
+        s += ev[t][nt][e] + ev[t][nt][2 + e];
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      hs[nt][e] = s;
+    }
+  if (r0 == 0) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        ctl.wm[warp][nt * 8 + 2 * q4 + e] = hm[nt][e];
+        ctl.ws[warp][nt * 8 + 2 * q4 + e] = hs[nt][e];
+      }
+  }
+  __syncthreads();
+  if (tid < d.G) {  // warps merged in a fixed order (deterministic)
+    float mm = -CUDART_INF_F, ss = 0.f;
+    for (int w = 0; w < kWarps; ++w) stat_merge(mm, ss, ctl.wm[w][tid], ctl.ws[w][tid]);
+    s_hm[tid] = mm;
+    s_hz[tid] = ss;
+  }
+  // ---- merge the nch chunks' statistics of the pair through DSMEM, in chunk order ----
+  TLS_STAMP(3)
+  cluster_sync_all();
+  TLS_STAMP(4)
+  if (tid < d.G) {  // all remote loads first (<= 16 ranks), then the ordered merge
+    float rm[16], rz[16];
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr)
+      if (rr < (int)gridDim.x) rm[rr] = *dsmem(&s_hm[tid], rr), rz[rr] = *dsmem(&s_hz[tid], rr);
+    float M = -CUDART_INF_F, Z = 0.f;
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr)
+      if (rr < (int)gridDim.x) stat_merge(M, Z, rm[rr], rz[rr]);
+    ctl.hlz[tid] = M + flog2(Z);
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");  // remote reads done
+  __syncthreads();
+  // ---- pass 2: ranking keys log2 sum_h exp2(L_hj - lz_h) ----
+  float cf[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int h = nt * 8 + 2 * q4 + e;
+      cf[nt][e] = (h < d.G && hm[nt][e] != -CUDART_INF_F) ? fexp2(hm[nt][e] - ctl.hlz[h] + kKeyOff) : 0.f;
+    }
+  uint32_t* kout = p.keys + (size_t)pair * p.kb_eff * d.B + ((size_t)cb0 << d.log2B);
+  const bool bit0 = q4 & 1, bit1 = q4 & 2;
+#pragma unroll
+  for (int t = 0; t < TPW; t += 2) {
+    if (warp + t * kWarps >= ntiles) break;  // warp-uniform
+    float pa = 0.f, pb = 0.f, pc = 0.f, pd = 0.f;  // (tile t, r0), (t, r0+8), (t+1, r0), (t+1, r0+8)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        pa = fmaf(ev[t][nt][e], cf[nt][e], pa);
+        pb = fmaf(ev[t][nt][2 + e], cf[nt][e], pb);
+        pc = fmaf(ev[t + 1][nt][e], cf[nt][e], pc);
+        pd = fmaf(ev[t + 1][nt][2 + e], cf[nt][e], pd);
+      }
+    // transposed butterfly: lane q4 ends with the head-sum of token q4 of (pa, pb, pc, pd)
+    float k1 = bit0 ? pb : pa, k2 = bit0 ? pd : pc;
+    k1 += __shfl_xor_sync(0xffffffffu, bit0 ? pa : pb, 1);
+    k2 += __shfl_xor_sync(0xffffffffu, bit0 ? pc : pd, 1);
+    float mine = bit1 ? k2 : k1;
+    mine += __shfl_xor_sync(0xffffffffu, bit1 ? k1 : k2, 2);
+    const int tile = warp + (t + (bit1 ? 1 : 0)) * kWarps;
+    const int row = r0 + (bit0 ? 8 : 0);
+    if (tile < ntiles) {
+      const int blk = cblk[cb0 + (tile >> tshift)];
+      const int tok = (blk << d.log2B) + ((tile & ((1 << tshift) - 1)) << 4) + row;
+      const bool v = tok < n;
+      const float kf = flog2(mine) - kKeyOff;
+      kout[tile * 16 + row] = v ? f2key(kf) : 0u;
+      if (v) atomicAdd(&lhist[key_bin(kf)], 1u);
+    }
+  }
+  __syncthreads();
+  uint32_t* gh = p.khist + (size_t)pair * kKeyBins;
+  for (int i = tid; i < kKeyBins; i += kThreads)
+    if (lhist[i]) atomicAdd(&gh[i], lhist[i]);
+  TLS_STAMP(5)
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");  // keep smem alive for remote readers
+  TLS_STAMP(6)
+#undef TLS_STAMP
 }
 
 // ============================================================== launchers
@@ -520,7 +895,7 @@ cudaError_t launch_block_scores(const ScoreParams& p, cudaStream_t st) {
 
 template <typename T, int KS, int NT, int NSPLIT>
 static cudaError_t launch_k2(const SelectParams& p, cudaStream_t st) {
-  auto kern = token_cluster_kernel<T, KS, NT, NSPLIT>;
+  auto kern = p.tpw > 0 ? token_reg_kernel<T, KS, NT, NSPLIT, 8 / NT> : token_cluster_kernel<T, KS, NT, NSPLIT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);

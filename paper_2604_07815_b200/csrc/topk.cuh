@@ -74,4 +74,61 @@ __device__ void topk_emit(const uint32_t* keys, int nloc, const TopK& t, TopKCtl
   __syncthreads();
 }
 
+
+// One-pass emit when the caller already knows, for the segmentation used by
+// topk_emit (warp w owns [w*seg, (w+1)*seg), seg = ceil(n/8) rounded up to
+// 128), each warp's count of keys > thr (wgt_in) and == thr (weq_in).  Four
+// 32-key groups per iteration (independent ballots first, then the writes).
+template <class F>
+__device__ void topk_emit_counted(const uint32_t* keys, int nloc, const TopK& t, const int* wgt_in, const int* weq_in,
+                                  F f) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int seg = (((nloc + kWarps - 1) / kWarps) + 127) & ~127;
+  const int s0 = min(warp * seg, nloc), s1 = min(s0 + seg, nloc);
+  int eq_seen = 0, pos = t.offset;
+  for (int w = 0; w < warp; ++w) {
+    const int take = t.eq_mode ? min(max(t.take_eq - eq_seen, 0), weq_in[w]) : 0;
+    pos += wgt_in[w] + take;
+    eq_seen += weq_in[w];
+  }
+  for (int base = s0; base < s1; base += 128) {
+    uint32_t k[4];
+    unsigned beq[4], bgt[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = base + 32 * u + lane;
+      k[u] = i < s1 ? keys[i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      bgt[u] = __ballot_sync(0xffffffffu, k[u] > t.thr);
+      beq[u] = __ballot_sync(0xffffffffu, t.eq_mode && k[u] != 0u && k[u] == t.thr);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      // ties taken in index order: this group's eq lanes below `lane` plus all earlier ones
+      const int room = t.take_eq - eq_seen;  // ties still allowed before this group
+      unsigned tie_ok = 0u;
+      if (beq[u]) {
+        if (room >= __popc(beq[u])) {
+          tie_ok = beq[u];
+        } else if (room > 0) {
+          unsigned m = beq[u];
+          for (int r = 0; r < room; ++r) {
+            const unsigned low = m & (~m + 1u);
+            tie_ok |= low;
+            m &= m - 1u;
+          }
+        }
+      }
+      const unsigned bsel = bgt[u] | tie_ok;
+      if ((bsel >> lane) & 1u) f(base + 32 * u + lane, pos + __popc(bsel & lt));
+      pos += __popc(bsel);
+      eq_seen += __popc(beq[u]);
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace tls

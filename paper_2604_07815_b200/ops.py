@@ -28,6 +28,9 @@ __all__ = [
     "sparse_attend",
     "decode",
     "cluster_size",
+    "KERNELS",
+    "timing_enable",
+    "timing_read",
 ]
 
 _DT = {torch.bfloat16: _lib.TLS_BF16, torch.float32: _lib.TLS_FP32}
@@ -292,3 +295,20 @@ def cluster_size(cfg: TLSConfig, which: int = 2) -> int:
     """CTAs per (batch, KV-head) pair: token-select kernel (which 0/2) or attention kernel (1)."""
     cc = cfg.c()
     return int(_lib.load().tls_cluster_size(ctypes.byref(cc), which))
+
+
+KERNELS = ("block_score_kernel", "block_topk_kernel", "token_cluster_kernel", "attend_kernel")
+
+
+def timing_enable(n_calls: int) -> None:
+    """Record CUDA events around each launch of the next select/decode calls
+    (tls_timing_enable); 0 disables."""
+    _lib.check(_lib.load().tls_timing_enable(int(n_calls)))
+
+
+def timing_read() -> tuple[dict, int]:
+    """(kernel name -> summed ms, number of calls) since the last read (tls_timing_read)."""
+    ms = (ctypes.c_double * 4)()
+    calls = ctypes.c_int64(0)
+    _lib.check(_lib.load().tls_timing_read(ms, ctypes.byref(calls)))
+    return {k: float(ms[i]) for i, k in enumerate(KERNELS)}, int(calls.value)

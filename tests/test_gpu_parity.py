@@ -324,3 +324,28 @@ def test_block_scores_match_direct_form(name):
             got = sc[b, g, : len(ref)].double().cpu().numpy()
             bound = 2e-6 * (np.abs(q).sum() * np.maximum(np.abs(kmax), np.abs(kmin)).max(axis=1) + 1.0)
             assert np.all(np.abs(got - ref) <= bound)
+
+
+def test_kernel_timing_hook_records_every_launch():
+    """tls_timing_enable/read: one record per select/decode call, 4 slots, and
+    recording does not change the results."""
+    w = SMALL["gqa8"]
+    cfg, inputs, idx = setup_case(w, seed=3)
+    ref = run_decode(cfg, inputs, idx)
+    tls.timing_enable(2)
+    try:
+        res = run_decode(cfg, inputs, idx)
+        tls.select(cfg, inputs["q"], inputs["seq_lens"], idx)
+        run_decode(cfg, inputs, idx)  # more calls than reserved: events created on demand
+        ms, calls = tls.timing_read()
+        assert calls == 3
+        assert set(ms) == set(tls.KERNELS) and all(v > 0 for v in ms.values())
+        ms2, calls2 = tls.timing_read()
+        assert calls2 == 0 and all(v == 0 for v in ms2.values())
+    finally:
+        tls.timing_enable(0)
+    run_decode(cfg, inputs, idx)
+    assert tls.timing_read()[1] == 0  # disabled: nothing recorded
+    torch.cuda.synchronize()
+    for a, b in zip(ref, res):
+        assert torch.equal(a, b)

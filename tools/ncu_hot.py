@@ -5,7 +5,11 @@ import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]
-data = rows[2:]
+data = []
+for r in rows[2:]:  # first kernel section only
+    if r and r[0] == "Kernel Name":
+        break
+    data.append(r)
 ix = {h: i for i, h in enumerate(hdr)}
 samp = ix["Warp Stall Sampling (All Samples)"]
 stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]

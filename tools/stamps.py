@@ -1,0 +1,38 @@
+"""Diagnostic: per-phase latency of the token-cluster kernel (K2) and of K3's
+selection prologue, from %globaltimer stamps (TLS_DEBUG_BUF)."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2604_07815_b200 as tls  # noqa: E402
+from paper_2604_07815_b200 import workloads as W  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+w = W.CONFIGS[name]
+cfg, inputs, idx, queries = bench.build_state(w, 0, torch.device("cuda"), "outlier")
+buf = torch.zeros(2 * 65536 * 8, dtype=torch.int64, device="cuda")
+for it in range(3):
+    if it == 2:
+        os.environ["TLS_DEBUG_BUF"] = hex(buf.data_ptr())
+    tls.decode(cfg, queries[it], inputs["k_cache"], inputs["v_cache"], inputs["seq_lens"], idx)
+    torch.cuda.synchronize()
+os.environ.pop("TLS_DEBUG_BUF")
+pairs = w.batch * w.num_kv_heads
+k2 = buf[: pairs * 8 * 8].view(pairs, 8, 8).cpu().double()
+k3 = buf[65536 * 8: 65536 * 8 + pairs * 8].view(pairs, 8).cpu().double()
+t0 = k2[:, :, 0][k2[:, :, 0] > 0].min()
+def med(x):
+    x = x[x == x]
+    return float(x.median()) / 1e3 if len(x) else float("nan")
+valid = k2[:, :, 0] > 0
+d = (k2[:, :, 1:7] - k2[:, :, 0:6])[valid]
+print(f"{name}: K2 span {(k2[:, :, 6][valid].max() - t0) / 1e3:.1f} us; CTA lifetime median {med(k2[:, :, 6][valid] - k2[:, :, 0][valid]):.1f} us")
+for i, nm in enumerate(["setup (cand, q, TMA issue)", "wait staged index", "pass 1 stats", "cluster sync", "merge + pass 2 keys", "cluster wait"]):
+    print(f"  K2 {nm:28s} median {med(d[:, i]):6.2f} us")
+k3t0 = k3[:, 0].min()
+print(f"K3 start (rel. K2 start) median {(k3[:, 0] - t0).median() / 1e3:.1f} us, K3 span {(k3[:, 5].max() - k3t0) / 1e3:.1f} us")
+for i, nm in enumerate(["load keys+hist (TMA)", "histogram scan", "boundary select", "emit", "attention"]):
+    print(f"  K3 {nm:28s} median {med(k3[:, i + 1] - k3[:, i]):6.2f} us")
