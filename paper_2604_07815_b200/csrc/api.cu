@@ -202,7 +202,7 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
       return fail(TLS_ERR_INPUT, "GQA needs a 16-byte aligned v_cache");
     if (!out) return fail(TLS_ERR_INPUT, "out is required");
   }
-  tls::SelectParams sp;
+  tls::SelectParams sp{};
   s = plan_select(cfg, sp);
   if (s) return s;
   tls::AttendParams ap;
@@ -214,7 +214,7 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
     return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes, 16-byte aligned (got %zu)", w.total + watt,
                 workspace_bytes);
   char* ws = static_cast<char*>(workspace);
-  tls::ScoreParams k1;
+  tls::ScoreParams k1{};
   k1.d = sp.d;
   k1.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
   if (k1.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
@@ -228,6 +228,8 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
   k1.khist = reinterpret_cast<uint32_t*>(ws + w.khist);
   k1.guide = guide;
   k1.block_ids = block_ids;
+  k1.channels = idx->channels;
+  k1.qfrag = reinterpret_cast<uint8_t*>(ws + w.qfrag);
   if (g_timer.on && g_timer.used % 5 != 0) g_timer.used -= g_timer.used % 5;  // drop a partial record
   g_timer.mark(st);
   cudaError_t e = tls::launch_block_scores(k1, st);
@@ -246,6 +248,7 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
   sp.block_ids = block_ids;
   sp.keys = reinterpret_cast<uint32_t*>(ws + w.keys);
   sp.khist = k1.khist;
+  sp.qfrag = k1.qfrag;
   sp.dbg = env_debug_buf();
   e = tls::launch_token_cluster(sp, st);
   if (e != cudaSuccess) return cuda_fail(e, "token_cluster_kernel launch");
@@ -377,7 +380,7 @@ tls_status tls_block_scores(const tls_config* cfg, const void* q, const int32_t*
   if (!q || !aligned16(q)) return fail(TLS_ERR_INPUT, "q must be a non-NULL 16-byte aligned device pointer");
   if (!seq_lens || !block_minmax || !scores || !aligned16(block_minmax))
     return fail(TLS_ERR_INPUT, "seq_lens, block_minmax (16-byte aligned) and scores are required");
-  tls::ScoreParams k1;
+  tls::ScoreParams k1{};
   k1.d = dims_of(cfg);
   k1.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
   if (k1.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");

@@ -38,6 +38,8 @@ struct ScoreParams {  // K1 (+ the pair's top-k_b in its last CTA)
   float* scores;       // workspace [pairs, M] fp32
   int* done;           // unused (NULL)
   uint32_t* khist;     // workspace [pairs, kKeyBins] key histogram, zeroed here for K2 pass 2
+  const int* channels; // K1b: the index channels (for the q-fragment blob)
+  uint8_t* qfrag;      // K1b out: [pairs, qfrag_bytes(d)] q-fragment blobs for K2 (NULL: not built)
   const int* guide;    // lag mode: the pair's candidates are the guide (M_t is still reported)
   int* block_ids;      // [pairs, Kb] out: M_t ascending, -1 padded
 };
@@ -61,6 +63,7 @@ struct SelectParams {  // K2 (token_reg_kernel, or token_cluster_kernel when a c
   uint32_t* khist; // workspace [pairs, kKeyBins] histogram of the keys (PASS 2 adds)
   unsigned long long* dbg;  // diagnostics only (env TLS_DEBUG_BUF): per-CTA phase stamps
   int qtma;  // 1: the q rows of the pair arrive by TMA into smem (off_qrows)
+  const uint8_t* qfrag;  // token_reg_kernel: K1b's q-fragment blobs [pairs, qfrag_bytes(d)]
   unsigned off_cblk, off_qb, off_qsum, off_qc, off_qrows, off_stage, smem_bytes;
 };
 
@@ -185,19 +188,30 @@ static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
 
 static inline size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 // Workspace of tls_select: K1's fp32 block scores | chunk statistics | keys.
+// Per-pair q-fragment blob (K1b -> K2): the B fragments of q~ (NSPLIT x NT x
+// KS x 32 lanes x 2 words) followed by sum_c q~_h[c] for the NT*8 padded heads,
+// laid out exactly as K2's shared-memory regions off_qb .. off_qsum.
+static inline int qfrag_nt(const Dims& d) {
+  const int nt0 = (d.G + 7) / 8;
+  return nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);
+}
+static inline int qfrag_bytes(const Dims& d) {
+  const int nsplit = d.bf16 ? 1 : 3;
+  return nsplit * qfrag_nt(d) * (d.d_c / 16) * 256 + qfrag_nt(d) * 8 * 4;
+}
+
 struct SelectWs {
-  size_t scores, stats, keys, khist, done, total;
+  size_t scores, keys, khist, qfrag, total;
 };
 static inline SelectWs select_workspace(const Dims& d) {
   SelectWs w;
   const size_t pairs = (size_t)d.batch * d.Hkv;
   const size_t kb = (size_t)kb_effective(d);
   w.scores = 0;
-  w.stats = a256(pairs * d.Ms * 4);
-  w.keys = w.stats;
+  w.keys = a256(pairs * d.Ms * 4);
   w.khist = w.keys + a256(pairs * kb * d.B * 4);
-  w.done = w.khist + a256(pairs * kKeyBins * 4);
-  w.total = w.done;
+  w.qfrag = w.khist + a256(pairs * kKeyBins * 4);
+  w.total = w.qfrag + a256(pairs * (size_t)qfrag_bytes(d));
   return w;
 }
 static inline size_t select_workspace_bytes(const Dims& d) { return select_workspace(d).total; }

@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(kThreads, 4) block_score_kernel(const __grid_c
   }
 }
 
+__device__ void build_qfrag(const ScoreParams& p, int pair, float* qc);
+
 // ============================================================== K1b: a2
 // One CTA per pair: M_t = top-k_b blocks from the pair's L2-resident
 // scores, ties -> lower block id (U2), written ascending and -1 padded.
@@ -182,6 +184,8 @@ __global__ void __launch_bounds__(kThreads) block_topk_kernel(const __grid_const
     mbar_arrive_expect_tx(&sbar, bytes);
     tma_bulk_g2s(bkeys, p.scores + (size_t)pair * p.sstride, bytes, &sbar);
   }
+  // while the scores arrive: the pair's q-fragment blob for K2 (scratch as q~ staging)
+  if (p.qfrag) build_qfrag(p, pair, reinterpret_cast<float*>(scratch));
   __syncthreads();
   if (m > 0) mbar_wait(&sbar, 0);
   for (int i = tid; i < m; i += kThreads) bkeys[i] = f2key(__uint_as_float(bkeys[i]));
@@ -221,6 +225,51 @@ __device__ __forceinline__ float split_piece(float x, int sp) {
   float mid = __bfloat162float(__float2bfloat16_rn(r1));
   if (sp == 1) return mid;
   return __bfloat162float(__float2bfloat16_rn(r1 - mid));
+}
+
+// The pair's q-fragment blob (see params.h qfrag_bytes): q~_h[c] = q_h[ch_c]
+// for the NT*8 padded heads, packed as K2's mma B fragments in the
+// permuted channel order of token_tile_mma, then sum_c q~_h[c].  qc: >= NT*8*d_c
+// floats of shared scratch.  Called by all threads of K1b.
+__device__ void build_qfrag(const ScoreParams& p, int pair, float* qc) {
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = pair / d.Hkv, g = pair - b * d.Hkv;
+  const int nt0 = (d.G + 7) / 8, NT = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);
+  const int DC = d.d_c, KS = DC / 16, WPT = KS / 2, NSPLIT = d.bf16 ? 1 : 3;
+  const int* ch = p.channels + (size_t)g * DC;
+  const size_t qoff = ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
+  for (int i = tid; i < NT * 8 * DC; i += kThreads) {
+    const int h = i / DC, c = i - h * DC;
+    float v = 0.f;
+    if (h < d.G) {
+      const size_t o = qoff + (size_t)h * d.d_k + ch[c];
+      v = d.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.q)[o])
+                 : reinterpret_cast<const float*>(p.q)[o];
+    }
+    qc[i] = v;
+  }
+  __syncthreads();
+  const int qfb = NSPLIT * NT * KS * 256 + NT * 32;
+  uint32_t* qb = reinterpret_cast<uint32_t*>(p.qfrag + (size_t)pair * qfb);
+  for (int idx = tid; idx < NSPLIT * NT * KS * 32; idx += kThreads) {
+    const int ln = idx & 31, rest = idx >> 5;
+    const int s = rest % KS, nt = (rest / KS) % NT, sp = rest / (KS * NT);
+    const float* qh = qc + (nt * 8 + (ln >> 2)) * DC;
+    const int cb = 8 * ((ln & 3) * WPT + (s >> 1)) + 2 * (s & 1);
+    uint2 v;
+    v.x = pack_bf16x2(split_piece(qh[cb], sp), split_piece(qh[cb + 4], sp));
+    v.y = pack_bf16x2(split_piece(qh[cb + 1], sp), split_piece(qh[cb + 5], sp));
+    reinterpret_cast<uint2*>(qb)[idx] = v;
+  }
+  float* qsum = reinterpret_cast<float*>(qb + 2 * NSPLIT * NT * KS * 32);
+  for (int h = warp; h < NT * 8; h += kWarps) {
+    float sum = 0.f;
+    for (int c = lane; c < DC; c += 32) sum += qc[h * DC + c];
+    sum = warp_sum(sum);
+    if (lane == 0) qsum[h] = sum;
+  }
+  __syncthreads();  // qc (scratch) is reused by the caller
 }
 
 // merge two online-softmax states (m, s) in log2 units
@@ -573,14 +622,18 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
 // ~2^-126 are affected.
 constexpr float kKeyOff = 64.f;
 
+// 4 CTAs / SM (64 registers) where the variant fits without spilling, else 3.
+template <int KS, int NT, int NSPLIT>
+constexpr int k2_min_blocks() { return (NT == 1 && KS * NSPLIT <= 6) ? 4 : 3; }
+
 template <typename T, int KS, int NT, int NSPLIT, int TPW>
-__global__ void __launch_bounds__(kThreads, 3) token_reg_kernel(const __grid_constant__ SelectParams p) {
+__global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) token_reg_kernel(const __grid_constant__ SelectParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ SelCtl ctl;
   __shared__ __align__(8) uint64_t bar;
   __shared__ __align__(8) uint64_t qbar;
   __shared__ uint32_t lhist[kKeyBins];
-  __shared__ float s_hm[32], s_hz[32];
+  __shared__ float s_cm[16][32], s_cz[16][32];  // [chunk rank][head]: every chunk's stats, pushed by that chunk
   const Dims& d = p.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q4 = lane & 3, r0 = lane >> 2;
   const int chunk = blockIdx.x, pair = blockIdx.y;
@@ -593,27 +646,20 @@ __global__ void __launch_bounds__(kThreads, 3) token_reg_kernel(const __grid_con
   const int n = min(max(p.seq_lens[b], 0), d.S);
   const int m = (n + d.B - 1) >> d.log2B;
   int* cblk = reinterpret_cast<int*>(smem + p.off_cblk);
-  uint32_t* qb = reinterpret_cast<uint32_t*>(smem + p.off_qb);
   float* qsum = reinterpret_cast<float*>(smem + p.off_qsum);
-  float* qc = reinterpret_cast<float*>(smem + p.off_qc);
   uint8_t* stc = smem + p.off_stage;
   float2* stz = reinterpret_cast<float2*>(smem + p.off_stage + (size_t)p.cb * d.B * (d.d_c / 2));
-  const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
-  T* qrows = reinterpret_cast<T*>(smem + p.off_qrows);
-  int* chan_s = reinterpret_cast<int*>(smem + p.off_qrows + (size_t)d.G * d.d_k * sizeof(T));
   if (tid == 0) {
     mbar_init(&bar, 1);
     mbar_init(&qbar, 1);
     mbar_fence_init();
-    if (p.qtma) {
-      const uint32_t qb_ = (uint32_t)(d.G * d.d_k * sizeof(T)), cb_ = (uint32_t)(d.d_c * 4);
-      mbar_arrive_expect_tx(&qbar, qb_ + cb_);
-      tma_bulk_g2s(qrows, qg, qb_, &qbar);
-      tma_bulk_g2s(chan_s, p.channels + (size_t)g * d.d_c, cb_, &qbar);
-    }
+    // the pair's q-fragment blob from K1b: one TMA bulk copy into [off_qb, off_qsum + NT*32)
+    const uint32_t qfb = (uint32_t)(NSPLIT * NT * KS * 256 + NT * 32);
+    mbar_arrive_expect_tx(&qbar, qfb);
+    tma_bulk_g2s(smem + p.off_qb, p.qfrag + (size_t)pair * qfb, qfb, &qbar);
   }
   __syncthreads();  // mbarriers initialised before any wait / copy issue
-  if (!p.qtma && tid < KS * 16) ctl.chan[tid] = p.channels[(size_t)g * d.d_c + tid];
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");  // started (matched before the DSMEM push)
   const int rowbytes = d.d_c / 2;
   const uint8_t* cbase = p.codes + (size_t)pair * d.S * rowbytes;
   const float2* zbase = reinterpret_cast<const float2*>(p.scale_zero) + (size_t)pair * d.S;
@@ -623,21 +669,31 @@ __global__ void __launch_bounds__(kThreads, 3) token_reg_kernel(const __grid_con
   if (p.guide == nullptr) {
     // K1b's M_t is already compact: min(kb_eff, m) ascending valid ids, -1 padded.
     // Warp 0 reads this chunk's ids and issues the TMA copies straight away.
-    const int kc = min(p.kb_eff, m);
-    nbl = max(0, min(p.cb, kc - cb0));
-    if (warp == 0 && nbl > 0) {
+    // (-1 padding marks the end, so no dependence on seq_lens.)
+    nbl = 0;
+    if (warp == 0) {
       const int* cand = p.block_ids + (size_t)pair * d.Kb + cb0;
+      const int lim = min(p.cb, p.kb_eff - cb0);
       uint32_t bytes = 0;
-      for (int k = lane; k < nbl; k += 32) {
-        const int blk = cand[k];
-        cblk[cb0 + k] = blk;
-        const int rows = min(d.B, d.S - blk * d.B);
-        bytes += rows * rowbytes + (zal ? rows * 8 : 0);
+      int cntv = 0;
+      for (int k0 = 0; k0 < lim; k0 += 32) {
+        const int k = k0 + lane;
+        const int blk = k < lim ? cand[k] : -1;
+        const bool ok = blk >= 0;
+        cntv += __popc(__ballot_sync(0xffffffffu, ok));
+        if (ok) {
+          cblk[cb0 + k] = blk;
+          const int rows = min(d.B, d.S - blk * d.B);
+          bytes += rows * rowbytes + (zal ? rows * 8 : 0);
+        }
       }
       bytes = warp_sum_u32(bytes);
-      if (lane == 0) mbar_arrive_expect_tx(&bar, bytes);
+      if (lane == 0) {
+        ctl.kc = cntv;
+        if (cntv > 0) mbar_arrive_expect_tx(&bar, bytes);
+      }
       __syncwarp();
-      for (int k = lane; k < nbl; k += 32) {
+      for (int k = lane; k < cntv; k += 32) {
         const int blk = cblk[cb0 + k];
         const int rows = min(d.B, d.S - blk * d.B);
         tma_bulk_g2s(stc + (size_t)k * d.B * rowbytes, cbase + (size_t)blk * d.B * rowbytes, rows * rowbytes, &bar);
@@ -674,37 +730,10 @@ __global__ void __launch_bounds__(kThreads, 3) token_reg_kernel(const __grid_con
       }
     }
   }
-  // channel-projected query q~, its B fragments and sum
-  constexpr int DC = KS * 16;
-  if (p.qtma) {
-    mbar_wait(&qbar, 0);
-    for (int i = tid; i < NT * 8 * DC; i += kThreads) {
-      const int h = i / DC, c = i - h * DC;
-      qc[i] = h < d.G ? to_f32<T>(qrows[(size_t)h * d.d_k + chan_s[c]]) : 0.f;
-    }
-  } else {
-    for (int i = tid; i < NT * 8 * DC; i += kThreads) {
-      const int h = i / DC, c = i - h * DC;
-      qc[i] = h < d.G ? to_f32<T>(qg[(size_t)h * d.d_k + ctl.chan[c]]) : 0.f;
-    }
-  }
-  __syncthreads();
-  constexpr int WPT = KS / 2;
-  for (int idx = tid; idx < NSPLIT * NT * KS * 32; idx += kThreads) {
-    const int ln = idx & 31, rest = idx >> 5;
-    const int s = rest % KS, nt = (rest / KS) % NT, sp = rest / (KS * NT);
-    const float* qh = qc + (nt * 8 + (ln >> 2)) * DC;
-    const int cb = 8 * ((ln & 3) * WPT + (s >> 1)) + 2 * (s & 1);
-    qb[2 * idx] = pack_bf16x2(split_piece(qh[cb], sp), split_piece(qh[cb + 4], sp));
-    qb[2 * idx + 1] = pack_bf16x2(split_piece(qh[cb + 1], sp), split_piece(qh[cb + 5], sp));
-  }
-  if (tid < NT * 8) {
-    float s = 0.f;
-    for (int c = 0; c < DC; ++c) s += qc[tid * DC + c];
-    qsum[tid] = s;
-  }
-  __syncthreads();
+  __syncthreads();  // cblk / ctl.kc published
+  if (p.guide == nullptr) nbl = ctl.kc;
   TLS_STAMP(1)
+  mbar_wait(&qbar, 0);
   if (nbl > 0) mbar_wait(&bar, 0);
   TLS_STAMP(2)
   const float sm2 = d.sm_scale * kLog2e;
@@ -713,7 +742,7 @@ __global__ void __launch_bounds__(kThreads, 3) token_reg_kernel(const __grid_con
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
     for (int e = 0; e < 2; ++e) sq[nt][e] = sm2 * qsum[nt * 8 + 2 * q4 + e];
-  const uint2* qb2 = reinterpret_cast<const uint2*>(qb);
+  const uint2* qb2 = reinterpret_cast<const uint2*>(smem + p.off_qb);
   const int tshift = d.log2B - 4;
   const int ntiles = nbl << tshift;
   // ---- pass 1: logits of every tile (tile = warp + t * kWarps), per-warp head max ----
@@ -777,28 +806,44 @@ __global__ void __launch_bounds__(kThreads, 3) token_reg_kernel(const __grid_con
       }
   }
   __syncthreads();
-  if (tid < d.G) {  // warps merged in a fixed order (deterministic)
-    float mm = -CUDART_INF_F, ss = 0.f;
-    for (int w = 0; w < kWarps; ++w) stat_merge(mm, ss, ctl.wm[w][tid], ctl.ws[w][tid]);
-    s_hm[tid] = mm;
-    s_hz[tid] = ss;
+  {  // CTA merge of the 8 warps' (max, sum) per head: 8 lanes per head; push the result to every chunk CTA
+    const int w = tid & 7, nch = (int)gridDim.x;
+    const unsigned my = blockIdx.x;
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");  // every chunk CTA has started (DSMEM rule)
+    {
+      const int h = tid >> 3;  // G <= 32 = kThreads / 8: one pass, warp-uniform shuffles
+      const bool okh = h < d.G;
+      const float mv = okh ? ctl.wm[w][h] : -CUDART_INF_F, sv = okh ? ctl.ws[w][h] : 0.f;
+      float M = mv;
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      float S = (mv == -CUDART_INF_F) ? 0.f : sv * fexp2(mv - M);
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+      if (okh)
+        for (int rr = w; rr < nch; rr += 8) {
+          *dsmem(&s_cm[my][h], rr) = M;
+          *dsmem(&s_cz[my][h], rr) = S;
+        }
+    }
   }
-  // ---- merge the nch chunks' statistics of the pair through DSMEM, in chunk order ----
   TLS_STAMP(3)
-  cluster_sync_all();
+  cluster_sync_all();  // every chunk's statistics have landed in every CTA
   TLS_STAMP(4)
-  if (tid < d.G) {  // all remote loads first (<= 16 ranks), then the ordered merge
-    float rm[16], rz[16];
+  {  // cluster merge, local: 16 lanes per head over the nch chunk ranks
+    const int r = tid & 15, nch = (int)gridDim.x;
+    for (int h = tid >> 4; h < ((d.G + 15) & ~15); h += kThreads / 16) {
+      const bool ok = r < nch && h < d.G;
+      const float mv = ok ? s_cm[r][h] : -CUDART_INF_F, sv = ok ? s_cz[r][h] : 0.f;
+      float M = mv;
 #pragma unroll
-    for (int rr = 0; rr < 16; ++rr)
-      if (rr < (int)gridDim.x) rm[rr] = *dsmem(&s_hm[tid], rr), rz[rr] = *dsmem(&s_hz[tid], rr);
-    float M = -CUDART_INF_F, Z = 0.f;
+      for (int o = 1; o < 16; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      float S = (mv == -CUDART_INF_F) ? 0.f : sv * fexp2(mv - M);
 #pragma unroll
-    for (int rr = 0; rr < 16; ++rr)
-      if (rr < (int)gridDim.x) stat_merge(M, Z, rm[rr], rz[rr]);
-    ctl.hlz[tid] = M + flog2(Z);
+      for (int o = 1; o < 16; o <<= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+      if (r == 0 && h < d.G) ctl.hlz[h] = M + flog2(S);
+    }
   }
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");  // remote reads done
   __syncthreads();
   // ---- pass 2: ranking keys log2 sum_h exp2(L_hj - lz_h) ----
   float cf[NT][2];
@@ -846,7 +891,6 @@ __global__ void __launch_bounds__(kThreads, 3) token_reg_kernel(const __grid_con
   for (int i = tid; i < kKeyBins; i += kThreads)
     if (lhist[i]) atomicAdd(&gh[i], lhist[i]);
   TLS_STAMP(5)
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");  // keep smem alive for remote readers
   TLS_STAMP(6)
 #undef TLS_STAMP
 }
@@ -874,7 +918,9 @@ static cudaError_t launch_k1(const ScoreParams& p, cudaStream_t st) {
 }
 
 cudaError_t launch_block_topk(const ScoreParams& p, cudaStream_t st) {
-  const size_t smem = (size_t)((p.d.M + 31) & ~31) * 4 + (size_t)kBracketCap * 4 + sizeof(FastTopKCtl);
+  const size_t sel = (size_t)kBracketCap * 4 + sizeof(FastTopKCtl);
+  const size_t qstage = (size_t)qfrag_nt(p.d) * 8 * p.d.d_c * 4;  // build_qfrag's q~ staging
+  const size_t smem = (size_t)((p.d.M + 31) & ~31) * 4 + (sel > qstage ? sel : qstage);
   cudaError_t e = cudaFuncSetAttribute(block_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   block_topk_kernel<<<p.d.batch * p.d.Hkv, kThreads, smem, st>>>(p);
