@@ -8,8 +8,9 @@
  * Conventions shared by every call
  * --------------------------------
  * - Every pointer is a caller-owned DEVICE pointer unless noted otherwise.
- *   The library allocates no device memory and keeps no global state other
- *   than a thread-local error string.
+ *   The library allocates no device memory.  Host-side state: a thread-local
+ *   error string and, only when TLS_NSPLIT > 1 pipelines a call over
+ *   sub-batches, per-thread internal CUDA streams and events.
  * - Every call validates its host-visible arguments synchronously, then
  *   enqueues its kernels on `stream` and returns; outputs are valid once the
  *   stream reaches that point.  No call synchronises the host.
@@ -130,12 +131,13 @@ tls_status tls_build_index(const tls_config* cfg, const void* k_cache, const int
                            int32_t start_token, const tls_index* idx, tls_stream_t stream);
 
 /*
- * Block scores alone (step a1, P:99 via the P:104-118 GEMM identity):
+ * Block scores alone (step a1, P:99 via the P:104-118 GEMM identity; the
+ * scoring phase of select_kernel, mode 0):
  *   scores[b, g, i] = sum_h sum_c max(q_hc k^max_ic, q_hc k^min_ic)   (fp32)
  * for every block i < ceil(seq_lens[b] / B); entries at or beyond that are
  * left untouched.  scores: [batch, Hkv, ceil(max_seq_len / B)] fp32 device
- * memory.  This is the first kernel of tls_select (also usable on its own,
- * e.g. for block-only Quest-style selection).
+ * memory.  This is phase a1 of tls_select (also usable on its own, e.g. for
+ * block-only Quest-style selection).
  */
 tls_status tls_block_scores(const tls_config* cfg, const void* q, const int32_t* seq_lens,
                             const void* block_minmax, float* scores, tls_stream_t stream);
@@ -159,6 +161,11 @@ tls_status tls_block_scores(const tls_config* cfg, const void* q, const int32_t*
  *   those blocks (one-step-lag form S_t = TokenSelect(q_t, M_{t-1})).
  * workspace: >= tls_workspace_bytes(cfg, 0) bytes of device memory, 256-B
  *   aligned, not shared with a concurrently running call.
+ * Kernels (fused.cu, select.cu, attend.cu): select_kernel scores every
+ * pair's blocks tile by tile; the pair's last tile CTA waits for the others'
+ * completion flags and runs the pair's top-k_b (a2) while other pairs' tiles
+ * still stream; token_cluster_kernel (a3, one thread-block cluster per pair)
+ * and the attention kernel's selection prologue (a4) follow.
  */
 tls_status tls_select(const tls_config* cfg, const void* q, const int32_t* seq_lens,
                       const tls_index* idx, const int32_t* guide_block_ids, int32_t* block_ids,
@@ -180,7 +187,10 @@ tls_status tls_sparse_attend(const tls_config* cfg, const void* q, const void* k
                              size_t workspace_bytes, tls_stream_t stream);
 
 /* tls_select followed by tls_sparse_attend on the same stream (one decode step
- * of the operator).  workspace >= tls_workspace_bytes(cfg, 2). */
+ * of the operator).  workspace >= tls_workspace_bytes(cfg, 2).
+ * TLS_NSPLIT=n (environment, tuning) cuts the batch into n sub-batches whose
+ * launch chains run on internal streams (results identical up to the
+ * attention's split-K rounding). */
 tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
                       const void* v_cache, const int32_t* seq_lens, const tls_index* idx,
                       const int32_t* guide_block_ids, int32_t* block_ids, int32_t* token_ids,
@@ -191,19 +201,29 @@ tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
  * 2 tls_decode.  The select part holds the fp32 block scores of every pair,
  * per-chunk softmax statistics, the ranking key of every candidate token and a
  * per-pair key histogram; the attention part the
- * per-CTA partial (max, sum, o) of the split-K attention.  Sizes are rounded
- * up to 256 B.  No initialisation is needed (every word is written before it
- * is read within a call).  Do not share one workspace between calls that may
- * run concurrently.  (size_t)-1 for an invalid configuration or
- * `which`.  A NULL / too small / misaligned workspace -> TLS_ERR_WORKSPACE. */
+ * per-CTA partial (max, sum, o) of the split-K attention, plus the pair
+ * completion words of select_kernel: a call generation per pair and one flag
+ * per score tile (a tile publishes generation + 1; the pair's worker waits for
+ * it and advances the generation).  Sizes are rounded up to 256 B.  Contract:
+ * the workspace is zero-filled before its first use (or holds what an
+ * earlier call left there), and it is not written by anything else between
+ * calls -- reuse the same buffer for a configuration.  Do not share one
+ * workspace between calls that may run concurrently.  (size_t)-1 for an
+ * invalid configuration or `which`.  A NULL / too small / misaligned
+ * workspace -> TLS_ERR_WORKSPACE. */
 size_t tls_workspace_bytes(const tls_config* cfg, int32_t which);
 
 /* Number of kernel launches one call enqueues (which as above; 3 =
  * tls_build_index, 4 = tls_calibrate_channels), for launch accounting:
- * tls_select 4 (block scores, block top-k, token scores, token top-k),
- * tls_sparse_attend 1, tls_decode 4 (the last one also attends);
+ * tls_select and tls_decode 3 each (select_kernel, token_cluster_kernel,
+ * attend_kernel), times TLS_NSPLIT sub-batches; tls_sparse_attend 1.
  * -1 for an invalid configuration. */
 int32_t tls_launch_count(const tls_config* cfg, int32_t which);
+
+/* Selection mode of tls_select / tls_decode: 1 = select_kernel a1-a2,
+ * token_cluster_kernel a3, the attention kernel's prologue a4 (the only mode
+ * of this build).  -1 for an invalid configuration. */
+int32_t tls_select_mode(const tls_config* cfg);
 
 /* CTAs per (batch, KV-head) pair -- the thread-block cluster size -- of the
  * token-select kernel (which = 0 or 2) or of the attention kernel (which = 1);
@@ -214,15 +234,15 @@ int32_t tls_cluster_size(const tls_config* cfg, int32_t which);
 /* Live per-kernel device timing (diagnostics; used by bench.py for the
  * roofline of the dominant kernel).  While enabled, every tls_select /
  * tls_decode call records library-owned CUDA events on its stream before and
- * after each of its four launches (no extra synchronisation; events sit
- * between launches that are already stream-ordered).  Slots: 0 =
- * block_score_kernel (K1), 1 = block_topk_kernel (K1b), 2 =
- * token_cluster_kernel (K2), 3 = attend kernel (K3: token top-k [+ sparse
- * attention]).
+ * after each of its launches (no extra synchronisation; events sit between
+ * launches that are already stream-ordered).  Slots: 0 = select_kernel
+ * (a1-a2), 1 = token_cluster_kernel (a3), 2 = attend kernel (a4 prologue +
+ * a5).  With TLS_NSPLIT > 1
+ * the whole overlapped step is recorded in slot 2.
  *   tls_timing_enable(n): n > 0 enables and pre-creates events for n calls
  *     (more are created on demand), clearing previous records; n == 0
  *     disables and frees the events.
- *   tls_timing_read(ms_sum[4], calls): synchronises the recorded events,
+ *   tls_timing_read(ms_sum[3], calls): synchronises the recorded events,
  *     writes the summed milliseconds per slot and the number of calls
  *     recorded, and clears the records (enable state unchanged).
  * Process-global, not thread-safe: enable/read from one host thread. */

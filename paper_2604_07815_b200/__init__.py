@@ -14,6 +14,7 @@ from .ops import (  # noqa: F401
     cluster_size,
     decode,
     select,
+    select_mode,
     sparse_attend,
     KERNELS,
     timing_enable,

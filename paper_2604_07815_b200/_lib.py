@@ -27,6 +27,7 @@ EXPORTS = (
     "tls_workspace_bytes",
     "tls_launch_count",
     "tls_cluster_size",
+    "tls_select_mode",
     "tls_timing_enable",
     "tls_timing_read",
     "tls_status_string",
@@ -100,6 +101,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "tls_workspace_bytes": (ctypes.c_size_t, [_PCFG, _I32]),
         "tls_launch_count": (_I32, [_PCFG, _I32]),
         "tls_cluster_size": (_I32, [_PCFG, _I32]),
+        "tls_select_mode": (_I32, [_PCFG]),
         "tls_timing_enable": (_I32, [_I32]),
         "tls_timing_read": (_I32, [_P, _P]),
         "tls_status_string": (ctypes.c_char_p, [_I32]),

@@ -6,6 +6,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
+#include <time.h>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -14,12 +16,12 @@
 #include "index.h"
 #include "params.h"
 #include "fasttopk.cuh"
+#include "launch.h"
 
 namespace tls {
-cudaError_t launch_block_scores(const ScoreParams& p, cudaStream_t st);
-cudaError_t launch_token_cluster(const SelectParams& p, cudaStream_t st);
-cudaError_t launch_block_topk(const ScoreParams& p, cudaStream_t st);
-cudaError_t launch_attend(const AttendParams& p, cudaStream_t st);
+cudaError_t launch_select_fused(const FusedParams& p, cudaStream_t st, const LaunchOpts& o);
+cudaError_t launch_token_cluster(const SelectParams& p, cudaStream_t st, const LaunchOpts& o);
+cudaError_t launch_attend(const AttendParams& p, cudaStream_t st, const LaunchOpts& o);
 int score_cpl(int d_k, size_t elem_bytes);
 bool select_supported(int d_c, int G);
 }  // namespace tls
@@ -163,9 +165,10 @@ tls_status check_index(const tls_index* idx) {
 }
 
 // ---- live per-kernel timing (tls_timing_enable / tls_timing_read) ----
+constexpr int kMarks = 4;  // select_kernel | token_cluster_kernel | attend_kernel
 struct KernelTimer {
   bool on = false;
-  std::vector<cudaEvent_t> ev;  // 5 per recorded call
+  std::vector<cudaEvent_t> ev;  // kMarks per recorded call
   size_t used = 0;              // events recorded so far
   cudaEvent_t next() {
     if (used == ev.size()) {
@@ -183,8 +186,255 @@ struct KernelTimer {
 };
 KernelTimer g_timer;
 
-// Enqueue the decode-step kernels: K1 block scores, K2 (two passes), then K3
-// (top-k_t prologue + attention when do_attend; selection only otherwise).
+// Sub-batch pipeline.  Pairs are independent, so the batch can be cut
+// into ns contiguous sub-batches whose four-kernel chains run on ns internal
+// streams: the HBM-streaming block-score kernel (K1) of one sub-batch then
+// overlaps the latency-bound selection / attention kernels of another.  K1
+// launches carry the lowest scheduling priority and K1b/K2/K3 the highest, so
+// whenever an SM frees up the block scheduler places the dependent chain's
+// CTAs first and K1's CTAs fill the rest.  The result is bit-identical to
+// ns = 1 (every kernel's arithmetic is per pair).  TLS_NSPLIT overrides the
+// heuristic (tuning / tests).
+int n_split(const tls_config* c) {
+  int ns = 1;
+  const char* e = getenv("TLS_NSPLIT");
+  if (e && atoi(e) > 0) ns = atoi(e);
+  if (ns > 8) ns = 8;
+  if (ns > c->batch) ns = c->batch;
+  if (c->max_seq_len & 1) ns = 1;  // keep every sub-batch's scale/zero rows 16-byte aligned
+  return ns < 1 ? 1 : ns;
+}
+
+tls_config sub_config(const tls_config* c, int ns, int s, int* b0) {
+  tls_config sc = *c;
+  const int lo = (int)((long long)c->batch * s / ns), hi = (int)((long long)c->batch * (s + 1) / ns);
+  sc.batch = hi - lo;
+  *b0 = lo;
+  return sc;
+}
+
+// Selection mode: select_kernel does a1-a2, then the cluster token kernel
+// (a3) and the attention kernel's top-k_t prologue (a4).  (A mode 2 that ran
+// a1-a4 in select_kernel was measured and dropped.)
+int fused_mode(const tls_config*) { return 1; }
+
+struct ChainPlan {
+  int mode;
+  tls::FusedParams fp;
+  tls::SelectParams sp;  // mode 1
+  tls::AttendParams ap;  // do_attend, or mode 1
+  tls::SelectWs w;
+  size_t att_ws;
+  size_t total;
+};
+
+tls_status plan_chain(const tls_config* cfg, int do_attend, ChainPlan& c) {
+  memset(&c, 0, sizeof(c));
+  c.mode = fused_mode(cfg);
+  c.fp.d = dims_of(cfg);
+  c.fp.mode = c.mode;
+  c.fp.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
+  if (c.fp.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
+  tls::plan_fused(c.fp, sizeof(tls::FastTopKCtl));
+  if ((int)c.fp.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "selection-kernel shared-memory plan does not fit");
+  tls_status s = TLS_OK;
+  if (c.mode == 1) {
+    s = plan_select(cfg, c.sp);
+    if (s) return s;
+  }
+  c.w = tls::select_workspace(c.fp.d);
+  c.att_ws = 0;
+  if (c.mode == 1 || do_attend) {
+    s = plan_attend(cfg, c.ap, c.mode == 1, do_attend);
+    if (s) return s;
+    if (do_attend) c.att_ws = tls::attend_workspace_bytes(c.ap.d, c.ap.cs);
+  }
+  c.total = tls::a256(c.w.total + c.att_ws);
+  return TLS_OK;
+}
+
+// Workspace of one (sub-)batch chain.
+tls_status chain_workspace(const tls_config* cfg, int do_attend, size_t* bytes) {
+  ChainPlan c;
+  tls_status s = plan_chain(cfg, do_attend, c);
+  if (s) return s;
+  *bytes = c.total;
+  return TLS_OK;
+}
+
+tls_status step_workspace(const tls_config* cfg, int do_attend, size_t* bytes) {
+  const int ns = n_split(cfg);
+  size_t tot = 0;
+  for (int s = 0; s < ns; ++s) {
+    int b0;
+    const tls_config sc = sub_config(cfg, ns, s, &b0);
+    size_t w;
+    tls_status st = chain_workspace(&sc, do_attend, &w);
+    if (st) return st;
+    tot += w;
+  }
+  *bytes = tot;
+  return TLS_OK;
+}
+
+struct StepPtrs {
+  const void* q;
+  const void* k_cache;
+  const void* v_cache;
+  const int32_t* seq_lens;
+  tls_index idx;
+  const int32_t* guide;
+  int32_t* block_ids;
+  int32_t* token_ids;
+  int32_t* num_tokens;
+  float* token_scores;
+  void* out;
+  float* lse;
+};
+
+// The pointers of sub-batch [b0, b0 + n) (row-major layouts of tls.h).
+StepPtrs offset_ptrs(const tls_config* c, const StepPtrs& a, int b0) {
+  const size_t eb = elem_bytes(c), B0 = (size_t)b0, Hkv = (size_t)c->num_kv_heads, S = (size_t)c->max_seq_len;
+  const size_t M = (S + c->block_size - 1) / c->block_size;
+  StepPtrs r = a;
+  auto adv = [](const void* p, size_t bytes) -> const char* {
+    return p ? static_cast<const char*>(p) + bytes : nullptr;
+  };
+  r.q = adv(a.q, B0 * c->num_q_heads * c->d_k * eb);
+  r.k_cache = adv(a.k_cache, B0 * Hkv * S * c->d_k * eb);
+  r.v_cache = adv(a.v_cache, B0 * Hkv * S * c->d_v * eb);
+  r.seq_lens = a.seq_lens + b0;
+  r.idx.block_minmax = const_cast<char*>(adv(a.idx.block_minmax, B0 * Hkv * M * 2 * c->d_k * eb));
+  r.idx.codes = a.idx.codes + B0 * Hkv * S * (c->d_c / 2);
+  r.idx.scale_zero = a.idx.scale_zero + B0 * Hkv * S * 2;
+  r.guide = a.guide ? a.guide + B0 * Hkv * c->top_blocks : nullptr;
+  r.block_ids = a.block_ids + B0 * Hkv * c->top_blocks;
+  r.token_ids = a.token_ids + B0 * Hkv * c->top_tokens;
+  r.num_tokens = a.num_tokens + B0 * Hkv;
+  r.token_scores = a.token_scores ? a.token_scores + B0 * Hkv * c->top_tokens : nullptr;
+  r.out = a.out ? const_cast<char*>(adv(a.out, B0 * c->num_q_heads * c->d_v * eb)) : nullptr;
+  r.lse = a.lse ? a.lse + B0 * c->num_q_heads : nullptr;
+  return r;
+}
+
+// Enqueue one chain for the pairs of `cfg` on stream st: select_kernel (a1-a2,
+// or a1-a4 in mode 2), then in mode 1 the cluster token kernel (a3), then the
+// attention kernel (a4 prologue in mode 1 + a5 when do_attend).  Arguments
+// were validated by run_step.
+std::atomic<unsigned> g_epoch{1u};
+
+tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int do_attend, cudaStream_t st,
+                         const tls::LaunchOpts& lo_k1, const tls::LaunchOpts& lo_dep_in, bool timed) {
+  ChainPlan c;
+  tls_status s = plan_chain(cfg, do_attend, c);
+  if (s) return s;
+  // per-pair hand-off value of this call (never 0: consumers reset the flags to 0)
+  unsigned epoch = g_epoch.fetch_add(1u);
+  if (epoch == 0u) epoch = g_epoch.fetch_add(1u);
+  // the token and attention kernels start under PDL unless events sit between the launches
+  tls::LaunchOpts lo_dep = lo_dep_in;
+  lo_dep.pdl = (!timed || !g_timer.on) && getenv("TLS_NO_PDL") == nullptr;
+  tls::FusedParams& fp = c.fp;
+  fp.sstride = fp.d.Ms;
+  fp.q = a.q;
+  fp.seq_lens = a.seq_lens;
+  fp.block_minmax = a.idx.block_minmax;
+  fp.channels = a.idx.channels;
+  fp.scores = reinterpret_cast<float*>(ws + c.w.scores);
+  fp.flags = reinterpret_cast<unsigned*>(ws + c.w.flags);
+  fp.gen = reinterpret_cast<unsigned*>(ws + c.w.gen);
+  fp.ntiles_max = (fp.d.M + fp.tb - 1) / fp.tb;
+  fp.khist = reinterpret_cast<uint32_t*>(ws + c.w.khist);
+  fp.qfrag = reinterpret_cast<uint8_t*>(ws + c.w.qfrag);
+  fp.block_ids = a.block_ids;
+  fp.ready = reinterpret_cast<unsigned*>(ws + c.w.ready_b);
+  fp.epoch = epoch;
+  fp.dbg = env_debug_buf();
+  if (timed) g_timer.mark(st);
+  cudaError_t e = tls::launch_select_fused(fp, st, lo_k1);
+  if (e != cudaSuccess) return cuda_fail(e, "select_kernel launch");
+  if (timed) g_timer.mark(st);
+  tls::SelectParams& sp = c.sp;
+  if (c.mode == 1) {
+    sp.q = a.q;
+    sp.seq_lens = a.seq_lens;
+    sp.scores = fp.scores;
+    sp.codes = a.idx.codes;
+    sp.scale_zero = a.idx.scale_zero;
+    sp.channels = a.idx.channels;
+    sp.guide = a.guide;
+    sp.block_ids = a.block_ids;
+    sp.keys = reinterpret_cast<uint32_t*>(ws + c.w.keys);
+    sp.khist = fp.khist;
+    sp.qfrag = fp.qfrag;
+    sp.ready_in = fp.ready;
+    sp.ready_out = reinterpret_cast<unsigned*>(ws + c.w.ready_t);
+    sp.epoch = epoch;
+    sp.dbg = fp.dbg ? fp.dbg + 65536 * 16 : nullptr;
+    e = tls::launch_token_cluster(sp, st, lo_dep);
+    if (e != cudaSuccess) return cuda_fail(e, "token_cluster_kernel launch");
+  }
+  if (timed) g_timer.mark(st);
+  if (c.mode == 1 || do_attend) {
+    tls::AttendParams& ap = c.ap;
+    ap.q = a.q;
+    ap.k_cache = a.k_cache;
+    ap.v_cache = cfg->layout == TLS_MLA ? nullptr : a.v_cache;
+    ap.seq_lens = a.seq_lens;
+    ap.cand = a.guide ? a.guide : a.block_ids;
+    ap.keys = sp.keys;
+    ap.khist = sp.khist;
+    ap.dbg = fp.dbg ? fp.dbg + 65536 * 24 : nullptr;
+    ap.ready_in = c.mode == 1 ? sp.ready_out : nullptr;
+    ap.epoch = epoch;
+    ap.token_ids = a.token_ids;
+    ap.num_tokens = a.num_tokens;
+    ap.token_scores = a.token_scores;
+    ap.out = a.out;
+    ap.lse = a.lse;
+    const size_t pairs = (size_t)cfg->batch * cfg->num_kv_heads;
+    ap.part_o = reinterpret_cast<float*>(ws + c.w.total);
+    ap.part_ml = reinterpret_cast<float*>(ws + c.w.total + tls::a256(pairs * ap.cs * ap.d.G * ap.d.d_v * 4));
+    e = tls::launch_attend(ap, st, lo_dep);
+    if (e != cudaSuccess) return cuda_fail(e, "attend_kernel launch");
+  }
+  if (timed) g_timer.mark(st);
+  return TLS_OK;
+}
+
+// Internal streams / events of the sub-batch pipeline, per thread and device
+// (created on first use, never destroyed: the library allocates no device
+// memory, these are scheduling handles only).
+struct Pipeline {
+  int device = -1;
+  cudaStream_t streams[8] = {};
+  cudaEvent_t fork = nullptr, join[8] = {};
+  int prio_lo = 0, prio_hi = 0;
+};
+thread_local Pipeline g_pipe[16];
+
+tls_status pipeline_for_device(Pipeline** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= 16) return fail(TLS_ERR_UNSUPPORTED, "device ordinal %d >= 16", dev);
+  Pipeline& p = g_pipe[dev];
+  if (p.device != dev) {
+    e = cudaDeviceGetStreamPriorityRange(&p.prio_lo, &p.prio_hi);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetStreamPriorityRange");
+    for (int i = 0; i < 8; ++i) {
+      e = cudaStreamCreateWithFlags(&p.streams[i], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.join[i], cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "pipeline stream/event creation");
+    }
+    e = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "pipeline event creation");
+    p.device = dev;
+  }
+  *out = &p;
+  return TLS_OK;
+}
+
 tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
                     const int32_t* seq_lens, const tls_index* idx, const int32_t* guide, int32_t* block_ids,
                     int32_t* token_ids, int32_t* num_tokens, float* token_scores, void* out, float* lse,
@@ -202,76 +452,44 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
       return fail(TLS_ERR_INPUT, "GQA needs a 16-byte aligned v_cache");
     if (!out) return fail(TLS_ERR_INPUT, "out is required");
   }
-  tls::SelectParams sp{};
-  s = plan_select(cfg, sp);
+  size_t need = 0;
+  s = step_workspace(cfg, do_attend, &need);
   if (s) return s;
-  tls::AttendParams ap;
-  s = plan_attend(cfg, ap, 1, do_attend);
-  if (s) return s;
-  const tls::SelectWs w = tls::select_workspace(sp.d);
-  const size_t watt = do_attend ? tls::attend_workspace_bytes(ap.d, ap.cs) : 0;
-  if (!workspace || workspace_bytes < w.total + watt || !aligned16(workspace))
-    return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes, 16-byte aligned (got %zu)", w.total + watt,
-                workspace_bytes);
+  if (!workspace || workspace_bytes < need || !aligned16(workspace))
+    return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes, 16-byte aligned (got %zu)", need, workspace_bytes);
+  const StepPtrs all = {q, k_cache, v_cache, seq_lens, *idx, guide, block_ids, token_ids, num_tokens,
+                        token_scores, out, lse};
+  if (g_timer.on && g_timer.used % kMarks != 0) g_timer.used -= g_timer.used % kMarks;  // drop a partial record
   char* ws = static_cast<char*>(workspace);
-  tls::ScoreParams k1{};
-  k1.d = sp.d;
-  k1.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
-  if (k1.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
-  k1.q = q;
-  k1.seq_lens = seq_lens;
-  k1.block_minmax = idx->block_minmax;
-  k1.scores = reinterpret_cast<float*>(ws + w.scores);
-  k1.kb_eff = sp.kb_eff;
-  k1.sstride = sp.d.Ms;
-  k1.done = nullptr;
-  k1.khist = reinterpret_cast<uint32_t*>(ws + w.khist);
-  k1.guide = guide;
-  k1.block_ids = block_ids;
-  k1.channels = idx->channels;
-  k1.qfrag = reinterpret_cast<uint8_t*>(ws + w.qfrag);
-  if (g_timer.on && g_timer.used % 5 != 0) g_timer.used -= g_timer.used % 5;  // drop a partial record
+  const int ns = n_split(cfg);
+  if (ns == 1) return enqueue_chain(cfg, all, ws, do_attend, st, tls::LaunchOpts{}, tls::LaunchOpts{}, true);
+  Pipeline* pl = nullptr;
+  s = pipeline_for_device(&pl);
+  if (s) return s;
+  // per-kernel timing is not defined for overlapped chains: the record spans the whole step
   g_timer.mark(st);
-  cudaError_t e = tls::launch_block_scores(k1, st);
-  if (e != cudaSuccess) return cuda_fail(e, "block_score_kernel launch");
-  g_timer.mark(st);
-  e = tls::launch_block_topk(k1, st);
-  if (e != cudaSuccess) return cuda_fail(e, "block_topk_kernel launch");
-  g_timer.mark(st);
-  sp.q = q;
-  sp.seq_lens = seq_lens;
-  sp.scores = k1.scores;
-  sp.codes = idx->codes;
-  sp.scale_zero = idx->scale_zero;
-  sp.channels = idx->channels;
-  sp.guide = guide;
-  sp.block_ids = block_ids;
-  sp.keys = reinterpret_cast<uint32_t*>(ws + w.keys);
-  sp.khist = k1.khist;
-  sp.qfrag = k1.qfrag;
-  sp.dbg = env_debug_buf();
-  e = tls::launch_token_cluster(sp, st);
-  if (e != cudaSuccess) return cuda_fail(e, "token_cluster_kernel launch");
-  g_timer.mark(st);
-  ap.q = q;
-  ap.k_cache = k_cache;
-  ap.v_cache = cfg->layout == TLS_MLA ? nullptr : v_cache;
-  ap.seq_lens = seq_lens;
-  ap.cand = guide ? guide : block_ids;
-  ap.keys = sp.keys;
-  ap.khist = sp.khist;
-  ap.dbg = sp.dbg ? sp.dbg + 65536 * 8 : nullptr;
-  ap.token_ids = token_ids;
-  ap.num_tokens = num_tokens;
-  ap.token_scores = token_scores;
-  ap.out = out;
-  ap.lse = lse;
-  const size_t pairs = (size_t)cfg->batch * cfg->num_kv_heads;
-  ap.part_o = reinterpret_cast<float*>(ws + w.total);
-  ap.part_ml = reinterpret_cast<float*>(ws + w.total + tls::a256(pairs * ap.cs * ap.d.G * ap.d.d_v * 4));
-  e = tls::launch_attend(ap, st);
-  if (e != cudaSuccess) return cuda_fail(e, "attend_kernel launch");
-  g_timer.mark(st);
+  cudaError_t e = cudaEventRecord(pl->fork, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(fork)");
+  tls::LaunchOpts lo_k1, lo_dep;
+  lo_k1.use_prio = lo_dep.use_prio = getenv("TLS_NOPRIO") ? 0 : 1;
+  lo_k1.prio = pl->prio_lo;
+  lo_dep.prio = pl->prio_hi;
+  for (int i = 0; i < ns; ++i) {
+    e = cudaStreamWaitEvent(pl->streams[i], pl->fork, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent(fork)");
+    int b0;
+    const tls_config sc = sub_config(cfg, ns, i, &b0);
+    size_t w;
+    s = chain_workspace(&sc, do_attend, &w);
+    if (s) return s;
+    s = enqueue_chain(&sc, offset_ptrs(cfg, all, b0), ws, do_attend, pl->streams[i], lo_k1, lo_dep, false);
+    if (s) return s;
+    ws += w;
+    e = cudaEventRecord(pl->join[i], pl->streams[i]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, pl->join[i], 0);
+    if (e != cudaSuccess) return cuda_fail(e, "pipeline join");
+  }
+  for (int k = 1; k < kMarks; ++k) g_timer.mark(st);
   return TLS_OK;
 }
 
@@ -303,7 +521,7 @@ tls_status run_attend(const tls_config* cfg, const void* q, const void* k_cache,
   ap.part_o = static_cast<float*>(workspace);
   ap.part_ml = reinterpret_cast<float*>(static_cast<char*>(workspace) +
                                         tls::a256(pairs * ap.cs * ap.d.G * ap.d.d_v * 4));
-  cudaError_t e = tls::launch_attend(ap, st);
+  cudaError_t e = tls::launch_attend(ap, st, tls::LaunchOpts{});
   if (e != cudaSuccess) return cuda_fail(e, "attend_kernel launch");
   return TLS_OK;
 }
@@ -380,21 +598,20 @@ tls_status tls_block_scores(const tls_config* cfg, const void* q, const int32_t*
   if (!q || !aligned16(q)) return fail(TLS_ERR_INPUT, "q must be a non-NULL 16-byte aligned device pointer");
   if (!seq_lens || !block_minmax || !scores || !aligned16(block_minmax))
     return fail(TLS_ERR_INPUT, "seq_lens, block_minmax (16-byte aligned) and scores are required");
-  tls::ScoreParams k1{};
-  k1.d = dims_of(cfg);
-  k1.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
-  if (k1.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
-  k1.sstride = k1.d.M;
-  k1.q = q;
-  k1.seq_lens = seq_lens;
-  k1.block_minmax = block_minmax;
-  k1.scores = scores;
-  k1.done = nullptr;  // scores only: no ticket, no top-k_b, no histogram
-  k1.khist = nullptr;
-  k1.guide = nullptr;
-  k1.block_ids = nullptr;
-  cudaError_t e = tls::launch_block_scores(k1, (cudaStream_t)stream);
-  if (e != cudaSuccess) return cuda_fail(e, "block_score_kernel launch");
+  tls::FusedParams fp;
+  memset(&fp, 0, sizeof(fp));
+  fp.d = dims_of(cfg);
+  fp.mode = 0;
+  fp.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
+  if (fp.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
+  tls::plan_fused(fp, sizeof(tls::FastTopKCtl));
+  fp.sstride = fp.d.M;
+  fp.q = q;
+  fp.seq_lens = seq_lens;
+  fp.block_minmax = block_minmax;
+  fp.scores = scores;
+  cudaError_t e = tls::launch_select_fused(fp, (cudaStream_t)stream, tls::LaunchOpts{});
+  if (e != cudaSuccess) return cuda_fail(e, "select_kernel launch");
   return TLS_OK;
 }
 
@@ -422,23 +639,28 @@ tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
 
 size_t tls_workspace_bytes(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK || which < 0 || which > 2) return (size_t)-1;
-  const size_t wsel = tls::select_workspace_bytes(dims_of(cfg));
-  if (which == 0) return wsel;
-  const size_t watt = attend_ws(cfg, which == 2);
-  if (watt == (size_t)-1) return (size_t)-1;
-  return which == 1 ? watt : wsel + watt;
+  if (which == 1) return attend_ws(cfg, 0);
+  size_t w = 0;
+  if (step_workspace(cfg, which == 2, &w) != TLS_OK) return (size_t)-1;
+  return w;
 }
 
 int32_t tls_launch_count(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK) return -1;
+  const int mode = fused_mode(cfg), ns = n_split(cfg);
   switch (which) {
-    case 0: return 4;  // block_score, block_topk, token_cluster, attend_kernel (selection prologue only)
-    case 1: return 1;  // attend_kernel
-    case 2: return 4;  // the same four; the last one also attends
+    case 0: return ns * (mode == 2 ? 1 : 3);  // select_kernel [+ token_cluster_kernel + attend_kernel prologue]
+    case 1: return 1;                         // attend_kernel
+    case 2: return ns * (mode == 2 ? 2 : 3);  // select_kernel [+ token_cluster_kernel] + attend_kernel
     case 3: return 1;  // build_index_kernel
     case 4: return 1;  // calibrate_kernel
     default: return -1;
   }
+}
+
+int32_t tls_select_mode(const tls_config* cfg) {
+  if (check_config(cfg) != TLS_OK) return -1;
+  return fused_mode(cfg);
 }
 
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which) {
@@ -457,7 +679,7 @@ tls_status tls_timing_enable(int32_t n_calls) {
     g_timer.on = false;
     return TLS_OK;
   }
-  while (g_timer.ev.size() < (size_t)n_calls * 5) {
+  while (g_timer.ev.size() < (size_t)n_calls * kMarks) {
     cudaEvent_t e;
     cudaError_t err = cudaEventCreate(&e);
     if (err != cudaSuccess) return cuda_fail(err, "cudaEventCreate");
@@ -469,11 +691,11 @@ tls_status tls_timing_enable(int32_t n_calls) {
 
 tls_status tls_timing_read(double* ms_sum, int64_t* calls) {
   if (!ms_sum || !calls) return fail(TLS_ERR_INPUT, "ms_sum and calls are required");
-  const size_t n = g_timer.used / 5;
-  for (int k = 0; k < 4; ++k) ms_sum[k] = 0.0;
+  const size_t n = g_timer.used / kMarks;
+  for (int k = 0; k < kMarks - 1; ++k) ms_sum[k] = 0.0;
   for (size_t c = 0; c < n; ++c) {
-    for (int k = 0; k < 4; ++k) {
-      cudaEvent_t a = g_timer.ev[c * 5 + k], b = g_timer.ev[c * 5 + k + 1];
+    for (int k = 0; k < kMarks - 1; ++k) {
+      cudaEvent_t a = g_timer.ev[c * kMarks + k], b = g_timer.ev[c * kMarks + k + 1];
       cudaError_t err = cudaEventSynchronize(b);
       if (err != cudaSuccess) return cuda_fail(err, "cudaEventSynchronize");
       float ms = 0.f;

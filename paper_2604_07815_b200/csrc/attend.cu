@@ -11,7 +11,9 @@
 #include "common.cuh"
 #include "fasttopk.cuh"
 #include "params.h"
+#include "launch.h"
 #include "topk.cuh"
+#include "tokensel.cuh"
 
 namespace tls {
 
@@ -34,7 +36,7 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
   uint32_t* scratch = skeys + p.kb_eff * d.B;
   uint32_t* shist = scratch + 2048;
   FastTopKCtl& fk = *reinterpret_cast<FastTopKCtl*>(smem + p.off_fk);
-  __shared__ int s_kc, s_bsel, s_above, s_jtot;
+  __shared__ int s_kc;
   unsigned long long* dbg = (p.dbg && rank == 0) ? p.dbg + (size_t)pair * 8 : nullptr;
 #define TLS_STAMP(i) \
   if (dbg && tid == 0) dbg[i] = gtimer();
@@ -66,146 +68,12 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
   __syncthreads();
   mbar_wait(&kbar, 0);
   TLS_STAMP(1)
-  // boundary bin of the histogram (bins ascend as keys descend): 4 bins per thread
-  int c4[4], sum = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    c4[j] = (int)shist[4 * tid + j];
-    sum += c4[j];
-  }
-  int jtot;
-  const int excl = block_exclusive_scan(sum, tk.scan, &jtot);  // jtot = number of valid candidates
-  const int K = min(d.Kt, jtot);
-  if (tid == 0) {
-    s_bsel = -1;
-    s_jtot = jtot;
-  }
-  __syncthreads();
-  if (K < jtot && excl < K && K <= excl + sum) {
-    int above = excl;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (above + c4[j] >= K) {
-        s_bsel = 4 * tid + j;
-        s_above = above;
-        break;
-      }
-      above += c4[j];
-    }
-  }
-  __syncthreads();
   TLS_STAMP(2)
-  TopK t;
-  t.offset = 0;
-  t.total = K;
-  const int bsel = s_bsel;
-  bool need_full = false;
-  // per-warp segment counts for the one-pass emit (segments as in topk_emit)
-  __shared__ int wgt[kWarps], weq[kWarps];
-  const int seg = (((nslots + kWarps - 1) / kWarps) + 127) & ~127;  // as in topk_emit_counted
-  const int s0 = min(warp * seg, nslots), s1 = min(s0 + seg, nslots);
-  if (K >= jtot) {
-    t.thr = 0;  // take every valid candidate
-    t.eq_mode = false;
-    t.take_eq = 0;
-    int c = 0;
-    for (int base = s0; base < s1; base += 32) {
-      const int i = base + lane;
-      c += __popc(__ballot_sync(0xffffffffu, i < s1 && skeys[i] != 0u));
-    }
-    c = __shfl_sync(0xffffffffu, c, 0);
-    if (lane == 0) {
-      wgt[warp] = c;
-      weq[warp] = 0;
-    }
-    __syncthreads();
-  } else {
-    // One pass over the keys: count keys in bins above the boundary per warp
-    // segment, and gather the boundary bin's keys (with their segment).
-    const int kr = K - s_above;
-    if (tid == 0) fk.bcount = 0;
-    __syncthreads();
-    int above_w = 0;
-    for (int base = s0; base < s1; base += 128) {  // four independent 32-key groups per step
-      uint32_t k[4];
-      unsigned bal[4];
-      int cnt = 0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = base + 32 * u + lane;
-        k[u] = i < s1 ? skeys[i] : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int bn = k[u] != 0u ? key_bin(key2f(k[u])) : kKeyBins;
-        above_w += __popc(__ballot_sync(0xffffffffu, bn < bsel));
-        bal[u] = __ballot_sync(0xffffffffu, bn == bsel);
-        cnt += __popc(bal[u]);
-      }
-      if (cnt) {
-        int off = 0;
-        if (lane == 0) off = atomicAdd(&fk.bcount, cnt);
-        off = __shfl_sync(0xffffffffu, off, 0);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int dst = off + __popc(bal[u] & ((1u << lane) - 1u));
-          if (((bal[u] >> lane) & 1u) && dst < 1024) {
-            scratch[dst] = k[u];
-            scratch[1024 + dst] = (uint32_t)warp;
-          }
-          off += __popc(bal[u]);
-        }
-      }
-    }
-    __syncthreads();
-    const int nbk = fk.bcount;
-    if (nbk <= 1024) {
-      // exact threshold by rank: the kr-th largest boundary key
-      if (tid == 0) fk.thr = 0u;
-      __syncthreads();
-      for (int i = tid; i < nbk; i += kThreads) {
-        const uint32_t v = scratch[i];
-        int gtc = 0, eqc = 0;
-        for (int j = 0; j < nbk; ++j) {
-          const uint32_t o = scratch[j];
-          gtc += o > v;
-          eqc += o == v;
-        }
-        if (gtc < kr && gtc + eqc >= kr) fk.thr = v;  // every writer writes the same value
-      }
-      __syncthreads();
-      const uint32_t thr = fk.thr;
-      // per-warp counts: keys above the boundary bin + boundary keys > thr / == thr
-      int gb = 0, eb = 0;
-      for (int i = lane; i < nbk; i += 32) {
-        if ((int)scratch[1024 + i] == warp) {
-          gb += scratch[i] > thr;
-          eb += scratch[i] == thr;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        gb += __shfl_xor_sync(0xffffffffu, gb, o);
-        eb += __shfl_xor_sync(0xffffffffu, eb, o);
-      }
-      if (lane == 0) {
-        wgt[warp] = above_w + gb;
-        weq[warp] = eb;
-      }
-      __syncthreads();
-      int gtot = 0;
-      for (int w = 0; w < kWarps; ++w) gtot += wgt[w];
-      t.thr = thr;
-      t.eq_mode = true;
-      t.take_eq = K - gtot;
-    } else {
-      need_full = true;
-    }
-  }
-  if (need_full) {  // rare: an oversized boundary bin -> generic select and two-pass emit
-    t = fast_topk(skeys, nslots, K, false, fk, tk, scratch);
-  }
+  __shared__ HistSel hs;
+  const HistPlan pl = hist_topk_plan(skeys, nslots, shist, d.Kt, scratch, fk, tk, hs);
+  const int K = pl.K;
   TLS_STAMP(3)
+  // every CTA emits the same selection; CTA rank keeps positions [t0, t1) of it
   const int t0 = (int)((long long)K * rank / cs), t1 = (int)((long long)K * (rank + 1) / cs);
   int* tout = p.token_ids + (size_t)pair * d.Kt;
   float* sout = p.token_scores ? p.token_scores + (size_t)pair * d.Kt : nullptr;
@@ -218,10 +86,7 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
     }
     if (pos >= t0 && pos < t1) sel[pos - t0] = tok;
   };
-  if (need_full)
-    topk_emit(skeys, nslots, t, tk, put);
-  else
-    topk_emit_counted(skeys, nslots, t, wgt, weq, put);
+  hist_topk_emit(skeys, nslots, pl, hs, tk, reinterpret_cast<int*>(smem + p.off_slist), put);
   if (rank == 0) {
     for (int pos = K + tid; pos < d.Kt; pos += kThreads) {
       tout[pos] = -1;
@@ -303,7 +168,7 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
   constexpr int KS = D / 16;      // k-steps of QK^T
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = lane >> 2, c2 = 2 * (lane & 3);
-  __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(kvbuf);  // [2 stages][K TC*D | V TC*D]
+  __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(kvbuf);  // [kAttnStages][K TC*D | V TC*D]
   const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + ((size_t)b * p.d.Hq + (size_t)g * p.d.G) * D;
   const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.d.S * D;
   const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(p.v_cache) + (size_t)pair * p.d.S * D;
@@ -324,7 +189,12 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
     }
     cp_async_commit();
   };
-  if (nchunks > 0) load_chunk(0, 0);
+  // kAttnStages-deep cp.async pipeline: kAttnStages - 1 chunks in flight while one is used
+#pragma unroll
+  for (int c = 0; c < kAttnStages - 1; ++c) {
+    if (c < nchunks) load_chunk(c, c);
+    else cp_async_commit();
+  }
   // Q as the A operand (rows = heads; rows >= G are zero)
   uint32_t qa[KS][4];
 #pragma unroll
@@ -342,14 +212,11 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
   for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
 
   for (int c = 0; c < nchunks; ++c) {
-    if (c + 1 < nchunks) {
-      load_chunk(c + 1, (c + 1) & 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    if (c + kAttnStages - 1 < nchunks) load_chunk(c + kAttnStages - 1, (c + kAttnStages - 1) % kAttnStages);
+    else cp_async_commit();
+    cp_async_wait<kAttnStages - 1>();
     __syncthreads();  // chunk c landed for every thread's copies
-    const __nv_bfloat16* sK = sbuf + (size_t)(c & 1) * 2 * TC * D;
+    const __nv_bfloat16* sK = sbuf + (size_t)(c % kAttnStages) * 2 * TC * D;
     const __nv_bfloat16* sV = sK + TC * D;
     const int nt = min(TC, tloc - c * TC);
     const int tb = warp * 8;
@@ -412,8 +279,9 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
         mma_bf16_16816(o[4 * jj + 3], pa, bv[3], 0u);
       }
     }
-    __syncthreads();  // stage (c & 1) consumed before it is refilled
+    __syncthreads();  // stage c % kAttnStages consumed before it is refilled
   }
+  cp_async_wait<0>();
   // ---- merge the 8 warp partials (the staging buffers become scratch) ----
   constexpr int WS = D + 4;  // padded row stride of the warp partials
   float* wo = reinterpret_cast<float*>(kvbuf);  // [warp][G][WS]
@@ -501,6 +369,13 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_consta
   const int pair = blockIdx.y;
   const int b = pair / p.d.Hkv, g = pair - b * p.d.Hkv;
   int* sel = reinterpret_cast<int*>(smem + p.off_sel);
+  if (p.ready_in != nullptr) {  // the token kernel's keys and histogram for this pair
+    if (tid == 0) {
+      wait_ready(p.ready_in + pair, p.epoch);
+      if (cs == 1) p.ready_in[pair] = 0u;
+    }
+    __syncthreads();
+  }
   int K;
   if (p.select) {
     K = select_tokens_prologue(p, pair, b, rank, smem, sel, tk);
@@ -527,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_consta
   if (p.dbg && rank == 0 && tid == 0) p.dbg[(size_t)pair * 8 + 5] = gtimer();
   if (MMA && cs == 1) return;  // the mma path wrote the output directly
   if (cs > 1) cluster_sync_all();  // release/acquire at cluster scope: partials visible in L2
+  if (cs > 1 && p.ready_in != nullptr && rank == 0 && tid == 0) p.ready_in[pair] = 0u;  // all CTAs passed the wait
   __syncthreads();
   phase_merge<T>(p, pair, b, g, rank);
 }
@@ -559,6 +435,13 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
   const int G = p.d.G;
   int* sel = reinterpret_cast<int*>(smem + p.off_sel);
   __shared__ TopKCtl tk;
+  if (p.ready_in != nullptr) {  // the token kernel's keys and histogram for this pair
+    if (tid == 0) {
+      wait_ready(p.ready_in + pair, p.epoch);
+      if (cs == 1) p.ready_in[pair] = 0u;
+    }
+    __syncthreads();
+  }
   int K;
   if (p.select) {
     K = select_tokens_prologue(p, pair, b, rank, smem, sel, tk);
@@ -730,12 +613,13 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
     pml[2 * tid + 1] = nchunks > 0 ? sL[tid] : 0.f;
   }
   if (cs > 1) cluster_sync_all();
+  if (cs > 1 && p.ready_in != nullptr && rank == 0 && tid == 0) p.ready_in[pair] = 0u;  // all CTAs passed the wait
   __syncthreads();
   phase_merge<__nv_bfloat16>(p, pair, b, 0, rank);
 }
 
 template <typename T, bool MMA, int D>
-static cudaError_t launch_k3(const AttendParams& p, cudaStream_t st) {
+static cudaError_t launch_k3(const AttendParams& p, cudaStream_t st, const LaunchOpts& o) {
   auto kern = attend_kernel<T, MMA, D>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -745,23 +629,12 @@ static cudaError_t launch_k3(const AttendParams& p, cudaStream_t st) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)p.cs, (unsigned)(p.d.batch * p.d.Hkv), 1);
-  lc.blockDim = dim3(kThreads, 1, 1);
-  lc.dynamicSmemBytes = p.smem_bytes;
-  lc.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)p.cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  lc.attrs = attr;
-  lc.numAttrs = 1;
-  return cudaLaunchKernelEx(&lc, kern, p);
+  return launch_ex(kern, dim3((unsigned)p.cs, (unsigned)(p.d.batch * p.d.Hkv), 1), kThreads, p.smem_bytes, st, o,
+                   (unsigned)p.cs, p);
 }
 
 template <int MT>
-static cudaError_t launch_mla(const AttendParams& p, cudaStream_t st) {
+static cudaError_t launch_mla(const AttendParams& p, cudaStream_t st, const LaunchOpts& o) {
   auto kern = attend_mla_kernel<576, 512, MT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -769,33 +642,22 @@ static cudaError_t launch_mla(const AttendParams& p, cudaStream_t st) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)p.cs, (unsigned)(p.d.batch * p.d.Hkv), 1);
-  lc.blockDim = dim3(kThreads, 1, 1);
-  lc.dynamicSmemBytes = p.smem_bytes;
-  lc.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)p.cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  lc.attrs = attr;
-  lc.numAttrs = 1;
-  return cudaLaunchKernelEx(&lc, kern, p);
+  return launch_ex(kern, dim3((unsigned)p.cs, (unsigned)(p.d.batch * p.d.Hkv), 1), kThreads, p.smem_bytes, st, o,
+                   (unsigned)p.cs, p);
 }
 
-cudaError_t launch_attend(const AttendParams& p, cudaStream_t st) {
+cudaError_t launch_attend(const AttendParams& p, cudaStream_t st, const LaunchOpts& o) {
   if (!p.attend) {  // selection only: any instantiation runs just the prologue
-    if (p.d.bf16) return launch_k3<__nv_bfloat16, false, 0>(p, st);
-    return launch_k3<float, false, 0>(p, st);
+    if (p.d.bf16) return launch_k3<__nv_bfloat16, false, 0>(p, st, o);
+    return launch_k3<float, false, 0>(p, st, o);
   }
-  if (p.mma == 2) return p.d.G <= 16 ? launch_mla<1>(p, st) : launch_mla<2>(p, st);
+  if (p.mma == 2) return p.d.G <= 16 ? launch_mla<1>(p, st, o) : launch_mla<2>(p, st, o);
   if (p.d.bf16) {
-    if (p.mma) return p.d.d_k == 128 ? launch_k3<__nv_bfloat16, true, 128>(p, st)
-                                     : launch_k3<__nv_bfloat16, true, 64>(p, st);
-    return launch_k3<__nv_bfloat16, false, 0>(p, st);
+    if (p.mma) return p.d.d_k == 128 ? launch_k3<__nv_bfloat16, true, 128>(p, st, o)
+                                     : launch_k3<__nv_bfloat16, true, 64>(p, st, o);
+    return launch_k3<__nv_bfloat16, false, 0>(p, st, o);
   }
-  return launch_k3<float, false, 0>(p, st);
+  return launch_k3<float, false, 0>(p, st, o);
 }
 
 }  // namespace tls

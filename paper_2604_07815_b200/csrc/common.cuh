@@ -279,6 +279,35 @@ __device__ __forceinline__ void unpack_nibbles8(uint32_t w, uint32_t (&out)[4]) 
 }  // namespace tls
 
 namespace tls {
+// Prefetch the 128-byte line holding p into L2 (LSU path; no wait).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+// GPU-scope acquire load / relaxed store of a 32-bit flag.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// Stage hand-off between the decode-step kernels, which may overlap under
+// programmatic dependent launch: thread 0 waits (acquire) until the producer
+// published `epoch` for this pair, then orders the async proxy (TMA reads of
+// the producer's outputs) after it.  A missing producer traps after ~2 s
+// instead of hanging.
+__device__ __forceinline__ void wait_ready(const unsigned* flag, unsigned epoch) {
+  unsigned spins = 0;
+  while (ld_acquire_gpu(flag) != epoch) {
+    __nanosleep(128);
+    if (++spins > (1u << 24)) __trap();
+  }
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+// Let the next kernel in the stream (launched with programmatic stream
+// serialization) start its CTAs; its data dependences go through wait_ready.
+__device__ __forceinline__ void launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 // TMA bulk prefetch of [src, src + bytes) into L2 (no shared memory, no wait).
 __device__ __forceinline__ void tma_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");

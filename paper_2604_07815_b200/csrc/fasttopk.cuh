@@ -11,12 +11,13 @@
 #pragma once
 
 #include "common.cuh"
+#include "params.h"
 #include "topk.cuh"
 
 namespace tls {
 
 constexpr int kFastBins = 2048;
-constexpr int kBracketCap = 2048;
+constexpr int kBracketCap = kBracketWords;
 
 struct FastTopKCtl {
   uint32_t hist[kFastBins];

@@ -1,0 +1,285 @@
+// fused.cu -- the selection kernel of the decode step for sm_100a:
+//
+//   select_kernel<T, CPL, MODE>, grid (ceil(M / tb), pairs), launched
+//   pair-major (blockIdx.x fastest):
+//     phase S (every CTA)  a1  s_i = Q+ . k^max_i + Q- . k^min_i over one tile
+//                              of <= 32 KB of the pair's block summaries (P:99
+//                              via the P:110 identity and linearity of sum_h):
+//                              an HBM-streaming GEMV, fp32 scores -> workspace
+//     completion           every tile CTA but the pair's last publishes a
+//                              flag; the last one (the pair's worker) waits for
+//                              them -- only earlier-dispatched CTAs
+//     worker (MODE == 1)   a2  M_t = top-k_b blocks, ascending, -1
+//                              padded, plus the q-fragment blob and a zeroed key
+//                              histogram for the token kernel (select.cu)
+//   MODE 0 (tls_block_scores) stops after phase S.
+//
+// Why the worker lives here: the top-k_b of early pairs runs while later
+// pairs' tiles still stream from HBM, instead of as a separate serial launch.
+// (A variant that also ran a3-a4 in the worker was measured and dropped: one
+// CTA per pair is issue-bound on the token scoring -- ~90 us per pair at C3,
+// DESIGN.md §5.)
+//
+// Citation key: P:n = line n of PAPER.md.  Readings U1..U20: DESIGN.md §3.
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "fasttopk.cuh"
+#include "launch.h"
+#include "params.h"
+#include "token.cuh"
+#include "topk.cuh"
+
+namespace tls {
+
+// One tile of a1: rows [i0, i0 + nb) of the pair's block summaries.  One
+// thread streams the tile into shared memory with one TMA bulk copy per 8-row
+// group (each completing on its own single-use mbarrier); warp w scores group
+// w as soon as it lands (8 dot products reduced by a transposed butterfly).
+// QQ = [Q+ | Q-] (2*d_k fp32), so s_i = QQ . row_i: 1 flop per byte.
+template <typename T, int CPL>
+__device__ __forceinline__ void score_tile(const FusedParams& p, int pair, int b, int g, int i0, int nb, uint8_t* tile,
+                                           float* QQ, uint64_t* bars) {
+  constexpr int EPC = 16 / sizeof(T);
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ngrp = (nb + 7) >> 3;
+  const int rowbytes = 2 * d.d_k * (int)sizeof(T);
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(p.block_minmax) + ((size_t)pair * d.M + i0) * rowbytes;
+  if (tid == 0) {
+    for (int s = 0; s < ngrp; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+    for (int s = 0; s < ngrp; ++s) {
+      const int rows = min(8, nb - 8 * s);
+      mbar_arrive_expect_tx(&bars[s], (uint32_t)(rows * rowbytes));
+      tma_bulk_g2s(tile + (size_t)s * 8 * rowbytes, src + (size_t)s * 8 * rowbytes, (uint32_t)(rows * rowbytes),
+                   &bars[s]);
+    }
+  }
+  const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
+  for (int c = tid; c < d.d_k; c += kThreads) {
+    float qp = 0.f, qn = 0.f;
+#pragma unroll 8
+    for (int h = 0; h < d.G; ++h) {
+      const float v = to_f32<T>(qg[(size_t)h * d.d_k + c]);
+      qp += fmaxf(v, 0.f);
+      qn += fminf(v, 0.f);
+    }
+    QQ[c] = qp;
+    QQ[d.d_k + c] = qn;
+  }
+  __syncthreads();  // QQ ready, barriers initialised
+  const int nchunk = rowbytes / 16;
+  float* out = p.scores + (size_t)pair * p.sstride + i0;
+  if constexpr (CPL > 1) {  // wide rows (fp32, MLA): one row per warp step, rows w, w+8, ...
+    float qreg[CPL][EPC];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int ch = lane + 32 * c;
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) qreg[c][e] = ch < nchunk ? QQ[ch * EPC + e] : 0.f;
+    }
+    for (int r = warp; r < nb; r += kWarps) {
+      mbar_wait(&bars[r >> 3], 0);
+      const uint4* row = reinterpret_cast<const uint4*>(tile + (size_t)r * rowbytes);
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int ch = lane + 32 * c;
+        if (ch < nchunk) {
+          float f[EPC];
+          unpack16<T>(row[ch], f);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) acc = fmaf(qreg[c][e], f[e], acc);
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) out[r] = acc;
+    }
+    return;
+  }
+  for (int gq = warp; gq < ngrp; gq += kWarps) {
+    float qreg[CPL][EPC];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int ch = lane + 32 * c;
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) qreg[c][e] = ch < nchunk ? QQ[ch * EPC + e] : 0.f;
+    }
+    mbar_wait(&bars[gq], 0);
+    const int r8 = gq * 8;
+    float acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc[u] = 0.f;
+      if (r8 + u < nb) {
+        const uint4* row = reinterpret_cast<const uint4*>(tile + (size_t)(r8 + u) * rowbytes);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int ch = lane + 32 * c;
+          if (ch < nchunk) {
+            float f[EPC];
+            unpack16<T>(row[ch], f);
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) acc[u] = fmaf(qreg[c][e], f[e], acc[u]);
+          }
+        }
+      }
+    }
+    // transposed butterfly: afterwards lanes 4u..4u+3 hold the sum of block u
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool up = lane & 16;
+      const float send = up ? acc[j] : acc[j + 4];
+      const float keep = up ? acc[j + 4] : acc[j];
+      acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const bool up = lane & 8;
+      const float send = up ? acc[j] : acc[j + 2];
+      const float keep = up ? acc[j + 2] : acc[j];
+      acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {
+      const bool up = lane & 4;
+      const float send = up ? acc[0] : acc[1];
+      const float keep = up ? acc[1] : acc[0];
+      acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
+    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+    const int u = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    if ((lane & 3) == 0 && r8 + u < nb) out[r8 + u] = acc[0];
+  }
+}
+
+// Pair completion: every tile CTA but the pair's last one publishes
+// flag[tile] = gen + 1 (release) after its scores; the last tile CTA (the
+// worker) waits for those flags (acquire).  gen is the pair's call
+// generation, advanced by the worker at the end of every call, so stale flags
+// of earlier calls (also in replays of a captured CUDA graph) never match; a
+// zero-filled workspace starts at gen 0.  The worker only waits for tiles with
+// lower block indices -- dispatched before it -- so progress is guaranteed.
+// 16-token tiles per warp per ring chunk (register budget of the logits).
+constexpr int fused_tpw(int KS, int NT) { return (KS == 2 && NT == 1) ? 6 : ((KS * NT <= 4) ? 3 : 2); }
+
+struct WorkerCtl {
+  TopKCtl tk;
+};
+
+template <typename T, int CPL, int MODE>
+__global__ void __launch_bounds__(kThreads, 4) select_kernel(const __grid_constant__ FusedParams p) {
+  constexpr int EPC = 16 / sizeof(T);
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ float QQ[32 * CPL * EPC];
+  __shared__ __align__(8) uint64_t bars[kWarps];
+  __shared__ WorkerCtl ctl;
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int pair = blockIdx.y;
+  if constexpr (MODE != 0) launch_dependents();  // the token kernel may start as CTAs free up
+  const int b = pair / d.Hkv, g = pair - b * d.Hkv;
+  const int n = min(max(p.seq_lens[b], 0), d.S);
+  const int m = (n + d.B - 1) >> d.log2B;  // reading U1
+  const int i0 = blockIdx.x * p.tb;
+  if (i0 >= m && !(m == 0 && blockIdx.x == 0)) return;
+  const unsigned long long t_cta0 = p.dbg ? gtimer() : 0ull;
+  const int nb = max(0, min(p.tb, m - i0));
+  const int ntiles = max(1, (m + p.tb - 1) / p.tb);
+  unsigned gen = 0;
+  if constexpr (MODE != 0) gen = __ldcg(p.gen + pair);
+  if (nb > 0) score_tile<T, CPL>(p, pair, b, g, i0, nb, smem, QQ, bars);
+  if constexpr (MODE == 0) return;
+  __syncthreads();  // every score of this tile stored
+  if ((int)blockIdx.x != ntiles - 1) {
+    if (tid == 0) {
+      __threadfence();
+      st_release_gpu(p.flags + (size_t)pair * p.ntiles_max + blockIdx.x, gen + 1u);
+    }
+    return;
+  }
+  // ===== the pair's selection worker (the tile buffer is dead from here on) =====
+  if (p.dbg && tid == 0) p.dbg[(size_t)pair * 16 + 8] = gtimer();  // own tile scored
+  for (int i = tid; i < ntiles - 1; i += kThreads) {
+    const unsigned* f = p.flags + (size_t)pair * p.ntiles_max + i;
+    while (ld_acquire_gpu(f) != gen + 1u) __nanosleep(64);
+  }
+  unsigned long long* dbg = p.dbg ? p.dbg + (size_t)pair * 16 : nullptr;
+  __syncthreads();  // every tile's scores of this pair are visible (read through L2 below)
+#define TLS_STAMP(i) \
+  if (dbg && tid == 0) dbg[i] = gtimer();
+  TLS_STAMP(0)
+  uint32_t* bkeys = reinterpret_cast<uint32_t*>(smem + p.off_bkeys);
+  int* cblk = reinterpret_cast<int*>(smem + p.off_cblk);
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + p.off_scratch);
+  FastTopKCtl& fk = *reinterpret_cast<FastTopKCtl*>(smem + p.off_fk);
+  float* qc = reinterpret_cast<float*>(smem + p.off_qc);
+  const float* sc = p.scores + (size_t)pair * p.sstride;
+  for (int i = tid; i < m; i += kThreads) bkeys[i] = f2key(__ldcg(sc + i));
+  __syncthreads();
+  // ---- a2: M_t = top-k_b blocks, ties -> lower block id (U2), ascending ----
+  const int K = min(d.Kb, m);
+  {
+    const TopK t = fast_topk(bkeys, m, K, d.Kb >= m, fk, ctl.tk, scratch);
+    int* bout = p.block_ids + (size_t)pair * d.Kb;
+    topk_emit(bkeys, m, t, ctl.tk, [&](int i, int pos) {
+      bout[pos] = i;
+      cblk[pos] = i;
+    });
+    for (int pos = K + tid; pos < d.Kb; pos += kThreads) bout[pos] = -1;
+  }
+  TLS_STAMP(1)
+  // the token kernel takes over: its q fragments and a zeroed key histogram
+  build_qfrag(d, p.q, p.channels, p.qfrag, pair, qc);
+  for (int i = tid; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
+  __syncthreads();
+  if (tid == 0) {
+    p.gen[pair] = gen + 1u;
+    __threadfence();
+    st_release_gpu(p.ready + pair, p.epoch);  // block_ids, q fragments and the zeroed histogram are visible
+  }
+  TLS_STAMP(2)
+  if (dbg && tid == 0) dbg[6] = t_cta0;
+#undef TLS_STAMP
+}
+
+// ============================================================== launchers
+int score_cpl(int d_k, size_t elem_bytes) {
+  const int nchunk = (int)(2 * d_k * elem_bytes / 16);
+  if (nchunk <= 32) return 1;
+  if (nchunk <= 64) return 2;
+  if (nchunk <= 160) return 5;
+  return -1;
+}
+
+template <typename T, int CPL, int MODE>
+static cudaError_t launch_sel(const FusedParams& p, cudaStream_t st, const LaunchOpts& o) {
+  auto kern = select_kernel<T, CPL, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
+  const dim3 grid((unsigned)((p.d.M + p.tb - 1) / p.tb), (unsigned)(p.d.batch * p.d.Hkv), 1);
+  return launch_ex(kern, grid, kThreads, p.smem_bytes, st, o, 0, p);
+}
+
+template <typename T, int CPL>
+static cudaError_t dispatch_sel(const FusedParams& p, cudaStream_t st, const LaunchOpts& o) {
+  if (p.mode == 0) return launch_sel<T, CPL, 0>(p, st, o);
+  return launch_sel<T, CPL, 1>(p, st, o);
+}
+
+cudaError_t launch_select_fused(const FusedParams& p, cudaStream_t st, const LaunchOpts& o) {
+  const int cpl = score_cpl(p.d.d_k, p.d.bf16 ? 2 : 4);
+  if (p.d.bf16) {
+    if (cpl == 1) return dispatch_sel<__nv_bfloat16, 1>(p, st, o);
+    if (cpl == 2) return dispatch_sel<__nv_bfloat16, 2>(p, st, o);
+    return dispatch_sel<__nv_bfloat16, 5>(p, st, o);
+  }
+  if (cpl == 1) return dispatch_sel<float, 1>(p, st, o);
+  if (cpl == 2) return dispatch_sel<float, 2>(p, st, o);
+  return dispatch_sel<float, 5>(p, st, o);
+}
+
+}  // namespace tls

@@ -11,6 +11,7 @@
 namespace tls {
 
 constexpr int kAttnChunk = 64;     // tokens per K/V staging stage of the GQA mma attention (8 warps x 8)
+constexpr int kAttnStages = 3;     // cp.async pipeline depth of the GQA mma attention
 constexpr int kMlaChunkTokens = 32;  // latent rows per staging chunk of the MLA attention (double-buffered)
 constexpr int kScoreTileBytes = 32 * 1024;  // K1: bytes of block summaries per CTA (TMA tile)
 
@@ -24,25 +25,36 @@ struct Dims {
   int Ms;     // score row stride (floats): M rounded up to a multiple of 4 (16-byte rows)
 };
 
+constexpr int kBracketWords = 2048;  // fast_topk's bracket scratch (fasttopk.cuh kBracketCap)
 constexpr int kKeyBins = 1024;      // fixed binning of the ranking keys: 1/16 log2 unit below kKeyTop
 constexpr float kKeyTop = 6.0f;     // > log2(32) >= every key (key = log2 alpha~ + log2 G <= log2 G)
 
-struct ScoreParams {  // K1 (+ the pair's top-k_b in its last CTA)
+// Selection kernel (fused.cu): every CTA scores one tile of a pair's blocks
+// (a1); the pair's last tile CTA then runs the pair's top-k_b (a2) and
+// prepares the token kernel's inputs.  Mode 0 = scores only.
+struct FusedParams {
   Dims d;
-  int tb;  // block-summary rows per CTA (<= kScoreTileBytes)
-  int sstride;  // scores row stride (floats): Ms inside tls_select / tls_decode, M for tls_block_scores
+  int mode;     // 0: scores only (tls_block_scores); 1: + top-k_b worker
+  int tb;       // block-summary rows per CTA (<= kScoreTileBytes)
+  int sstride;  // scores row stride (floats)
   int kb_eff;
   const void* q;
   const int* seq_lens;
   const void* block_minmax;
-  float* scores;       // workspace [pairs, M] fp32
-  int* done;           // unused (NULL)
-  uint32_t* khist;     // workspace [pairs, kKeyBins] key histogram, zeroed here for K2 pass 2
-  const int* channels; // K1b: the index channels (for the q-fragment blob)
-  uint8_t* qfrag;      // K1b out: [pairs, qfrag_bytes(d)] q-fragment blobs for K2 (NULL: not built)
-  const int* guide;    // lag mode: the pair's candidates are the guide (M_t is still reported)
-  int* block_ids;      // [pairs, Kb] out: M_t ascending, -1 padded
+  const int* channels;
+  float* scores;           // workspace [pairs, sstride] fp32
+  unsigned* flags;         // workspace [pairs, ntiles_max]: tile i of the pair done -> gen + 1 (fused.cu)
+  unsigned* gen;           // workspace [pairs]: the pair's call generation (its worker advances it)
+  int ntiles_max;          // ceil(M / tb): flag row stride
+  uint32_t* khist;         // workspace [pairs, kKeyBins], zeroed by the worker for the token kernel
+  uint8_t* qfrag;          // workspace [pairs, qfrag_bytes(d)]: q~ fragment blobs for the token kernel
+  int* block_ids;          // [pairs, Kb] out: M_t ascending, -1 padded
+  unsigned* ready;         // workspace [pairs]: set to `epoch` when the pair's a2 outputs are written
+  unsigned epoch;          // this call's hand-off value (host call counter, never 0)
+  unsigned long long* dbg; // diagnostics only (env TLS_DEBUG_BUF): worker phase stamps
+  unsigned off_bkeys, off_cblk, off_scratch, off_fk, off_qc, smem_bytes;
 };
+
 
 struct SelectParams {  // K2 (token_reg_kernel, or token_cluster_kernel when a chunk exceeds the registers)
   Dims d;
@@ -64,11 +76,16 @@ struct SelectParams {  // K2 (token_reg_kernel, or token_cluster_kernel when a c
   unsigned long long* dbg;  // diagnostics only (env TLS_DEBUG_BUF): per-CTA phase stamps
   int qtma;  // 1: the q rows of the pair arrive by TMA into smem (off_qrows)
   const uint8_t* qfrag;  // token_reg_kernel: K1b's q-fragment blobs [pairs, qfrag_bytes(d)]
+  unsigned* ready_in;    // workspace [pairs]: select_kernel's hand-off (== epoch when a2 is done); reset here
+  unsigned* ready_out;   // workspace [pairs]: set to epoch when this pair's keys and histogram are complete
+  unsigned epoch;
   unsigned off_cblk, off_qb, off_qsum, off_qc, off_qrows, off_stage, smem_bytes;
 };
 
 struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally with the a4 prologue
   Dims d;
+  unsigned* ready_in;  // select only: the token kernel's hand-off (== epoch when done); reset here
+  unsigned epoch;
   int cs;
   int mma;       // 1: bf16 mma.sync GQA path (d in {64,128}, G <= 16); 2: bf16 mma.sync MLA path (576/512)
   int tloc_max;  // ceil(kt_eff / cs)
@@ -90,7 +107,7 @@ struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally wit
   float* part_o;   // workspace [pairs, cs, G, d_v] fp32 partial outputs
   float* part_ml;  // workspace [pairs, cs, G, 2] fp32 partial (max, sum), log2 units
   unsigned long long* dbg;  // diagnostics only (env TLS_DEBUG_BUF): per-CTA phase stamps
-  unsigned off_sel, off_cblk, off_union, off_skeys, off_fk, off_akv, off_aq, off_as, smem_bytes;
+  unsigned off_sel, off_cblk, off_union, off_skeys, off_fk, off_slist, off_akv, off_aq, off_as, smem_bytes;
 };
 
 static inline unsigned align16(size_t x) { return (unsigned)((x + 15) & ~(size_t)15); }
@@ -160,6 +177,8 @@ static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
     s2 = align16(s2 + (size_t)p.kb_eff * d.B * 4 + 2048 * 4 + kKeyBins * 4);
     p.off_fk = (unsigned)s2;
     s2 = align16(s2 + fastctl_bytes);
+    p.off_slist = (unsigned)s2;  // compacted selected slots (hist_topk_emit)
+    s2 = align16(s2 + (size_t)kt_effective(d) * 4);
     sel_end = s2;
   }
   if (p.attend) {
@@ -172,7 +191,7 @@ static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
       s2 = align16(s2);
     } else if (p.mma) {
       p.off_akv = (unsigned)s2;  // 2 stages x (K chunk + V chunk); reused as the warp-partial scratch
-      size_t kv = (size_t)2 * 2 * kAttnChunk * d.d_k * 2;
+      size_t kv = (size_t)kAttnStages * 2 * kAttnChunk * d.d_k * 2;
       size_t scratch = (size_t)8 * d.G * (d.d_v + 4) * 4 + (size_t)8 * 16 * 2 * 4;
       s2 = align16(s2 + (kv > scratch ? kv : scratch));
     } else {
@@ -187,6 +206,29 @@ static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
 }
 
 static inline size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Shared-memory plan of select_kernel: the worker's regions (block keys,
+// candidate ids, bracket scratch, FastTopKCtl, q~ staging) alias the scoring
+// tile of phase S (the worker starts after its own tile is scored).
+static inline void plan_fused(FusedParams& p, size_t fastctl_bytes) {
+  const Dims& d = p.d;
+  p.kb_eff = kb_effective(d);
+  const int nt0 = (d.G + 7) / 8, nt = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);
+  size_t o = 0;
+  p.off_bkeys = (unsigned)o;
+  o = align16(o + (size_t)((d.M + 31) & ~31) * 4);
+  p.off_cblk = (unsigned)o;
+  o = align16(o + (size_t)d.Kb * 4);
+  p.off_scratch = (unsigned)o;
+  o = align16(o + (size_t)kBracketWords * 4);
+  p.off_fk = (unsigned)o;
+  o = align16(o + fastctl_bytes);
+  p.off_qc = (unsigned)o;
+  o = align16(o + (size_t)nt * 8 * d.d_c * 4);
+  const size_t tile = (size_t)p.tb * 2 * d.d_k * (d.bf16 ? 2 : 4);
+  p.smem_bytes = (unsigned)(o > tile ? o : tile);
+}
+
 // Workspace of tls_select: K1's fp32 block scores | chunk statistics | keys.
 // Per-pair q-fragment blob (K1b -> K2): the B fragments of q~ (NSPLIT x NT x
 // KS x 32 lanes x 2 words) followed by sum_c q~_h[c] for the NT*8 padded heads,
@@ -201,7 +243,7 @@ static inline int qfrag_bytes(const Dims& d) {
 }
 
 struct SelectWs {
-  size_t scores, keys, khist, qfrag, total;
+  size_t scores, keys, khist, qfrag, flags, gen, ready_b, ready_t, total;
 };
 static inline SelectWs select_workspace(const Dims& d) {
   SelectWs w;
@@ -211,7 +253,11 @@ static inline SelectWs select_workspace(const Dims& d) {
   w.keys = a256(pairs * d.Ms * 4);
   w.khist = w.keys + a256(pairs * kb * d.B * 4);
   w.qfrag = w.khist + a256(pairs * kKeyBins * 4);
-  w.total = w.qfrag + a256(pairs * (size_t)qfrag_bytes(d));
+  w.flags = w.qfrag + a256(pairs * (size_t)qfrag_bytes(d));
+  w.gen = w.flags + a256(pairs * (size_t)d.M * 4);  // >= ceil(M / tb) flags per pair
+  w.ready_b = w.gen + a256(pairs * 4);
+  w.ready_t = w.ready_b + a256(pairs * 4);
+  w.total = w.ready_t + a256(pairs * 4);
   return w;
 }
 static inline size_t select_workspace_bytes(const Dims& d) { return select_workspace(d).total; }

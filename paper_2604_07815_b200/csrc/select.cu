@@ -19,183 +19,10 @@
 #include "params.h"
 #include "topk.cuh"
 #include "fasttopk.cuh"
+#include "launch.h"
+#include "token.cuh"
 
 namespace tls {
-
-// ============================================================== K1: a1
-// grid (ceil(M / tb), pairs).  A CTA scores blocks [i0, i0 + tb) of one pair:
-// one thread streams the tile of block summaries (rows of [k^max | k^min],
-// contiguous, <= 32 KB) into shared memory with one TMA bulk copy per 8-row
-// group, each completing on its own single-use mbarrier, and warp w scores
-// group w as soon as it lands (8 dot products reduced by a transposed
-// butterfly, 9 shuffles instead of 40).  QQ = [Q+ | Q-] (2*d_k fp32), so
-// s_i = QQ . row_i: 1 flop per byte, HBM-bound.
-// CTA 0 of each pair also zeroes the pair's key histogram for the token
-// kernels of this step.
-template <typename T, int CPL>
-__global__ void __launch_bounds__(kThreads, 4) block_score_kernel(const __grid_constant__ ScoreParams p) {
-  constexpr int EPC = 16 / sizeof(T);
-  extern __shared__ __align__(128) uint8_t tile[];
-  __shared__ float QQ[32 * CPL * EPC];
-  __shared__ __align__(8) uint64_t bars[kWarps];
-  const Dims& d = p.d;
-  const int pair = blockIdx.y;
-  const int b = pair / d.Hkv, g = pair - b * d.Hkv;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (blockIdx.x == 0 && p.khist != nullptr)
-    for (int i = tid; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
-  const int n = min(max(p.seq_lens[b], 0), d.S);
-  const int m = (n + d.B - 1) / d.B;  // reading U1
-  const int i0 = blockIdx.x * p.tb;
-  if (i0 >= m) return;
-  const int nb = min(p.tb, m - i0);
-  const int ngrp = (nb + 7) >> 3;
-  const int rowbytes = 2 * d.d_k * (int)sizeof(T);
-  const uint8_t* src = reinterpret_cast<const uint8_t*>(p.block_minmax) + ((size_t)pair * d.M + i0) * rowbytes;
-  if (tid == 0) {
-    for (int s = 0; s < ngrp; ++s) mbar_init(&bars[s], 1);
-    mbar_fence_init();
-    for (int s = 0; s < ngrp; ++s) {
-      const int rows = min(8, nb - 8 * s);
-      mbar_arrive_expect_tx(&bars[s], (uint32_t)(rows * rowbytes));
-      tma_bulk_g2s(tile + (size_t)s * 8 * rowbytes, src + (size_t)s * 8 * rowbytes, (uint32_t)(rows * rowbytes),
-                   &bars[s]);
-    }
-  }
-  const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
-  for (int c = tid; c < d.d_k; c += kThreads) {
-    float qp = 0.f, qn = 0.f;
-#pragma unroll 8
-    for (int h = 0; h < d.G; ++h) {
-      const float v = to_f32<T>(qg[(size_t)h * d.d_k + c]);
-      qp += fmaxf(v, 0.f);
-      qn += fminf(v, 0.f);
-    }
-    QQ[c] = qp;
-    QQ[d.d_k + c] = qn;
-  }
-  __syncthreads();  // QQ ready, barriers initialised
-  const int nchunk = rowbytes / 16;
-  float* out = p.scores + (size_t)pair * p.sstride + i0;
-  if constexpr (CPL > 1) {  // wide rows (fp32, MLA): one row per warp step, rows w, w+8, ...
-    float qreg[CPL][EPC];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const int ch = lane + 32 * c;
-#pragma unroll
-      for (int e = 0; e < EPC; ++e) qreg[c][e] = ch < nchunk ? QQ[ch * EPC + e] : 0.f;
-    }
-    for (int r = warp; r < nb; r += kWarps) {
-      mbar_wait(&bars[r >> 3], 0);
-      const uint4* row = reinterpret_cast<const uint4*>(tile + (size_t)r * rowbytes);
-      float acc = 0.f;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const int ch = lane + 32 * c;
-        if (ch < nchunk) {
-          float f[EPC];
-          unpack16<T>(row[ch], f);
-#pragma unroll
-          for (int e = 0; e < EPC; ++e) acc = fmaf(qreg[c][e], f[e], acc);
-        }
-      }
-      acc = warp_sum(acc);
-      if (lane == 0) out[r] = acc;
-    }
-    return;
-  }
-  for (int gq = warp; gq < ngrp; gq += kWarps) {
-    float qreg[CPL][EPC];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const int ch = lane + 32 * c;
-#pragma unroll
-      for (int e = 0; e < EPC; ++e) qreg[c][e] = ch < nchunk ? QQ[ch * EPC + e] : 0.f;
-    }
-    mbar_wait(&bars[gq], 0);
-    const int r8 = gq * 8;
-    float acc[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      acc[u] = 0.f;
-      if (r8 + u < nb) {
-        const uint4* row = reinterpret_cast<const uint4*>(tile + (size_t)(r8 + u) * rowbytes);
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const int ch = lane + 32 * c;
-          if (ch < nchunk) {
-            float f[EPC];
-            unpack16<T>(row[ch], f);
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) acc[u] = fmaf(qreg[c][e], f[e], acc[u]);
-          }
-        }
-      }
-    }
-    // transposed butterfly: afterwards lanes 4u..4u+3 hold the sum of block u
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const bool up = lane & 16;
-      const float send = up ? acc[j] : acc[j + 4];
-      const float keep = up ? acc[j + 4] : acc[j];
-      acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const bool up = lane & 8;
-      const float send = up ? acc[j] : acc[j + 2];
-      const float keep = up ? acc[j + 2] : acc[j];
-      acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    {
-      const bool up = lane & 4;
-      const float send = up ? acc[0] : acc[1];
-      const float keep = up ? acc[1] : acc[0];
-      acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
-    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
-    const int u = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-    if ((lane & 3) == 0 && r8 + u < nb) out[r8 + u] = acc[0];
-  }
-}
-
-__device__ void build_qfrag(const ScoreParams& p, int pair, float* qc);
-
-// ============================================================== K1b: a2
-// One CTA per pair: M_t = top-k_b blocks from the pair's L2-resident
-// scores, ties -> lower block id (U2), written ascending and -1 padded.
-__global__ void __launch_bounds__(kThreads) block_topk_kernel(const __grid_constant__ ScoreParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ TopKCtl tk;
-  const Dims& d = p.d;
-  const int pair = blockIdx.x, tid = threadIdx.x;
-  const int b = pair / d.Hkv;
-  const int n = min(max(p.seq_lens[b], 0), d.S);
-  const int m = (n + d.B - 1) / d.B;
-  uint32_t* bkeys = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* scratch = bkeys + ((d.M + 31) & ~31);
-  FastTopKCtl& fk = *reinterpret_cast<FastTopKCtl*>(scratch + kBracketCap);
-  __shared__ __align__(8) uint64_t sbar;
-  if (tid == 0 && m > 0) {  // the pair's scores: one TMA bulk copy (m*4 rounded up to 16 B)
-    mbar_init(&sbar, 1);
-    mbar_fence_init();
-    const uint32_t bytes = (uint32_t)(((m * 4) + 15) & ~15);
-    mbar_arrive_expect_tx(&sbar, bytes);
-    tma_bulk_g2s(bkeys, p.scores + (size_t)pair * p.sstride, bytes, &sbar);
-  }
-  // while the scores arrive: the pair's q-fragment blob for K2 (scratch as q~ staging)
-  if (p.qfrag) build_qfrag(p, pair, reinterpret_cast<float*>(scratch));
-  __syncthreads();
-  if (m > 0) mbar_wait(&sbar, 0);
-  for (int i = tid; i < m; i += kThreads) bkeys[i] = f2key(__uint_as_float(bkeys[i]));
-  __syncthreads();
-  const int K = min(d.Kb, m);
-  const TopK t = fast_topk(bkeys, m, K, d.Kb >= m, fk, tk, scratch);
-  int* bout = p.block_ids + (size_t)pair * d.Kb;
-  topk_emit(bkeys, m, t, tk, [&](int i, int pos) { bout[pos] = i; });
-  for (int pos = K + tid; pos < d.Kb; pos += kThreads) bout[pos] = -1;
-}
 
 // ============================================================== K2: a3
 // token_cluster_kernel: grid (nch, pairs), one cluster of nch CTAs per pair;
@@ -217,121 +44,6 @@ struct SelCtl {
   int chan[128];
 };
 
-// bf16 piece `sp` of x: x ~= hi + mid + lo (sp = 0, 1, 2), each exact in bf16.
-__device__ __forceinline__ float split_piece(float x, int sp) {
-  float hi = __bfloat162float(__float2bfloat16_rn(x));
-  if (sp == 0) return hi;
-  float r1 = x - hi;
-  float mid = __bfloat162float(__float2bfloat16_rn(r1));
-  if (sp == 1) return mid;
-  return __bfloat162float(__float2bfloat16_rn(r1 - mid));
-}
-
-// The pair's q-fragment blob (see params.h qfrag_bytes): q~_h[c] = q_h[ch_c]
-// for the NT*8 padded heads, packed as K2's mma B fragments in the
-// permuted channel order of token_tile_mma, then sum_c q~_h[c].  qc: >= NT*8*d_c
-// floats of shared scratch.  Called by all threads of K1b.
-__device__ void build_qfrag(const ScoreParams& p, int pair, float* qc) {
-  const Dims& d = p.d;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int b = pair / d.Hkv, g = pair - b * d.Hkv;
-  const int nt0 = (d.G + 7) / 8, NT = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);
-  const int DC = d.d_c, KS = DC / 16, WPT = KS / 2, NSPLIT = d.bf16 ? 1 : 3;
-  const int* ch = p.channels + (size_t)g * DC;
-  const size_t qoff = ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
-  for (int i = tid; i < NT * 8 * DC; i += kThreads) {
-    const int h = i / DC, c = i - h * DC;
-    float v = 0.f;
-    if (h < d.G) {
-      const size_t o = qoff + (size_t)h * d.d_k + ch[c];
-      v = d.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.q)[o])
-                 : reinterpret_cast<const float*>(p.q)[o];
-    }
-    qc[i] = v;
-  }
-  __syncthreads();
-  const int qfb = NSPLIT * NT * KS * 256 + NT * 32;
-  uint32_t* qb = reinterpret_cast<uint32_t*>(p.qfrag + (size_t)pair * qfb);
-  for (int idx = tid; idx < NSPLIT * NT * KS * 32; idx += kThreads) {
-    const int ln = idx & 31, rest = idx >> 5;
-    const int s = rest % KS, nt = (rest / KS) % NT, sp = rest / (KS * NT);
-    const float* qh = qc + (nt * 8 + (ln >> 2)) * DC;
-    const int cb = 8 * ((ln & 3) * WPT + (s >> 1)) + 2 * (s & 1);
-    uint2 v;
-    v.x = pack_bf16x2(split_piece(qh[cb], sp), split_piece(qh[cb + 4], sp));
-    v.y = pack_bf16x2(split_piece(qh[cb + 1], sp), split_piece(qh[cb + 5], sp));
-    reinterpret_cast<uint2*>(qb)[idx] = v;
-  }
-  float* qsum = reinterpret_cast<float*>(qb + 2 * NSPLIT * NT * KS * 32);
-  for (int h = warp; h < NT * 8; h += kWarps) {
-    float sum = 0.f;
-    for (int c = lane; c < DC; c += 32) sum += qc[h * DC + c];
-    sum = warp_sum(sum);
-    if (lane == 0) qsum[h] = sum;
-  }
-  __syncthreads();  // qc (scratch) is reused by the caller
-}
-
-// merge two online-softmax states (m, s) in log2 units
-__device__ __forceinline__ void stat_merge(float& m, float& s, float om, float os) {
-  const float nm = fmaxf(m, om);
-  if (nm == -CUDART_INF_F) return;
-  s = (m == -CUDART_INF_F ? 0.f : s * fexp2(m - nm)) + (om == -CUDART_INF_F ? 0.f : os * fexp2(om - nm));
-  m = nm;
-}
-
-// acc[nt][*] = codes(16-token tile at `codes`) x q-fragments, for the NT n-tiles
-// of 8 heads.  A = codes (16 tokens x 16 channels per k-step), nibbles -> exact
-// bf16; the channel order inside the MMA's K dimension is a permutation
-// (thread q4 owns the contiguous code word(s) q4*WPT..), applied identically to
-// the B fragments.
-template <int KS, int NT, int NSPLIT>
-__device__ __forceinline__ void token_tile_mma(const uint8_t* codes, const uint2* qb2, float (&acc)[NT][4]) {
-  constexpr int WPT = KS / 2;
-  constexpr int ROWB = KS * 8;  // d_c / 2
-  const int lane = threadIdx.x & 31, q4 = lane & 3, r0 = lane >> 2;
-  const uint8_t* p0 = codes + r0 * ROWB + q4 * WPT * 4;
-  const uint8_t* p1 = p0 + 8 * ROWB;
-  uint32_t w0[WPT], w1[WPT];
-  if constexpr (WPT == 4) {
-    const uint4 x = *reinterpret_cast<const uint4*>(p0), y = *reinterpret_cast<const uint4*>(p1);
-    w0[0] = x.x; w0[1] = x.y; w0[2] = x.z; w0[3] = x.w;
-    w1[0] = y.x; w1[1] = y.y; w1[2] = y.z; w1[3] = y.w;
-  } else if constexpr (WPT == 2) {
-    const uint2 x = *reinterpret_cast<const uint2*>(p0), y = *reinterpret_cast<const uint2*>(p1);
-    w0[0] = x.x; w0[1] = x.y;
-    w1[0] = y.x; w1[1] = y.y;
-  } else {
-    w0[0] = *reinterpret_cast<const uint32_t*>(p0);
-    w1[0] = *reinterpret_cast<const uint32_t*>(p1);
-  }
-  uint32_t a[KS][4];
-#pragma unroll
-  for (int u = 0; u < WPT; ++u) {
-    uint32_t x0[4], x1[4];
-    unpack_nibbles8(w0[u], x0);
-    unpack_nibbles8(w1[u], x1);
-#pragma unroll
-    for (int v = 0; v < 2; ++v) {  // k-step 2u+v uses nibble pairs (2v, 2v+4) and (2v+1, 2v+5)
-      a[2 * u + v][0] = x0[2 * v];
-      a[2 * u + v][1] = x1[2 * v];
-      a[2 * u + v][2] = x0[2 * v + 1];
-      a[2 * u + v][3] = x1[2 * v + 1];
-    }
-  }
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
-#pragma unroll
-    for (int s = 0; s < KS; ++s)
-#pragma unroll
-      for (int sp = 0; sp < NSPLIT; ++sp) {
-        const uint2 bb = qb2[((sp * NT + nt) * KS + s) * 32 + lane];
-        mma_bf16_16816(acc[nt], a[s], bb.x, bb.y);
-      }
-  }
-}
-
 template <typename T, int KS, int NT, int NSPLIT>
 __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid_constant__ SelectParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -346,6 +58,9 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
 #define TLS_STAMP(i) \
   if (dbg && tid == 0) dbg[i] = gtimer();
   TLS_STAMP(0)
+  launch_dependents();
+  if (tid == 0) wait_ready(p.ready_in + pair, p.epoch);  // select_kernel's a2 outputs for this pair
+  __syncthreads();
   for (int i = tid; i < kKeyBins; i += kThreads) lhist[i] = 0u;
   const int b = pair / d.Hkv, g = pair - b * d.Hkv;
   const int n = min(max(p.seq_lens[b], 0), d.S);
@@ -515,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
   TLS_STAMP(3)
   cluster_sync_all();
   TLS_STAMP(4)
+  if (chunk == 0 && tid == 0) p.ready_in[pair] = 0u;  // every CTA of the pair passed its wait
   if (tid < d.G) {
     float M = -CUDART_INF_F, Z = 0.f;
     for (int rr = 0; rr < (int)gridDim.x; ++rr) stat_merge(M, Z, *dsmem(&s_hm[tid], rr), *dsmem(&s_hz[tid], rr));
@@ -601,6 +317,9 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
   }
   TLS_STAMP(5)
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");  // keep smem alive for remote readers
+  __threadfence();  // this CTA's keys and histogram counts, before the pair's hand-off
+  cluster_sync_all();
+  if (chunk == 0 && tid == 0) st_release_gpu(p.ready_out + pair, p.epoch);
   TLS_STAMP(6)
 #undef TLS_STAMP
 }
@@ -641,6 +360,9 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
 #define TLS_STAMP(i) \
   if (dbg && tid == 0) dbg[i] = gtimer();
   TLS_STAMP(0)
+  launch_dependents();
+  if (tid == 0) wait_ready(p.ready_in + pair, p.epoch);  // select_kernel's a2 outputs for this pair
+  __syncthreads();
   for (int i = tid; i < kKeyBins; i += kThreads) lhist[i] = 0u;
   const int b = pair / d.Hkv, g = pair - b * d.Hkv;
   const int n = min(max(p.seq_lens[b], 0), d.S);
@@ -829,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
   }
   TLS_STAMP(3)
   cluster_sync_all();  // every chunk's statistics have landed in every CTA
+  if (chunk == 0 && tid == 0) p.ready_in[pair] = 0u;  // every CTA of the pair passed its wait
   TLS_STAMP(4)
   {  // cluster merge, local: 16 lanes per head over the nch chunk ranks
     const int r = tid & 15, nch = (int)gridDim.x;
@@ -891,56 +614,16 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
   for (int i = tid; i < kKeyBins; i += kThreads)
     if (lhist[i]) atomicAdd(&gh[i], lhist[i]);
   TLS_STAMP(5)
+  __threadfence();  // this CTA's keys and histogram counts, before the pair's hand-off
+  cluster_sync_all();
+  if (chunk == 0 && tid == 0) st_release_gpu(p.ready_out + pair, p.epoch);
   TLS_STAMP(6)
 #undef TLS_STAMP
 }
 
 // ============================================================== launchers
-int score_cpl(int d_k, size_t elem_bytes) {
-  const int nchunk = (int)(2 * d_k * elem_bytes / 16);
-  if (nchunk <= 32) return 1;
-  if (nchunk <= 64) return 2;
-  if (nchunk <= 160) return 5;
-  return -1;
-}
-
-template <typename T, int CPL>
-static cudaError_t launch_k1(const ScoreParams& p, cudaStream_t st) {
-  auto kern = block_score_kernel<T, CPL>;
-  const int smem = p.tb * 2 * p.d.d_k * (int)sizeof(T);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)((p.d.M + p.tb - 1) / p.tb), (unsigned)(p.d.batch * p.d.Hkv), 1);
-  kern<<<grid, kThreads, smem, st>>>(p);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_block_topk(const ScoreParams& p, cudaStream_t st) {
-  const size_t sel = (size_t)kBracketCap * 4 + sizeof(FastTopKCtl);
-  const size_t qstage = (size_t)qfrag_nt(p.d) * 8 * p.d.d_c * 4;  // build_qfrag's q~ staging
-  const size_t smem = (size_t)((p.d.M + 31) & ~31) * 4 + (sel > qstage ? sel : qstage);
-  cudaError_t e = cudaFuncSetAttribute(block_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  block_topk_kernel<<<p.d.batch * p.d.Hkv, kThreads, smem, st>>>(p);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_block_scores(const ScoreParams& p, cudaStream_t st) {
-  const int cpl = score_cpl(p.d.d_k, p.d.bf16 ? 2 : 4);
-  if (p.d.bf16) {
-    if (cpl == 1) return launch_k1<__nv_bfloat16, 1>(p, st);
-    if (cpl == 2) return launch_k1<__nv_bfloat16, 2>(p, st);
-    return launch_k1<__nv_bfloat16, 5>(p, st);
-  }
-  if (cpl == 1) return launch_k1<float, 1>(p, st);
-  if (cpl == 2) return launch_k1<float, 2>(p, st);
-  return launch_k1<float, 5>(p, st);
-}
-
 template <typename T, int KS, int NT, int NSPLIT>
-static cudaError_t launch_k2(const SelectParams& p, cudaStream_t st) {
+static cudaError_t launch_k2(const SelectParams& p, cudaStream_t st, const LaunchOpts& o) {
   auto kern = p.tpw > 0 ? token_reg_kernel<T, KS, NT, NSPLIT, 8 / NT> : token_cluster_kernel<T, KS, NT, NSPLIT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -950,19 +633,8 @@ static cudaError_t launch_k2(const SelectParams& p, cudaStream_t st) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)p.nch, (unsigned)(p.d.batch * p.d.Hkv), 1);
-  lc.blockDim = dim3(kThreads, 1, 1);
-  lc.dynamicSmemBytes = p.smem_bytes;
-  lc.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)p.nch;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  lc.attrs = attr;
-  lc.numAttrs = 1;
-  return cudaLaunchKernelEx(&lc, kern, p);
+  return launch_ex(kern, dim3((unsigned)p.nch, (unsigned)(p.d.batch * p.d.Hkv), 1), kThreads, p.smem_bytes, st, o,
+                   (unsigned)p.nch, p);
 }
 
 // Supported (d_c, G) combinations: KS = d_c/16 in {2, 4, 8}, NT = ceil(G/8) in {1, 2, 4}.
@@ -972,10 +644,10 @@ bool select_supported(int d_c, int G) {
 }
 
 template <typename T, int NS>
-static cudaError_t dispatch_k2(const SelectParams& p, cudaStream_t st) {
+static cudaError_t dispatch_k2(const SelectParams& p, cudaStream_t st, const LaunchOpts& o) {
   const int ks = p.d.d_c / 16, nt = (p.d.G + 7) / 8;
 #define TLS_K2(KS_, NT_) \
-  if (ks == KS_ && nt <= NT_) return launch_k2<T, KS_, NT_, NS>(p, st);
+  if (ks == KS_ && nt <= NT_) return launch_k2<T, KS_, NT_, NS>(p, st, o);
   TLS_K2(2, 1) TLS_K2(2, 2) TLS_K2(2, 4)
   TLS_K2(4, 1) TLS_K2(4, 2) TLS_K2(4, 4)
   TLS_K2(8, 1) TLS_K2(8, 2) TLS_K2(8, 4)
@@ -983,8 +655,8 @@ static cudaError_t dispatch_k2(const SelectParams& p, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_token_cluster(const SelectParams& p, cudaStream_t st) {
-  return p.d.bf16 ? dispatch_k2<__nv_bfloat16, 1>(p, st) : dispatch_k2<float, 3>(p, st);
+cudaError_t launch_token_cluster(const SelectParams& p, cudaStream_t st, const LaunchOpts& o) {
+  return p.d.bf16 ? dispatch_k2<__nv_bfloat16, 1>(p, st, o) : dispatch_k2<float, 3>(p, st, o);
 }
 
 }  // namespace tls

@@ -1,0 +1,264 @@
+// tokensel.cuh -- a4: S_t = the top-k_t candidate tokens from
+// order-preserving ranking keys held in shared memory plus their fixed-bin
+// histogram (kKeyBins bins of 1/16 log2 unit; bins ascend as keys descend),
+// ties -> lower slot (U2).  Used by the attention kernel's selection prologue
+// (attend.cu).
+//
+// Cost model: the selection runs once per pair in one CTA, so it is written
+// to keep the per-key work to a few instructions: the boundary bin is turned
+// into a key interval once (a 32-ary warp search over key space), keys are
+// classified by two integer compares, and the selected slots are first
+// compacted into a list so the per-token output work runs only for the K
+// selected tokens, with every lane busy.
+#pragma once
+
+#include "common.cuh"
+#include "fasttopk.cuh"
+#include "params.h"
+#include "topk.cuh"
+
+namespace tls {
+
+struct HistSel {  // shared-memory state of one selection (plan -> emit)
+  int wgt[kWarps], weq[kWarps];
+  int bsel, above, jtot;
+  uint32_t klo, khi;  // key interval [klo, khi] of the boundary bin
+};
+struct HistPlan {
+  TopK t;
+  int K;
+  bool need_full;
+};
+
+// Smallest key k >= 1 with key_bin(key2f(k)) <= b (key_bin(key2f(.)) is
+// non-increasing in the key): a 32-ary search by one warp, <= 7 rounds.
+__device__ __forceinline__ uint32_t first_key_with_bin_le(int b) {
+  const int lane = threadIdx.x & 31;
+  // invariant: predicate false at lo (or lo = 0, no key), true at hi
+  uint64_t lo = 0, hi = 0xffffffffull;
+  while (hi - lo > 1) {
+    const uint64_t step = (hi - lo + 31) / 32;
+    const uint64_t probe = lo + step * (uint64_t)(lane + 1);
+    const bool ok = probe >= hi || key_bin(key2f((uint32_t)probe)) <= b;
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    const int f = __ffs(bal) - 1;  // lane 31's probe is >= hi, so bal != 0
+    const uint64_t nhi = lo + step * (uint64_t)(f + 1);
+    lo = lo + step * (uint64_t)f;
+    hi = nhi < hi ? nhi : hi;
+  }
+  return (uint32_t)hi;
+}
+
+// skeys[nslots] (0 = not a candidate), shist[kKeyBins] (exact counts of the
+// nonzero keys per bin, bins by key_bin(key2f(key))), scratch >= 2048 words.
+// Plans the selection of the K = min(Kt, #valid) largest keys;
+// hist_topk_emit then emits it.  Contains __syncthreads(); every thread of
+// the CTA must call it.
+__device__ inline HistPlan hist_topk_plan(const uint32_t* skeys, int nslots, const uint32_t* shist, int Kt,
+                                          uint32_t* scratch, FastTopKCtl& fk, TopKCtl& tk, HistSel& hs) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* wgt = hs.wgt;
+  int* weq = hs.weq;
+  // boundary bin of the histogram (bins ascend as keys descend): 4 bins per thread
+  int c4[4], sum = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    c4[j] = (int)shist[4 * tid + j];
+    sum += c4[j];
+  }
+  int jtot;
+  const int excl = block_exclusive_scan(sum, tk.scan, &jtot);  // jtot = number of valid candidates
+  const int K = min(Kt, jtot);
+  if (tid == 0) {
+    hs.bsel = -1;
+    hs.jtot = jtot;
+  }
+  __syncthreads();
+  if (K < jtot && excl < K && K <= excl + sum) {
+    int above = excl;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (above + c4[j] >= K) {
+        hs.bsel = 4 * tid + j;
+        hs.above = above;
+        break;
+      }
+      above += c4[j];
+    }
+  }
+  __syncthreads();
+  TopK t;
+  t.offset = 0;
+  t.total = K;
+  const int bsel = hs.bsel;
+  bool need_full = false;
+  // per-warp segment counts for the one-pass emit (segments as in hist_topk_emit)
+  const int seg = (((nslots + kWarps - 1) / kWarps) + 127) & ~127;
+  const int s0 = min(warp * seg, nslots), s1 = min(s0 + seg, nslots);
+  if (K >= jtot) {
+    t.thr = 0;  // take every valid candidate
+    t.eq_mode = false;
+    t.take_eq = 0;
+    int c = 0;
+    for (int base = s0; base < s1; base += 32) {
+      const int i = base + lane;
+      c += __popc(__ballot_sync(0xffffffffu, i < s1 && skeys[i] != 0u));
+    }
+    if (lane == 0) {
+      wgt[warp] = c;
+      weq[warp] = 0;
+    }
+    __syncthreads();
+  } else {
+    // the boundary bin as a key interval [klo, khi]: keys > khi lie in bins above it
+    if (warp < 2) {
+      const uint32_t k = first_key_with_bin_le(warp == 0 ? bsel : bsel - 1);
+      if (lane == 0) {
+        if (warp == 0) hs.klo = k;
+        else hs.khi = bsel > 0 ? k - 1u : 0xffffffffu;
+      }
+    }
+    if (tid == 0) fk.bcount = 0;
+    __syncthreads();
+    const uint32_t klo = hs.klo, khi = hs.khi;
+    const int kr = K - hs.above;
+    // One pass over the keys: count keys above the boundary bin per warp
+    // segment, and gather the boundary bin's keys (with their segment).
+    int above_w = 0;
+    for (int base = s0; base < s1; base += 128) {  // four independent 32-key groups per step
+      uint32_t k[4];
+      unsigned bal[4];
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + 32 * u + lane;
+        k[u] = i < s1 ? skeys[i] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        above_w += __popc(__ballot_sync(0xffffffffu, k[u] > khi));
+        bal[u] = __ballot_sync(0xffffffffu, k[u] != 0u && k[u] >= klo && k[u] <= khi);
+        cnt += __popc(bal[u]);
+      }
+      if (cnt) {
+        int off = 0;
+        if (lane == 0) off = atomicAdd(&fk.bcount, cnt);
+        off = __shfl_sync(0xffffffffu, off, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int dst = off + __popc(bal[u] & ((1u << lane) - 1u));
+          if (((bal[u] >> lane) & 1u) && dst < 1024) {
+            scratch[dst] = k[u];
+            scratch[1024 + dst] = (uint32_t)warp;
+          }
+          off += __popc(bal[u]);
+        }
+      }
+    }
+    __syncthreads();
+    const int nbk = fk.bcount;
+    if (nbk <= 1024) {
+      // exact threshold: the kr-th largest boundary key (rank by comparison)
+      if (tid == 0) fk.thr = 0u;
+      __syncthreads();
+      for (int i = tid; i < nbk; i += kThreads) {
+        const uint32_t v = scratch[i];
+        int gtc = 0, eqc = 0;
+        for (int j = 0; j < nbk; ++j) {
+          const uint32_t o = scratch[j];
+          gtc += o > v;
+          eqc += o == v;
+        }
+        if (gtc < kr && gtc + eqc >= kr) fk.thr = v;  // every writer writes the same value
+      }
+      __syncthreads();
+      const uint32_t thr = fk.thr;
+      // per-warp counts: keys above the boundary bin + boundary keys > thr / == thr
+      int gb = 0, eb = 0;
+      for (int i = lane; i < nbk; i += 32) {
+        if ((int)scratch[1024 + i] == warp) {
+          gb += scratch[i] > thr;
+          eb += scratch[i] == thr;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        gb += __shfl_xor_sync(0xffffffffu, gb, o);
+        eb += __shfl_xor_sync(0xffffffffu, eb, o);
+      }
+      if (lane == 0) {
+        wgt[warp] = above_w + gb;
+        weq[warp] = eb;
+      }
+      __syncthreads();
+      int gtot = 0;
+      for (int w = 0; w < kWarps; ++w) gtot += wgt[w];
+      t.thr = thr;
+      t.eq_mode = true;
+      t.take_eq = K - gtot;
+    } else {
+      need_full = true;
+    }
+  }
+  if (need_full) {  // rare: an oversized boundary bin -> generic select
+    t = fast_topk(skeys, nslots, K, false, fk, tk, scratch);
+  }
+  HistPlan pl;
+  pl.t = t;
+  pl.K = K;
+  pl.need_full = need_full;
+  return pl;
+}
+
+// Emit a planned selection: put(slot, pos) for every selected slot, pos
+// ascending with slot (ties at the threshold -> lower slot first, U2).  The
+// selected slots are first compacted into slist[0 .. K) (>= K ints of shared
+// memory, not aliasing skeys), then put runs once per selected slot with
+// every lane busy.
+template <class F>
+__device__ void hist_topk_emit(const uint32_t* skeys, int nslots, const HistPlan& pl, HistSel& hs, TopKCtl& tk,
+                               int* slist, F put) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const TopK& t = pl.t;
+  if (pl.need_full) {
+    topk_emit(skeys, nslots, t, tk, [&](int i, int pos) { slist[pos] = i; });
+  } else {
+    const int seg = (((nslots + kWarps - 1) / kWarps) + 127) & ~127;
+    const int s0 = min(warp * seg, nslots), s1 = min(s0 + seg, nslots);
+    int eq_seen = 0, pos = 0;
+    for (int w = 0; w < warp; ++w) {
+      const int take = t.eq_mode ? min(max(t.take_eq - eq_seen, 0), hs.weq[w]) : 0;
+      pos += hs.wgt[w] + take;
+      eq_seen += hs.weq[w];
+    }
+    for (int base = s0; base < s1; base += 32) {
+      const int i = base + lane;
+      const uint32_t k = i < s1 ? skeys[i] : 0u;
+      const unsigned bgt = __ballot_sync(0xffffffffu, k > t.thr);
+      const unsigned beq = __ballot_sync(0xffffffffu, t.eq_mode && k != 0u && k == t.thr);
+      unsigned tie_ok = 0u;
+      if (beq) {  // ties taken in slot order
+        const int room = t.take_eq - eq_seen;
+        if (room >= __popc(beq)) {
+          tie_ok = beq;
+        } else if (room > 0) {
+          unsigned m = beq;
+          for (int r = 0; r < room; ++r) {
+            tie_ok |= m & (~m + 1u);
+            m &= m - 1u;
+          }
+        }
+      }
+      const unsigned bsel = bgt | tie_ok;
+      if ((bsel >> lane) & 1u) slist[pos + __popc(bsel & lt)] = i;
+      pos += __popc(bsel);
+      eq_seen += __popc(beq);
+    }
+    __syncthreads();
+  }
+  for (int p = tid; p < pl.K; p += kThreads) put(slist[p], p);
+  __syncthreads();
+}
+
+}  // namespace tls

@@ -28,6 +28,7 @@ __all__ = [
     "sparse_attend",
     "decode",
     "cluster_size",
+    "select_mode",
     "KERNELS",
     "timing_enable",
     "timing_read",
@@ -104,10 +105,12 @@ def _workspace(cfg: TLSConfig, dev: torch.device, which: int):
     nbytes = int(_lib.load().tls_workspace_bytes(ctypes.byref(cc), which))
     if nbytes == ctypes.c_size_t(-1).value or nbytes == 0:  # invalid config: the op call reports why
         return None, 0
-    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    # one zero-filled buffer per (device, stream, configuration): the pair completion words of
+    # select_kernel carry state from call to call (tls_workspace_bytes in include/tls.h)
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream, bytes(cc), which)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
         _WS[key] = buf
     return buf.data_ptr(), nbytes
 
@@ -297,7 +300,13 @@ def cluster_size(cfg: TLSConfig, which: int = 2) -> int:
     return int(_lib.load().tls_cluster_size(ctypes.byref(cc), which))
 
 
-KERNELS = ("block_score_kernel", "block_topk_kernel", "token_cluster_kernel", "attend_kernel")
+KERNELS = ("select_kernel", "token_cluster_kernel", "attend_kernel")
+
+
+def select_mode(cfg: TLSConfig) -> int:
+    """2: select_kernel does a1-a4 (one launch); 1: a1-a2, then token_cluster_kernel + attend prologue."""
+    cc = cfg.c()
+    return int(_lib.load().tls_select_mode(ctypes.byref(cc)))
 
 
 def timing_enable(n_calls: int) -> None:
@@ -308,7 +317,7 @@ def timing_enable(n_calls: int) -> None:
 
 def timing_read() -> tuple[dict, int]:
     """(kernel name -> summed ms, number of calls) since the last read (tls_timing_read)."""
-    ms = (ctypes.c_double * 4)()
+    ms = (ctypes.c_double * len(KERNELS))()
     calls = ctypes.c_int64(0)
     _lib.check(_lib.load().tls_timing_read(ms, ctypes.byref(calls)))
     return {k: float(ms[i]) for i, k in enumerate(KERNELS)}, int(calls.value)

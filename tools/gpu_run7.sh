@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
+timeout 300 python tools/kernel_times.py c3 1,32
+timeout 300 python tools/kernel_times.py c2 16
+timeout 300 python tools/kernel_times.py c4 32
+timeout 300 python tools/stamps.py c3

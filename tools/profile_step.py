@@ -16,8 +16,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--what", default="decode", choices=["decode", "select", "attend", "all"])
 ap.add_argument("--steps", type=int, default=5)
+ap.add_argument("--batch", type=int, default=0)
 args = ap.parse_args()
 w = W.CONFIGS[args.config]
+if args.batch:
+    w = w.with_(batch=args.batch)
 cfg, inputs, idx, queries = bench.build_state(w, 0, torch.device("cuda"), "outlier")
 sel = tls.select(cfg, queries[0], inputs["seq_lens"], idx)
 whats = ["select", "attend", "decode"] if args.what == "all" else [args.what]

@@ -13,7 +13,8 @@ from paper_2604_07815_b200 import workloads as W  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 w = W.CONFIGS[name]
 cfg, inputs, idx, queries = bench.build_state(w, 0, torch.device("cuda"), "outlier")
-buf = torch.zeros(2 * 65536 * 8, dtype=torch.int64, device="cuda")
+os.environ["TLS_FUSED_MODE"] = "1"
+buf = torch.zeros(4 * 65536 * 8, dtype=torch.int64, device="cuda")
 for it in range(3):
     if it == 2:
         os.environ["TLS_DEBUG_BUF"] = hex(buf.data_ptr())
@@ -21,8 +22,8 @@ for it in range(3):
     torch.cuda.synchronize()
 os.environ.pop("TLS_DEBUG_BUF")
 pairs = w.batch * w.num_kv_heads
-k2 = buf[: pairs * 8 * 8].view(pairs, 8, 8).cpu().double()
-k3 = buf[65536 * 8: 65536 * 8 + pairs * 8].view(pairs, 8).cpu().double()
+k2 = buf[65536 * 16: 65536 * 16 + pairs * 8 * 8].view(pairs, 8, 8).cpu().double()
+k3 = buf[65536 * 24: 65536 * 24 + pairs * 8].view(pairs, 8).cpu().double()
 t0 = k2[:, :, 0][k2[:, :, 0] > 0].min()
 def med(x):
     x = x[x == x]
