@@ -202,16 +202,27 @@ tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
  * per-chunk softmax statistics, the ranking key of every candidate token and a
  * per-pair key histogram; the attention part the
  * per-CTA partial (max, sum, o) of the split-K attention, plus the pair
- * completion words of select_kernel: a call generation per pair and one flag
- * per score tile (a tile publishes generation + 1; the pair's worker waits for
- * it and advances the generation).  Sizes are rounded up to 256 B.  Contract:
- * the workspace is zero-filled before its first use (or holds what an
- * earlier call left there), and it is not written by anything else between
- * calls -- reuse the same buffer for a configuration.  Do not share one
- * workspace between calls that may run concurrently.  (size_t)-1 for an
- * invalid configuration or `which`.  A NULL / too small / misaligned
- * workspace -> TLS_ERR_WORKSPACE. */
+ * completion words of the selection kernels (tile flags and a call
+ * generation per pair; per-pair hand-off flags between the kernels).  Sizes
+ * are rounded up to 256 B.  Contract: initialise the workspace once with
+ * tls_workspace_init (every call leaves it ready for the next one), do not
+ * write it from outside between calls -- reuse one buffer per configuration
+ * -- and do not share it between calls that may run concurrently.
+ * (size_t)-1 for an invalid configuration or `which`.  A NULL / too small /
+ * misaligned workspace -> TLS_ERR_WORKSPACE. */
 size_t tls_workspace_bytes(const tls_config* cfg, int32_t which);
+
+/* Initialise a workspace before its first use (and after any outside write
+ * to it): zero-fills it and sets every block-score word to the completion
+ * sentinel 0xffffffff (a NaN no arithmetic produces).  select_kernel's pair
+ * worker waits until the pair's scores differ from the sentinel -- the
+ * scores themselves signal completion, so the tile CTAs need no fences or
+ * flags -- and writes the sentinel back after use, so every call leaves the
+ * workspace ready for the next.  Enqueued on `stream`.  Errors:
+ * TLS_ERR_WORKSPACE if the buffer is smaller than
+ * tls_workspace_bytes(cfg, which). */
+tls_status tls_workspace_init(const tls_config* cfg, int32_t which, void* workspace, size_t workspace_bytes,
+                              tls_stream_t stream);
 
 /* Number of kernel launches one call enqueues (which as above; 3 =
  * tls_build_index, 4 = tls_calibrate_channels), for launch accounting:

@@ -28,6 +28,7 @@ EXPORTS = (
     "tls_launch_count",
     "tls_cluster_size",
     "tls_select_mode",
+    "tls_workspace_init",
     "tls_timing_enable",
     "tls_timing_read",
     "tls_status_string",
@@ -102,6 +103,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "tls_launch_count": (_I32, [_PCFG, _I32]),
         "tls_cluster_size": (_I32, [_PCFG, _I32]),
         "tls_select_mode": (_I32, [_PCFG]),
+        "tls_workspace_init": (_I32, [_PCFG, _I32, _P, ctypes.c_size_t, _P]),
         "tls_timing_enable": (_I32, [_I32]),
         "tls_timing_read": (_I32, [_P, _P]),
         "tls_status_string": (ctypes.c_char_p, [_I32]),

@@ -47,6 +47,19 @@ bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 size_t elem_bytes(const tls_config* c) { return c->dtype == TLS_BF16 ? 2 : 4; }
 
 constexpr int kMaxSmem = 227 * 1024 - 8 * 1024;  // dynamic budget (static control blocks < 8 KB)
+
+// SM count of the current device (cached per device ordinal).
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int v = 0;
+    cache[dev] = (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) ? v : 148;
+  }
+  return cache[dev];
+}
+
 constexpr int kSMs = 148;
 
 // Shape / hyper-parameter checks shared by every call.
@@ -218,6 +231,13 @@ tls_config sub_config(const tls_config* c, int ns, int s, int* b0) {
 // a1-a4 in select_kernel was measured and dropped.)
 int fused_mode(const tls_config*) { return 1; }
 
+// Bytes of block summaries per select_kernel CTA (TLS_TILE_KB overrides; tuning).
+int score_tile_bytes() {
+  const char* e = getenv("TLS_TILE_KB");
+  const int kb = e ? atoi(e) : 0;
+  return (kb >= 4 && kb <= 32) ? kb * 1024 : tls::kScoreTileBytes;  // <= 8 TMA groups of 8 rows (kWarps mbarriers)
+}
+
 struct ChainPlan {
   int mode;
   tls::FusedParams fp;
@@ -233,7 +253,7 @@ tls_status plan_chain(const tls_config* cfg, int do_attend, ChainPlan& c) {
   c.mode = fused_mode(cfg);
   c.fp.d = dims_of(cfg);
   c.fp.mode = c.mode;
-  c.fp.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
+  c.fp.tb = score_tile_bytes() / (2 * cfg->d_k * (int)elem_bytes(cfg));
   if (c.fp.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
   tls::plan_fused(c.fp, sizeof(tls::FastTopKCtl));
   if ((int)c.fp.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "selection-kernel shared-memory plan does not fit");
@@ -341,15 +361,13 @@ tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int
   fp.block_minmax = a.idx.block_minmax;
   fp.channels = a.idx.channels;
   fp.scores = reinterpret_cast<float*>(ws + c.w.scores);
-  fp.flags = reinterpret_cast<unsigned*>(ws + c.w.flags);
-  fp.gen = reinterpret_cast<unsigned*>(ws + c.w.gen);
-  fp.ntiles_max = (fp.d.M + fp.tb - 1) / fp.tb;
   fp.khist = reinterpret_cast<uint32_t*>(ws + c.w.khist);
   fp.qfrag = reinterpret_cast<uint8_t*>(ws + c.w.qfrag);
   fp.block_ids = a.block_ids;
   fp.ready = reinterpret_cast<unsigned*>(ws + c.w.ready_b);
   fp.epoch = epoch;
   fp.dbg = env_debug_buf();
+  fp.dbg_flags = getenv("TLS_TOPK_SAMPLE") ? 1 : 0;
   if (timed) g_timer.mark(st);
   cudaError_t e = tls::launch_select_fused(fp, st, lo_k1);
   if (e != cudaSuccess) return cuda_fail(e, "select_kernel launch");
@@ -643,6 +661,34 @@ size_t tls_workspace_bytes(const tls_config* cfg, int32_t which) {
   size_t w = 0;
   if (step_workspace(cfg, which == 2, &w) != TLS_OK) return (size_t)-1;
   return w;
+}
+
+tls_status tls_workspace_init(const tls_config* cfg, int32_t which, void* workspace, size_t workspace_bytes,
+                              tls_stream_t stream) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if (which < 0 || which > 2) return fail(TLS_ERR_INPUT, "which must be 0, 1 or 2");
+  const size_t need = tls_workspace_bytes(cfg, which);
+  if (need == (size_t)-1) return fail(TLS_ERR_CONFIG, "invalid configuration");
+  if (!workspace || workspace_bytes < need) return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes", need);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(workspace, 0, need, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  if (which == 1) return TLS_OK;
+  // every chain's block-score buffer starts as the completion sentinel (fused.cu kScoreSentinel)
+  char* ws = static_cast<char*>(workspace);
+  const int ns = n_split(cfg);
+  for (int i = 0; i < ns; ++i) {
+    int b0;
+    const tls_config sc = sub_config(cfg, ns, i, &b0);
+    ChainPlan c;
+    s = plan_chain(&sc, which == 2, c);
+    if (s) return s;
+    e = cudaMemsetAsync(ws + c.w.scores, 0xff, (size_t)sc.batch * sc.num_kv_heads * c.fp.d.Ms * 4, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+    ws += c.total;
+  }
+  return TLS_OK;
 }
 
 int32_t tls_launch_count(const tls_config* cfg, int32_t which) {

@@ -154,20 +154,85 @@ __device__ __forceinline__ void score_tile(const FusedParams& p, int pair, int b
   }
 }
 
-// Pair completion: every tile CTA but the pair's last one publishes
-// flag[tile] = gen + 1 (release) after its scores; the last tile CTA (the
-// worker) waits for those flags (acquire).  gen is the pair's call
-// generation, advanced by the worker at the end of every call, so stale flags
-// of earlier calls (also in replays of a captured CUDA graph) never match; a
-// zero-filled workspace starts at gen 0.  The worker only waits for tiles with
-// lower block indices -- dispatched before it -- so progress is guaranteed.
-// 16-token tiles per warp per ring chunk (register budget of the logits).
-constexpr int fused_tpw(int KS, int NT) { return (KS == 2 && NT == 1) ? 6 : ((KS * NT <= 4) ? 3 : 2); }
+// Diagnostics: the sample-bracket select path of fast_topk is used when
+// FusedParams::dbg_flags bit 0 is set (env TLS_TOPK_SAMPLE); else the range
+// histogram select.
+__device__ __forceinline__ bool getenv_flag_sample(const FusedParams& p) { return p.dbg_flags & 1; }
+
+// Completion sentinel of the block-score buffer (all-ones bits: a NaN that no
+// arithmetic produces; set by tls_workspace_init, restored by every worker).
+constexpr uint32_t kScoreSentinel = 0xffffffffu;
+
+// The pair's selection worker (a2): M_t = top-k_b blocks from the pair's
+// scores (already converted to keys in smem at off_bkeys), ties -> lower block id (U2),
+// written ascending and -1 padded; then the token kernel's inputs (q
+// fragments, a zeroed key histogram), the pair's generation and the hand-off
+// flag.  Every thread of the CTA calls it; smem holds the worker regions of
+// plan_fused.
+__device__ __noinline__ void pair_worker(const FusedParams& p, int pair, int m, uint8_t* smem,
+                                         TopKCtl& tk, unsigned long long* dbg) {
+  const Dims& d = p.d;
+  const int tid = threadIdx.x;
+#define TLS_STAMP(i) \
+  if (dbg && tid == 0) dbg[i] = gtimer();
+  uint32_t* bkeys = reinterpret_cast<uint32_t*>(smem + p.off_bkeys);
+  int* cblk = reinterpret_cast<int*>(smem + p.off_cblk);
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + p.off_scratch);
+  FastTopKCtl& fk = *reinterpret_cast<FastTopKCtl*>(smem + p.off_fk);
+  float* qc = reinterpret_cast<float*>(smem + p.off_qc);
+  // prefetch the token kernel's inputs (channel ids, small query rows) while top-k_b runs
+  const int b = pair / d.Hkv, g = pair - b * d.Hkv;
+  const size_t eb = d.bf16 ? 2 : 4;
+  const uint8_t* qsrc = reinterpret_cast<const uint8_t*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k * eb;
+  const int qbytes = d.G * d.d_k * (int)eb;
+  const bool qpre = p.off_qrows != 0;  // plan_fused reserved room for the rows
+  int* chan_s = reinterpret_cast<int*>(smem + p.off_chan);
+  for (int o = tid; o < d.d_c / 4; o += kThreads)
+    cp_async16(chan_s + 4 * o, p.channels + (size_t)g * d.d_c + 4 * o, true);
+  if (qpre)
+    for (int o = tid; o < qbytes / 16; o += kThreads) cp_async16(smem + p.off_qrows + 16 * o, qsrc + 16 * o, true);
+  cp_async_commit();
+  TLS_STAMP(3)
+  // ---- a2: M_t = top-k_b blocks, ties -> lower block id (U2), ascending ----
+  const int K = min(d.Kb, m);
+  {
+    // range-histogram select (the sample-bracket path measured 2x slower on 1.5k scores)
+    const TopK t = fast_topk(bkeys, m, K, d.Kb >= m, fk, tk, getenv_flag_sample(p) ? scratch : nullptr);
+    TLS_STAMP(4)
+    int* bout = p.block_ids + (size_t)pair * d.Kb;
+    topk_emit(bkeys, m, t, tk, [&](int i, int pos) {
+      bout[pos] = i;
+      cblk[pos] = i;
+    });
+    for (int pos = K + tid; pos < d.Kb; pos += kThreads) bout[pos] = -1;
+  }
+  {  // the pair's scores back to the sentinel for the next call (ordered before it by the stream)
+    unsigned* sc = reinterpret_cast<unsigned*>(p.scores + (size_t)pair * p.sstride);
+    for (int i = tid; i < m; i += kThreads) sc[i] = kScoreSentinel;
+  }
+  TLS_STAMP(1)
+  // the token kernel takes over: its q fragments and a zeroed key histogram
+  cp_async_wait<0>();
+  __syncthreads();
+  build_qfrag(d, qpre ? static_cast<const void*>(smem + p.off_qrows) : static_cast<const void*>(qsrc), chan_s, p.qfrag,
+              pair, qc);
+  for (int i = tid; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release_gpu(p.ready + pair, p.epoch);  // block_ids, q fragments and the zeroed histogram are visible
+  }
+  TLS_STAMP(2)
+#undef TLS_STAMP
+}
 
 struct WorkerCtl {
   TopKCtl tk;
 };
 
+// Tile-per-CTA form (fp32, d_k != 128 bf16, MLA): grid (ceil(M / tb), pairs),
+// pair-major; every tile CTA but the pair's last publishes a flag, the last
+// one waits for them (only earlier-dispatched CTAs) and runs pair_worker.
 template <typename T, int CPL, int MODE>
 __global__ void __launch_bounds__(kThreads, 4) select_kernel(const __grid_constant__ FusedParams p) {
   constexpr int EPC = 16 / sizeof(T);
@@ -176,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const __grid_consta
   __shared__ __align__(8) uint64_t bars[kWarps];
   __shared__ WorkerCtl ctl;
   const Dims& d = p.d;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int pair = blockIdx.y;
   if constexpr (MODE != 0) launch_dependents();  // the token kernel may start as CTAs free up
   const int b = pair / d.Hkv, g = pair - b * d.Hkv;
@@ -186,62 +251,34 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const __grid_consta
   if (i0 >= m && !(m == 0 && blockIdx.x == 0)) return;
   const unsigned long long t_cta0 = p.dbg ? gtimer() : 0ull;
   const int nb = max(0, min(p.tb, m - i0));
-  const int ntiles = max(1, (m + p.tb - 1) / p.tb);
-  unsigned gen = 0;
-  if constexpr (MODE != 0) gen = __ldcg(p.gen + pair);
+  const int ntiles = max(1, (m + p.tb - 1) / p.tb);  // the pair's last tile CTA is its worker
   if (nb > 0) score_tile<T, CPL>(p, pair, b, g, i0, nb, smem, QQ, bars);
   if constexpr (MODE == 0) return;
-  __syncthreads();  // every score of this tile stored
-  if ((int)blockIdx.x != ntiles - 1) {
-    if (tid == 0) {
-      __threadfence();
-      st_release_gpu(p.flags + (size_t)pair * p.ntiles_max + blockIdx.x, gen + 1u);
-    }
-    return;
-  }
+  if ((int)blockIdx.x != ntiles - 1) return;  // the scores themselves signal completion (sentinel)
   // ===== the pair's selection worker (the tile buffer is dead from here on) =====
-  if (p.dbg && tid == 0) p.dbg[(size_t)pair * 16 + 8] = gtimer();  // own tile scored
-  for (int i = tid; i < ntiles - 1; i += kThreads) {
-    const unsigned* f = p.flags + (size_t)pair * p.ntiles_max + i;
-    while (ld_acquire_gpu(f) != gen + 1u) __nanosleep(64);
-  }
+  __syncthreads();  // this CTA's own scores stored
   unsigned long long* dbg = p.dbg ? p.dbg + (size_t)pair * 16 : nullptr;
-  __syncthreads();  // every tile's scores of this pair are visible (read through L2 below)
-#define TLS_STAMP(i) \
-  if (dbg && tid == 0) dbg[i] = gtimer();
-  TLS_STAMP(0)
-  uint32_t* bkeys = reinterpret_cast<uint32_t*>(smem + p.off_bkeys);
-  int* cblk = reinterpret_cast<int*>(smem + p.off_cblk);
-  uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + p.off_scratch);
-  FastTopKCtl& fk = *reinterpret_cast<FastTopKCtl*>(smem + p.off_fk);
-  float* qc = reinterpret_cast<float*>(smem + p.off_qc);
-  const float* sc = p.scores + (size_t)pair * p.sstride;
-  for (int i = tid; i < m; i += kThreads) bkeys[i] = f2key(__ldcg(sc + i));
-  __syncthreads();
-  // ---- a2: M_t = top-k_b blocks, ties -> lower block id (U2), ascending ----
-  const int K = min(d.Kb, m);
+  if (dbg && tid == 0) {
+    dbg[6] = t_cta0;
+    dbg[8] = gtimer();  // own tile scored
+  }
+  // wait for every tile's scores: the buffer holds the sentinel between calls, and the values are
+  // the data, so relaxed L2 loads suffice (no flags, no fences in the tile CTAs)
   {
-    const TopK t = fast_topk(bkeys, m, K, d.Kb >= m, fk, ctl.tk, scratch);
-    int* bout = p.block_ids + (size_t)pair * d.Kb;
-    topk_emit(bkeys, m, t, ctl.tk, [&](int i, int pos) {
-      bout[pos] = i;
-      cblk[pos] = i;
-    });
-    for (int pos = K + tid; pos < d.Kb; pos += kThreads) bout[pos] = -1;
+    uint32_t* bkeys = reinterpret_cast<uint32_t*>(smem + p.off_bkeys);
+    const unsigned* sc = reinterpret_cast<const unsigned*>(p.scores + (size_t)pair * p.sstride);
+    for (int i = tid; i < m; i += kThreads) {
+      unsigned v, spins = 0;
+      while ((v = ld_relaxed_gpu(sc + i)) == kScoreSentinel) {
+        __nanosleep(100);
+        if (++spins > (1u << 24)) __trap();
+      }
+      bkeys[i] = f2key(__uint_as_float(v));
+    }
+    __syncthreads();
   }
-  TLS_STAMP(1)
-  // the token kernel takes over: its q fragments and a zeroed key histogram
-  build_qfrag(d, p.q, p.channels, p.qfrag, pair, qc);
-  for (int i = tid; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
-  __syncthreads();
-  if (tid == 0) {
-    p.gen[pair] = gen + 1u;
-    __threadfence();
-    st_release_gpu(p.ready + pair, p.epoch);  // block_ids, q fragments and the zeroed histogram are visible
-  }
-  TLS_STAMP(2)
-  if (dbg && tid == 0) dbg[6] = t_cta0;
-#undef TLS_STAMP
+  if (dbg && tid == 0) dbg[0] = gtimer();
+  pair_worker(p, pair, m, smem, ctl.tk, dbg);
 }
 
 // ============================================================== launchers

@@ -42,17 +42,15 @@ struct FusedParams {
   const int* seq_lens;
   const void* block_minmax;
   const int* channels;
-  float* scores;           // workspace [pairs, sstride] fp32
-  unsigned* flags;         // workspace [pairs, ntiles_max]: tile i of the pair done -> gen + 1 (fused.cu)
-  unsigned* gen;           // workspace [pairs]: the pair's call generation (its worker advances it)
-  int ntiles_max;          // ceil(M / tb): flag row stride
+  float* scores;           // workspace [pairs, sstride] fp32; the completion sentinel between calls (fused.cu)
   uint32_t* khist;         // workspace [pairs, kKeyBins], zeroed by the worker for the token kernel
   uint8_t* qfrag;          // workspace [pairs, qfrag_bytes(d)]: q~ fragment blobs for the token kernel
   int* block_ids;          // [pairs, Kb] out: M_t ascending, -1 padded
   unsigned* ready;         // workspace [pairs]: set to `epoch` when the pair's a2 outputs are written
   unsigned epoch;          // this call's hand-off value (host call counter, never 0)
   unsigned long long* dbg; // diagnostics only (env TLS_DEBUG_BUF): worker phase stamps
-  unsigned off_bkeys, off_cblk, off_scratch, off_fk, off_qc, smem_bytes;
+  int dbg_flags;           // tuning: bit 0 = sample-bracket top-k_b (env TLS_TOPK_SAMPLE)
+  unsigned off_bkeys, off_cblk, off_scratch, off_fk, off_qc, off_chan, off_qrows, smem_bytes;
 };
 
 
@@ -225,6 +223,14 @@ static inline void plan_fused(FusedParams& p, size_t fastctl_bytes) {
   o = align16(o + fastctl_bytes);
   p.off_qc = (unsigned)o;
   o = align16(o + (size_t)nt * 8 * d.d_c * 4);
+  p.off_chan = (unsigned)o;
+  o = align16(o + (size_t)d.d_c * 4);
+  const size_t qbytes = (size_t)d.G * d.d_k * (d.bf16 ? 2 : 4);
+  p.off_qrows = 0;  // 0: the q rows are gathered from global memory (too large to stage)
+  if (qbytes <= 8192) {
+    p.off_qrows = (unsigned)o;
+    o = align16(o + qbytes);
+  }
   const size_t tile = (size_t)p.tb * 2 * d.d_k * (d.bf16 ? 2 : 4);
   p.smem_bytes = (unsigned)(o > tile ? o : tile);
 }
@@ -243,7 +249,7 @@ static inline int qfrag_bytes(const Dims& d) {
 }
 
 struct SelectWs {
-  size_t scores, keys, khist, qfrag, flags, gen, ready_b, ready_t, total;
+  size_t scores, keys, khist, qfrag, ready_b, ready_t, total;
 };
 static inline SelectWs select_workspace(const Dims& d) {
   SelectWs w;
@@ -253,9 +259,7 @@ static inline SelectWs select_workspace(const Dims& d) {
   w.keys = a256(pairs * d.Ms * 4);
   w.khist = w.keys + a256(pairs * kb * d.B * 4);
   w.qfrag = w.khist + a256(pairs * kKeyBins * 4);
-  w.flags = w.qfrag + a256(pairs * (size_t)qfrag_bytes(d));
-  w.gen = w.flags + a256(pairs * (size_t)d.M * 4);  // >= ceil(M / tb) flags per pair
-  w.ready_b = w.gen + a256(pairs * 4);
+  w.ready_b = w.qfrag + a256(pairs * (size_t)qfrag_bytes(d));
   w.ready_t = w.ready_b + a256(pairs * 4);
   w.total = w.ready_t + a256(pairs * 4);
   return w;

@@ -25,21 +25,20 @@ __device__ __forceinline__ float split_piece(float x, int sp) {
 // for the NT*8 padded heads, packed as K2's mma B fragments in the
 // permuted channel order of token_tile_mma, then sum_c q~_h[c].  qc: >= NT*8*d_c
 // floats of shared scratch.  Called by all threads of K1b.
-__device__ inline void build_qfrag(const Dims& d, const void* q, const int* channels, uint8_t* qfrag, int pair,
+// qrows: the pair's G query rows [G][d_k] (global or shared memory); ch: the
+// pair's d_c channel ids (global or shared memory).
+__device__ inline void build_qfrag(const Dims& d, const void* qrows, const int* ch, uint8_t* qfrag, int pair,
                                    float* qc) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int b = pair / d.Hkv, g = pair - b * d.Hkv;
   const int nt0 = (d.G + 7) / 8, NT = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);
   const int DC = d.d_c, KS = DC / 16, WPT = KS / 2, NSPLIT = d.bf16 ? 1 : 3;
-  const int* ch = channels + (size_t)g * DC;
-  const size_t qoff = ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
   for (int i = tid; i < NT * 8 * DC; i += kThreads) {
     const int h = i / DC, c = i - h * DC;
     float v = 0.f;
     if (h < d.G) {
-      const size_t o = qoff + (size_t)h * d.d_k + ch[c];
-      v = d.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(q)[o])
-                 : reinterpret_cast<const float*>(q)[o];
+      const size_t o = (size_t)h * d.d_k + ch[c];
+      v = d.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(qrows)[o])
+                 : reinterpret_cast<const float*>(qrows)[o];
     }
     qc[i] = v;
   }

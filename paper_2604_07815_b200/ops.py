@@ -110,7 +110,9 @@ def _workspace(cfg: TLSConfig, dev: torch.device, which: int):
     key = (dev, torch.cuda.current_stream(dev).cuda_stream, bytes(cc), which)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        _lib.check(_lib.load().tls_workspace_init(ctypes.byref(cc), which, buf.data_ptr(), nbytes,
+                                                  torch.cuda.current_stream(dev).cuda_stream))
         _WS[key] = buf
     return buf.data_ptr(), nbytes
 
