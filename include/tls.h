@@ -207,7 +207,8 @@ tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
  * are rounded up to 256 B.  Contract: initialise the workspace once with
  * tls_workspace_init (every call leaves it ready for the next one), do not
  * write it from outside between calls -- reuse one buffer per configuration
- * -- and do not share it between calls that may run concurrently.
+ * (and per TLS_NSPLIT, which changes the layout) -- and do not share it
+ * between calls that may run concurrently.
  * (size_t)-1 for an invalid configuration or `which`.  A NULL / too small /
  * misaligned workspace -> TLS_ERR_WORKSPACE. */
 size_t tls_workspace_bytes(const tls_config* cfg, int32_t which);

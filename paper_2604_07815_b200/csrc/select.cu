@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid
   const int rowbytes = d.d_c / 2;
   const uint8_t* cbase = p.codes + (size_t)pair * d.S * rowbytes;
   const float2* zbase = reinterpret_cast<const float2*>(p.scale_zero) + (size_t)pair * d.S;
-  const bool zal = (((size_t)pair * d.S) & 1) == 0;
+  const bool zal = (d.S & 1) == 0;  // every block's scale/zero rows 16-byte aligned and sized -> TMA
   if (nbl > 0 && tid == 0) {  // stage this chunk's candidate index (TMA bulk, one barrier)
     uint32_t bytes = 0;
     for (int k = 0; k < nbl; ++k) {
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
   const int rowbytes = d.d_c / 2;
   const uint8_t* cbase = p.codes + (size_t)pair * d.S * rowbytes;
   const float2* zbase = reinterpret_cast<const float2*>(p.scale_zero) + (size_t)pair * d.S;
-  const bool zal = (((size_t)pair * d.S) & 1) == 0;
+  const bool zal = (d.S & 1) == 0;  // every block's scale/zero rows 16-byte aligned and sized -> TMA
   const int cb0 = chunk * p.cb;
   int nbl;
   if (p.guide == nullptr) {

@@ -10,6 +10,7 @@ Citation key: P:n = line n of PAPER.md (arXiv 2604.07815).
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 from dataclasses import dataclass, field
 
@@ -107,7 +108,8 @@ def _workspace(cfg: TLSConfig, dev: torch.device, which: int):
         return None, 0
     # one zero-filled buffer per (device, stream, configuration): the pair completion words of
     # select_kernel carry state from call to call (tls_workspace_bytes in include/tls.h)
-    key = (dev, torch.cuda.current_stream(dev).cuda_stream, bytes(cc), which)
+    # (the sub-batch pipeline depth TLS_NSPLIT changes the workspace layout as well)
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream, bytes(cc), which, os.environ.get("TLS_NSPLIT", ""))
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)

@@ -121,3 +121,11 @@ def test_cluster_override(lib, monkeypatch):
         monkeypatch.setenv("TLS_CLUSTER", str(cs))
         assert lib.tls_cluster_size(ctypes.byref(c), 2) == cs
         assert lib.tls_cluster_size(ctypes.byref(c), 1) == cs
+
+
+def test_workspace_init_validates(lib):
+    c = cfg()
+    need = lib.tls_workspace_bytes(ctypes.byref(c), 2)
+    # too small -> TLS_ERR_WORKSPACE before anything is enqueued (no GPU needed)
+    assert lib.tls_workspace_init(ctypes.byref(c), 2, 16, need - 1, None) == _lib.TLS_ERR_WORKSPACE
+    assert lib.tls_workspace_init(ctypes.byref(c), 7, 16, need, None) == _lib.TLS_ERR_INPUT

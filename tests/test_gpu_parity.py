@@ -349,3 +349,48 @@ def test_kernel_timing_hook_records_every_launch():
     torch.cuda.synchronize()
     for a, b in zip(ref, res):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["gqa8", "mla", "c1"])
+def test_repeated_calls_and_launch_modes_agree(name, monkeypatch):
+    """The pair-completion protocol across calls: select_kernel's workers wait
+    for the score sentinel and restore it, and the token / attention kernels
+    wait for per-pair ready flags (epoch per call) under PDL.  Ten back-to-back
+    calls on one workspace, the same calls without PDL, and a fresh
+    (tls_workspace_init) workspace must all give bit-identical results; a
+    different query in between must not leak into the next call."""
+    w = SMALL[name]
+    cfg, inputs, idx = setup_case(w, seed=4)
+    ref = run_decode(cfg, inputs, idx)
+    q2 = inputs["q"].flip(0).contiguous()
+    for i in range(10):
+        res = run_decode(cfg, inputs, idx) if i % 2 == 0 else tls.decode(
+            cfg, q2, inputs["k_cache"], inputs["v_cache"], inputs["seq_lens"], idx)
+        if i % 2 == 0:
+            torch.cuda.synchronize()
+            for a, b in zip(ref, res):
+                assert a is None and b is None or torch.equal(a, b)
+    monkeypatch.setenv("TLS_NO_PDL", "1")
+    res = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    for a, b in zip(ref, res):
+        assert a is None and b is None or torch.equal(a, b)
+
+
+def test_sub_batch_pipeline_and_tile_size_agree(monkeypatch):
+    """TLS_NSPLIT (sub-batch chains on internal streams) and TLS_TILE_KB (block
+    rows per scoring CTA) change only scheduling: selections identical, outputs
+    equal up to the attention split-K rounding."""
+    w = SMALL["gqa4"]
+    cfg, inputs, idx = setup_case(w, seed=5)
+    ref = run_decode(cfg, inputs, idx)
+    for env in ({"TLS_NSPLIT": "3"}, {"TLS_TILE_KB": "8"}, {"TLS_TILE_KB": "16", "TLS_NSPLIT": "2"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        res = run_decode(cfg, inputs, idx)
+        torch.cuda.synchronize()
+        for i, (a, b) in enumerate(zip(ref[2:], res[2:])):
+            assert torch.equal(a, b), (env, i, (a != b).sum().item(), a.flatten()[:8], b.flatten()[:8])
+        torch.testing.assert_close(res[0].float(), ref[0].float(), rtol=0, atol=2e-2)
+        for k in env:
+            monkeypatch.delenv(k)
