@@ -232,28 +232,39 @@ __device__ void hist_topk_emit(const uint32_t* skeys, int nslots, const HistPlan
       pos += hs.wgt[w] + take;
       eq_seen += hs.weq[w];
     }
-    for (int base = s0; base < s1; base += 32) {
-      const int i = base + lane;
-      const uint32_t k = i < s1 ? skeys[i] : 0u;
-      const unsigned bgt = __ballot_sync(0xffffffffu, k > t.thr);
-      const unsigned beq = __ballot_sync(0xffffffffu, t.eq_mode && k != 0u && k == t.thr);
-      unsigned tie_ok = 0u;
-      if (beq) {  // ties taken in slot order
-        const int room = t.take_eq - eq_seen;
-        if (room >= __popc(beq)) {
-          tie_ok = beq;
-        } else if (room > 0) {
-          unsigned m = beq;
-          for (int r = 0; r < room; ++r) {
-            tie_ok |= m & (~m + 1u);
-            m &= m - 1u;
+    for (int base = s0; base < s1; base += 128) {  // four independent 32-key groups per step (ILP)
+      uint32_t k[4];
+      unsigned bgt[4], beq[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + 32 * u + lane;
+        k[u] = i < s1 ? skeys[i] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        bgt[u] = __ballot_sync(0xffffffffu, k[u] > t.thr);
+        beq[u] = __ballot_sync(0xffffffffu, t.eq_mode && k[u] != 0u && k[u] == t.thr);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        unsigned tie_ok = 0u;
+        if (beq[u]) {  // ties taken in slot order
+          const int room = t.take_eq - eq_seen;
+          if (room >= __popc(beq[u])) {
+            tie_ok = beq[u];
+          } else if (room > 0) {
+            unsigned m = beq[u];
+            for (int r = 0; r < room; ++r) {
+              tie_ok |= m & (~m + 1u);
+              m &= m - 1u;
+            }
           }
         }
+        const unsigned bsel = bgt[u] | tie_ok;
+        if ((bsel >> lane) & 1u) slist[pos + __popc(bsel & lt)] = base + 32 * u + lane;
+        pos += __popc(bsel);
+        eq_seen += __popc(beq[u]);
       }
-      const unsigned bsel = bgt | tie_ok;
-      if ((bsel >> lane) & 1u) slist[pos + __popc(bsel & lt)] = i;
-      pos += __popc(bsel);
-      eq_seen += __popc(beq);
     }
     __syncthreads();
   }
