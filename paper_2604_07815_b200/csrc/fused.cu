@@ -234,7 +234,7 @@ struct WorkerCtl {
 // pair-major; every tile CTA but the pair's last publishes a flag, the last
 // one waits for them (only earlier-dispatched CTAs) and runs pair_worker.
 template <typename T, int CPL, int MODE>
-__global__ void __launch_bounds__(kThreads, 4) select_kernel(const __grid_constant__ FusedParams p) {
+__global__ void __launch_bounds__(kThreads, 6) select_kernel(const __grid_constant__ FusedParams p) {
   constexpr int EPC = 16 / sizeof(T);
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float QQ[32 * CPL * EPC];
