@@ -137,6 +137,7 @@ tls_status plan_select(const tls_config* c, tls::SelectParams& p) {
   p.d = dims_of(c);
   const char* cbe = getenv("TLS_CHUNK_BLOCKS");
   p.cb_override = cbe ? atoi(cbe) : 0;
+  p.two_pass = getenv("TLS_K2_TWO_PASS") ? 1 : 0;
   tls::plan_select(p);
   if ((int)p.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "token-kernel shared-memory plan does not fit");
   return TLS_OK;

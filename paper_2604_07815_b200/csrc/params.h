@@ -60,6 +60,7 @@ struct SelectParams {  // K2 (token_reg_kernel, or token_cluster_kernel when a c
   int cb;              // candidate blocks per chunk CTA
   int tpw;             // > 0: token_reg_kernel with tpw 16-token tiles per warp; 0: token_cluster_kernel
   int cb_override;     // tuning: env TLS_CHUNK_BLOCKS (0 = heuristic)
+  int two_pass;        // tuning: env TLS_K2_TWO_PASS forces token_cluster_kernel
   int nch;             // chunks per pair = ceil(kb_eff / cb)
   const void* q;
   const int* seq_lens;
@@ -135,6 +136,7 @@ static inline void plan_select(SelectParams& p) {
   } else {
     p.tpw = 0;
   }
+  if (p.two_pass) p.tpw = 0;  // tuning: env TLS_K2_TWO_PASS
   if (p.cb_override > 0 && (p.tpw == 0 || p.cb_override <= cb_reg)) p.cb = p.cb_override;  // tuning
   if (p.cb > p.kb_eff) p.cb = p.kb_eff;
   p.nch = (p.kb_eff + p.cb - 1) / p.cb;

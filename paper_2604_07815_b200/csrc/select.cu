@@ -45,7 +45,7 @@ struct SelCtl {
 };
 
 template <typename T, int KS, int NT, int NSPLIT>
-__global__ void __launch_bounds__(kThreads, 3) token_cluster_kernel(const __grid_constant__ SelectParams p) {
+__global__ void __launch_bounds__(kThreads, (NT == 1 && KS * NSPLIT <= 2) ? 5 : 3) token_cluster_kernel(const __grid_constant__ SelectParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ SelCtl ctl;
   __shared__ __align__(8) uint64_t bar;
