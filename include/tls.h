@@ -227,8 +227,9 @@ tls_status tls_workspace_init(const tls_config* cfg, int32_t which, void* worksp
 
 /* Number of kernel launches one call enqueues (which as above; 3 =
  * tls_build_index, 4 = tls_calibrate_channels), for launch accounting:
- * tls_select and tls_decode 3 each (select_kernel, token_cluster_kernel,
- * attend_kernel), times TLS_NSPLIT sub-batches; tls_sparse_attend 1.
+ * tls_select and tls_decode 4 each (qq_kernel, select_kernel,
+ * token_cluster_kernel, attend_kernel), times TLS_NSPLIT sub-batches;
+ * tls_sparse_attend 1.
  * -1 for an invalid configuration. */
 int32_t tls_launch_count(const tls_config* cfg, int32_t which);
 
@@ -247,9 +248,9 @@ int32_t tls_cluster_size(const tls_config* cfg, int32_t which);
  * roofline of the dominant kernel).  While enabled, every tls_select /
  * tls_decode call records library-owned CUDA events on its stream before and
  * after each of its launches (no extra synchronisation; events sit between
- * launches that are already stream-ordered).  Slots: 0 = select_kernel
- * (a1-a2), 1 = token_cluster_kernel (a3), 2 = attend kernel (a4 prologue +
- * a5).  With TLS_NSPLIT > 1
+ * launches that are already stream-ordered).  Slots: 0 = qq_kernel +
+ * select_kernel (a1-a2), 1 = token_cluster_kernel (a3), 2 = attend kernel
+ * (a4 prologue + a5).  With TLS_NSPLIT > 1
  * the whole overlapped step is recorded in slot 2.
  *   tls_timing_enable(n): n > 0 enables and pre-creates events for n calls
  *     (more are created on demand), clearing previous records; n == 0

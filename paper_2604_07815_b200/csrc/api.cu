@@ -20,6 +20,7 @@
 
 namespace tls {
 cudaError_t launch_select_fused(const FusedParams& p, cudaStream_t st, const LaunchOpts& o);
+cudaError_t launch_qq(const FusedParams& p, cudaStream_t st, const LaunchOpts& o);
 cudaError_t launch_token_cluster(const SelectParams& p, cudaStream_t st, const LaunchOpts& o);
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t st, const LaunchOpts& o);
 int score_cpl(int d_k, size_t elem_bytes);
@@ -158,8 +159,13 @@ tls_status plan_attend(const tls_config* c, tls::AttendParams& p, int select, in
   int cs = env_cluster();
   if (!attend) cs = 1;  // selection only: one CTA per pair
   if (!cs) {
+    // split a pair's tokens over more CTAs only while the whole grid stays one wave of
+    // co-resident CTAs (MLA: one 117 KB CTA per SM; GQA mma: two) and each CTA keeps >= 64
+    // tokens (measured, C4: cs 4 -> 62 us, cs 8 -> 113 us; C2: cs 2 best)
+    const int per_sm = p.mma == 2 ? 1 : 2;
+    const int sms = num_sms();
     cs = 1;
-    while (cs < 16 && pairs * cs < kSMs && (kt + 2 * cs - 1) / (2 * cs) >= 64) cs *= 2;
+    while (cs < 16 && pairs * cs * 2 <= (long long)sms * per_sm && (kt + 2 * cs - 1) / (2 * cs) >= 64) cs *= 2;
   }
   for (;; cs *= 2) {
     if (cs > 16) return fail(TLS_ERR_UNSUPPORTED, "attention shared-memory plan does not fit");
@@ -369,8 +375,13 @@ tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int
   fp.epoch = epoch;
   fp.dbg = env_debug_buf();
   fp.dbg_flags = getenv("TLS_TOPK_SAMPLE") ? 1 : 0;
+  fp.qq = reinterpret_cast<float*>(ws + c.w.qq);
   if (timed) g_timer.mark(st);
-  cudaError_t e = tls::launch_select_fused(fp, st, lo_k1);
+  cudaError_t e = tls::launch_qq(fp, st, lo_k1);
+  if (e != cudaSuccess) return cuda_fail(e, "qq_kernel launch");
+  tls::LaunchOpts lo_sel = lo_k1;
+  lo_sel.pdl = lo_dep.pdl;  // select_kernel streams its tiles while qq_kernel finishes
+  e = tls::launch_select_fused(fp, st, lo_sel);
   if (e != cudaSuccess) return cuda_fail(e, "select_kernel launch");
   if (timed) g_timer.mark(st);
   tls::SelectParams& sp = c.sp;
@@ -696,9 +707,9 @@ int32_t tls_launch_count(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK) return -1;
   const int mode = fused_mode(cfg), ns = n_split(cfg);
   switch (which) {
-    case 0: return ns * (mode == 2 ? 1 : 3);  // select_kernel [+ token_cluster_kernel + attend_kernel prologue]
+    case 0: return ns * (mode == 2 ? 1 : 4);  // qq, select, token and attend (selection prologue only) kernels
     case 1: return 1;                         // attend_kernel
-    case 2: return ns * (mode == 2 ? 2 : 3);  // select_kernel [+ token_cluster_kernel] + attend_kernel
+    case 2: return ns * (mode == 2 ? 2 : 4);  // qq, select, token and attend kernels
     case 3: return 1;  // build_index_kernel
     case 4: return 1;  // calibrate_kernel
     default: return -1;

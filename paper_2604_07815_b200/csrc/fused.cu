@@ -56,17 +56,24 @@ __device__ __forceinline__ void score_tile(const FusedParams& p, int pair, int b
                    &bars[s]);
     }
   }
-  const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
-  for (int c = tid; c < d.d_k; c += kThreads) {
-    float qp = 0.f, qn = 0.f;
+  if (p.qq != nullptr) {
+    // QQ of the pair from qq_kernel (PDL primary): the tile copies above are already in flight
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    const float* qq = p.qq + (size_t)pair * 2 * d.d_k;
+    for (int c = tid; c < 2 * d.d_k; c += kThreads) QQ[c] = __ldcg(qq + c);
+  } else {
+    const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
+    for (int c = tid; c < d.d_k; c += kThreads) {
+      float qp = 0.f, qn = 0.f;
 #pragma unroll 8
-    for (int h = 0; h < d.G; ++h) {
-      const float v = to_f32<T>(qg[(size_t)h * d.d_k + c]);
-      qp += fmaxf(v, 0.f);
-      qn += fminf(v, 0.f);
+      for (int h = 0; h < d.G; ++h) {
+        const float v = to_f32<T>(qg[(size_t)h * d.d_k + c]);
+        qp += fmaxf(v, 0.f);
+        qn += fminf(v, 0.f);
+      }
+      QQ[c] = qp;
+      QQ[d.d_k + c] = qn;
     }
-    QQ[c] = qp;
-    QQ[d.d_k + c] = qn;
   }
   __syncthreads();  // QQ ready, barriers initialised
   const int nchunk = rowbytes / 16;
@@ -234,7 +241,7 @@ struct WorkerCtl {
 // pair-major; every tile CTA but the pair's last publishes a flag, the last
 // one waits for them (only earlier-dispatched CTAs) and runs pair_worker.
 template <typename T, int CPL, int MODE>
-__global__ void __launch_bounds__(kThreads, 6) select_kernel(const __grid_constant__ FusedParams p) {
+__global__ void __launch_bounds__(kThreads, CPL <= 2 ? 6 : 3) select_kernel(const __grid_constant__ FusedParams p) {
   constexpr int EPC = 16 / sizeof(T);
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float QQ[32 * CPL * EPC];
@@ -281,6 +288,30 @@ __global__ void __launch_bounds__(kThreads, 6) select_kernel(const __grid_consta
   pair_worker(p, pair, m, smem, ctl.tk, dbg);
 }
 
+// QQ = [Q+ | Q-] of every pair (fp32, P:110 + linearity of sum_h) once per call,
+// so that the ceil(M / tb) tile CTAs of a pair do not each re-read the pair's G
+// query rows (MLA: 32 x 576 bf16 per tile); select_kernel, launched as its PDL
+// secondary, issues its tile copies before waiting for it.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) qq_kernel(const __grid_constant__ FusedParams p) {
+  launch_dependents();
+  const Dims& d = p.d;
+  const int pair = blockIdx.x, b = pair / d.Hkv, g = pair - b * d.Hkv;
+  const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
+  float* qq = p.qq + (size_t)pair * 2 * d.d_k;
+  for (int c = threadIdx.x; c < d.d_k; c += kThreads) {
+    float qp = 0.f, qn = 0.f;
+#pragma unroll 8
+    for (int h = 0; h < d.G; ++h) {
+      const float v = to_f32<T>(qg[(size_t)h * d.d_k + c]);
+      qp += fmaxf(v, 0.f);
+      qn += fminf(v, 0.f);
+    }
+    qq[c] = qp;
+    qq[d.d_k + c] = qn;
+  }
+}
+
 // ============================================================== launchers
 int score_cpl(int d_k, size_t elem_bytes) {
   const int nchunk = (int)(2 * d_k * elem_bytes / 16);
@@ -305,6 +336,11 @@ template <typename T, int CPL>
 static cudaError_t dispatch_sel(const FusedParams& p, cudaStream_t st, const LaunchOpts& o) {
   if (p.mode == 0) return launch_sel<T, CPL, 0>(p, st, o);
   return launch_sel<T, CPL, 1>(p, st, o);
+}
+
+cudaError_t launch_qq(const FusedParams& p, cudaStream_t st, const LaunchOpts& o) {
+  auto kern = p.d.bf16 ? qq_kernel<__nv_bfloat16> : qq_kernel<float>;
+  return launch_ex(kern, dim3((unsigned)(p.d.batch * p.d.Hkv)), kThreads, 0, st, o, 0, p);
 }
 
 cudaError_t launch_select_fused(const FusedParams& p, cudaStream_t st, const LaunchOpts& o) {

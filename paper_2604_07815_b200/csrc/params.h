@@ -43,6 +43,7 @@ struct FusedParams {
   const void* block_minmax;
   const int* channels;
   float* scores;           // workspace [pairs, sstride] fp32; the completion sentinel between calls (fused.cu)
+  float* qq;               // workspace [pairs, 2 d_k] fp32 [Q+ | Q-] from qq_kernel (NULL: computed per tile)
   uint32_t* khist;         // workspace [pairs, kKeyBins], zeroed by the worker for the token kernel
   uint8_t* qfrag;          // workspace [pairs, qfrag_bytes(d)]: q~ fragment blobs for the token kernel
   int* block_ids;          // [pairs, Kb] out: M_t ascending, -1 padded
@@ -251,7 +252,7 @@ static inline int qfrag_bytes(const Dims& d) {
 }
 
 struct SelectWs {
-  size_t scores, keys, khist, qfrag, ready_b, ready_t, total;
+  size_t scores, keys, khist, qfrag, ready_b, ready_t, qq, total;
 };
 static inline SelectWs select_workspace(const Dims& d) {
   SelectWs w;
@@ -263,7 +264,8 @@ static inline SelectWs select_workspace(const Dims& d) {
   w.qfrag = w.khist + a256(pairs * kKeyBins * 4);
   w.ready_b = w.qfrag + a256(pairs * (size_t)qfrag_bytes(d));
   w.ready_t = w.ready_b + a256(pairs * 4);
-  w.total = w.ready_t + a256(pairs * 4);
+  w.qq = w.ready_t + a256(pairs * 4);
+  w.total = w.qq + a256(pairs * 2 * (size_t)d.d_k * 4);
   return w;
 }
 static inline size_t select_workspace_bytes(const Dims& d) { return select_workspace(d).total; }

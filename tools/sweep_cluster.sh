@@ -1,3 +1,2 @@
-for cs in 1 2 4; do for c in c3 c2; do echo "cs=$cs"; TLS_CLUSTER=$cs timeout 300 python bench.py --config $c --steps 200 --warmup 10 --no-cpu-baseline 2>&1 | tail -1 | python -c "
-import json, sys; d = json.loads(sys.stdin.read())
-print(d['config']['workload'], 'us/step', round(d['us_per_step'], 1), {k: round(v['avg_us'], 1) for k, v in d['kernels'].items()})"; done; done
+# attention cluster size sweep (TLS_CLUSTER) for one config: bash tools/sweep_cluster.sh c4 "2 4 8 16"
+c=${1:-c3}; for cs in ${2:-1 2 4}; do echo "cs=$cs"; TLS_CLUSTER=$cs timeout 300 python tools/kernel_times.py $c 2>&1 | tail -1; done
