@@ -621,14 +621,8 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
 template <typename T, bool MMA, int D>
 static cudaError_t launch_k3(const AttendParams& p, cudaStream_t st, const LaunchOpts& o) {
   auto kern = attend_kernel<T, MMA, D>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, p.cs > 8);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  if (e != cudaSuccess) return e;
-  if (p.cs > 8) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
   return launch_ex(kern, dim3((unsigned)p.cs, (unsigned)(p.d.batch * p.d.Hkv), 1), kThreads, p.smem_bytes, st, o,
                    (unsigned)p.cs, p);
 }
@@ -636,12 +630,8 @@ static cudaError_t launch_k3(const AttendParams& p, cudaStream_t st, const Launc
 template <int MT>
 static cudaError_t launch_mla(const AttendParams& p, cudaStream_t st, const LaunchOpts& o) {
   auto kern = attend_mla_kernel<576, 512, MT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, p.cs > 8);
   if (e != cudaSuccess) return e;
-  if (p.cs > 8) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
   return launch_ex(kern, dim3((unsigned)p.cs, (unsigned)(p.d.batch * p.d.Hkv), 1), kThreads, p.smem_bytes, st, o,
                    (unsigned)p.cs, p);
 }

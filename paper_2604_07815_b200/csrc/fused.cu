@@ -324,9 +324,7 @@ int score_cpl(int d_k, size_t elem_bytes) {
 template <typename T, int CPL, int MODE>
 static cudaError_t launch_sel(const FusedParams& p, cudaStream_t st, const LaunchOpts& o) {
   auto kern = select_kernel<T, CPL, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, false);
   if (e != cudaSuccess) return e;
   const dim3 grid((unsigned)((p.d.M + p.tb - 1) / p.tb), (unsigned)(p.d.batch * p.d.Hkv), 1);
   return launch_ex(kern, grid, kThreads, p.smem_bytes, st, o, 0, p);

@@ -11,7 +11,48 @@
 
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 namespace tls {
+
+// cudaFuncSetAttribute is a host round trip; the decode step launches four
+// kernels per call, so the attributes are set once per (kernel, device) and
+// again only when a larger dynamic shared-memory size is needed.
+static inline cudaError_t prepare_kernel(const void* kern, size_t smem, bool nonportable_cluster) {
+  struct Entry {
+    const void* k;
+    int dev;
+    size_t smem;
+    bool np;
+  };
+  static Entry cache[256];
+  static int n = 0;
+  static std::mutex mu;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  int i = 0;
+  for (; i < n; ++i)
+    if (cache[i].k == kern && cache[i].dev == dev) break;
+  if (i < n && cache[i].smem >= smem && (cache[i].np || !nonportable_cluster)) return cudaSuccess;
+  const size_t want = (i < n && cache[i].smem > smem) ? cache[i].smem : smem;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
+  if (nonportable_cluster) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  if (i == n && n < 256) {
+    cache[n++] = Entry{kern, dev, smem, nonportable_cluster};
+  } else if (i < n) {
+    cache[i].smem = smem > cache[i].smem ? smem : cache[i].smem;
+    cache[i].np = cache[i].np || nonportable_cluster;
+  }
+  return cudaSuccess;
+}
 
 struct LaunchOpts {
   int prio = 0;     // cudaLaunchAttributePriority value (0 = default / lowest; more negative = higher)

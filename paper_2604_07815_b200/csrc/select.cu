@@ -625,14 +625,8 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
 template <typename T, int KS, int NT, int NSPLIT>
 static cudaError_t launch_k2(const SelectParams& p, cudaStream_t st, const LaunchOpts& o) {
   auto kern = p.tpw > 0 ? token_reg_kernel<T, KS, NT, NSPLIT, 8 / NT> : token_cluster_kernel<T, KS, NT, NSPLIT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, p.nch > 8);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  if (e != cudaSuccess) return e;
-  if (p.nch > 8) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
   return launch_ex(kern, dim3((unsigned)p.nch, (unsigned)(p.d.batch * p.d.Hkv), 1), kThreads, p.smem_bytes, st, o,
                    (unsigned)p.nch, p);
 }
