@@ -171,10 +171,9 @@ __device__ __forceinline__ bool getenv_flag_sample(const FusedParams& p) { retur
 constexpr uint32_t kScoreSentinel = 0xffffffffu;
 
 // The pair's selection worker (a2): M_t = top-k_b blocks from the pair's
-// scores (already converted to keys in smem at off_bkeys), ties -> lower block id (U2),
-// written ascending and -1 padded; then the token kernel's inputs (q
-// fragments, a zeroed key histogram), the pair's generation and the hand-off
-// flag.  Every thread of the CTA calls it; smem holds the worker regions of
+// scores (already converted to keys in smem at off_bkeys), ties -> lower block
+// id (U2), written ascending and -1 padded; the scores go back to the sentinel
+// and the pair's hand-off flag is published.  Every thread of the CTA calls it; smem holds the worker regions of
 // plan_fused.
 __device__ __noinline__ void pair_worker(const FusedParams& p, int pair, int m, uint8_t* smem,
                                          TopKCtl& tk, unsigned long long* dbg) {
@@ -183,22 +182,8 @@ __device__ __noinline__ void pair_worker(const FusedParams& p, int pair, int m, 
 #define TLS_STAMP(i) \
   if (dbg && tid == 0) dbg[i] = gtimer();
   uint32_t* bkeys = reinterpret_cast<uint32_t*>(smem + p.off_bkeys);
-  int* cblk = reinterpret_cast<int*>(smem + p.off_cblk);
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + p.off_scratch);
   FastTopKCtl& fk = *reinterpret_cast<FastTopKCtl*>(smem + p.off_fk);
-  float* qc = reinterpret_cast<float*>(smem + p.off_qc);
-  // prefetch the token kernel's inputs (channel ids, small query rows) while top-k_b runs
-  const int b = pair / d.Hkv, g = pair - b * d.Hkv;
-  const size_t eb = d.bf16 ? 2 : 4;
-  const uint8_t* qsrc = reinterpret_cast<const uint8_t*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k * eb;
-  const int qbytes = d.G * d.d_k * (int)eb;
-  const bool qpre = p.off_qrows != 0;  // plan_fused reserved room for the rows
-  int* chan_s = reinterpret_cast<int*>(smem + p.off_chan);
-  for (int o = tid; o < d.d_c / 4; o += kThreads)
-    cp_async16(chan_s + 4 * o, p.channels + (size_t)g * d.d_c + 4 * o, true);
-  if (qpre)
-    for (int o = tid; o < qbytes / 16; o += kThreads) cp_async16(smem + p.off_qrows + 16 * o, qsrc + 16 * o, true);
-  cp_async_commit();
   TLS_STAMP(3)
   // ---- a2: M_t = top-k_b blocks, ties -> lower block id (U2), ascending ----
   const int K = min(d.Kb, m);
@@ -207,10 +192,7 @@ __device__ __noinline__ void pair_worker(const FusedParams& p, int pair, int m, 
     const TopK t = fast_topk(bkeys, m, K, d.Kb >= m, fk, tk, getenv_flag_sample(p) ? scratch : nullptr);
     TLS_STAMP(4)
     int* bout = p.block_ids + (size_t)pair * d.Kb;
-    topk_emit(bkeys, m, t, tk, [&](int i, int pos) {
-      bout[pos] = i;
-      cblk[pos] = i;
-    });
+    topk_emit(bkeys, m, t, tk, [&](int i, int pos) { bout[pos] = i; });
     for (int pos = K + tid; pos < d.Kb; pos += kThreads) bout[pos] = -1;
   }
   {  // the pair's scores back to the sentinel for the next call (ordered before it by the stream)
@@ -218,16 +200,10 @@ __device__ __noinline__ void pair_worker(const FusedParams& p, int pair, int m, 
     for (int i = tid; i < m; i += kThreads) sc[i] = kScoreSentinel;
   }
   TLS_STAMP(1)
-  // the token kernel takes over: its q fragments and a zeroed key histogram
-  cp_async_wait<0>();
-  __syncthreads();
-  build_qfrag(d, qpre ? static_cast<const void*>(smem + p.off_qrows) : static_cast<const void*>(qsrc), chan_s, p.qfrag,
-              pair, qc);
-  for (int i = tid; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    st_release_gpu(p.ready + pair, p.epoch);  // block_ids, q fragments and the zeroed histogram are visible
+    st_release_gpu(p.ready + pair, p.epoch);  // block_ids visible (q fragments and the zeroed histogram: qq_kernel)
   }
   TLS_STAMP(2)
 #undef TLS_STAMP
@@ -288,10 +264,12 @@ __global__ void __launch_bounds__(kThreads, CPL <= 2 ? 6 : 3) select_kernel(cons
   pair_worker(p, pair, m, smem, ctl.tk, dbg);
 }
 
-// QQ = [Q+ | Q-] of every pair (fp32, P:110 + linearity of sum_h) once per call,
-// so that the ceil(M / tb) tile CTAs of a pair do not each re-read the pair's G
-// query rows (MLA: 32 x 576 bf16 per tile); select_kernel, launched as its PDL
-// secondary, issues its tile copies before waiting for it.
+// Per-pair query-side work once per call: QQ = [Q+ | Q-] (fp32, P:110 +
+// linearity of sum_h), so that the ceil(M / tb) tile CTAs of a pair do not each
+// re-read the pair's G query rows (MLA: 32 x 576 bf16 per tile), and the token
+// kernel's q~ fragment blob and zeroed key histogram, off the selection
+// worker's critical path.  select_kernel, launched as its PDL secondary, issues
+// its tile copies before waiting for it.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) qq_kernel(const __grid_constant__ FusedParams p) {
   launch_dependents();
@@ -310,6 +288,12 @@ __global__ void __launch_bounds__(kThreads) qq_kernel(const __grid_constant__ Fu
     qq[c] = qp;
     qq[d.d_k + c] = qn;
   }
+  // the token kernel's inputs that do not depend on the scores: the pair's q~ fragments
+  // and a zeroed key histogram
+  __shared__ float qc[4 * 8 * 128];  // NT * 8 * d_c <= 4096
+  const int* ch = p.channels + (size_t)g * d.d_c;
+  build_qfrag(d, qg, ch, p.qfrag, pair, qc);
+  for (int i = threadIdx.x; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
 }
 
 // ============================================================== launchers

@@ -51,7 +51,7 @@ struct FusedParams {
   unsigned epoch;          // this call's hand-off value (host call counter, never 0)
   unsigned long long* dbg; // diagnostics only (env TLS_DEBUG_BUF): worker phase stamps
   int dbg_flags;           // tuning: bit 0 = sample-bracket top-k_b (env TLS_TOPK_SAMPLE)
-  unsigned off_bkeys, off_cblk, off_scratch, off_fk, off_qc, off_chan, off_qrows, smem_bytes;
+  unsigned off_bkeys, off_scratch, off_fk, smem_bytes;
 };
 
 
@@ -209,31 +209,18 @@ static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
 static inline size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // Shared-memory plan of select_kernel: the worker's regions (block keys,
-// candidate ids, bracket scratch, FastTopKCtl, q~ staging) alias the scoring
-// tile of phase S (the worker starts after its own tile is scored).
+// bracket scratch, FastTopKCtl) alias the scoring tile of phase S (the worker
+// starts after its own tile is scored).
 static inline void plan_fused(FusedParams& p, size_t fastctl_bytes) {
   const Dims& d = p.d;
   p.kb_eff = kb_effective(d);
-  const int nt0 = (d.G + 7) / 8, nt = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);
   size_t o = 0;
   p.off_bkeys = (unsigned)o;
   o = align16(o + (size_t)((d.M + 31) & ~31) * 4);
-  p.off_cblk = (unsigned)o;
-  o = align16(o + (size_t)d.Kb * 4);
   p.off_scratch = (unsigned)o;
   o = align16(o + (size_t)kBracketWords * 4);
   p.off_fk = (unsigned)o;
   o = align16(o + fastctl_bytes);
-  p.off_qc = (unsigned)o;
-  o = align16(o + (size_t)nt * 8 * d.d_c * 4);
-  p.off_chan = (unsigned)o;
-  o = align16(o + (size_t)d.d_c * 4);
-  const size_t qbytes = (size_t)d.G * d.d_k * (d.bf16 ? 2 : 4);
-  p.off_qrows = 0;  // 0: the q rows are gathered from global memory (too large to stage)
-  if (qbytes <= 8192) {
-    p.off_qrows = (unsigned)o;
-    o = align16(o + qbytes);
-  }
   const size_t tile = (size_t)p.tb * 2 * d.d_k * (d.bf16 ? 2 : 4);
   p.smem_bytes = (unsigned)(o > tile ? o : tile);
 }
