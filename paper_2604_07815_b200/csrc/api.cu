@@ -416,6 +416,7 @@ tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int
     ap.khist = sp.khist;
     ap.dbg = fp.dbg ? fp.dbg + 65536 * 24 : nullptr;
     ap.ready_in = c.mode == 1 ? sp.ready_out : nullptr;
+    ap.ready_count = sp.nch;
     ap.epoch = epoch;
     ap.token_ids = a.token_ids;
     ap.num_tokens = a.num_tokens;

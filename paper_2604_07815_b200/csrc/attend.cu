@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_consta
   int* sel = reinterpret_cast<int*>(smem + p.off_sel);
   if (p.ready_in != nullptr) {  // the token kernel's keys and histogram for this pair
     if (tid == 0) {
-      wait_ready(p.ready_in + pair, p.epoch);
+      wait_count(p.ready_in + pair, (unsigned)p.ready_count);
       if (cs == 1) p.ready_in[pair] = 0u;
     }
     __syncthreads();
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
   __shared__ TopKCtl tk;
   if (p.ready_in != nullptr) {  // the token kernel's keys and histogram for this pair
     if (tid == 0) {
-      wait_ready(p.ready_in + pair, p.epoch);
+      wait_count(p.ready_in + pair, (unsigned)p.ready_count);
       if (cs == 1) p.ready_in[pair] = 0u;
     }
     __syncthreads();

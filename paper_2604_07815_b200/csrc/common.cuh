@@ -310,6 +310,16 @@ __device__ __forceinline__ void wait_ready(const unsigned* flag, unsigned epoch)
   }
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
+// The same for a per-pair completion count (>= n: done; a count above n --
+// e.g. an uninitialised workspace -- is accepted rather than waited on).
+__device__ __forceinline__ void wait_count(const unsigned* ctr, unsigned n) {
+  unsigned spins = 0;
+  while (ld_acquire_gpu(ctr) < n) {
+    __nanosleep(128);
+    if (++spins > (1u << 24)) __trap();
+  }
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
 // Let the next kernel in the stream (launched with programmatic stream
 // serialization) start its CTAs; its data dependences go through wait_ready.
 __device__ __forceinline__ void launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }

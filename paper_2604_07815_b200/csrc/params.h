@@ -77,14 +77,15 @@ struct SelectParams {  // K2 (token_reg_kernel, or token_cluster_kernel when a c
   int qtma;  // 1: the q rows of the pair arrive by TMA into smem (off_qrows)
   const uint8_t* qfrag;  // token_reg_kernel: K1b's q-fragment blobs [pairs, qfrag_bytes(d)]
   unsigned* ready_in;    // workspace [pairs]: select_kernel's hand-off (== epoch when a2 is done); reset here
-  unsigned* ready_out;   // workspace [pairs]: set to epoch when this pair's keys and histogram are complete
+  unsigned* ready_out;   // workspace [pairs]: +1 per chunk CTA once its keys and histogram counts are visible
   unsigned epoch;
   unsigned off_cblk, off_qb, off_qsum, off_qc, off_qrows, off_stage, smem_bytes;
 };
 
 struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally with the a4 prologue
   Dims d;
-  unsigned* ready_in;  // select only: the token kernel's hand-off (== epoch when done); reset here
+  unsigned* ready_in;  // select only: the token kernel's per-pair count of finished chunk CTAs; reset here
+  int ready_count;     // the count that means "done" (the token kernel's nch)
   unsigned epoch;
   int cs;
   int mma;       // 1: bf16 mma.sync GQA path (d in {64,128}, G <= 16); 2: bf16 mma.sync MLA path (576/512)

@@ -317,9 +317,11 @@ __global__ void __launch_bounds__(kThreads, (NT == 1 && KS * NSPLIT <= 2) ? 5 : 
   }
   TLS_STAMP(5)
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");  // keep smem alive for remote readers
-  __threadfence();  // this CTA's keys and histogram counts, before the pair's hand-off
-  cluster_sync_all();
-  if (chunk == 0 && tid == 0) st_release_gpu(p.ready_out + pair, p.epoch);
+  __syncthreads();
+  if (tid == 0) {  // hand-off: one count per chunk CTA (no cluster barrier; the attention kernel waits for nch)
+    __threadfence();
+    atomicAdd(p.ready_out + pair, 1u);
+  }
   TLS_STAMP(6)
 #undef TLS_STAMP
 }
@@ -614,9 +616,11 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
   for (int i = tid; i < kKeyBins; i += kThreads)
     if (lhist[i]) atomicAdd(&gh[i], lhist[i]);
   TLS_STAMP(5)
-  __threadfence();  // this CTA's keys and histogram counts, before the pair's hand-off
-  cluster_sync_all();
-  if (chunk == 0 && tid == 0) st_release_gpu(p.ready_out + pair, p.epoch);
+  __syncthreads();
+  if (tid == 0) {  // hand-off: one count per chunk CTA (no cluster barrier; the attention kernel waits for nch)
+    __threadfence();  // this CTA's keys and histogram counts (cumulative over the CTA barrier)
+    atomicAdd(p.ready_out + pair, 1u);
+  }
   TLS_STAMP(6)
 #undef TLS_STAMP
 }

@@ -17,3 +17,5 @@ done
 for c in c3 c2 c4; do
   timeout 600 python bench.py --config $c > gpurun_out/bench_${c}_${V}.json 2> gpurun_out/bench_${c}_${V}.err
 done
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${V}.log 2>&1
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_${V}.json 2> gpurun_out/bench_ref_${V}.err
