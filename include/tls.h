@@ -197,6 +197,37 @@ tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
                       int32_t* num_tokens, float* token_scores, void* out, float* lse,
                       void* workspace, size_t workspace_bytes, tls_stream_t stream);
 
+/*
+ * KV offload (AsyncTLS §4.2): the full K/V caches live in pinned,
+ * device-mapped host memory (cudaHostAlloc(..., cudaHostAllocMapped), layouts
+ * of k_cache / v_cache above); every pair owns a GPU token cache of
+ * `capacity` slots.  tls_cache_fetch makes a selection S_t (token_ids /
+ * num_tokens from tls_select) resident: tokens already cached are hits (the
+ * step-to-step locality of the selection), slots of tokens that
+ * left the selection are evicted (the cache keeps the current selection, the
+ * token-granular form of C_{t+1} = M_t), and every miss is copied from
+ * host memory by a zero-copy gather kernel.  slot_ids [batch, Hkv, top_tokens]
+ * receives the cache row of each selected token in selection order, so
+ * tls_sparse_attend over (k_slots, v_slots, slot_ids) with max_seq_len =
+ * capacity computes exactly the attention over S_t.  miss_count [batch, Hkv]
+ * (nullable) receives the number of rows fetched.  One launch (one CTA per
+ * pair); the cache state is deterministic.
+ * Errors: TLS_ERR_CONFIG if capacity < top_tokens; TLS_ERR_INPUT for NULL
+ * buffers or host caches that are not device-mapped.
+ */
+typedef struct {
+  int32_t capacity;       /* slots per pair, >= top_tokens                          */
+  void* k_slots;          /* [batch, Hkv, capacity, d_k] dtype, device              */
+  void* v_slots;          /* [batch, Hkv, capacity, d_v] dtype, device (NULL: MLA)  */
+  int32_t* slot_of_token; /* [batch, Hkv, max_seq_len], -1 = not resident; init -1  */
+  int32_t* token_of_slot; /* [batch, Hkv, capacity], -1 = free; init -1             */
+} tls_token_cache;
+
+tls_status tls_cache_fetch(const tls_config* cfg, const void* k_host, const void* v_host,
+                           const int32_t* token_ids, const int32_t* num_tokens,
+                           const tls_token_cache* cache, int32_t* slot_ids, int32_t* miss_count,
+                           tls_stream_t stream);
+
 /* Workspace bytes needed by: which = 0 tls_select, 1 tls_sparse_attend,
  * 2 tls_decode.  The select part holds the fp32 block scores of every pair,
  * per-chunk softmax statistics, the ranking key of every candidate token and a

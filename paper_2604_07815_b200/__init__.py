@@ -19,6 +19,11 @@ from .ops import (  # noqa: F401
     KERNELS,
     timing_enable,
     timing_read,
+    TLSTokenCache,
+    alloc_token_cache,
+    host_kv,
+    cache_fetch,
+    offload_decode,
 )
 from ._lib import TLSError, load  # noqa: F401
 

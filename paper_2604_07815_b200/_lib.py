@@ -29,6 +29,7 @@ EXPORTS = (
     "tls_cluster_size",
     "tls_select_mode",
     "tls_workspace_init",
+    "tls_cache_fetch",
     "tls_timing_enable",
     "tls_timing_read",
     "tls_status_string",
@@ -61,6 +62,16 @@ class TLSIndexC(ctypes.Structure):
         ("codes", ctypes.c_void_p),
         ("scale_zero", ctypes.c_void_p),
         ("channels", ctypes.c_void_p),
+    ]
+
+
+class TLSTokenCacheC(ctypes.Structure):
+    _fields_ = [
+        ("capacity", ctypes.c_int32),
+        ("k_slots", ctypes.c_void_p),
+        ("v_slots", ctypes.c_void_p),
+        ("slot_of_token", ctypes.c_void_p),
+        ("token_of_slot", ctypes.c_void_p),
     ]
 
 
@@ -98,6 +109,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "tls_block_scores": (_I32, [_PCFG, _P, _P, _P, _P, _P]),
         "tls_select": (_I32, [_PCFG, _P, _P, _PIDX, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_sparse_attend": (_I32, [_PCFG, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+        "tls_cache_fetch": (_I32, [_PCFG, _P, _P, _P, _P, ctypes.POINTER(TLSTokenCacheC), _P, _P, _P]),
         "tls_decode": (_I32, [_PCFG, _P, _P, _P, _P, _PIDX, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_workspace_bytes": (ctypes.c_size_t, [_PCFG, _I32]),
         "tls_launch_count": (_I32, [_PCFG, _I32]),

@@ -21,6 +21,7 @@
 namespace tls {
 cudaError_t launch_select_fused(const FusedParams& p, cudaStream_t st, const LaunchOpts& o);
 cudaError_t launch_qq(const FusedParams& p, cudaStream_t st, const LaunchOpts& o);
+cudaError_t launch_cache_fetch(const CacheFetchParams& p, cudaStream_t st);
 cudaError_t launch_token_cluster(const SelectParams& p, cudaStream_t st, const LaunchOpts& o);
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t st, const LaunchOpts& o);
 int score_cpl(int d_k, size_t elem_bytes);
@@ -701,6 +702,52 @@ tls_status tls_workspace_init(const tls_config* cfg, int32_t which, void* worksp
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
     ws += c.total;
   }
+  return TLS_OK;
+}
+
+tls_status tls_cache_fetch(const tls_config* cfg, const void* k_host, const void* v_host, const int32_t* token_ids,
+                           const int32_t* num_tokens, const tls_token_cache* cache, int32_t* slot_ids,
+                           int32_t* miss_count, tls_stream_t stream) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if (!cache || !cache->k_slots || !cache->slot_of_token || !cache->token_of_slot)
+    return fail(TLS_ERR_INPUT, "cache buffers must be non-NULL");
+  if (cfg->layout == TLS_GQA && (!cache->v_slots || !v_host)) return fail(TLS_ERR_INPUT, "GQA needs v_host and v_slots");
+  if (!k_host || !token_ids || !num_tokens || !slot_ids)
+    return fail(TLS_ERR_INPUT, "k_host, token_ids, num_tokens and slot_ids are required");
+  if (cache->capacity < cfg->top_tokens)
+    return fail(TLS_ERR_CONFIG, "cache capacity (%d) must be >= top_tokens (%d)", cache->capacity, cfg->top_tokens);
+  // the host caches must be reachable from the device (pinned + mapped, or managed / device memory)
+  const void* dk = nullptr;
+  const void* dv = nullptr;
+  for (int i = 0; i < 2; ++i) {
+    const void* h = i == 0 ? k_host : v_host;
+    if (!h) continue;
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, h);
+    if (e != cudaSuccess || at.devicePointer == nullptr)
+      return fail(TLS_ERR_INPUT, "k_host / v_host must be pinned, device-mapped host memory (cudaHostAlloc mapped)");
+    (i == 0 ? dk : dv) = at.devicePointer;
+  }
+  tls::CacheFetchParams p;
+  memset(&p, 0, sizeof(p));
+  p.d = dims_of(cfg);
+  p.capacity = cache->capacity;
+  p.bitmap_words = (cfg->max_seq_len + 31) / 32;
+  const size_t smem = (size_t)p.bitmap_words * 4 + (size_t)p.capacity * 4 + (size_t)cfg->top_tokens * 4;
+  if ((int)smem > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "cache_fetch shared-memory plan does not fit");
+  p.k_host = static_cast<const uint8_t*>(dk);
+  p.v_host = cfg->layout == TLS_GQA ? static_cast<const uint8_t*>(dv) : nullptr;
+  p.token_ids = token_ids;
+  p.num_tokens = num_tokens;
+  p.k_slots = static_cast<uint8_t*>(cache->k_slots);
+  p.v_slots = cfg->layout == TLS_GQA ? static_cast<uint8_t*>(cache->v_slots) : nullptr;
+  p.slot_of_token = cache->slot_of_token;
+  p.token_of_slot = cache->token_of_slot;
+  p.slot_ids = slot_ids;
+  p.miss_count = miss_count;
+  cudaError_t e = tls::launch_cache_fetch(p, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cache_fetch_kernel launch");
   return TLS_OK;
 }
 

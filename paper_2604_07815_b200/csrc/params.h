@@ -111,6 +111,23 @@ struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally wit
   unsigned off_sel, off_cblk, off_union, off_skeys, off_fk, off_slist, off_akv, off_aq, off_as, smem_bytes;
 };
 
+// GPU token cache of the offload engine (offload.cu): make S_t resident.
+struct CacheFetchParams {
+  Dims d;
+  int capacity;      // slots per pair (>= top_tokens)
+  int bitmap_words;  // ceil(S / 32)
+  const uint8_t* k_host;  // device-accessible pointer to the pinned host K cache (layout of k_cache)
+  const uint8_t* v_host;  // ... V cache (NULL for MLA)
+  const int* token_ids;   // [pairs, Kt] S_t (tls_select)
+  const int* num_tokens;  // [pairs]
+  uint8_t* k_slots;       // [pairs, capacity, d_k]
+  uint8_t* v_slots;       // [pairs, capacity, d_v] (NULL for MLA)
+  int* slot_of_token;     // [pairs, S], -1 = not resident
+  int* token_of_slot;     // [pairs, capacity], -1 = free
+  int* slot_ids;          // [pairs, Kt] out: the cache row of each selected token
+  int* miss_count;        // [pairs] out, nullable
+};
+
 static inline unsigned align16(size_t x) { return (unsigned)((x + 15) & ~(size_t)15); }
 
 static inline int kb_effective(const Dims& d) { return d.Kb < d.M ? d.Kb : d.M; }

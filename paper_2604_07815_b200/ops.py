@@ -32,6 +32,11 @@ __all__ = [
     "select_mode",
     "KERNELS",
     "timing_enable",
+    "TLSTokenCache",
+    "alloc_token_cache",
+    "host_kv",
+    "cache_fetch",
+    "offload_decode",
     "timing_read",
 ]
 
@@ -325,3 +330,73 @@ def timing_read() -> tuple[dict, int]:
     calls = ctypes.c_int64(0)
     _lib.check(_lib.load().tls_timing_read(ms, ctypes.byref(calls)))
     return {k: float(ms[i]) for i, k in enumerate(KERNELS)}, int(calls.value)
+
+
+# ------------------------------------------------------------------ KV offload
+@dataclass
+class TLSTokenCache:
+    """GPU token cache of the offload engine (tls_token_cache, include/tls.h)."""
+
+    capacity: int
+    k_slots: torch.Tensor  # [batch, Hkv, capacity, d_k]
+    v_slots: torch.Tensor | None  # [batch, Hkv, capacity, d_v] (None for MLA)
+    slot_of_token: torch.Tensor  # [batch, Hkv, S] int32, -1 = not resident
+    token_of_slot: torch.Tensor  # [batch, Hkv, capacity] int32, -1 = free
+
+    def c(self) -> _lib.TLSTokenCacheC:
+        return _lib.TLSTokenCacheC(self.capacity, self.k_slots.data_ptr(),
+                                   self.v_slots.data_ptr() if self.v_slots is not None else 0,
+                                   self.slot_of_token.data_ptr(), self.token_of_slot.data_ptr())
+
+
+def alloc_token_cache(cfg: TLSConfig, capacity: int, device) -> TLSTokenCache:
+    """An empty token cache of ``capacity`` (>= top_tokens) slots per pair."""
+    hk = cfg.num_kv_heads if cfg.layout == "gqa" else 1
+    slots = (cfg.batch, hk, capacity) if cfg.layout == "gqa" else (cfg.batch, capacity)  # the k_cache layouts
+    return TLSTokenCache(
+        capacity=capacity,
+        k_slots=torch.empty(slots + (cfg.d_k,), dtype=cfg.dtype, device=device),
+        v_slots=torch.empty(slots + (cfg.d_v,), dtype=cfg.dtype, device=device) if cfg.layout == "gqa" else None,
+        slot_of_token=torch.full((cfg.batch, hk, cfg.max_seq_len), -1, dtype=torch.int32, device=device),
+        token_of_slot=torch.full((cfg.batch, hk, capacity), -1, dtype=torch.int32, device=device),
+    )
+
+
+def host_kv(t: torch.Tensor) -> torch.Tensor:
+    """A pinned (page-locked, device-mapped under UVA) host copy of a KV cache tensor."""
+    return t.cpu().pin_memory()
+
+
+def cache_fetch(cfg: TLSConfig, k_host: torch.Tensor, v_host: torch.Tensor | None, token_ids: torch.Tensor,
+                num_tokens: torch.Tensor, cache: TLSTokenCache, slot_ids=None, miss_count=None):
+    """Make the selection resident in ``cache`` (tls_cache_fetch).  Returns (slot_ids, miss_count)."""
+    lib = _lib.load()
+    dev = token_ids.device
+    if not (k_host.is_pinned() and (v_host is None or v_host.is_pinned())):
+        raise ValueError("k_host / v_host must be pinned host tensors (host_kv)")
+    _need(token_ids, "token_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_tokens), torch.int32, dev)
+    _need(num_tokens, "num_tokens", (cfg.batch, cfg.num_kv_heads), torch.int32, dev)
+    if slot_ids is None:
+        slot_ids = torch.empty_like(token_ids)
+    if miss_count is None:
+        miss_count = torch.empty_like(num_tokens)
+    cc, kc = cfg.c(), cache.c()
+    _lib.check(lib.tls_cache_fetch(ctypes.byref(cc), k_host.data_ptr(),
+                                   v_host.data_ptr() if (v_host is not None and cfg.layout == "gqa") else 0,
+                                   token_ids.data_ptr(), num_tokens.data_ptr(), ctypes.byref(kc), slot_ids.data_ptr(),
+                                   miss_count.data_ptr(), _stream(dev)))
+    return slot_ids, miss_count
+
+
+def offload_decode(cfg: TLSConfig, q: torch.Tensor, k_host: torch.Tensor, v_host: torch.Tensor | None,
+                   seq_lens: torch.Tensor, index: TLSIndex, cache: TLSTokenCache, guide_block_ids=None):
+    """One decode step with the KV cache in host memory: select on the GPU index (lag mode with
+    ``guide_block_ids``), fetch the missed selected tokens into the GPU token cache, attend over the
+    cache rows.  Returns (out, lse, block_ids, token_ids, num_tokens, token_scores, slot_ids, miss_count)."""
+    bids, tids, nt, ts = select(cfg, q, seq_lens, index, guide_block_ids=guide_block_ids)
+    slot_ids, miss = cache_fetch(cfg, k_host, v_host, tids, nt, cache)
+    ccfg = TLSConfig(**{**{f: getattr(cfg, f) for f in ("batch", "num_q_heads", "num_kv_heads", "d_k", "d_v",
+                                                        "block_size", "d_c", "top_blocks", "top_tokens", "sm_scale",
+                                                        "dtype", "layout")}, "max_seq_len": cache.capacity})
+    out, lse = sparse_attend(ccfg, q, cache.k_slots, cache.v_slots, slot_ids, nt)
+    return out, lse, bids, tids, nt, ts, slot_ids, miss
