@@ -242,8 +242,12 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
       x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, 2));
       x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 1));
       x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 2));
-      const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);  // finite: token tb is valid
-      const float a0 = fexp2(m0 - n0), a1 = fexp2(m1 - n1);
+      // lazy rescaling: the running reference max moves only when a score exceeds it by more than
+      // 8 (log2 units); p = 2^(s - m) <= 2^8 stays well inside fp32 / bf16 and o / l is unchanged,
+      // so most chunks skip the rescale of the 64 accumulators
+      const bool g0 = x0 > m0 + 8.f, g1 = x1 > m1 + 8.f;  // m = -inf at first: true (token tb is valid)
+      const float n0 = g0 ? x0 : m0, n1 = g1 ? x1 : m1;
+      const float a0 = g0 ? fexp2(m0 - n0) : 1.f, a1 = g1 ? fexp2(m1 - n1) : 1.f;
       const float p0 = fexp2(s[0] - n0), p1 = fexp2(s[1] - n0), p2 = fexp2(s[2] - n1), p3 = fexp2(s[3] - n1);
       float r0s = p0 + p1, r1s = p2 + p3;
       r0s += __shfl_xor_sync(0xffffffffu, r0s, 1);
@@ -254,12 +258,14 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
       l1 = l1 * a1 + r1s;
       m0 = n0;
       m1 = n1;
+      if (__any_sync(0xffffffffu, g0 || g1)) {
 #pragma unroll
-      for (int j = 0; j < D / 8; ++j) {
-        o[j][0] *= a0;
-        o[j][1] *= a0;
-        o[j][2] *= a1;
-        o[j][3] *= a1;
+        for (int j = 0; j < D / 8; ++j) {
+          o[j][0] *= a0;
+          o[j][1] *= a0;
+          o[j][2] *= a1;
+          o[j][3] *= a1;
+        }
       }
       // P (16 x 16, tokens 8..15 of the k-step zero) x V (8 tokens of this warp)
       uint32_t pa[4];
