@@ -155,6 +155,7 @@ tls_status plan_attend(const tls_config* c, tls::AttendParams& p, int select, in
   p.mma = c->dtype == TLS_BF16 && c->layout == TLS_GQA && c->d_k == c->d_v && (c->d_k == 64 || c->d_k == 128) &&
           p.d.G <= 16;
   if (c->dtype == TLS_BF16 && c->layout == TLS_MLA && c->d_k == 576 && c->d_v == 512 && p.d.G <= 32) p.mma = 2;
+  p.heads_as_m = getenv("TLS_ATTN_HEADS_AS_M") ? 1 : 0;
   const long long pairs = (long long)c->batch * c->num_kv_heads;
   const int kt = tls::kt_effective(p.d);
   int cs = env_cluster();

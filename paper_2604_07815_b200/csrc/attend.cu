@@ -70,14 +70,15 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
   TLS_STAMP(1)
   TLS_STAMP(2)
   __shared__ HistSel hs;
-  const HistPlan pl = hist_topk_plan(skeys, nslots, shist, d.Kt, scratch, fk, tk, hs);
-  const int K = pl.K;
-  TLS_STAMP(3)
-  // every CTA emits the same selection; CTA rank keeps positions [t0, t1) of it
-  const int t0 = (int)((long long)K * rank / cs), t1 = (int)((long long)K * (rank + 1) / cs);
+  // every CTA selects the same S_t; CTA rank keeps positions [t0, t1) of it
   int* tout = p.token_ids + (size_t)pair * d.Kt;
   float* sout = p.token_scores ? p.token_scores + (size_t)pair * d.Kt : nullptr;
   const float lnG = logf((float)d.G);
+  int t0 = 0, t1 = 0;
+  auto on_k = [&](int K) {
+    t0 = K * (int)rank / cs;  // K <= top_tokens, cs <= 16: no overflow
+    t1 = K * ((int)rank + 1) / cs;
+  };
   auto put = [&](int i, int pos) {
     const int tok = (cblk[i >> d.log2B] << d.log2B) + (i & (d.B - 1));
     if (rank == 0) {
@@ -86,7 +87,17 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
     }
     if (pos >= t0 && pos < t1) sel[pos - t0] = tok;
   };
-  hist_topk_emit(skeys, nslots, pl, hs, tk, reinterpret_cast<int*>(smem + p.off_slist), put);
+  int* slist = reinterpret_cast<int*>(smem + p.off_slist);
+  int K;
+  if (nslots <= kSelRunMax * kThreads) {
+    K = hist_topk_select(skeys, nslots, shist, d.Kt, scratch, fk, tk, hs, slist, on_k, put, dbg);
+  } else {
+    const HistPlan pl = hist_topk_plan(skeys, nslots, shist, d.Kt, scratch, fk, tk, hs, dbg);
+    K = pl.K;
+    on_k(K);
+    hist_topk_emit(skeys, nslots, pl, hs, tk, slist, put);
+  }
+  TLS_STAMP(3)
   if (rank == 0) {
     for (int pos = K + tid; pos < d.Kt; pos += kThreads) {
       tout[pos] = -1;
@@ -336,6 +347,197 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
   }
 }
 
+// --------------------------------------------------------------------------
+// Phase E, tokens-as-M tensor-core form (bf16 GQA, D = 128, G <= 8): the
+// group's G heads fill the N = 8 side of mma.sync m16n8k16 exactly, instead of
+// half of a 16-row M tile.  Warp w owns the 16 tokens 16*(w/2) .. +15 of each
+// 64-token chunk and the output dims 64*(w%2) .. +63:
+//   S^T (16 tokens x 8 heads) = K Q^T      8 k-steps: A = K rows (ldmatrix),
+//                                          B = Q^T fragments held in registers
+//   online softmax per head over the tokens (lazy rescaling as above); P^T
+//   goes through a 256-byte per-warp buffer into the B layout
+//   O^T (64 dims x 8 heads) += V^T P^T     4 m-tiles: A = V^T (ldmatrix.trans)
+// 12 mma per warp per chunk instead of 24, 16 accumulator registers instead of
+// 64.  The two warps of a token group compute the same S^T (no exchange).  At
+// the end the 4 token groups' partials merge in shared memory.
+// --------------------------------------------------------------------------
+template <int D>
+__device__ void phase_attend_mma_t(const AttendParams& p, int pair, int b, int g, const int* sel, int tloc,
+                                   uint8_t* kvbuf, float* po, float* pml) {
+  static_assert(D == 128, "tokens-as-M attention: D = 128");
+  constexpr int TC = kAttnChunk;  // 64 tokens per stage
+  constexpr int CPR = D / 8;      // 16-byte chunks per row
+  constexpr int KS = D / 16;      // k-steps of K Q^T
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  const int tg = warp >> 1, dh = warp & 1;
+  __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(kvbuf);  // [kAttnStages][K TC*D | V TC*D]
+  __nv_bfloat16* pbuf = reinterpret_cast<__nv_bfloat16*>(kvbuf + (size_t)kAttnStages * 2 * TC * D * 2) + warp * 128;
+  const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + ((size_t)b * p.d.Hq + (size_t)g * p.d.G) * D;
+  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.d.S * D;
+  const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(p.v_cache) + (size_t)pair * p.d.S * D;
+  const int nchunks = (tloc + TC - 1) / TC;
+  auto load_chunk = [&](int c, int stage) {
+    __nv_bfloat16* sK = sbuf + (size_t)stage * 2 * TC * D;
+    __nv_bfloat16* sV = sK + TC * D;
+    const int nt = min(TC, tloc - c * TC);
+#pragma unroll
+    for (int it = 0; it < (TC * CPR) / kThreads; ++it) {
+      const int i = tid + it * kThreads;
+      const int row = i / CPR, ch = i - row * CPR;
+      const bool ok = row < nt;
+      const int tok = ok ? sel[c * TC + row] : 0;
+      const int dst = row * D + ((ch ^ (row & 7)) << 3);
+      cp_async16(sK + dst, kb + (size_t)tok * D + ch * 8, ok);
+      cp_async16(sV + dst, vb + (size_t)tok * D + ch * 8, ok);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int c = 0; c < kAttnStages - 1; ++c) {
+    if (c < nchunks) load_chunk(c, c);
+    else cp_async_commit();
+  }
+  // Q^T as the B operand: b0 = Q[head r][16k + 2q, +1], b1 = Q[head r][16k + 2q + 8, +9] (heads >= G: 0)
+  uint32_t qb[KS][2];
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    qb[k][0] = r < p.d.G ? *reinterpret_cast<const uint32_t*>(qg + r * D + 16 * k + 2 * q) : 0u;
+    qb[k][1] = r < p.d.G ? *reinterpret_cast<const uint32_t*>(qg + r * D + 16 * k + 2 * q + 8) : 0u;
+  }
+  const float sm2 = p.d.sm_scale * kLog2e;
+  float m[2] = {-CUDART_INF_F, -CUDART_INF_F}, l[2] = {0.f, 0.f};  // heads 2q, 2q + 1 over this warp's tokens
+  float o[4][4];  // O^T: m-tile mt = dims 64*dh + 16*mt + (r, r + 8), heads (2q, 2q + 1)
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + kAttnStages - 1 < nchunks) load_chunk(c + kAttnStages - 1, (c + kAttnStages - 1) % kAttnStages);
+    else cp_async_commit();
+    cp_async_wait<kAttnStages - 1>();
+    __syncthreads();  // chunk c landed for every thread's copies
+    const __nv_bfloat16* sK = sbuf + (size_t)(c % kAttnStages) * 2 * TC * D;
+    const __nv_bfloat16* sV = sK + TC * D;
+    const int nt = min(TC, tloc - c * TC);
+    const int t0 = tg * 16;
+    if (t0 < nt) {
+      // ---- S^T (16 tokens x 8 heads) = K Q^T ----
+      float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        const int row = t0 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int ch = 2 * k + (lane >> 4);
+        uint32_t a[4];
+        ldsm_x4(a, sK + row * D + ((ch ^ (row & 7)) << 3));
+        mma_bf16_16816(s, a, qb[k][0], qb[k][1]);
+      }
+      // s = S^T[token t0 + r][heads 2q, 2q + 1], S^T[token t0 + r + 8][...]
+      const bool v0 = t0 + r < nt, v1 = t0 + r + 8 < nt;
+      s[0] = v0 ? s[0] * sm2 : -CUDART_INF_F;
+      s[1] = v0 ? s[1] * sm2 : -CUDART_INF_F;
+      s[2] = v1 ? s[2] * sm2 : -CUDART_INF_F;
+      s[3] = v1 ? s[3] * sm2 : -CUDART_INF_F;
+      float x0 = fmaxf(s[0], s[2]), x1 = fmaxf(s[1], s[3]);  // per head, over the lane's two tokens
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+        x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+      }
+      // lazy rescaling (x is finite: token t0 is valid)
+      const bool g0 = x0 > m[0] + 8.f, g1 = x1 > m[1] + 8.f;
+      const float n0 = g0 ? x0 : m[0], n1 = g1 ? x1 : m[1];
+      const float a0 = g0 ? fexp2(m[0] - n0) : 1.f, a1 = g1 ? fexp2(m[1] - n1) : 1.f;
+      const float p0 = fexp2(s[0] - n0), p1 = fexp2(s[1] - n1), p2 = fexp2(s[2] - n0), p3 = fexp2(s[3] - n1);
+      float r0s = p0 + p2, r1s = p1 + p3;
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        r0s += __shfl_xor_sync(0xffffffffu, r0s, off);
+        r1s += __shfl_xor_sync(0xffffffffu, r1s, off);
+      }
+      l[0] = l[0] * a0 + r0s;
+      l[1] = l[1] * a1 + r1s;
+      m[0] = n0;
+      m[1] = n1;
+      if (__any_sync(0xffffffffu, g0 || g1)) {
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          o[mt][0] *= a0;
+          o[mt][1] *= a1;
+          o[mt][2] *= a0;
+          o[mt][3] *= a1;
+        }
+      }
+      // ---- P^T into the B layout: P[head][token] in a per-warp buffer ----
+      pbuf[(2 * q) * 16 + r] = __float2bfloat16_rn(p0);
+      pbuf[(2 * q + 1) * 16 + r] = __float2bfloat16_rn(p1);
+      pbuf[(2 * q) * 16 + r + 8] = __float2bfloat16_rn(p2);
+      pbuf[(2 * q + 1) * 16 + r + 8] = __float2bfloat16_rn(p3);
+      __syncwarp();
+      const uint32_t pb0 = *reinterpret_cast<const uint32_t*>(pbuf + r * 16 + 2 * q);
+      const uint32_t pb1 = *reinterpret_cast<const uint32_t*>(pbuf + r * 16 + 2 * q + 8);
+      __syncwarp();
+      // ---- O^T (64 dims x 8 heads) += V^T (dims x 16 tokens) P^T ----
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int token = t0 + (lane & 7) + ((lane >> 4) & 1) * 8;
+        const int ch = (dh * 64 + 16 * mt) / 8 + ((lane >> 3) & 1);
+        uint32_t a[4];
+        ldsm_x4_trans(a, sV + token * D + ((ch ^ (token & 7)) << 3));
+        mma_bf16_16816(o[mt], a, pb0, pb1);
+      }
+    }
+    __syncthreads();  // stage c % kAttnStages consumed before it is refilled
+  }
+  cp_async_wait<0>();
+  // ---- merge the 4 token groups (the staging buffers become scratch) ----
+  constexpr int WS = D + 4;
+  float* wo = reinterpret_cast<float*>(kvbuf);  // [tg][8 heads][WS]
+  float* wml = wo + 4 * 8 * WS;                  // [tg][8 heads][2]
+  if (dh == 0 && r == 0) {
+    wml[(tg * 8 + 2 * q) * 2] = m[0];
+    wml[(tg * 8 + 2 * q) * 2 + 1] = l[0];
+    wml[(tg * 8 + 2 * q + 1) * 2] = m[1];
+    wml[(tg * 8 + 2 * q + 1) * 2 + 1] = l[1];
+  }
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int d0 = dh * 64 + 16 * mt + r;
+    wo[(tg * 8 + 2 * q) * WS + d0] = o[mt][0];
+    wo[(tg * 8 + 2 * q + 1) * WS + d0] = o[mt][1];
+    wo[(tg * 8 + 2 * q) * WS + d0 + 8] = o[mt][2];
+    wo[(tg * 8 + 2 * q + 1) * WS + d0 + 8] = o[mt][3];
+  }
+  __syncthreads();
+  const bool direct = p.cs == 1;
+  __nv_bfloat16* outg =
+      reinterpret_cast<__nv_bfloat16*>(p.out) + ((size_t)b * p.d.Hq + (size_t)g * p.d.G) * p.d.d_v;
+  const int ngroups = min(4, (min(tloc, TC) + 15) / 16);  // token groups that saw at least one token
+  for (int idx = tid; idx < p.d.G * D; idx += kThreads) {
+    const int h = idx / D, dcol = idx - h * D;
+    float M = -CUDART_INF_F;
+    for (int t = 0; t < ngroups; ++t) M = fmaxf(M, wml[(t * 8 + h) * 2]);
+    float L = 0.f, acc = 0.f;
+    if (M != -CUDART_INF_F) {
+      for (int t = 0; t < ngroups; ++t) {
+        const float mw = wml[(t * 8 + h) * 2];
+        const float sc = mw == -CUDART_INF_F ? 0.f : fexp2(mw - M);
+        L = fmaf(wml[(t * 8 + h) * 2 + 1], sc, L);
+        acc = fmaf(wo[(t * 8 + h) * WS + dcol], sc, acc);
+      }
+    }
+    if (direct) {
+      outg[idx] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+      if (dcol == 0 && p.lse != nullptr)
+        p.lse[(size_t)b * p.d.Hq + (size_t)g * p.d.G + h] = L > 0.f ? (M + flog2(L)) * kLn2 : -CUDART_INF_F;
+    } else {
+      po[idx] = acc;
+      if (dcol == 0) {
+        pml[2 * h] = M;
+        pml[2 * h + 1] = L;
+      }
+    }
+  }
+}
+
 // Merge the cs CTA partials of the pair (flash-decoding LSE merge, T10) from
 // the L2-resident workspace and write out / lse; CTA `rank` writes a 1/cs
 // slice of the G*d_v outputs.
@@ -400,7 +602,12 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_consta
   float* po = p.part_o + ((size_t)pair * cs + rank) * tot;
   float* pml = p.part_ml + ((size_t)pair * cs + rank) * p.d.G * 2;
   if constexpr (MMA) {
-    phase_attend_mma<D>(p, pair, b, g, sel, tloc, smem + p.off_akv, po, pml);
+    if constexpr (D == 128) {
+      if (p.d.G <= 8 && !p.heads_as_m) phase_attend_mma_t<D>(p, pair, b, g, sel, tloc, smem + p.off_akv, po, pml);
+      else phase_attend_mma<D>(p, pair, b, g, sel, tloc, smem + p.off_akv, po, pml);
+    } else {
+      phase_attend_mma<D>(p, pair, b, g, sel, tloc, smem + p.off_akv, po, pml);
+    }
   } else {
     phase_attend_generic<T>(p, pair, b, g, sel, tloc, reinterpret_cast<float*>(smem + p.off_aq),
                             reinterpret_cast<float*>(smem + p.off_as), po, pml);

@@ -90,6 +90,7 @@ struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally wit
   int cs;
   int mma;       // 1: bf16 mma.sync GQA path (d in {64,128}, G <= 16); 2: bf16 mma.sync MLA path (576/512)
   int tloc_max;  // ceil(kt_eff / cs)
+  int heads_as_m;  // tuning: env TLS_ATTN_HEADS_AS_M=1 keeps the heads-as-M mma form for G <= 8
   int select;    // 1: first select S_t = top-k_t from the keys (a4); 0: read token_ids / num_tokens
   int attend;    // 1: attention (a5); 0: selection only (tls_select)
   int kb_eff;
@@ -210,7 +211,7 @@ static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
       s2 = align16(s2);
     } else if (p.mma) {
       p.off_akv = (unsigned)s2;  // 2 stages x (K chunk + V chunk); reused as the warp-partial scratch
-      size_t kv = (size_t)kAttnStages * 2 * kAttnChunk * d.d_k * 2;
+      size_t kv = (size_t)kAttnStages * 2 * kAttnChunk * d.d_k * 2 + (size_t)8 * 256;  // + per-warp P^T buffers
       size_t scratch = (size_t)8 * d.G * (d.d_v + 4) * 4 + (size_t)8 * 16 * 2 * 4;
       s2 = align16(s2 + (kv > scratch ? kv : scratch));
     } else {

@@ -55,7 +55,8 @@ __device__ __forceinline__ uint32_t first_key_with_bin_le(int b) {
 // hist_topk_emit then emits it.  Contains __syncthreads(); every thread of
 // the CTA must call it.
 __device__ inline HistPlan hist_topk_plan(const uint32_t* skeys, int nslots, const uint32_t* shist, int Kt,
-                                          uint32_t* scratch, FastTopKCtl& fk, TopKCtl& tk, HistSel& hs) {
+                                          uint32_t* scratch, FastTopKCtl& fk, TopKCtl& tk, HistSel& hs,
+                                          unsigned long long* dbg = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int* wgt = hs.wgt;
   int* weq = hs.weq;
@@ -157,6 +158,10 @@ __device__ inline HistPlan hist_topk_plan(const uint32_t* skeys, int nslots, con
     }
     __syncthreads();
     const int nbk = fk.bcount;
+    if (dbg && threadIdx.x == 0) {  // diagnostics: gather-pass end, boundary-bin size
+      dbg[6] = gtimer();
+      dbg[7] = (unsigned long long)nbk;
+    }
     if (nbk <= 1024) {
       // exact threshold: the kr-th largest boundary key (rank by comparison)
       if (tid == 0) fk.thr = 0u;
@@ -270,6 +275,209 @@ __device__ void hist_topk_emit(const uint32_t* skeys, int nslots, const HistPlan
   }
   for (int p = tid; p < pl.K; p += kThreads) put(slist[p], p);
   __syncthreads();
+}
+
+// Smallest key k >= 1 with key_bin(key2f(k)) <= b, 0 <= b < 1023, by one warp
+// in one round when possible: key_bin(f) <= b iff (6 - f) * 16 < b + 1, whose
+// exact boundary f* = 6 - (b + 1) / 16 is an fp32 value, so the answer lies
+// within a few ulps of f2key(f*); the 32 keys around it are tested at once and
+// the 32-ary search runs only if the window misses.
+__device__ __forceinline__ uint32_t bin_lower_key(int b) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t kc = f2key(6.0f - (float)(b + 1) * 0.0625f);
+  const uint32_t probe = kc - 15u + (uint32_t)lane;
+  const bool ok = probe >= 1u && probe <= 0xfffffff0u && key_bin(key2f(probe)) <= b;
+  const unsigned bal = __ballot_sync(0xffffffffu, ok);
+  if (bal != 0u && !(bal & 1u) && (bal >> 31)) {  // false .. true inside the window: monotone boundary found
+    return kc - 15u + (uint32_t)(__ffs(bal) - 1);
+  }
+  return first_key_with_bin_le(b);
+}
+
+// One-pass form of plan + emit for nslots <= kSelRunMax * kThreads: thread t
+// owns the contiguous slots [t*R, t*R + R), R = 4 * ceil(nslots / (4 *
+// kThreads)), read as 16-byte chunks in a rotated order (conflict-free banks),
+// and keeps two bitmasks over them: keys above the boundary bin and keys in it.
+// The boundary bin's few keys are gathered and ranked exactly; one packed block
+// scan of (#greater, #equal-to-threshold) per thread then gives every thread
+// its output position, and it emits its selected slots in slot order.  Same
+// result as hist_topk_plan + hist_topk_emit (ties at the threshold -> lower
+// slot, U2).  on_k(K) runs once per thread as soon as K is known, then
+// put(slot, pos) once per selected slot.  Returns K.
+constexpr int kSelRunMax = 64;  // keys per thread (two 32-bit masks)
+
+template <class FK, class F>
+__device__ int hist_topk_select(const uint32_t* skeys, int nslots, const uint32_t* shist, int Kt, uint32_t* scratch,
+                                FastTopKCtl& fk, TopKCtl& tk, HistSel& hs, int* slist, FK on_k, F put,
+                                unsigned long long* dbg = nullptr) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long cyc0 = clock64();
+#define TLS_CYC(i) \
+  if (dbg && tid == 0) dbg[65536 * 4 + (i)] = (unsigned long long)(clock64() - cyc0);
+  // this thread's run of keys (issued first; consumed after the interval is known)
+  const int nch = (nslots + 4 * kThreads - 1) / (4 * kThreads);  // 16-byte chunks per thread (<= 16)
+  const int r0 = tid * 4 * nch;
+  const int c0 = nch > 0 ? tid % nch : 0;
+  const uint4* k4 = reinterpret_cast<const uint4*>(skeys) + (r0 >> 2);
+  uint4 kv[kSelRunMax / 4];
+#pragma unroll
+  for (int j = 0; j < kSelRunMax / 4; ++j) {
+    if (j < nch) {
+      int c = c0 + j;  // rotated: the 8 threads of a phase hit distinct banks
+      if (c >= nch) c -= nch;
+      kv[j] = k4[c];
+    }
+  }
+  // boundary bin of the histogram (bins ascend as keys descend): 4 bins per thread
+  int c4[4], sum = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    c4[j] = (int)shist[4 * tid + j];
+    sum += c4[j];
+  }
+  int jtot;
+  const int excl = block_exclusive_scan(sum, tk.scan, &jtot);  // jtot = number of valid candidates
+  const int K = min(Kt, jtot);
+  on_k(K);
+  if (tid == 0) {
+    hs.bsel = -1;
+    fk.bcount = 0;
+  }
+  __syncthreads();
+  if (K < jtot && excl < K && K <= excl + sum) {
+    int above = excl;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (above + c4[j] >= K) {
+        hs.bsel = 4 * tid + j;
+        hs.above = above;
+        break;
+      }
+      above += c4[j];
+    }
+  }
+  __syncthreads();
+  TLS_CYC(0)
+  const int bsel = hs.bsel;
+  const bool take_all = K >= jtot;
+  if (!take_all && warp < 2) {  // the boundary bin as a key interval [klo, khi]
+    if (warp == 0) {
+      const uint32_t k = bsel >= 1023 ? 1u : bin_lower_key(bsel);
+      if (lane == 0) hs.klo = k;
+    } else {
+      const uint32_t k = bsel > 0 ? bin_lower_key(bsel - 1) - 1u : 0xffffffffu;
+      if (lane == 0) hs.khi = k;
+    }
+  }
+  __syncthreads();
+  TLS_CYC(1)
+  // keys above the boundary bin (every valid key when all are taken) and keys in it
+  const uint32_t khi = take_all ? 0u : hs.khi;
+  const uint32_t klo = take_all ? 0xffffffffu : hs.klo;
+  const uint32_t span = khi - klo;  // in-bin test: key - klo <= span (unsigned)
+  uint64_t gt = 0, bd = 0;
+#pragma unroll
+  for (int j = 0; j < kSelRunMax / 4; ++j) {
+    if (j < nch) {
+      int c = c0 + j;
+      if (c >= nch) c -= nch;
+      const uint32_t e[4] = {kv[j].x, kv[j].y, kv[j].z, kv[j].w};
+      uint32_t na = 0, nb = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        na |= (uint32_t)(e[u] > khi) << u;
+        nb |= (uint32_t)(e[u] - klo <= span) << u;
+      }
+      gt |= (uint64_t)na << (4 * c);
+      bd |= (uint64_t)nb << (4 * c);
+    }
+  }
+  {  // slots past nslots are not candidates
+    const int lim = nslots - r0;
+    const uint64_t live = lim >= 64 ? ~0ull : (lim <= 0 ? 0ull : (1ull << lim) - 1ull);
+    gt &= live;
+    bd = take_all ? 0ull : (bd & live);
+  }
+  const int nb_own = __popcll(bd);
+  if (nb_own) {  // gather the boundary bin's keys (few)
+    int dst = atomicAdd(&fk.bcount, nb_own);
+    for (uint64_t m = bd; m; m &= m - 1, ++dst) {
+      const int bit = __ffsll((long long)m) - 1;
+      if (dst < 1024) scratch[dst] = skeys[r0 + bit];
+    }
+  }
+  __syncthreads();
+  TLS_CYC(2)
+  const int nbk = take_all ? 0 : fk.bcount;
+  if (dbg && tid == 0) {  // diagnostics: classification-pass end, boundary-bin size
+    dbg[6] = gtimer();
+    dbg[7] = (unsigned long long)nbk;
+  }
+  if (nbk > 1024) {  // rare: an oversized boundary bin -> generic select into slist
+    const TopK t = fast_topk(skeys, nslots, K, false, fk, tk, scratch);
+    topk_emit(skeys, nslots, t, tk, [&](int i, int pos) { slist[pos] = i; });
+    for (int p = tid; p < K; p += kThreads) put(slist[p], p);
+    __syncthreads();
+    return K;
+  }
+  uint32_t thr = 0u;
+  if (!take_all) {
+    // exact threshold: the kr-th largest boundary key (rank by comparison)
+    const int kr = K - hs.above;
+    if (nbk <= 32) {  // one warp, keys in lanes, the others' keys by shuffle
+      if (warp == 0) {
+        const uint32_t v = lane < nbk ? scratch[lane] : 0u;
+        int gtc = 0, eqc = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t o = __shfl_sync(0xffffffffu, v, j);
+          gtc += o > v;
+          eqc += o == v;
+        }
+        if (lane < nbk && gtc < kr && gtc + eqc >= kr) fk.thr = v;  // every writer writes the same value
+      }
+    } else {
+      for (int i = tid; i < nbk; i += kThreads) {
+        const uint32_t v = scratch[i];
+        int gtc = 0, eqc = 0;
+        for (int j = 0; j < nbk; ++j) {
+          const uint32_t o = scratch[j];
+          gtc += o > v;
+          eqc += o == v;
+        }
+        if (gtc < kr && gtc + eqc >= kr) fk.thr = v;  // every writer writes the same value
+      }
+    }
+    __syncthreads();
+    thr = fk.thr;
+  }
+  TLS_CYC(3)
+  // boundary keys of this run: > thr joins gt, == thr is a tie
+  uint64_t eq = 0;
+  for (uint64_t m = bd; m; m &= m - 1) {
+    const int bit = __ffsll((long long)m) - 1;
+    const uint32_t k = skeys[r0 + bit];
+    if (k > thr) gt |= 1ull << bit;
+    else if (k == thr) eq |= 1ull << bit;
+  }
+  const int ngt = __popcll(gt), neq = __popcll(eq);
+  int tot;
+  const int pre = block_exclusive_scan(ngt | (neq << 16), tk.scan, &tot);
+  TLS_CYC(4)
+  const int gt_before = pre & 0xffff, eq_before = pre >> 16;
+  const int take_eq = K - (tot & 0xffff);  // ties taken in slot order
+  int ntake = min(max(take_eq - eq_before, 0), neq);
+  uint64_t selm = gt;
+  for (uint64_t m = eq; ntake > 0; --ntake, m &= m - 1) selm |= m & (~m + 1ull);
+  int pos = gt_before + min(eq_before, max(take_eq, 0));
+  // selected slots -> slist in slot order, then put over the list with every lane busy
+  for (uint64_t m = selm; m; m &= m - 1) slist[pos++] = r0 + __ffsll((long long)m) - 1;
+  __syncthreads();
+  for (int p = tid; p < K; p += kThreads) put(slist[p], p);
+  __syncthreads();
+  TLS_CYC(5)
+#undef TLS_CYC
+  return K;
 }
 
 }  // namespace tls
