@@ -79,14 +79,18 @@ __global__ void __launch_bounds__(kThreads, (NT == 1 && KS * NSPLIT <= 2) ? 5 : 
     mbar_init(&bar, 1);
     mbar_init(&qbar, 1);
     mbar_fence_init();
-    if (p.qtma) {  // the pair's q rows and channel ids: two TMA bulk copies
+    if (p.qfrag != nullptr) {  // the pair's q~ fragment blob built by qq_kernel: one TMA bulk copy
+      const uint32_t qfb = (uint32_t)(NSPLIT * NT * KS * 256 + NT * 32);
+      mbar_arrive_expect_tx(&qbar, qfb);
+      tma_bulk_g2s(smem + p.off_qb, p.qfrag + (size_t)pair * qfb, qfb, &qbar);
+    } else if (p.qtma) {  // the pair's q rows and channel ids: two TMA bulk copies
       const uint32_t qb_ = (uint32_t)(d.G * d.d_k * sizeof(T)), cb_ = (uint32_t)(d.d_c * 4);
       mbar_arrive_expect_tx(&qbar, qb_ + cb_);
       tma_bulk_g2s(qrows, qg, qb_, &qbar);
       tma_bulk_g2s(chan_s, p.channels + (size_t)g * d.d_c, cb_, &qbar);
     }
   }
-  if (!p.qtma && tid < KS * 16) ctl.chan[tid] = p.channels[(size_t)g * d.d_c + tid];
+  if (p.qfrag == nullptr && !p.qtma && tid < KS * 16) ctl.chan[tid] = p.channels[(size_t)g * d.d_c + tid];
   const int* cand = p.guide ? p.guide + (size_t)pair * d.Kb : p.block_ids + (size_t)pair * d.Kb;
   // ---- candidate blocks (ascending): M_t from K1 (block_ids) or the lag-mode guide ----
   {
@@ -124,6 +128,9 @@ __global__ void __launch_bounds__(kThreads, (NT == 1 && KS * NSPLIT <= 2) ? 5 : 
   }
   // ---- channel-projected query q~, its B fragments and sum ----
   constexpr int DC = KS * 16;
+  if (p.qfrag != nullptr) {
+    mbar_wait(&qbar, 0);
+  } else {
   if (p.qtma) {
     mbar_wait(&qbar, 0);
     for (int i = tid; i < NT * 8 * DC; i += kThreads) {
@@ -152,6 +159,7 @@ __global__ void __launch_bounds__(kThreads, (NT == 1 && KS * NSPLIT <= 2) ? 5 : 
     qsum[tid] = s;
   }
   __syncthreads();
+  }
   TLS_STAMP(1)
   if (nbl > 0) mbar_wait(&bar, 0);
   TLS_STAMP(2)

@@ -32,15 +32,24 @@ __device__ inline void build_qfrag(const Dims& d, const void* qrows, const int* 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt0 = (d.G + 7) / 8, NT = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);
   const int DC = d.d_c, KS = DC / 16, WPT = KS / 2, NSPLIT = d.bf16 ? 1 : 3;
-  for (int i = tid; i < NT * 8 * DC; i += kThreads) {
-    const int h = i / DC, c = i - h * DC;
-    float v = 0.f;
-    if (h < d.G) {
-      const size_t o = (size_t)h * d.d_k + ch[c];
-      v = d.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(qrows)[o])
-                 : reinterpret_cast<const float*>(qrows)[o];
+  for (int i0 = 0; i0 < NT * 8 * DC; i0 += 8 * kThreads) {  // 8 independent loads in flight per thread
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * kThreads + tid;
+      const int h = i / DC, c = i - h * DC;
+      v[u] = 0.f;
+      if (i < NT * 8 * DC && h < d.G) {
+        const size_t o = (size_t)h * d.d_k + ch[c];
+        v[u] = d.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(qrows)[o])
+                      : reinterpret_cast<const float*>(qrows)[o];
+      }
     }
-    qc[i] = v;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * kThreads + tid;
+      if (i < NT * 8 * DC) qc[i] = v[u];
+    }
   }
   __syncthreads();
   const int qfb = NSPLIT * NT * KS * 256 + NT * 32;
