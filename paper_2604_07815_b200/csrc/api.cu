@@ -17,6 +17,7 @@
 #include "params.h"
 #include "fasttopk.cuh"
 #include "launch.h"
+#include <algorithm>
 
 namespace tls {
 cudaError_t launch_select_fused(const FusedParams& p, cudaStream_t st, const LaunchOpts& o);
@@ -241,10 +242,14 @@ tls_config sub_config(const tls_config* c, int ns, int s, int* b0) {
 int fused_mode(const tls_config*) { return 1; }
 
 // Bytes of block summaries per select_kernel CTA (TLS_TILE_KB overrides; tuning).
-int score_tile_bytes() {
+// Block-summary rows per K1 tile CTA: <= 64 rows (8 TMA groups of 8 rows, one
+// mbarrier per warp), 32 KB of rows by default (C4 measured: 32 KB 129.9 us/step,
+// 64 KB 133.6, 96 KB 132.9, 128 KB 153.2).  Tuning: env TLS_TILE_KB (4..192).
+int score_tile_rows(int rowbytes) {
   const char* e = getenv("TLS_TILE_KB");
   const int kb = e ? atoi(e) : 0;
-  return (kb >= 4 && kb <= 32) ? kb * 1024 : tls::kScoreTileBytes;  // <= 8 TMA groups of 8 rows (kWarps mbarriers)
+  const int bytes = (kb >= 4 && kb <= 192) ? kb * 1024 : tls::kScoreTileBytes;
+  return std::min(64, bytes / rowbytes);
 }
 
 struct ChainPlan {
@@ -262,7 +267,7 @@ tls_status plan_chain(const tls_config* cfg, int do_attend, ChainPlan& c) {
   c.mode = fused_mode(cfg);
   c.fp.d = dims_of(cfg);
   c.fp.mode = c.mode;
-  c.fp.tb = score_tile_bytes() / (2 * cfg->d_k * (int)elem_bytes(cfg));
+  c.fp.tb = score_tile_rows(2 * cfg->d_k * (int)elem_bytes(cfg));
   if (c.fp.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
   tls::plan_fused(c.fp, sizeof(tls::FastTopKCtl));
   if ((int)c.fp.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "selection-kernel shared-memory plan does not fit");
@@ -635,7 +640,7 @@ tls_status tls_block_scores(const tls_config* cfg, const void* q, const int32_t*
   memset(&fp, 0, sizeof(fp));
   fp.d = dims_of(cfg);
   fp.mode = 0;
-  fp.tb = tls::kScoreTileBytes / (2 * cfg->d_k * (int)elem_bytes(cfg));
+  fp.tb = score_tile_rows(2 * cfg->d_k * (int)elem_bytes(cfg));
   if (fp.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
   tls::plan_fused(fp, sizeof(tls::FastTopKCtl));
   fp.sstride = fp.d.M;

@@ -60,7 +60,19 @@ __device__ __forceinline__ void score_tile(const FusedParams& p, int pair, int b
     // QQ of the pair from qq_kernel (PDL primary): the tile copies above are already in flight
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     const float* qq = p.qq + (size_t)pair * 2 * d.d_k;
-    for (int c = tid; c < 2 * d.d_k; c += kThreads) QQ[c] = __ldcg(qq + c);
+    for (int c0 = 0; c0 < 2 * d.d_k; c0 += 8 * kThreads) {  // loads batched ahead of the stores (no aliasing chain)
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * kThreads + tid;
+        v[u] = c < 2 * d.d_k ? __ldcg(qq + c) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * kThreads + tid;
+        if (c < 2 * d.d_k) QQ[c] = v[u];
+      }
+    }
   } else {
     const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
     for (int c = tid; c < d.d_k; c += kThreads) {
@@ -84,7 +96,13 @@ __device__ __forceinline__ void score_tile(const FusedParams& p, int pair, int b
     for (int c = 0; c < CPL; ++c) {
       const int ch = lane + 32 * c;
 #pragma unroll
-      for (int e = 0; e < EPC; ++e) qreg[c][e] = ch < nchunk ? QQ[ch * EPC + e] : 0.f;
+      for (int e = 0; e < EPC; e += 4) {  // 16-byte loads
+        const float4 v = ch < nchunk ? *reinterpret_cast<const float4*>(QQ + ch * EPC + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        qreg[c][e] = v.x;
+        qreg[c][e + 1] = v.y;
+        qreg[c][e + 2] = v.z;
+        qreg[c][e + 3] = v.w;
+      }
     }
     for (int r = warp; r < nb; r += kWarps) {
       mbar_wait(&bars[r >> 3], 0);
@@ -220,7 +238,7 @@ template <typename T, int CPL, int MODE>
 __global__ void __launch_bounds__(kThreads, CPL <= 2 ? 6 : 3) select_kernel(const __grid_constant__ FusedParams p) {
   constexpr int EPC = 16 / sizeof(T);
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ float QQ[32 * CPL * EPC];
+  __shared__ __align__(16) float QQ[32 * CPL * EPC];
   __shared__ __align__(8) uint64_t bars[kWarps];
   __shared__ WorkerCtl ctl;
   const Dims& d = p.d;
