@@ -541,29 +541,64 @@ __device__ void phase_attend_mma_t(const AttendParams& p, int pair, int b, int g
 // Merge the cs CTA partials of the pair (flash-decoding LSE merge, T10) from
 // the L2-resident workspace and write out / lse; CTA `rank` writes a 1/cs
 // slice of the G*d_v outputs.
-template <typename T>
+template <typename T, int U>
 __device__ void phase_merge(const AttendParams& p, int pair, int b, int g, unsigned rank) {
-  const int tot = p.d.G * p.d.d_v;
-  const int lo = (int)((long long)tot * rank / p.cs), hi = (int)((long long)tot * (rank + 1) / p.cs);
-  const float* po = p.part_o + (size_t)pair * p.cs * tot;
-  const float* pml = p.part_ml + (size_t)pair * p.cs * p.d.G * 2;
-  T* outg = reinterpret_cast<T*>(p.out) + ((size_t)b * p.d.Hq + (size_t)g * p.d.G) * p.d.d_v;
-  for (int idx = lo + (int)threadIdx.x; idx < hi; idx += kThreads) {
-    const int h = idx / p.d.d_v, c = idx - h * p.d.d_v;
+  // per-head merge weights once (G <= 32 heads, cs <= 16 partials), then every
+  // output element is a cs-term dot product with its loads batched ahead (U
+  // elements per thread per step)
+  __shared__ float s_w[16][32], s_inv[32];
+  const int G = p.d.G, cs = p.cs;
+  const int tot = G * p.d.d_v;
+  const int lo = (int)((long long)tot * rank / cs), hi = (int)((long long)tot * (rank + 1) / cs);
+  const float* po = p.part_o + (size_t)pair * cs * tot;
+  const float* pml = p.part_ml + (size_t)pair * cs * G * 2;
+  T* outg = reinterpret_cast<T*>(p.out) + ((size_t)b * p.d.Hq + (size_t)g * G) * p.d.d_v;
+  if ((int)threadIdx.x < G) {
+    const int h = threadIdx.x;
     float M = -CUDART_INF_F;
-    for (int rr = 0; rr < p.cs; ++rr) M = fmaxf(M, __ldcg(pml + (rr * p.d.G + h) * 2));
-    float L = 0.f, o = 0.f;
-    if (M != -CUDART_INF_F) {
-      for (int rr = 0; rr < p.cs; ++rr) {
-        const float mr = __ldcg(pml + (rr * p.d.G + h) * 2);
-        const float w = mr == -CUDART_INF_F ? 0.f : fexp2(mr - M);
-        L = fmaf(__ldcg(pml + (rr * p.d.G + h) * 2 + 1), w, L);
-        o = fmaf(__ldcg(po + (size_t)rr * tot + idx), w, o);
+    for (int rr = 0; rr < cs; ++rr) M = fmaxf(M, __ldcg(pml + (rr * G + h) * 2));
+    float L = 0.f;
+    for (int rr = 0; rr < cs; ++rr) {
+      const float mr = __ldcg(pml + (rr * G + h) * 2);
+      const float w = (M == -CUDART_INF_F || mr == -CUDART_INF_F) ? 0.f : fexp2(mr - M);
+      L = fmaf(__ldcg(pml + (rr * G + h) * 2 + 1), w, L);
+      s_w[rr][h] = w;
+    }
+    s_inv[h] = L > 0.f ? 1.f / L : 0.f;
+    if (rank == 0 && p.lse != nullptr)
+      p.lse[(size_t)b * p.d.Hq + (size_t)g * G + h] = L > 0.f ? (M + flog2(L)) * kLn2 : -CUDART_INF_F;
+  }
+  __syncthreads();
+  if constexpr (U == 1) {
+    for (int idx = lo + (int)threadIdx.x; idx < hi; idx += kThreads) {
+      const int h = idx / p.d.d_v;
+      float o = 0.f;
+#pragma unroll 4
+      for (int rr = 0; rr < cs; ++rr) o = fmaf(__ldcg(po + (size_t)rr * tot + idx), s_w[rr][h], o);
+      outg[idx] = from_f32<T>(o * s_inv[h]);
+    }
+  } else {
+    for (int i0 = lo; i0 < hi; i0 += U * kThreads) {
+      float v[U][16];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = i0 + u * kThreads + (int)threadIdx.x;
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr) v[u][rr] = (rr < cs && idx < hi) ? __ldcg(po + (size_t)rr * tot + idx) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = i0 + u * kThreads + (int)threadIdx.x;
+        if (idx < hi) {
+          const int h = idx / p.d.d_v;
+          float o = 0.f;
+#pragma unroll
+          for (int rr = 0; rr < 16; ++rr)
+            if (rr < cs) o = fmaf(v[u][rr], s_w[rr][h], o);
+          outg[idx] = from_f32<T>(o * s_inv[h]);
+        }
       }
     }
-    outg[idx] = from_f32<T>(L > 0.f ? o / L : 0.f);
-    if (c == 0 && p.lse != nullptr)
-      p.lse[(size_t)b * p.d.Hq + (size_t)g * p.d.G + h] = L > 0.f ? (M + flog2(L)) * kLn2 : -CUDART_INF_F;
   }
 }
 
@@ -617,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_consta
   if (cs > 1) cluster_sync_all();  // release/acquire at cluster scope: partials visible in L2
   if (cs > 1 && p.ready_in != nullptr && rank == 0 && tid == 0) p.ready_in[pair] = 0u;  // all CTAs passed the wait
   __syncthreads();
-  phase_merge<T>(p, pair, b, g, rank);
+  phase_merge<T, 1>(p, pair, b, g, rank);  // U = 1: within the 128-register budget
 }
 
 // --------------------------------------------------------------------------
@@ -663,8 +698,8 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
     K = min(min(max(p.num_tokens[pair], 0), p.d.Kt), p.tloc_max * cs);
   }
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem + p.off_akv);
-  __nv_bfloat16* sKV = sQ + MT * 16 * DK;           // 2 buffers of TC rows
-  float* sS = reinterpret_cast<float*>(sKV + 2 * TC * DK);
+  __nv_bfloat16* sKV = sQ + MT * 16 * DK;           // kMlaStages buffers of TC rows
+  float* sS = reinterpret_cast<float*>(sKV + kMlaStages * TC * DK);
   __nv_bfloat16* sP = reinterpret_cast<__nv_bfloat16*>(sS + MT * 16 * SST);
   float* sAlpha = reinterpret_cast<float*>(sP + MT * 16 * PST);
   float* sM = sAlpha + MT * 16;
@@ -698,7 +733,11 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
     cp_async_commit();
   };
   const int nchunks = (tloc + TC - 1) / TC;
-  if (nchunks > 0) load_chunk(0, 0);
+#pragma unroll
+  for (int c = 0; c < kMlaStages - 1; ++c) {
+    if (c < nchunks) load_chunk(c, c);
+    else cp_async_commit();
+  }
   const float sm2 = p.d.sm_scale * kLog2e;
   float o[MT][8][4];
 #pragma unroll
@@ -707,29 +746,33 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
     for (int j = 0; j < 8; ++j) o[mt][j][0] = o[mt][j][1] = o[mt][j][2] = o[mt][j][3] = 0.f;
   const int r = lane >> 2, c2 = 2 * (lane & 3);
   for (int c = 0; c < nchunks; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < nchunks) {
-      load_chunk(c + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    const int buf = c % kMlaStages;
+    // refill the buffer chunk c-1 used (every warp passed the trailing barrier of c-1)
+    if (c + kMlaStages - 1 < nchunks) load_chunk(c + kMlaStages - 1, (c + kMlaStages - 1) % kMlaStages);
+    else cp_async_commit();
+    cp_async_wait<kMlaStages - 1>();
     __syncthreads();
     const __nv_bfloat16* sK = sKV + buf * TC * DK;
     // ---- S = Q K^T (log2 units) ----
     {
       const int mt = warp >> 2, nb = (warp & 3) * 8;
       if (mt < MT) {
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};  // two chains (even / odd k-steps)
+        static_assert(KS % 2 == 0, "even number of k-steps");
 #pragma unroll 4
-        for (int kk = 0; kk < KS; ++kk) {
-          uint32_t a[4], bk[4];
+        for (int kk = 0; kk < KS; kk += 2) {
+          uint32_t a[4], bk[4], a2[4], bk2[4];
           const int qrow = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, qch = kk * 2 + (lane >> 4);
           ldsm_x4(a, sQ + qrow * DK + ((qch ^ (qrow & 7)) << 3));
+          ldsm_x4(a2, sQ + qrow * DK + (((qch + 2) ^ (qrow & 7)) << 3));
           const int krow = nb + (lane & 7), kch = kk * 2 + ((lane >> 3) & 1);
           ldsm_x4(bk, sK + krow * DK + ((kch ^ (krow & 7)) << 3));  // lanes 16-31 duplicate 0-15
+          ldsm_x4(bk2, sK + krow * DK + (((kch + 2) ^ (krow & 7)) << 3));
           mma_bf16_16816(acc, a, bk[0], bk[1]);
+          mma_bf16_16816(acc2, a2, bk2[0], bk2[1]);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] += acc2[i];
         const int tk = nb + c2;
         const bool v0 = c * TC + tk < tloc, v1 = c * TC + tk + 1 < tloc;
         sS[(mt * 16 + r) * SST + tk] = v0 ? acc[0] * sm2 : -CUDART_INF_F;
@@ -808,6 +851,7 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
     }
     __syncthreads();  // buffer `buf` and sS / sP free for the next chunk
   }
+  if (p.dbg && rank == 0 && tid == 0) p.dbg[(size_t)pair * 8 + 5] = gtimer();
   // ---- this CTA's partial (unnormalised o, max, sum) -> workspace ----
   const int tot = G * DV;
   float* po = p.part_o + ((size_t)pair * cs + rank) * tot;
@@ -828,7 +872,7 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
   if (cs > 1) cluster_sync_all();
   if (cs > 1 && p.ready_in != nullptr && rank == 0 && tid == 0) p.ready_in[pair] = 0u;  // all CTAs passed the wait
   __syncthreads();
-  phase_merge<__nv_bfloat16>(p, pair, b, 0, rank);
+  phase_merge<__nv_bfloat16, 4>(p, pair, b, 0, rank);
 }
 
 template <typename T, bool MMA, int D>

@@ -60,18 +60,17 @@ __device__ __forceinline__ void score_tile(const FusedParams& p, int pair, int b
     // QQ of the pair from qq_kernel (PDL primary): the tile copies above are already in flight
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     const float* qq = p.qq + (size_t)pair * 2 * d.d_k;
-    for (int c0 = 0; c0 < 2 * d.d_k; c0 += 8 * kThreads) {  // loads batched ahead of the stores (no aliasing chain)
-      float v[8];
+    constexpr int NQ = (32 * CPL * EPC + kThreads - 1) / kThreads;  // QQ holds <= 32 * CPL * EPC floats
+    float v[NQ];  // loads batched ahead of the stores (no aliasing chain)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int c = c0 + u * kThreads + tid;
-        v[u] = c < 2 * d.d_k ? __ldcg(qq + c) : 0.f;
-      }
+    for (int u = 0; u < NQ; ++u) {
+      const int c = u * kThreads + tid;
+      v[u] = c < 2 * d.d_k ? __ldcg(qq + c) : 0.f;
+    }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int c = c0 + u * kThreads + tid;
-        if (c < 2 * d.d_k) QQ[c] = v[u];
-      }
+    for (int u = 0; u < NQ; ++u) {
+      const int c = u * kThreads + tid;
+      if (c < 2 * d.d_k) QQ[c] = v[u];
     }
   } else {
     const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
@@ -298,8 +297,8 @@ __global__ void __launch_bounds__(kThreads) qq_kernel(const __grid_constant__ Fu
   for (int c = threadIdx.x; c < d.d_k; c += kThreads) {
     float qp = 0.f, qn = 0.f;
 #pragma unroll 8
-    for (int h = 0; h < d.G; ++h) {
-      const float v = to_f32<T>(qg[(size_t)h * d.d_k + c]);
+    for (int h = 0; h < d.G; ++h) {  // read-only loads: batched ahead of the stores below
+      const float v = to_f32<T>(__ldg(qg + (size_t)h * d.d_k + c));
       qp += fmaxf(v, 0.f);
       qn += fminf(v, 0.f);
     }

@@ -12,7 +12,8 @@ namespace tls {
 
 constexpr int kAttnChunk = 64;     // tokens per K/V staging stage of the GQA mma attention (8 warps x 8)
 constexpr int kAttnStages = 3;     // cp.async pipeline depth of the GQA mma attention
-constexpr int kMlaChunkTokens = 32;  // latent rows per staging chunk of the MLA attention (double-buffered)
+constexpr int kMlaChunkTokens = 32;  // latent rows per staging chunk of the MLA attention
+constexpr int kMlaStages = 3;        // MLA attention cp.async pipeline depth (chunks in flight + 1)
 constexpr int kScoreTileBytes = 32 * 1024;  // K1: bytes of block summaries per CTA (TMA tile)
 
 struct Dims {
@@ -206,7 +207,7 @@ static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
     if (p.mma == 2) {  // MLA tensor-core path: Q, 2 latent-row chunks, S, P, alpha/m/l
       const int mt16 = d.G <= 16 ? 16 : 32;
       p.off_akv = (unsigned)s2;
-      s2 += (size_t)mt16 * d.d_k * 2 + (size_t)2 * kMlaChunkTokens * d.d_k * 2;
+      s2 += (size_t)mt16 * d.d_k * 2 + (size_t)kMlaStages * kMlaChunkTokens * d.d_k * 2;
       s2 += (size_t)mt16 * (kMlaChunkTokens + 4) * 4 + (size_t)mt16 * (kMlaChunkTokens + 8) * 2 + (size_t)3 * mt16 * 4;
       s2 = align16(s2);
     } else if (p.mma) {
