@@ -2,6 +2,13 @@
 device time of one TLS decode step vs a dense decode over the full context, on the
 same synthetic workload, L2 flushed before each call.  Not a bench line.
 
+Comparison operators of the paper expressed as configurations of this
+operator, same kernels, same inputs:
+  quest -- block selection only: K_t = K_b * B, so every token of the K_b selected
+           blocks is attended (the token scoring still runs, so this is an upper
+           bound on a Quest kernel built from these parts);
+  ds    -- token selection only: K_b = m, every block is a candidate (the channel-
+           index scoring runs over the whole context).
 Dense baselines: GQA -- flash_attn.flash_attn_with_kvcache (the library's FA2 decode
 kernel; the KV cache is re-laid out to [B, S, Hkv, D] once, untimed); MLA (d_k 576,
 beyond flash_attn's head dims) -- this repo's attention kernel over every token.
@@ -43,6 +50,15 @@ def main():
         t_tls = med(bench.time_steps(lambda i: tls.decode(cfg, queries[i % 8], inputs["k_cache"], inputs["v_cache"],
                                                            inputs["seq_lens"], idx), 50, 5, flush, st))
         rec = {"workload": w.name, "tls_us": t_tls * 1e3, "context": w.context, "batch": w.batch, "layout": w.layout}
+        for tag, kw in (("quest", {"top_tokens": w.top_blocks * w.block_size}), ("ds", {"top_blocks": cfg.num_blocks})):
+            try:
+                vcfg = tls.TLSConfig(**{**w.config_kwargs(), **kw})
+                t_v = med(bench.time_steps(lambda i: tls.decode(vcfg, queries[i % 8], inputs["k_cache"],
+                                                                inputs["v_cache"], inputs["seq_lens"], idx),
+                                           20, 3, flush, st))
+                rec.update({f"{tag}_us": t_v * 1e3, f"tls_speedup_vs_{tag}": t_v / t_tls})
+            except Exception as e:  # noqa: BLE001
+                rec[f"{tag}_error"] = f"{type(e).__name__}: {e}"[:200]
         if w.layout == "gqa":
             try:
                 from flash_attn import flash_attn_with_kvcache
