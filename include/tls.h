@@ -228,6 +228,60 @@ tls_status tls_cache_fetch(const tls_config* cfg, const void* k_host, const void
                            const tls_token_cache* cache, int32_t* slot_ids, int32_t* miss_count,
                            tls_stream_t stream);
 
+/*
+ * Block-granular, asynchronous form of the offload engine (AsyncTLS §4.2,
+ * P:373-383).  The GPU keeps whole B-token blocks: every
+ * pair owns `capacity` block slots (>= 2 * top_blocks).  With the one-step
+ * lag S_t = TokenSelect(q_t, M_{t-1}) (tls_select / tls_decode with
+ * guide_block_ids = M_{t-1}) the token selection of step t only reads
+ * blocks of M_{t-1}, so the blocks of M_t can be transferred while step t's
+ * attention runs and the next layer computes:
+ *   step t (main stream):  tls_select(q_t, guide = M_{t-1}) -> M_t, S_t
+ *                          wait for the update of step t-1 (event)
+ *                          tls_block_cache_rows(S_t) -> slot_rows
+ *                          tls_sparse_attend over (k_slots, v_slots, slot_rows)
+ *   step t (side stream):  after the select: tls_block_cache_update(keep =
+ *                          M_{t-1}, block_ids = M_t), record an event
+ * tls_block_cache_update frees the slots whose block is in neither M_{t-1}
+ * (still read by step t's attention) nor M_t, assigns free slots to the blocks
+ * of M_t that are not resident (in M_t order: the cache state is
+ * deterministic), copies their B rows of K (and V) from pinned, device-mapped
+ * host memory with a zero-copy gather, and writes the number of blocks fetched
+ * per pair to miss_count (nullable): the transfer T_t = M_t \ C_t of P:378.
+ * keep_block_ids may be NULL (nothing pinned).  tls_block_cache_rows writes
+ * the cache row slot_of_block[t / B] * B + t % B of every selected token
+ * (0 past num_tokens or when the token's block is not resident, counted in
+ * absent [batch, Hkv], nullable), so tls_sparse_attend with max_seq_len =
+ * capacity * B over the slot arrays computes exactly the attention over S_t.
+ * One launch each (one CTA per pair).
+ * Errors: TLS_ERR_CONFIG if capacity < 2 * top_blocks; TLS_ERR_INPUT for NULL
+ * buffers or host caches that are not device-mapped.
+ */
+typedef struct {
+  int32_t capacity;       /* block slots per pair, >= 2 * top_blocks                          */
+  void* k_slots;          /* [batch, Hkv, capacity * block_size, d_k] dtype, device           */
+  void* v_slots;          /* [batch, Hkv, capacity * block_size, d_v] dtype (NULL: MLA)       */
+  int32_t* slot_of_block; /* [batch, Hkv, ceil(max_seq_len / block_size)], -1 = not resident  */
+  int32_t* block_of_slot; /* [batch, Hkv, capacity], -1 = free; both initialised to -1        */
+} tls_block_cache;
+
+tls_status tls_block_cache_update(const tls_config* cfg, const void* k_host, const void* v_host,
+                                  const int32_t* keep_block_ids, const int32_t* block_ids,
+                                  const tls_block_cache* cache, int32_t* miss_count, tls_stream_t stream);
+tls_status tls_block_cache_rows(const tls_config* cfg, const int32_t* token_ids, const int32_t* num_tokens,
+                                const tls_block_cache* cache, int32_t* slot_rows, int32_t* absent,
+                                tls_stream_t stream);
+
+/* tls_decode with the K/V rows read from a block cache: the attention of token
+ * t reads row slot_of_block[t / B] * B + t % B of (k_slots, v_slots), so every
+ * block of the candidate set (M_t, or guide_block_ids = M_{t-1} in lag mode)
+ * must be resident (tls_block_cache_update).  Same outputs and workspace as
+ * tls_decode (which = 2); one fused launch chain. */
+tls_status tls_decode_block_cache(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
+                                  const int32_t* guide_block_ids, const tls_block_cache* cache, int32_t* block_ids,
+                                  int32_t* token_ids, int32_t* num_tokens, float* token_scores, void* out,
+                                  float* lse, void* workspace, size_t workspace_bytes, tls_stream_t stream);
+
 /* Workspace bytes needed by: which = 0 tls_select, 1 tls_sparse_attend,
  * 2 tls_decode.  The select part holds the fp32 block scores of every pair,
  * per-chunk softmax statistics, the ranking key of every candidate token and a

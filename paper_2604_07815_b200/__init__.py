@@ -24,6 +24,12 @@ from .ops import (  # noqa: F401
     host_kv,
     cache_fetch,
     offload_decode,
+    TLSBlockCache,
+    alloc_block_cache,
+    block_cache_update,
+    block_cache_rows,
+    decode_block_cache,
+    AsyncOffloadDecoder,
 )
 from ._lib import TLSError, load  # noqa: F401
 

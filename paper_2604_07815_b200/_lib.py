@@ -30,6 +30,9 @@ EXPORTS = (
     "tls_select_mode",
     "tls_workspace_init",
     "tls_cache_fetch",
+    "tls_block_cache_update",
+    "tls_block_cache_rows",
+    "tls_decode_block_cache",
     "tls_timing_enable",
     "tls_timing_read",
     "tls_status_string",
@@ -75,6 +78,16 @@ class TLSTokenCacheC(ctypes.Structure):
     ]
 
 
+class TLSBlockCacheC(ctypes.Structure):
+    _fields_ = [
+        ("capacity", ctypes.c_int32),
+        ("k_slots", ctypes.c_void_p),
+        ("v_slots", ctypes.c_void_p),
+        ("slot_of_block", ctypes.c_void_p),
+        ("block_of_slot", ctypes.c_void_p),
+    ]
+
+
 class TLSError(RuntimeError):
     def __init__(self, status: int, detail: str):
         self.status = status
@@ -110,6 +123,10 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "tls_select": (_I32, [_PCFG, _P, _P, _PIDX, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_sparse_attend": (_I32, [_PCFG, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_cache_fetch": (_I32, [_PCFG, _P, _P, _P, _P, ctypes.POINTER(TLSTokenCacheC), _P, _P, _P]),
+        "tls_block_cache_update": (_I32, [_PCFG, _P, _P, _P, _P, ctypes.POINTER(TLSBlockCacheC), _P, _P]),
+        "tls_block_cache_rows": (_I32, [_PCFG, _P, _P, ctypes.POINTER(TLSBlockCacheC), _P, _P, _P]),
+        "tls_decode_block_cache": (_I32, [_PCFG, _P, _P, _PIDX, _P, ctypes.POINTER(TLSBlockCacheC), _P, _P, _P, _P,
+                                          _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_decode": (_I32, [_PCFG, _P, _P, _P, _P, _PIDX, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_workspace_bytes": (ctypes.c_size_t, [_PCFG, _I32]),
         "tls_launch_count": (_I32, [_PCFG, _I32]),

@@ -23,6 +23,8 @@ namespace tls {
 cudaError_t launch_select_fused(const FusedParams& p, cudaStream_t st, const LaunchOpts& o);
 cudaError_t launch_qq(const FusedParams& p, cudaStream_t st, const LaunchOpts& o);
 cudaError_t launch_cache_fetch(const CacheFetchParams& p, cudaStream_t st);
+cudaError_t launch_block_cache_update(const BlockCacheParams& p, cudaStream_t st);
+cudaError_t launch_block_cache_rows(const BlockCacheParams& p, cudaStream_t st);
 cudaError_t launch_token_cluster(const SelectParams& p, cudaStream_t st, const LaunchOpts& o);
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t st, const LaunchOpts& o);
 int score_cpl(int d_k, size_t elem_bytes);
@@ -324,6 +326,8 @@ struct StepPtrs {
   float* token_scores;
   void* out;
   float* lse;
+  const int32_t* slot_of_block;  // block cache (tls_decode_block_cache): K/V rows via the slot map, else NULL
+  long long kv_rows;             // rows per pair of k_cache / v_cache (max_seq_len, or capacity * block_size)
 };
 
 // The pointers of sub-batch [b0, b0 + n) (row-major layouts of tls.h).
@@ -335,8 +339,10 @@ StepPtrs offset_ptrs(const tls_config* c, const StepPtrs& a, int b0) {
     return p ? static_cast<const char*>(p) + bytes : nullptr;
   };
   r.q = adv(a.q, B0 * c->num_q_heads * c->d_k * eb);
-  r.k_cache = adv(a.k_cache, B0 * Hkv * S * c->d_k * eb);
-  r.v_cache = adv(a.v_cache, B0 * Hkv * S * c->d_v * eb);
+  const size_t R = (size_t)a.kv_rows;
+  r.k_cache = adv(a.k_cache, B0 * Hkv * R * c->d_k * eb);
+  r.v_cache = adv(a.v_cache, B0 * Hkv * R * c->d_v * eb);
+  r.slot_of_block = a.slot_of_block ? a.slot_of_block + B0 * Hkv * M : nullptr;
   r.seq_lens = a.seq_lens + b0;
   r.idx.block_minmax = const_cast<char*>(adv(a.idx.block_minmax, B0 * Hkv * M * 2 * c->d_k * eb));
   r.idx.codes = a.idx.codes + B0 * Hkv * S * (c->d_c / 2);
@@ -417,6 +423,8 @@ tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int
     ap.q = a.q;
     ap.k_cache = a.k_cache;
     ap.v_cache = cfg->layout == TLS_MLA ? nullptr : a.v_cache;
+    ap.kv_rows = a.kv_rows;
+    ap.slot_of_block = a.slot_of_block;
     ap.seq_lens = a.seq_lens;
     ap.cand = a.guide ? a.guide : a.block_ids;
     ap.keys = sp.keys;
@@ -476,7 +484,8 @@ tls_status pipeline_for_device(Pipeline** out) {
 tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
                     const int32_t* seq_lens, const tls_index* idx, const int32_t* guide, int32_t* block_ids,
                     int32_t* token_ids, int32_t* num_tokens, float* token_scores, void* out, float* lse,
-                    void* workspace, size_t workspace_bytes, int do_attend, cudaStream_t st) {
+                    void* workspace, size_t workspace_bytes, int do_attend, cudaStream_t st,
+                    const int32_t* slot_of_block = nullptr, long long kv_rows = 0) {
   tls_status s = check_config(cfg);
   if (s) return s;
   if (!q || !aligned16(q)) return fail(TLS_ERR_INPUT, "q must be a non-NULL 16-byte aligned device pointer");
@@ -496,7 +505,7 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
   if (!workspace || workspace_bytes < need || !aligned16(workspace))
     return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes, 16-byte aligned (got %zu)", need, workspace_bytes);
   const StepPtrs all = {q, k_cache, v_cache, seq_lens, *idx, guide, block_ids, token_ids, num_tokens,
-                        token_scores, out, lse};
+                        token_scores, out, lse, slot_of_block, kv_rows > 0 ? kv_rows : cfg->max_seq_len};
   if (g_timer.on && g_timer.used % kMarks != 0) g_timer.used -= g_timer.used % kMarks;  // drop a partial record
   char* ws = static_cast<char*>(workspace);
   const int ns = n_split(cfg);
@@ -551,6 +560,7 @@ tls_status run_attend(const tls_config* cfg, const void* q, const void* k_cache,
   ap.q = q;
   ap.k_cache = k_cache;
   ap.v_cache = cfg->layout == TLS_MLA ? nullptr : v_cache;
+  ap.kv_rows = cfg->max_seq_len;
   ap.token_ids = const_cast<int32_t*>(token_ids);
   ap.num_tokens = const_cast<int32_t*>(num_tokens);
   ap.out = out;
@@ -675,6 +685,21 @@ tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache,
                   token_scores, out, lse, workspace, workspace_bytes, 1, (cudaStream_t)stream);
 }
 
+tls_status tls_decode_block_cache(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
+                                  const int32_t* guide_block_ids, const tls_block_cache* cache, int32_t* block_ids,
+                                  int32_t* token_ids, int32_t* num_tokens, float* token_scores, void* out,
+                                  float* lse, void* workspace, size_t workspace_bytes, tls_stream_t stream) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if (!cache || !cache->k_slots || !cache->slot_of_block || !cache->block_of_slot)
+    return fail(TLS_ERR_INPUT, "block cache buffers must be non-NULL");
+  if (cfg->layout == TLS_GQA && !cache->v_slots) return fail(TLS_ERR_INPUT, "GQA needs v_slots");
+  if (cache->capacity < 1) return fail(TLS_ERR_CONFIG, "block cache capacity must be >= 1");
+  return run_step(cfg, q, cache->k_slots, cache->v_slots, seq_lens, idx, guide_block_ids, block_ids, token_ids,
+                  num_tokens, token_scores, out, lse, workspace, workspace_bytes, 1, (cudaStream_t)stream,
+                  cache->slot_of_block, (long long)cache->capacity * cfg->block_size);
+}
+
 size_t tls_workspace_bytes(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK || which < 0 || which > 2) return (size_t)-1;
   if (which == 1) return attend_ws(cfg, 0);
@@ -754,6 +779,80 @@ tls_status tls_cache_fetch(const tls_config* cfg, const void* k_host, const void
   p.miss_count = miss_count;
   cudaError_t e = tls::launch_cache_fetch(p, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "cache_fetch_kernel launch");
+  return TLS_OK;
+}
+
+static tls_status host_device_ptr(const void* h, const void** dptr) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, h);
+  if (e != cudaSuccess || at.devicePointer == nullptr)
+    return fail(TLS_ERR_INPUT, "k_host / v_host must be pinned, device-mapped host memory (cudaHostAlloc mapped)");
+  *dptr = at.devicePointer;
+  return TLS_OK;
+}
+
+static tls_status check_block_cache(const tls_config* cfg, const tls_block_cache* cache) {
+  if (!cache || !cache->k_slots || !cache->slot_of_block || !cache->block_of_slot)
+    return fail(TLS_ERR_INPUT, "block cache buffers must be non-NULL");
+  if (cfg->layout == TLS_GQA && !cache->v_slots) return fail(TLS_ERR_INPUT, "GQA needs v_slots");
+  if (cache->capacity < 2 * cfg->top_blocks)
+    return fail(TLS_ERR_CONFIG, "block cache capacity (%d) must be >= 2 * top_blocks (%d)", cache->capacity,
+                2 * cfg->top_blocks);
+  return TLS_OK;
+}
+
+tls_status tls_block_cache_update(const tls_config* cfg, const void* k_host, const void* v_host,
+                                  const int32_t* keep_block_ids, const int32_t* block_ids,
+                                  const tls_block_cache* cache, int32_t* miss_count, tls_stream_t stream) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if ((s = check_block_cache(cfg, cache))) return s;
+  if (!k_host || !block_ids) return fail(TLS_ERR_INPUT, "k_host and block_ids are required");
+  if (cfg->layout == TLS_GQA && !v_host) return fail(TLS_ERR_INPUT, "GQA needs v_host");
+  tls::BlockCacheParams p;
+  memset(&p, 0, sizeof(p));
+  p.d = dims_of(cfg);
+  const void* dk = nullptr;
+  const void* dv = nullptr;
+  if ((s = host_device_ptr(k_host, &dk))) return s;
+  if (cfg->layout == TLS_GQA && (s = host_device_ptr(v_host, &dv))) return s;
+  p.capacity = cache->capacity;
+  p.bitmap_words = (p.d.M + 31) / 32;
+  const size_t smem = (size_t)p.bitmap_words * 4 + (size_t)p.capacity * 4 + (size_t)cfg->top_blocks * 4;
+  if ((int)smem > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "block cache shared-memory plan does not fit");
+  p.k_host = static_cast<const uint8_t*>(dk);
+  p.v_host = cfg->layout == TLS_GQA ? static_cast<const uint8_t*>(dv) : nullptr;
+  p.keep_ids = keep_block_ids;
+  p.block_ids = block_ids;
+  p.k_slots = static_cast<uint8_t*>(cache->k_slots);
+  p.v_slots = cfg->layout == TLS_GQA ? static_cast<uint8_t*>(cache->v_slots) : nullptr;
+  p.slot_of_block = cache->slot_of_block;
+  p.block_of_slot = cache->block_of_slot;
+  p.miss_count = miss_count;
+  cudaError_t e = tls::launch_block_cache_update(p, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "block_cache_update_kernel launch");
+  return TLS_OK;
+}
+
+tls_status tls_block_cache_rows(const tls_config* cfg, const int32_t* token_ids, const int32_t* num_tokens,
+                                const tls_block_cache* cache, int32_t* slot_rows, int32_t* absent,
+                                tls_stream_t stream) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if ((s = check_block_cache(cfg, cache))) return s;
+  if (!token_ids || !num_tokens || !slot_rows) return fail(TLS_ERR_INPUT, "token_ids, num_tokens, slot_rows required");
+  tls::BlockCacheParams p;
+  memset(&p, 0, sizeof(p));
+  p.d = dims_of(cfg);
+  p.capacity = cache->capacity;
+  p.slot_of_block = cache->slot_of_block;
+  p.block_of_slot = cache->block_of_slot;
+  p.token_ids = token_ids;
+  p.num_tokens = num_tokens;
+  p.slot_rows = slot_rows;
+  p.absent = absent;
+  cudaError_t e = tls::launch_block_cache_rows(p, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "block_cache_rows_kernel launch");
   return TLS_OK;
 }
 

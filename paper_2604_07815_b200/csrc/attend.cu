@@ -74,6 +74,7 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
   int* tout = p.token_ids + (size_t)pair * d.Kt;
   float* sout = p.token_scores ? p.token_scores + (size_t)pair * d.Kt : nullptr;
   const float lnG = logf((float)d.G);
+  const int* sob = p.slot_of_block ? p.slot_of_block + (size_t)pair * d.M : nullptr;  // block cache rows
   int t0 = 0, t1 = 0;
   auto on_k = [&](int K) {
     t0 = K * (int)rank / cs;  // K <= top_tokens, cs <= 16: no overflow
@@ -85,7 +86,7 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
       tout[pos] = tok;
       if (sout) sout[pos] = key2f(skeys[i]) * kLn2 - lnG;
     }
-    if (pos >= t0 && pos < t1) sel[pos - t0] = tok;
+    if (pos >= t0 && pos < t1) sel[pos - t0] = sob ? (sob[tok >> d.log2B] << d.log2B) + (tok & (d.B - 1)) : tok;
   };
   int* slist = reinterpret_cast<int*>(smem + p.off_slist);
   int K;
@@ -123,8 +124,8 @@ __device__ void phase_attend_generic(const AttendParams& p, int pair, int b, int
   const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * p.d.Hq + (size_t)g * p.d.G) * p.d.d_k;
   for (int i = tid; i < p.d.G * p.d.d_k; i += kThreads) aq[i] = to_f32<T>(qg[i]);
   __syncthreads();
-  const T* kb = reinterpret_cast<const T*>(p.k_cache) + (size_t)pair * p.d.S * p.d.d_k;
-  const T* vb = p.d.mla ? kb : reinterpret_cast<const T*>(p.v_cache) + (size_t)pair * p.d.S * p.d.d_v;
+  const T* kb = reinterpret_cast<const T*>(p.k_cache) + (size_t)pair * p.kv_rows * p.d.d_k;
+  const T* vb = p.d.mla ? kb : reinterpret_cast<const T*>(p.v_cache) + (size_t)pair * p.kv_rows * p.d.d_v;
   const int vstride = p.d.mla ? p.d.d_k : p.d.d_v;
   const float sm2 = p.d.sm_scale * kLog2e;
   for (int t = warp; t < tloc; t += kWarps) {
@@ -181,8 +182,8 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
   const int r = lane >> 2, c2 = 2 * (lane & 3);
   __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(kvbuf);  // [kAttnStages][K TC*D | V TC*D]
   const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + ((size_t)b * p.d.Hq + (size_t)g * p.d.G) * D;
-  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.d.S * D;
-  const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(p.v_cache) + (size_t)pair * p.d.S * D;
+  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.kv_rows * D;
+  const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(p.v_cache) + (size_t)pair * p.kv_rows * D;
   const int nchunks = (tloc + TC - 1) / TC;
   auto load_chunk = [&](int c, int stage) {
     __nv_bfloat16* sK = sbuf + (size_t)stage * 2 * TC * D;
@@ -374,8 +375,8 @@ __device__ void phase_attend_mma_t(const AttendParams& p, int pair, int b, int g
   __nv_bfloat16* sbuf = reinterpret_cast<__nv_bfloat16*>(kvbuf);  // [kAttnStages][K TC*D | V TC*D]
   __nv_bfloat16* pbuf = reinterpret_cast<__nv_bfloat16*>(kvbuf + (size_t)kAttnStages * 2 * TC * D * 2) + warp * 128;
   const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + ((size_t)b * p.d.Hq + (size_t)g * p.d.G) * D;
-  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.d.S * D;
-  const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(p.v_cache) + (size_t)pair * p.d.S * D;
+  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.kv_rows * D;
+  const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(p.v_cache) + (size_t)pair * p.kv_rows * D;
   const int nchunks = (tloc + TC - 1) / TC;
   auto load_chunk = [&](int c, int stage) {
     __nv_bfloat16* sK = sbuf + (size_t)stage * 2 * TC * D;
@@ -721,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
     sL[tid] = 0.f;
   }
   __syncthreads();  // sel visible
-  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.d.S * DK;
+  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.kv_rows * DK;
   auto load_chunk = [&](int c, int buf) {
     __nv_bfloat16* dst = sKV + buf * TC * DK;
     for (int i = tid; i < TC * CPR; i += kThreads) {

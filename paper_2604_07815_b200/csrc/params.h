@@ -98,6 +98,9 @@ struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally wit
   const void* q;
   const void* k_cache;
   const void* v_cache;
+  long long kv_rows;          // rows per pair of k_cache / v_cache (max_seq_len; block cache: capacity * B)
+  const int* slot_of_block;   // select only, nullable: block cache slot map [pairs, M]; the attention then reads
+                              // row slot_of_block[t / B] * B + t % B for token t
   const int* seq_lens;  // select only
   const int* cand;      // select only: candidate blocks (block_ids, or the lag-mode guide)
   const uint32_t* keys;  // select only: workspace keys [pairs, kb_eff*B]
@@ -128,6 +131,29 @@ struct CacheFetchParams {
   int* token_of_slot;     // [pairs, capacity], -1 = free
   int* slot_ids;          // [pairs, Kt] out: the cache row of each selected token
   int* miss_count;        // [pairs] out, nullable
+};
+
+// Block-granular offload cache (the paper's form): whole B-token
+// blocks of M_t, fetched asynchronously for the next step's one-step-lag
+// token selection.
+struct BlockCacheParams {
+  Dims d;
+  int capacity;           // block slots per pair (>= 2 * top_blocks: M_{t-1} in use + M_t arriving)
+  int bitmap_words;       // ceil(M / 32)
+  const uint8_t* k_host;  // device-accessible pointer to the pinned host K cache (layout of k_cache)
+  const uint8_t* v_host;  // ... V cache (NULL for MLA)
+  const int* keep_ids;    // [pairs, Kb] blocks still in use (M_{t-1}), -1 padded; nullable
+  const int* block_ids;   // [pairs, Kb] blocks to make resident (M_t), -1 padded
+  uint8_t* k_slots;       // [pairs, capacity * B, d_k]
+  uint8_t* v_slots;       // [pairs, capacity * B, d_v] (NULL for MLA)
+  int* slot_of_block;     // [pairs, M], -1 = not resident
+  int* block_of_slot;     // [pairs, capacity], -1 = free
+  int* miss_count;        // [pairs] out, nullable: blocks fetched
+  // tls_block_cache_rows
+  const int* token_ids;   // [pairs, Kt]
+  const int* num_tokens;  // [pairs]
+  int* slot_rows;         // [pairs, Kt] out: cache row of each selected token (0 if its block is not resident)
+  int* absent;            // [pairs] out, nullable: selected tokens whose block is not resident
 };
 
 static inline unsigned align16(size_t x) { return (unsigned)((x + 15) & ~(size_t)15); }

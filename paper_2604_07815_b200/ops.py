@@ -400,3 +400,147 @@ def offload_decode(cfg: TLSConfig, q: torch.Tensor, k_host: torch.Tensor, v_host
                                                         "dtype", "layout")}, "max_seq_len": cache.capacity})
     out, lse = sparse_attend(ccfg, q, cache.k_slots, cache.v_slots, slot_ids, nt)
     return out, lse, bids, tids, nt, ts, slot_ids, miss
+
+@dataclass
+class TLSBlockCache:
+    """GPU block cache of the asynchronous offload engine (tls_block_cache, include/tls.h)."""
+
+    capacity: int  # block slots per pair (>= 2 * top_blocks)
+    k_slots: torch.Tensor  # [batch, Hkv, capacity * B, d_k]
+    v_slots: torch.Tensor | None  # [batch, Hkv, capacity * B, d_v] (None for MLA)
+    slot_of_block: torch.Tensor  # [batch, Hkv, M] int32, -1 = not resident
+    block_of_slot: torch.Tensor  # [batch, Hkv, capacity] int32, -1 = free
+
+    def c(self) -> _lib.TLSBlockCacheC:
+        return _lib.TLSBlockCacheC(self.capacity, self.k_slots.data_ptr(),
+                                   self.v_slots.data_ptr() if self.v_slots is not None else 0,
+                                   self.slot_of_block.data_ptr(), self.block_of_slot.data_ptr())
+
+
+def alloc_block_cache(cfg: TLSConfig, capacity: int, device) -> TLSBlockCache:
+    """An empty block cache of ``capacity`` (>= 2 * top_blocks) block slots per pair."""
+    hk = cfg.num_kv_heads if cfg.layout == "gqa" else 1
+    rows = capacity * cfg.block_size
+    lead = (cfg.batch, hk, rows) if cfg.layout == "gqa" else (cfg.batch, rows)  # the k_cache layouts
+    return TLSBlockCache(
+        capacity=capacity,
+        k_slots=torch.empty(lead + (cfg.d_k,), dtype=cfg.dtype, device=device),
+        v_slots=torch.empty(lead + (cfg.d_v,), dtype=cfg.dtype, device=device) if cfg.layout == "gqa" else None,
+        slot_of_block=torch.full((cfg.batch, hk, cfg.num_blocks), -1, dtype=torch.int32, device=device),
+        block_of_slot=torch.full((cfg.batch, hk, capacity), -1, dtype=torch.int32, device=device),
+    )
+
+
+def block_cache_update(cfg: TLSConfig, k_host: torch.Tensor, v_host: torch.Tensor | None, block_ids: torch.Tensor,
+                       cache: TLSBlockCache, keep_block_ids=None, miss_count=None, stream=None):
+    """Make the blocks ``block_ids`` (M_t) resident, keeping ``keep_block_ids`` (M_{t-1}); enqueued on ``stream``
+    (default: the current stream).  Returns miss_count [batch, Hkv] (blocks fetched)."""
+    lib = _lib.load()
+    dev = block_ids.device
+    if not (k_host.is_pinned() and (v_host is None or v_host.is_pinned())):
+        raise ValueError("k_host / v_host must be pinned host tensors (host_kv)")
+    _need(block_ids, "block_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_blocks), torch.int32, dev)
+    if keep_block_ids is not None:
+        _need(keep_block_ids, "keep_block_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_blocks), torch.int32, dev)
+    if miss_count is None:
+        miss_count = torch.empty((cfg.batch, cfg.num_kv_heads), dtype=torch.int32, device=dev)
+    cc, bc = cfg.c(), cache.c()
+    st = stream.cuda_stream if stream is not None else _stream(dev)
+    _lib.check(lib.tls_block_cache_update(ctypes.byref(cc), k_host.data_ptr(),
+                                          v_host.data_ptr() if (v_host is not None and cfg.layout == "gqa") else 0,
+                                          keep_block_ids.data_ptr() if keep_block_ids is not None else 0,
+                                          block_ids.data_ptr(), ctypes.byref(bc), miss_count.data_ptr(), st))
+    return miss_count
+
+
+def block_cache_rows(cfg: TLSConfig, token_ids: torch.Tensor, num_tokens: torch.Tensor, cache: TLSBlockCache,
+                     slot_rows=None, absent=None):
+    """Cache rows of the selected tokens (tls_block_cache_rows).  Returns (slot_rows, absent)."""
+    lib = _lib.load()
+    dev = token_ids.device
+    _need(token_ids, "token_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_tokens), torch.int32, dev)
+    _need(num_tokens, "num_tokens", (cfg.batch, cfg.num_kv_heads), torch.int32, dev)
+    if slot_rows is None:
+        slot_rows = torch.empty_like(token_ids)
+    if absent is None:
+        absent = torch.empty_like(num_tokens)
+    cc, bc = cfg.c(), cache.c()
+    _lib.check(lib.tls_block_cache_rows(ctypes.byref(cc), token_ids.data_ptr(), num_tokens.data_ptr(),
+                                        ctypes.byref(bc), slot_rows.data_ptr(), absent.data_ptr(), _stream(dev)))
+    return slot_rows, absent
+
+
+def decode_block_cache(cfg: TLSConfig, q: torch.Tensor, seq_lens: torch.Tensor, index: TLSIndex,
+                       cache: TLSBlockCache, guide_block_ids: torch.Tensor | None = None, sel_out=None, out=None,
+                       lse=None):
+    """tls_decode with the K/V rows read from the block cache (tls_decode_block_cache): every block of the
+    candidate set must be resident.  Returns (out, lse, block_ids, token_ids, num_tokens, token_scores)."""
+    lib = _lib.load()
+    dev = q.device
+    _need(q, "q", (cfg.batch, cfg.num_q_heads, cfg.d_k), cfg.dtype, dev)
+    _need(seq_lens, "seq_lens", (cfg.batch,), torch.int32, dev)
+    bids, tids, nt, ts = _sel_outputs(cfg, dev, sel_out)
+    if out is None:
+        out = torch.empty((cfg.batch, cfg.num_q_heads, cfg.d_v), dtype=cfg.dtype, device=dev)
+    if lse is None:
+        lse = torch.empty((cfg.batch, cfg.num_q_heads), dtype=torch.float32, device=dev)
+    g = 0
+    if guide_block_ids is not None:
+        _need(guide_block_ids, "guide_block_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_blocks), torch.int32, dev)
+        g = guide_block_ids.data_ptr()
+    cc, ic, bc = cfg.c(), index.c(), cache.c()
+    ws, wsb = _workspace(cfg, dev, 2)
+    _lib.check(lib.tls_decode_block_cache(ctypes.byref(cc), q.data_ptr(), seq_lens.data_ptr(), ctypes.byref(ic), g,
+                                          ctypes.byref(bc), bids.data_ptr(), tids.data_ptr(), nt.data_ptr(),
+                                          ts.data_ptr() if ts is not None else 0, out.data_ptr(), lse.data_ptr(), ws,
+                                          wsb, _stream(dev)))
+    return out, lse, bids, tids, nt, ts
+
+
+class AsyncOffloadDecoder:
+    """The asynchronous offload engine: full K/V in pinned host memory, a GPU block cache, one-step
+    lag S_t = TokenSelect(q_t, M_{t-1}), and the transfer of M_t's missing blocks on a side stream, overlapped
+    with whatever the caller enqueues next.  ``step(q)`` returns (out, lse, block_ids, token_ids, num_tokens,
+    token_scores); ``last_miss`` holds the blocks fetched by the latest update."""
+
+    def __init__(self, cfg: TLSConfig, k_host, v_host, seq_lens, index: TLSIndex, capacity: int | None = None):
+        self.cfg, self.k_host, self.v_host, self.seq_lens, self.index = cfg, k_host, v_host, seq_lens, index
+        dev = seq_lens.device
+        self.cache = alloc_block_cache(cfg, capacity or 2 * cfg.top_blocks, dev)
+        self.side = torch.cuda.Stream(device=dev)
+        self.ready = None  # event: the update that brought M_{t-1} in
+        self.prev = None  # M_{t-1}
+        self.last_miss = None
+
+    def _update(self, bids, keep):
+        main = torch.cuda.current_stream(bids.device)
+        sel_done = torch.cuda.Event()
+        sel_done.record(main)
+        self.side.wait_event(sel_done)
+        with torch.cuda.stream(self.side):
+            self.last_miss = block_cache_update(self.cfg, self.k_host, self.v_host, bids, self.cache,
+                                                keep_block_ids=keep, stream=self.side)
+            bids.record_stream(self.side)
+            if keep is not None:
+                keep.record_stream(self.side)
+        ev = torch.cuda.Event()
+        ev.record(self.side)
+        return ev
+
+    def step(self, q):
+        """One decode step: one fused launch chain on the current stream (after the previous step's update),
+        then the update of the cache to M_t on the side stream, overlapped with whatever the caller enqueues
+        next (the other layers of the model)."""
+        cfg = self.cfg
+        main = torch.cuda.current_stream(q.device)
+        if self.prev is None:  # first step: M_0 from a synchronous selection, fetched before the attention
+            bids0 = select(cfg, q, self.seq_lens, self.index)[0]
+            main.wait_event(self._update(bids0, None))
+        else:
+            main.wait_event(self.ready)  # M_{t-1} resident
+        res = decode_block_cache(cfg, q, self.seq_lens, self.index, self.cache, guide_block_ids=self.prev)
+        bids = res[2]
+        # M_t's missing blocks go to free slots; M_{t-1} (read by this step) stays
+        self.ready = self._update(bids, self.prev)
+        self.prev = bids
+        return res

@@ -9,6 +9,13 @@ same selection order).  Cache invariants: after a fetch every selected token is
 resident, the two slot maps are mutually consistent, and with capacity = k_t
 the number of rows fetched equals |S_t \\ S_{t-1}| (the step-to-step locality
 the paper exploits).
+
+The asynchronous block-granular engine (tls_block_cache_update / _rows,
+AsyncOffloadDecoder): with the one-step lag its selections equal the
+resident lag-mode tls_decode (guide_block_ids = M_{t-1}) bit for bit, its output
+matches within the attention tolerance, every selected token's block is
+resident when the attention runs, the cache holds M_{t-1} u M_t, and each
+update fetches at most |M_t minus M_{t-1}| blocks.
 """
 from __future__ import annotations
 
@@ -88,3 +95,65 @@ def test_offload_steps_fetch_only_the_new_tokens():
         prev = (tids.clone(), nt.clone())
         # a drifting query: the selection changes a little from step to step
         q = (q.float() + 0.05 * torch.randn(q.shape, generator=g, device=q.device)).to(q.dtype)
+
+
+def check_block_cache(cfg, cache, keep_sets):
+    """slot_of_block / block_of_slot are mutually consistent and hold every block of the kept sets."""
+    rows = cfg.batch * cfg.num_kv_heads
+    sob = cache.slot_of_block.reshape(rows, -1)
+    bos = cache.block_of_slot.reshape(rows, -1)
+    for r in range(rows):
+        res = (sob[r] >= 0).nonzero().flatten()
+        assert torch.equal(bos[r][sob[r][res].long()].long(), res)  # slot -> block -> slot round trip
+        assert int((bos[r] >= 0).sum()) == len(res)
+        for ks in keep_sets:
+            for blk in ks[r]:
+                assert int(sob[r][blk]) >= 0
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_async_offload_matches_lag_mode_decode(name):
+    w = CASES[name]
+    cfg, inputs, idx = setup_case(w, seed=9)
+    k_host = tls.host_kv(inputs["k_cache"])
+    v_host = tls.host_kv(inputs["v_cache"]) if inputs["v_cache"] is not None else None
+    eng = tls.AsyncOffloadDecoder(cfg, k_host, v_host, inputs["seq_lens"], idx)
+    q = inputs["q"].clone()
+    g = torch.Generator(device=q.device).manual_seed(5)
+    prev = None
+    rows = cfg.batch * cfg.num_kv_heads
+    for step in range(4):
+        res = eng.step(q)
+        ref = tls.decode(cfg, q, inputs["k_cache"], inputs["v_cache"], inputs["seq_lens"], idx, guide_block_ids=prev)
+        torch.cuda.synchronize()
+        for a, b in zip(ref[2:6], res[2:6]):
+            assert torch.equal(a, b)
+        torch.testing.assert_close(res[0].float(), ref[0].float(), rtol=0, atol=2e-2)
+        torch.testing.assert_close(res[1], ref[1], rtol=0, atol=1e-3)
+        # the rows the attention read are the selected tokens' rows of resident blocks
+        _, absent = tls.block_cache_rows(cfg, res[3], res[4], eng.cache)
+        torch.cuda.synchronize()
+        assert int(absent.sum()) == 0
+        bids = res[2].reshape(rows, -1)
+        cur = [[int(x) for x in bids[r] if int(x) >= 0] for r in range(rows)]
+        keep = [cur] if prev is None else [cur, [[int(x) for x in prev.reshape(rows, -1)[r] if int(x) >= 0]
+                                                  for r in range(rows)]]
+        check_block_cache(cfg, eng.cache, keep)
+        if prev is not None:  # blocks fetched = M_t minus what was resident before the update
+            miss = eng.last_miss.reshape(-1)
+            for r in range(rows):
+                assert int(miss[r]) <= len(set(cur[r]) - set(keep[1][r]))
+        prev = res[2].clone()
+        q = (q.float() + 0.05 * torch.randn(q.shape, generator=g, device=q.device)).to(q.dtype)
+
+
+def test_block_cache_rejects_small_capacity():
+    w = CASES["gqa"]
+    cfg, inputs, idx = setup_case(w, seed=1)
+    k_host = tls.host_kv(inputs["k_cache"])
+    v_host = tls.host_kv(inputs["v_cache"])
+    cache = tls.alloc_block_cache(cfg, cfg.top_blocks, inputs["k_cache"].device)  # < 2 * top_blocks
+    bids = torch.zeros((cfg.batch, cfg.num_kv_heads, cfg.top_blocks), dtype=torch.int32, device=k_host.device
+                       if k_host.is_cuda else inputs["k_cache"].device)
+    with pytest.raises(tls.TLSError):
+        tls.block_cache_update(cfg, k_host, v_host, bids, cache)
