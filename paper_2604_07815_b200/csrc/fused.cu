@@ -29,6 +29,7 @@
 #include "params.h"
 #include "token.cuh"
 #include "topk.cuh"
+#include "tokensel.cuh"
 
 namespace tls {
 
@@ -205,22 +206,31 @@ __device__ __noinline__ void pair_worker(const FusedParams& p, int pair, int m, 
   // ---- a2: M_t = top-k_b blocks, ties -> lower block id (U2), ascending ----
   const int K = min(d.Kb, m);
   {
-    // range-histogram select (the sample-bracket path measured 2x slower on 1.5k scores)
-    const TopK t = fast_topk(bkeys, m, K, d.Kb >= m, fk, tk, getenv_flag_sample(p) ? scratch : nullptr);
-    TLS_STAMP(4)
     int* bout = p.block_ids + (size_t)pair * d.Kb;
-    topk_emit(bkeys, m, t, tk, [&](int i, int pos) { bout[pos] = i; });
+    __shared__ HistSel hs;
+    // one-pass register select (value-linear histogram); else / on an oversized boundary bin the generic
+    // range-histogram select (the sample-bracket path measured 2x slower on 1.5k scores)
+    bool done = false;
+    constexpr int kBlkChunks = 2;  // <= 8 keys per thread (m <= 2048 blocks) within the kernel register budget
+    if (K < m && m <= 4 * kBlkChunks * kThreads && !getenv_flag_sample(p))
+      done = range_topk_select<kBlkChunks>(bkeys, m, K, scratch, fk, tk, hs, [&](int i, int pos) { bout[pos] = i; });
+    TLS_STAMP(4)
+    if (!done) {
+      const TopK t = fast_topk(bkeys, m, K, d.Kb >= m, fk, tk, getenv_flag_sample(p) ? scratch : nullptr);
+      topk_emit(bkeys, m, t, tk, [&](int i, int pos) { bout[pos] = i; });
+    }
     for (int pos = K + tid; pos < d.Kb; pos += kThreads) bout[pos] = -1;
   }
-  {  // the pair's scores back to the sentinel for the next call (ordered before it by the stream)
-    unsigned* sc = reinterpret_cast<unsigned*>(p.scores + (size_t)pair * p.sstride);
-    for (int i = tid; i < m; i += kThreads) sc[i] = kScoreSentinel;
-  }
+  if (dbg && tid == 0) dbg[9] = gtimer();  // diagnostics: top-k_b emitted
   TLS_STAMP(1)
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    st_release_gpu(p.ready + pair, p.epoch);  // block_ids visible (q fragments and the zeroed histogram: qq_kernel)
+  if (tid == 0)  // release store (cumulative over the CTA barrier): block_ids visible (q fragments and the
+                  // zeroed histogram: qq_kernel)
+    st_release_gpu(p.ready + pair, p.epoch);
+  {  // then the pair's scores back to the sentinel for the next call (ordered before it by the stream; after
+     // the hand-off so the fence above does not wait for these stores)
+    unsigned* sc = reinterpret_cast<unsigned*>(p.scores + (size_t)pair * p.sstride);
+    for (int i = tid; i < m; i += kThreads) sc[i] = kScoreSentinel;
   }
   TLS_STAMP(2)
 #undef TLS_STAMP

@@ -326,10 +326,9 @@ __global__ void __launch_bounds__(kThreads, (NT == 1 && KS * NSPLIT <= 2) ? 5 : 
   TLS_STAMP(5)
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");  // keep smem alive for remote readers
   __syncthreads();
-  if (tid == 0) {  // hand-off: one count per chunk CTA (no cluster barrier; the attention kernel waits for nch)
-    __threadfence();
-    atomicAdd(p.ready_out + pair, 1u);
-  }
+  if (tid == 0)  // hand-off: one count per chunk CTA (the attention kernel waits for nch); a release add,
+                  // cumulative over the CTA barrier
+    red_release_add_gpu(p.ready_out + pair, 1u);
   TLS_STAMP(6)
 #undef TLS_STAMP
 }
@@ -625,10 +624,9 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
     if (lhist[i]) atomicAdd(&gh[i], lhist[i]);
   TLS_STAMP(5)
   __syncthreads();
-  if (tid == 0) {  // hand-off: one count per chunk CTA (no cluster barrier; the attention kernel waits for nch)
-    __threadfence();  // this CTA's keys and histogram counts (cumulative over the CTA barrier)
-    atomicAdd(p.ready_out + pair, 1u);
-  }
+  if (tid == 0)  // hand-off: one count per chunk CTA (no cluster barrier; the attention kernel waits for nch);
+                  // a release add: this CTA's keys and histogram counts (cumulative over the CTA barrier)
+    red_release_add_gpu(p.ready_out + pair, 1u);
   TLS_STAMP(6)
 #undef TLS_STAMP
 }

@@ -480,4 +480,167 @@ __device__ int hist_topk_select(const uint32_t* skeys, int nslots, const uint32_
   return K;
 }
 
+// Exact top-K of n order-preserving keys (no key 0 among the first n) for the
+// block selection a2, ties -> lower index (U2), emitted ascending: put(i, pos).
+// One pass in registers: thread t owns keys [t*R, t*R + R) (R = 4*ceil(n/1024)
+// <= 4*MAXC, 16-byte chunks loaded in rotated order); a 256-bin histogram that is
+// linear in the key's fp32 value between the min and max key (monotone in the
+// key, so bins never reorder keys) gives the boundary bin; its keys are ranked
+// exactly; one packed block scan places every thread's selected keys.  Returns
+// false (nothing emitted) when the boundary bin holds > 1024 keys: the caller
+// then runs the generic select.
+template <int MAXC, class F>
+__device__ bool range_topk_select(const uint32_t* keys, int n, int K, uint32_t* scratch, FastTopKCtl& fk, TopKCtl& tk,
+                                  HistSel& hs, F put) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ uint32_t s_hist[kThreads];
+  __shared__ uint32_t s_mn[kWarps], s_mx[kWarps];
+  const int nch = (n + 4 * kThreads - 1) / (4 * kThreads);  // <= MAXC (caller: n <= 4 * MAXC * kThreads)
+  const int r0 = tid * 4 * nch;
+  const int c0 = nch > 0 ? tid % nch : 0;
+  const uint4* k4 = reinterpret_cast<const uint4*>(keys) + (r0 >> 2);
+  const int lim = n - r0;  // valid keys of this run
+  uint4 kv[MAXC];
+  uint32_t mnk = 0xffffffffu, mxk = 0u;
+#pragma unroll
+  for (int j = 0; j < MAXC; ++j) {
+    if (j < nch) {
+      int c = c0 + j;
+      if (c >= nch) c -= nch;
+      kv[j] = 4 * c < lim ? k4[c] : make_uint4(0u, 0u, 0u, 0u);
+      const uint32_t e[4] = {kv[j].x, kv[j].y, kv[j].z, kv[j].w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (4 * c + u < lim) {
+          mnk = min(mnk, e[u]);
+          mxk = max(mxk, e[u]);
+        }
+    }
+  }
+  s_hist[tid] = 0u;
+  mnk = __reduce_min_sync(0xffffffffu, mnk);
+  mxk = __reduce_max_sync(0xffffffffu, mxk);
+  if (lane == 0) {
+    s_mn[warp] = mnk;
+    s_mx[warp] = mxk;
+  }
+  __syncthreads();
+  mnk = s_mn[0];
+  mxk = s_mx[0];
+#pragma unroll
+  for (int w = 1; w < kWarps; ++w) {
+    mnk = min(mnk, s_mn[w]);
+    mxk = max(mxk, s_mx[w]);
+  }
+  if (mnk == mxk) {  // every key equal: the first K
+    for (int i = tid; i < K; i += kThreads) put(i, i);
+    __syncthreads();
+    return true;
+  }
+  const float mn = key2f(mnk);
+  const float inv = 256.0f / (key2f(mxk) - mn);  // bins by value (inf / 0 range -> everything in one bin)
+  auto bin_of = [&](uint32_t k) -> int {
+    const float x = (key2f(k) - mn) * inv;
+    return x >= 255.f ? 255 : (x > 0.f ? (int)x : 0);
+  };
+#pragma unroll
+  for (int j = 0; j < MAXC; ++j) {
+    if (j < nch) {
+      int c = c0 + j;
+      if (c >= nch) c -= nch;
+      const uint32_t e[4] = {kv[j].x, kv[j].y, kv[j].z, kv[j].w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (4 * c + u < lim) atomicAdd(&s_hist[bin_of(e[u])], 1u);
+    }
+  }
+  __syncthreads();
+  // boundary bin: thread t holds bin 255 - t, so the exclusive prefix counts the keys in higher bins
+  const int cnt = (int)s_hist[kThreads - 1 - tid];
+  int tot;
+  const int above = block_exclusive_scan(cnt, tk.scan, &tot);
+  if (tid == 0) fk.bcount = 0;
+  if (above < K && K <= above + cnt) {
+    hs.bsel = kThreads - 1 - tid;
+    hs.above = above;
+  }
+  __syncthreads();
+  const int bsel = hs.bsel, kr = K - hs.above;
+  uint64_t gt = 0, bd = 0;
+#pragma unroll
+  for (int j = 0; j < MAXC; ++j) {
+    if (j < nch) {
+      int c = c0 + j;
+      if (c >= nch) c -= nch;
+      const uint32_t e[4] = {kv[j].x, kv[j].y, kv[j].z, kv[j].w};
+      uint32_t na = 0, nb = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool ok = 4 * c + u < lim;
+        const int bn = bin_of(e[u]);
+        na |= (uint32_t)(ok && bn > bsel) << u;
+        nb |= (uint32_t)(ok && bn == bsel) << u;
+      }
+      gt |= (uint64_t)na << (4 * c);
+      bd |= (uint64_t)nb << (4 * c);
+    }
+  }
+  const int nb_own = __popcll(bd);
+  if (nb_own) {
+    int dst = atomicAdd(&fk.bcount, nb_own);
+    for (uint64_t m = bd; m; m &= m - 1, ++dst) {
+      const int bit = __ffsll((long long)m) - 1;
+      if (dst < 1024) scratch[dst] = keys[r0 + bit];
+    }
+  }
+  __syncthreads();
+  const int nbk = fk.bcount;
+  if (nbk > 1024) return false;  // uniform: every thread read the same count
+  if (nbk <= 32) {
+    if (warp == 0) {
+      const uint32_t v = lane < nbk ? scratch[lane] : 0u;
+      int gtc = 0, eqc = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t o = __shfl_sync(0xffffffffu, v, j);
+        gtc += o > v;
+        eqc += o == v;
+      }
+      if (lane < nbk && gtc < kr && gtc + eqc >= kr) fk.thr = v;
+    }
+  } else {
+    for (int i = tid; i < nbk; i += kThreads) {
+      const uint32_t v = scratch[i];
+      int gtc = 0, eqc = 0;
+      for (int j = 0; j < nbk; ++j) {
+        const uint32_t o = scratch[j];
+        gtc += o > v;
+        eqc += o == v;
+      }
+      if (gtc < kr && gtc + eqc >= kr) fk.thr = v;
+    }
+  }
+  __syncthreads();
+  const uint32_t thr = fk.thr;
+  uint64_t eq = 0;
+  for (uint64_t m = bd; m; m &= m - 1) {
+    const int bit = __ffsll((long long)m) - 1;
+    const uint32_t k = keys[r0 + bit];
+    if (k > thr) gt |= 1ull << bit;
+    else if (k == thr) eq |= 1ull << bit;
+  }
+  const int ngt = __popcll(gt), neq = __popcll(eq);
+  int tot2;
+  const int pre = block_exclusive_scan(ngt | (neq << 16), tk.scan, &tot2);
+  const int gt_before = pre & 0xffff, eq_before = pre >> 16;
+  const int take_eq = K - (tot2 & 0xffff);
+  int ntake = min(max(take_eq - eq_before, 0), neq);
+  uint64_t selm = gt;
+  for (uint64_t m = eq; ntake > 0; --ntake, m &= m - 1) selm |= m & (~m + 1ull);
+  int pos = gt_before + min(eq_before, max(take_eq, 0));
+  for (uint64_t m = selm; m; m &= m - 1) put(r0 + __ffsll((long long)m) - 1, pos++);
+  __syncthreads();
+  return true;
+}
+
 }  // namespace tls

@@ -38,7 +38,8 @@ print(f"  worker start (flags seen) {q(s[:, 0] - t0)}")
 print(f"  worker end                {q(s[:, 2] - t0)}")
 print(f"  own tile: {q(s[:, 8] - s[:, 6])} | flag wait: {q(s[:, 0] - s[:, 8])}")
 print(f"  top-k_b: {q(s[:, 1] - s[:, 0])} | q frags + hist zero: {q(s[:, 2] - s[:, 1])}")
-print(f"    scores load {q(s[:, 3] - s[:, 0])} | fast_topk {q(s[:, 4] - s[:, 3])} | emit {q(s[:, 1] - s[:, 4])}")
+print(f"    scores load {q(s[:, 3] - s[:, 0])} | fast_topk {q(s[:, 4] - s[:, 3])} | emit {q(s[:, 9] - s[:, 4])}"
+      f" | sentinel restore {q(s[:, 1] - s[:, 9])}")
 st = buf[65536 * 8: 65536 * 8 + 148 * 4].view(148, 4).cpu().double()
 ok = st[:, 2] > 0
 if ok.any():
