@@ -41,6 +41,17 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
 #define TLS_STAMP(i) \
   if (dbg && tid == 0) dbg[i] = gtimer();
   TLS_STAMP(0)
+  // keys of every candidate slot (the whole region; only the first kc blocks' slots are read) and the key
+  // histogram: two TMA bulk copies, issued first so they overlap the candidate compaction below
+  __shared__ __align__(8) uint64_t kbar;
+  if (tid == 0) {
+    const uint32_t kbytes = (uint32_t)(p.kb_eff * d.B * 4);
+    mbar_init(&kbar, 1);
+    mbar_fence_init();
+    mbar_arrive_expect_tx(&kbar, kbytes + kKeyBins * 4);
+    tma_bulk_g2s(shist, p.khist + (size_t)pair * kKeyBins, kKeyBins * 4, &kbar);
+    tma_bulk_g2s(skeys, p.keys + (size_t)pair * p.kb_eff * d.B, kbytes, &kbar);
+  }
   // candidate blocks in the order the token kernels used (valid entries, in order)
   const int* cand = p.cand + (size_t)pair * d.Kb;
   {
@@ -49,23 +60,13 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
     int cnt = 0;
     for (int i = lo; i < hi; ++i) cnt += (cand[i] >= 0 && cand[i] < m);
     int total;
-    int pos = block_exclusive_scan(cnt, tk.scan, &total);
+    int pos = block_exclusive_scan(cnt, tk.scan, &total);  // (its barriers also order the mbarrier init)
     for (int i = lo; i < hi; ++i)
       if (cand[i] >= 0 && cand[i] < m && pos < p.kb_eff) cblk[pos++] = cand[i];
     if (tid == 0) s_kc = min(total, p.kb_eff);
   }
-  // keys of every candidate slot and the key histogram: two TMA bulk copies
-  __shared__ __align__(8) uint64_t kbar;
   __syncthreads();
   const int nslots = s_kc << d.log2B;
-  if (tid == 0) {
-    mbar_init(&kbar, 1);
-    mbar_fence_init();
-    mbar_arrive_expect_tx(&kbar, (uint32_t)(nslots * 4 + kKeyBins * 4));
-    tma_bulk_g2s(shist, p.khist + (size_t)pair * kKeyBins, kKeyBins * 4, &kbar);
-    if (nslots > 0) tma_bulk_g2s(skeys, p.keys + (size_t)pair * p.kb_eff * d.B, (uint32_t)(nslots * 4), &kbar);
-  }
-  __syncthreads();
   mbar_wait(&kbar, 0);
   TLS_STAMP(1)
   TLS_STAMP(2)
