@@ -370,9 +370,7 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
   if (dbg && tid == 0) dbg[i] = gtimer();
   TLS_STAMP(0)
   launch_dependents();
-  if (tid == 0) wait_ready(p.ready_in + pair, p.epoch);  // select_kernel's a2 outputs for this pair
-  __syncthreads();
-  for (int i = tid; i < kKeyBins; i += kThreads) lhist[i] = 0u;
+  for (int i = tid; i < kKeyBins; i += kThreads) lhist[i] = 0u;  // (overlaps the wait below)
   const int b = pair / d.Hkv, g = pair - b * d.Hkv;
   const int n = min(max(p.seq_lens[b], 0), d.S);
   const int m = (n + d.B - 1) >> d.log2B;
@@ -384,12 +382,13 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
     mbar_init(&bar, 1);
     mbar_init(&qbar, 1);
     mbar_fence_init();
+    wait_ready(p.ready_in + pair, p.epoch);  // select_kernel's a2 outputs for this pair
     // the pair's q-fragment blob from K1b: one TMA bulk copy into [off_qb, off_qsum + NT*32)
     const uint32_t qfb = (uint32_t)(NSPLIT * NT * KS * 256 + NT * 32);
     mbar_arrive_expect_tx(&qbar, qfb);
     tma_bulk_g2s(smem + p.off_qb, p.qfrag + (size_t)pair * qfb, qfb, &qbar);
   }
-  __syncthreads();  // mbarriers initialised before any wait / copy issue
+  __syncthreads();  // mbarriers initialised; the hand-off observed by thread 0 (cumulative through the barrier)
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");  // started (matched before the DSMEM push)
   const int rowbytes = d.d_c / 2;
   const uint8_t* cbase = p.codes + (size_t)pair * d.S * rowbytes;
