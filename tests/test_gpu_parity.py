@@ -394,3 +394,30 @@ def test_sub_batch_pipeline_and_tile_size_agree(monkeypatch):
         torch.testing.assert_close(res[0].float(), ref[0].float(), rtol=0, atol=2e-2)
         for k in env:
             monkeypatch.delenv(k)
+
+
+@pytest.mark.parametrize("pattern", ["all_equal", "four_values"])
+def test_block_topk_exact_ties(pattern):
+    """a2 with exactly tied block scores (ties -> lower block id, U2): blocks repeat so the k_b-th score
+    falls inside a large tie group (or every score is equal), m = 1200 blocks (the one-pass register select).
+    Expected = stable order by (-score, id) of the same library's block scores (tls_block_scores)."""
+    w = W.Workload("ties", 2, 8, 2, 128, 128, 64 * 1200, top_blocks=128, top_tokens=256)
+    cfg, inputs, idx = setup_case(w, seed=3, ragged=False)
+    k = inputs["k_cache"]
+    B = w.block_size
+    period = 1 if pattern == "all_equal" else 4
+    blocks = k.view(w.batch, w.num_kv_heads, -1, B, w.d_k)
+    src = blocks[:, :, :period].clone()
+    reps = blocks.shape[2] // period
+    blocks.copy_(src.repeat(1, 1, reps, 1, 1))
+    tls.build_index(cfg, k, inputs["seq_lens"], idx)
+    sc = tls.block_scores(cfg, inputs["q"], inputs["seq_lens"], idx)
+    bids = tls.select(cfg, inputs["q"], inputs["seq_lens"], idx)[0]
+    torch.cuda.synchronize()
+    m = blocks.shape[2]
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            s = sc[b, g, :m].double().cpu().numpy()
+            order = np.lexsort((np.arange(m), -s))  # by -score, then id
+            exp = np.sort(order[: w.top_blocks])
+            assert np.array_equal(bids[b, g].cpu().numpy(), exp), (pattern, b, g)
