@@ -421,3 +421,37 @@ def test_block_topk_exact_ties(pattern):
             order = np.lexsort((np.arange(m), -s))  # by -score, then id
             exp = np.sort(order[: w.top_blocks])
             assert np.array_equal(bids[b, g].cpu().numpy(), exp), (pattern, b, g)
+
+
+@pytest.mark.parametrize("period", [1, 12])
+def test_token_topk_exact_ties(period):
+    """a4 with exactly tied ranking keys (ties -> lower token id, U2): token t of every pair repeats the
+    content of token t mod period, so every block scores the same (M_t = the first k_b blocks) and the candidates
+    form `period` groups of bitwise-equal keys.  S_t must be whole groups plus the lowest-id prefix of at most one
+    group (period 12: a 683-key boundary group, the register select; period 1: one 8192-key group, the fallback)."""
+    w = W.Workload("tties", 1, 8, 2, 128, 128, 64 * 256, top_blocks=128, top_tokens=1024)
+    cfg, inputs, idx = setup_case(w, seed=4, ragged=False)
+    k, v = inputs["k_cache"], inputs["v_cache"]
+    S = k.shape[2]
+    src = torch.arange(S, device=k.device) % period
+    k.copy_(k[:, :, src])
+    v.copy_(v[:, :, src])
+    tls.build_index(cfg, k, inputs["seq_lens"], idx)
+    out, lse, bids, tids, nt, ts = tls.decode(cfg, inputs["q"], k, v, inputs["seq_lens"], idx)
+    torch.cuda.synchronize()
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            assert torch.equal(bids[b, g].cpu(), torch.arange(w.top_blocks, dtype=torch.int32))
+            n = int(nt[b, g])
+            assert n == w.top_tokens
+            sel = tids[b, g, :n].cpu().numpy()
+            assert np.all(np.diff(sel) > 0)  # ascending, distinct
+            cand = np.arange(w.top_blocks * w.block_size)
+            partial = 0
+            for grp in range(period):
+                members = cand[cand % period == grp]
+                chosen = np.intersect1d(sel, members)
+                if 0 < len(chosen) < len(members):
+                    partial += 1
+                    assert np.array_equal(chosen, members[: len(chosen)]), (period, grp)  # lowest ids first
+            assert partial <= 1
