@@ -389,6 +389,10 @@ tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int
   fp.dbg = env_debug_buf();
   fp.dbg_flags = getenv("TLS_TOPK_SAMPLE") ? 1 : 0;
   fp.qq = reinterpret_cast<float*>(ws + c.w.qq);
+  // small query groups (GQA, G * d_k <= 512 elements): every tile CTA forms QQ itself (the same fp32 ops as
+  // qq_kernel, so the same bits) and starts streaming without waiting for qq_kernel (A/B: C2 79.0 -> 77.2 us;
+  // at C3, G = 8, the per-tile work cost more than the wait: 127.4 -> 128.5); tuning: env TLS_QQ_WAIT
+  fp.qq_local = (cfg->layout == TLS_GQA && fp.d.G * cfg->d_k <= 512 && !getenv("TLS_QQ_WAIT")) ? 1 : 0;
   if (timed) g_timer.mark(st);
   cudaError_t e = tls::launch_qq(fp, st, lo_k1);
   if (e != cudaSuccess) return cuda_fail(e, "qq_kernel launch");

@@ -57,7 +57,7 @@ __device__ __forceinline__ void score_tile(const FusedParams& p, int pair, int b
                    &bars[s]);
     }
   }
-  if (p.qq != nullptr) {
+  if (p.qq != nullptr && !p.qq_local) {
     // QQ of the pair from qq_kernel (PDL primary): the tile copies above are already in flight
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     const float* qq = p.qq + (size_t)pair * 2 * d.d_k;
@@ -202,6 +202,9 @@ __device__ __noinline__ void pair_worker(const FusedParams& p, int pair, int m, 
   uint32_t* bkeys = reinterpret_cast<uint32_t*>(smem + p.off_bkeys);
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + p.off_scratch);
   FastTopKCtl& fk = *reinterpret_cast<FastTopKCtl*>(smem + p.off_fk);
+  // the hand-off below also certifies qq_kernel's outputs (q fragments, zeroed histogram): when the tile CTAs
+  // did not wait for it, the worker does (it has long finished by now)
+  if (p.qq != nullptr && p.qq_local) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   TLS_STAMP(3)
   // ---- a2: M_t = top-k_b blocks, ties -> lower block id (U2), ascending ----
   const int K = min(d.Kb, m);

@@ -45,6 +45,8 @@ struct FusedParams {
   const int* channels;
   float* scores;           // workspace [pairs, sstride] fp32; the completion sentinel between calls (fused.cu)
   float* qq;               // workspace [pairs, 2 d_k] fp32 [Q+ | Q-] from qq_kernel (NULL: computed per tile)
+  int qq_local;            // 1: tile CTAs form QQ from the pair's (small) q rows themselves and never wait for
+                           // qq_kernel; only the pair's worker waits for it (griddepcontrol.wait) before its hand-off
   uint32_t* khist;         // workspace [pairs, kKeyBins], zeroed by the worker for the token kernel
   uint8_t* qfrag;          // workspace [pairs, qfrag_bytes(d)]: q~ fragment blobs for the token kernel
   int* block_ids;          // [pairs, Kb] out: M_t ascending, -1 padded
