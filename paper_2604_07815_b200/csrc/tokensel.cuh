@@ -408,12 +408,54 @@ __device__ int hist_topk_select(const uint32_t* skeys, int nslots, const uint32_
   }
   __syncthreads();
   TLS_CYC(2)
-  const int nbk = take_all ? 0 : fk.bcount;
+  int nbk = take_all ? 0 : fk.bcount;
+  int kr = take_all ? 0 : K - hs.above;  // rank of the threshold among the boundary keys
   if (dbg && tid == 0) {  // diagnostics: classification-pass end, boundary-bin size
     dbg[6] = gtimer();
     dbg[7] = (unsigned long long)nbk;
   }
-  if (nbk > 1024) {  // rare: an oversized boundary bin -> generic select into slist
+  if (nbk > 32) {
+    // a large boundary bin (flat alpha~, e.g. uniform inputs: hundreds of keys, whose O(n^2) rank cost ~11 us):
+    // refine it with 256 sub-bins linear in the key over [klo, khi] (monotone); keys of higher sub-bins join
+    // gt, the sub-bin holding the kr-th largest boundary key becomes the new boundary
+    __shared__ uint32_t s_sub[kThreads];
+    s_sub[tid] = 0u;
+    __syncthreads();
+    const uint64_t span = (uint64_t)khi - (uint64_t)klo + 1ull;
+    auto sub_of = [&](uint32_t k) -> int { return (int)(((uint64_t)(k - klo) << 8) / span); };
+    for (uint64_t m = bd; m; m &= m - 1) atomicAdd(&s_sub[sub_of(skeys[r0 + __ffsll((long long)m) - 1])], 1u);
+    __syncthreads();
+    const int c = (int)s_sub[kThreads - 1 - tid];
+    int tot_;
+    const int ab = block_exclusive_scan(c, tk.scan, &tot_);
+    if (ab < kr && kr <= ab + c) {
+      hs.bsel = kThreads - 1 - tid;
+      hs.above = ab;
+    }
+    if (tid == 0) fk.bcount = 0;
+    __syncthreads();
+    const int sb = hs.bsel;
+    kr -= hs.above;
+    uint64_t nbd = 0;
+    for (uint64_t m = bd; m; m &= m - 1) {
+      const int bit = __ffsll((long long)m) - 1;
+      const int sbin = sub_of(skeys[r0 + bit]);
+      if (sbin > sb) gt |= 1ull << bit;
+      else if (sbin == sb) nbd |= 1ull << bit;
+    }
+    bd = nbd;
+    const int nb2 = __popcll(bd);
+    if (nb2) {
+      int dst = atomicAdd(&fk.bcount, nb2);
+      for (uint64_t m = bd; m; m &= m - 1, ++dst) {
+        const int bit = __ffsll((long long)m) - 1;
+        if (dst < 1024) scratch[dst] = skeys[r0 + bit];
+      }
+    }
+    __syncthreads();
+    nbk = fk.bcount;
+  }
+  if (nbk > 1024) {  // rare (e.g. thousands of equal keys): generic select into slist
     const TopK t = fast_topk(skeys, nslots, K, false, fk, tk, scratch);
     topk_emit(skeys, nslots, t, tk, [&](int i, int pos) { slist[pos] = i; });
     for (int p = tid; p < K; p += kThreads) put(slist[p], p);
@@ -423,7 +465,6 @@ __device__ int hist_topk_select(const uint32_t* skeys, int nslots, const uint32_
   uint32_t thr = 0u;
   if (!take_all) {
     // exact threshold: the kr-th largest boundary key (rank by comparison)
-    const int kr = K - hs.above;
     if (nbk <= 32) {  // one warp, keys in lanes, the others' keys by shuffle
       if (warp == 0) {
         const uint32_t v = lane < nbk ? scratch[lane] : 0u;

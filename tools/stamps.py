@@ -14,7 +14,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 w = W.CONFIGS[name]
 if len(sys.argv) > 2:
     w = w.with_(batch=int(sys.argv[2]))
-cfg, inputs, idx, queries = bench.build_state(w, 0, torch.device("cuda"), "outlier")
+cfg, inputs, idx, queries = bench.build_state(w, 0, torch.device("cuda"), os.environ.get("TLS_PATTERN", "outlier"))
 os.environ["TLS_FUSED_MODE"] = "1"
 buf = torch.zeros(4 * 65536 * 8, dtype=torch.int64, device="cuda")
 for it in range(3):
