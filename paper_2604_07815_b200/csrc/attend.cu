@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_consta
 // ldmatrix).  Online softmax per head in smem (P stored as bf16).  O += P V:
 // warp w owns output dims [64w, 64w + 64) (V^T fragments via ldmatrix.trans).
 // --------------------------------------------------------------------------
-constexpr int kMlaChunk = 32;
+constexpr int kMlaChunk = kMlaChunkTokens;  // 64 latent rows per stage
 
 template <int DK, int DV, int MT>
 __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_constant__ AttendParams p) {
@@ -757,41 +757,44 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
     const __nv_bfloat16* sK = sKV + buf * TC * DK;
     // ---- S = Q K^T (log2 units) ----
     {
+      // warp: head tile mt, token n-tiles nb..nb+7 and nb+32..nb+39 (one ldmatrix.x4 fetches both B fragments)
       const int mt = warp >> 2, nb = (warp & 3) * 8;
+      static_assert(TC == 64, "two 8-token n-tiles per warp");
       if (mt < MT) {
-        float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};  // two chains (even / odd k-steps)
-        static_assert(KS % 2 == 0, "even number of k-steps");
+        float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
-        for (int kk = 0; kk < KS; kk += 2) {
-          uint32_t a[4], bk[4], a2[4], bk2[4];
+        for (int kk = 0; kk < KS; ++kk) {
+          uint32_t a[4], bk[4];
           const int qrow = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, qch = kk * 2 + (lane >> 4);
           ldsm_x4(a, sQ + qrow * DK + ((qch ^ (qrow & 7)) << 3));
-          ldsm_x4(a2, sQ + qrow * DK + (((qch + 2) ^ (qrow & 7)) << 3));
-          const int krow = nb + (lane & 7), kch = kk * 2 + ((lane >> 3) & 1);
-          ldsm_x4(bk, sK + krow * DK + ((kch ^ (krow & 7)) << 3));  // lanes 16-31 duplicate 0-15
-          ldsm_x4(bk2, sK + krow * DK + (((kch + 2) ^ (krow & 7)) << 3));
+          const int krow = nb + (lane & 7) + ((lane >> 4) & 1) * 32, kch = kk * 2 + ((lane >> 3) & 1);
+          ldsm_x4(bk, sK + krow * DK + ((kch ^ (krow & 7)) << 3));
           mma_bf16_16816(acc, a, bk[0], bk[1]);
-          mma_bf16_16816(acc2, a2, bk2[0], bk2[1]);
+          mma_bf16_16816(acc2, a, bk[2], bk[3]);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i] += acc2[i];
-        const int tk = nb + c2;
-        const bool v0 = c * TC + tk < tloc, v1 = c * TC + tk + 1 < tloc;
-        sS[(mt * 16 + r) * SST + tk] = v0 ? acc[0] * sm2 : -CUDART_INF_F;
-        sS[(mt * 16 + r) * SST + tk + 1] = v1 ? acc[1] * sm2 : -CUDART_INF_F;
-        sS[(mt * 16 + r + 8) * SST + tk] = v0 ? acc[2] * sm2 : -CUDART_INF_F;
-        sS[(mt * 16 + r + 8) * SST + tk + 1] = v1 ? acc[3] * sm2 : -CUDART_INF_F;
+        for (int u = 0; u < 2; ++u) {
+          const float* ac = u ? acc2 : acc;
+          const int tk = nb + 32 * u + c2;
+          const bool v0 = c * TC + tk < tloc, v1 = c * TC + tk + 1 < tloc;
+          sS[(mt * 16 + r) * SST + tk] = v0 ? ac[0] * sm2 : -CUDART_INF_F;
+          sS[(mt * 16 + r) * SST + tk + 1] = v1 ? ac[1] * sm2 : -CUDART_INF_F;
+          sS[(mt * 16 + r + 8) * SST + tk] = v0 ? ac[2] * sm2 : -CUDART_INF_F;
+          sS[(mt * 16 + r + 8) * SST + tk + 1] = v1 ? ac[3] * sm2 : -CUDART_INF_F;
+        }
       }
     }
     __syncthreads();
-    // ---- online softmax: 8 threads per head, 4 tokens each ----
+    // ---- online softmax: 8 threads per head, 8 tokens each ----
     {
-      const int h = tid >> 3, tq = (tid & 7) * 4;
+      const int h = tid >> 3, tq = (tid & 7) * 8;
       if (h < MT * 16) {
-        float x[4];
+        float x[8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) x[i] = sS[h * SST + tq + i];
-        float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+        for (int i = 0; i < 8; ++i) x[i] = sS[h * SST + tq + i];
+        float mx = x[0];
+#pragma unroll
+        for (int i = 1; i < 8; ++i) mx = fmaxf(mx, x[i]);
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
@@ -799,7 +802,7 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
         const float mn = fmaxf(mo, mx);  // finite: every chunk has >= 1 valid token
         float ps = 0.f;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 8; ++i) {
           const float e = fexp2(x[i] - mn);
           ps += e;
           sP[h * PST + tq + i] = __float2bfloat16_rn(e);

@@ -12,8 +12,8 @@ namespace tls {
 
 constexpr int kAttnChunk = 64;     // tokens per K/V staging stage of the GQA mma attention (8 warps x 8)
 constexpr int kAttnStages = 3;     // cp.async pipeline depth of the GQA mma attention
-constexpr int kMlaChunkTokens = 32;  // latent rows per staging chunk of the MLA attention
-constexpr int kMlaStages = 3;        // MLA attention cp.async pipeline depth (chunks in flight + 1)
+constexpr int kMlaChunkTokens = 64;  // latent rows per staging chunk of the MLA attention
+constexpr int kMlaStages = 2;        // MLA attention cp.async pipeline depth (chunks in flight + 1)
 constexpr int kScoreTileBytes = 32 * 1024;  // K1: bytes of block summaries per CTA (TMA tile)
 
 struct Dims {
