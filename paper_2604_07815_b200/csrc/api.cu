@@ -172,13 +172,18 @@ tls_status plan_attend(const tls_config* c, tls::AttendParams& p, int select, in
     cs = 1;
     while (cs < 16 && pairs * cs * 2 <= (long long)sms * per_sm && (kt + 2 * cs - 1) / (2 * cs) >= 64) cs *= 2;
   }
-  for (;; cs *= 2) {
-    if (cs > 16) return fail(TLS_ERR_UNSUPPORTED, "attention shared-memory plan does not fit");
-    p.cs = cs;
-    tls::plan_attend(p, sizeof(tls::FastTopKCtl));
-    if ((int)p.smem_bytes <= kMaxSmem) break;
+  // more CTAs per pair first (shorter selected-token lists per CTA); MLA falls back to its 32-token staging
+  // only when no cluster size fits the 64-token one
+  for (const int tc : {64, 32}) {
+    p.mla_tc = tc;
+    for (int c = cs; c <= 16; c *= 2) {
+      p.cs = c;
+      tls::plan_attend(p, sizeof(tls::FastTopKCtl));
+      if ((int)p.smem_bytes <= kMaxSmem) return TLS_OK;
+    }
+    if (p.mma != 2) break;
   }
-  return TLS_OK;
+  return fail(TLS_ERR_UNSUPPORTED, "attention shared-memory plan does not fit");
 }
 
 tls_status check_index(const tls_index* idx) {

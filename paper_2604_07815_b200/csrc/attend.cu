@@ -666,12 +666,11 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_consta
 // ldmatrix).  Online softmax per head in smem (P stored as bf16).  O += P V:
 // warp w owns output dims [64w, 64w + 64) (V^T fragments via ldmatrix.trans).
 // --------------------------------------------------------------------------
-constexpr int kMlaChunk = kMlaChunkTokens;  // 64 latent rows per stage
 
-template <int DK, int DV, int MT>
+template <int DK, int DV, int MT, int TC>
 __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_constant__ AttendParams p) {
   static_assert(DV == 64 * kWarps, "each warp owns 64 output dims");
-  constexpr int TC = kMlaChunk;
+  constexpr int kMlaStages = mla_stages(TC);
   constexpr int CPR = DK / 8;       // 16-byte chunks per latent row
   constexpr int KS = DK / 16;       // k-steps of QK^T
   constexpr int PST = TC + 8;       // P row stride (bf16): 80 B, conflict-free ldmatrix
@@ -757,23 +756,42 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
     const __nv_bfloat16* sK = sKV + buf * TC * DK;
     // ---- S = Q K^T (log2 units) ----
     {
-      // warp: head tile mt, token n-tiles nb..nb+7 and nb+32..nb+39 (one ldmatrix.x4 fetches both B fragments)
+      // warp: head tile mt, token n-tile(s) nb..nb+7 (and nb+32..nb+39 for 64-token chunks: one ldmatrix.x4
+      // fetches both B fragments)
       const int mt = warp >> 2, nb = (warp & 3) * 8;
-      static_assert(TC == 64, "two 8-token n-tiles per warp");
+      static_assert(TC == 64 || TC == 32, "32- or 64-token chunks");
       if (mt < MT) {
         float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
+        if constexpr (TC == 64) {
 #pragma unroll 4
-        for (int kk = 0; kk < KS; ++kk) {
-          uint32_t a[4], bk[4];
-          const int qrow = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, qch = kk * 2 + (lane >> 4);
-          ldsm_x4(a, sQ + qrow * DK + ((qch ^ (qrow & 7)) << 3));
-          const int krow = nb + (lane & 7) + ((lane >> 4) & 1) * 32, kch = kk * 2 + ((lane >> 3) & 1);
-          ldsm_x4(bk, sK + krow * DK + ((kch ^ (krow & 7)) << 3));
-          mma_bf16_16816(acc, a, bk[0], bk[1]);
-          mma_bf16_16816(acc2, a, bk[2], bk[3]);
+          for (int kk = 0; kk < KS; ++kk) {
+            uint32_t a[4], bk[4];
+            const int qrow = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, qch = kk * 2 + (lane >> 4);
+            ldsm_x4(a, sQ + qrow * DK + ((qch ^ (qrow & 7)) << 3));
+            const int krow = nb + (lane & 7) + ((lane >> 4) & 1) * 32, kch = kk * 2 + ((lane >> 3) & 1);
+            ldsm_x4(bk, sK + krow * DK + ((kch ^ (krow & 7)) << 3));
+            mma_bf16_16816(acc, a, bk[0], bk[1]);
+            mma_bf16_16816(acc2, a, bk[2], bk[3]);
+          }
+        } else {  // one n-tile on two chains (even / odd k-steps), folded into acc
+          static_assert(KS % 2 == 0, "even number of k-steps");
+#pragma unroll 4
+          for (int kk = 0; kk < KS; kk += 2) {
+            uint32_t a[4], bk[4], a2[4], bk2[4];
+            const int qrow = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, qch = kk * 2 + (lane >> 4);
+            ldsm_x4(a, sQ + qrow * DK + ((qch ^ (qrow & 7)) << 3));
+            ldsm_x4(a2, sQ + qrow * DK + (((qch + 2) ^ (qrow & 7)) << 3));
+            const int krow = nb + (lane & 7), kch = kk * 2 + ((lane >> 3) & 1);
+            ldsm_x4(bk, sK + krow * DK + ((kch ^ (krow & 7)) << 3));  // lanes 16-31 duplicate 0-15
+            ldsm_x4(bk2, sK + krow * DK + (((kch + 2) ^ (krow & 7)) << 3));
+            mma_bf16_16816(acc, a, bk[0], bk[1]);
+            mma_bf16_16816(acc2, a2, bk2[0], bk2[1]);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[i] += acc2[i];
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < TC / 32; ++u) {
           const float* ac = u ? acc2 : acc;
           const int tk = nb + 32 * u + c2;
           const bool v0 = c * TC + tk < tloc, v1 = c * TC + tk + 1 < tloc;
@@ -785,16 +803,17 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
       }
     }
     __syncthreads();
-    // ---- online softmax: 8 threads per head, 8 tokens each ----
+    // ---- online softmax: 8 threads per head, TC / 8 tokens each ----
     {
-      const int h = tid >> 3, tq = (tid & 7) * 8;
+      constexpr int NV = TC / 8;
+      const int h = tid >> 3, tq = (tid & 7) * NV;
       if (h < MT * 16) {
-        float x[8];
+        float x[NV];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = sS[h * SST + tq + i];
+        for (int i = 0; i < NV; ++i) x[i] = sS[h * SST + tq + i];
         float mx = x[0];
 #pragma unroll
-        for (int i = 1; i < 8; ++i) mx = fmaxf(mx, x[i]);
+        for (int i = 1; i < NV; ++i) mx = fmaxf(mx, x[i]);
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
@@ -802,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
         const float mn = fmaxf(mo, mx);  // finite: every chunk has >= 1 valid token
         float ps = 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < NV; ++i) {
           const float e = fexp2(x[i] - mn);
           ps += e;
           sP[h * PST + tq + i] = __float2bfloat16_rn(e);
@@ -889,9 +908,9 @@ static cudaError_t launch_k3(const AttendParams& p, cudaStream_t st, const Launc
                    (unsigned)p.cs, p);
 }
 
-template <int MT>
+template <int MT, int TC>
 static cudaError_t launch_mla(const AttendParams& p, cudaStream_t st, const LaunchOpts& o) {
-  auto kern = attend_mla_kernel<576, 512, MT>;
+  auto kern = attend_mla_kernel<576, 512, MT, TC>;
   cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, p.cs > 8);
   if (e != cudaSuccess) return e;
   return launch_ex(kern, dim3((unsigned)p.cs, (unsigned)(p.d.batch * p.d.Hkv), 1), kThreads, p.smem_bytes, st, o,
@@ -903,7 +922,10 @@ cudaError_t launch_attend(const AttendParams& p, cudaStream_t st, const LaunchOp
     if (p.d.bf16) return launch_k3<__nv_bfloat16, false, 0>(p, st, o);
     return launch_k3<float, false, 0>(p, st, o);
   }
-  if (p.mma == 2) return p.d.G <= 16 ? launch_mla<1>(p, st, o) : launch_mla<2>(p, st, o);
+  if (p.mma == 2) {
+    if (p.mla_tc == 32) return p.d.G <= 16 ? launch_mla<1, 32>(p, st, o) : launch_mla<2, 32>(p, st, o);
+    return p.d.G <= 16 ? launch_mla<1, 64>(p, st, o) : launch_mla<2, 64>(p, st, o);
+  }
   if (p.d.bf16) {
     if (p.mma) return p.d.d_k == 128 ? launch_k3<__nv_bfloat16, true, 128>(p, st, o)
                                      : launch_k3<__nv_bfloat16, true, 64>(p, st, o);

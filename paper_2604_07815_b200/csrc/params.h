@@ -12,8 +12,9 @@ namespace tls {
 
 constexpr int kAttnChunk = 64;     // tokens per K/V staging stage of the GQA mma attention (8 warps x 8)
 constexpr int kAttnStages = 3;     // cp.async pipeline depth of the GQA mma attention
-constexpr int kMlaChunkTokens = 64;  // latent rows per staging chunk of the MLA attention
-constexpr int kMlaStages = 2;        // MLA attention cp.async pipeline depth (chunks in flight + 1)
+// MLA attention staging: 64-token chunks, double-buffered (default), or 32-token chunks, 3 stages (when the
+// selected-token list of a CTA leaves no room for the larger buffers)
+constexpr int mla_stages(int tc) { return tc == 64 ? 2 : 3; }
 constexpr int kScoreTileBytes = 32 * 1024;  // K1: bytes of block summaries per CTA (TMA tile)
 
 struct Dims {
@@ -94,6 +95,7 @@ struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally wit
   int mma;       // 1: bf16 mma.sync GQA path (d in {64,128}, G <= 16); 2: bf16 mma.sync MLA path (576/512)
   int tloc_max;  // ceil(kt_eff / cs)
   int heads_as_m;  // tuning: env TLS_ATTN_HEADS_AS_M=1 keeps the heads-as-M mma form for G <= 8
+  int mla_tc;      // MLA attention chunk tokens (64 or 32; see mla_stages)
   int select;    // 1: first select S_t = top-k_t from the keys (a4); 0: read token_ids / num_tokens
   int attend;    // 1: attention (a5); 0: selection only (tls_select)
   int kb_eff;
@@ -235,8 +237,9 @@ static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
     if (p.mma == 2) {  // MLA tensor-core path: Q, 2 latent-row chunks, S, P, alpha/m/l
       const int mt16 = d.G <= 16 ? 16 : 32;
       p.off_akv = (unsigned)s2;
-      s2 += (size_t)mt16 * d.d_k * 2 + (size_t)kMlaStages * kMlaChunkTokens * d.d_k * 2;
-      s2 += (size_t)mt16 * (kMlaChunkTokens + 4) * 4 + (size_t)mt16 * (kMlaChunkTokens + 8) * 2 + (size_t)3 * mt16 * 4;
+      const int tc = p.mla_tc == 32 ? 32 : 64;
+      s2 += (size_t)mt16 * d.d_k * 2 + (size_t)mla_stages(tc) * tc * d.d_k * 2;
+      s2 += (size_t)mt16 * (tc + 4) * 4 + (size_t)mt16 * (tc + 8) * 2 + (size_t)3 * mt16 * 4;
       s2 = align16(s2);
     } else if (p.mma) {
       p.off_akv = (unsigned)s2;  // 2 stages x (K chunk + V chunk); reused as the warp-partial scratch

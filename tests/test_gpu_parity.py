@@ -455,3 +455,23 @@ def test_token_topk_exact_ties(period):
                     partial += 1
                     assert np.array_equal(chosen, members[: len(chosen)]), (period, grp)  # lowest ids first
             assert partial <= 1
+
+
+def test_mla_attention_large_selection_uses_small_chunks():
+    """MLA attention over K_t = n = 131072 selected tokens (a5): the CTA's selected-token list leaves no room
+    for the 64-token double-buffered staging, so the plan falls back to 32-token chunks (3 stages); the output must
+    still equal dense attention (torch fp32 reference of the same definition, within the bf16 tolerance)."""
+    w = W.Workload("mla-big", 1, 32, 1, 576, 512, 131072, d_c=128, top_blocks=2048, top_tokens=131072, layout="mla",
+                   sm_scale=1.0 / math.sqrt(192.0))
+    cfg = tls.TLSConfig(**w.config_kwargs())
+    g = torch.Generator(device=DEV).manual_seed(11)
+    q = torch.randn((1, 32, 576), generator=g, device=DEV).to(torch.bfloat16)
+    k = torch.randn((1, w.context, 576), generator=g, device=DEV).to(torch.bfloat16)
+    tids = torch.arange(w.context, dtype=torch.int32, device=DEV).view(1, 1, -1).contiguous()
+    nt = torch.full((1, 1), w.context, dtype=torch.int32, device=DEV)
+    out, lse = tls.sparse_attend(cfg, q, k, None, tids, nt)
+    s = (q[0].float() @ k[0].float().T) * w.scale
+    ref = torch.softmax(s, dim=-1) @ k[0, :, :512].float()
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out[0].float(), ref, rtol=0, atol=2e-2)
+    torch.testing.assert_close(lse[0], torch.logsumexp(s, dim=-1), rtol=0, atol=1e-2)
