@@ -276,7 +276,11 @@ tls_status tls_block_cache_rows(const tls_config* cfg, const int32_t* token_ids,
  * t reads row slot_of_block[t / B] * B + t % B of (k_slots, v_slots), so every
  * block of the candidate set (M_t, or guide_block_ids = M_{t-1} in lag mode)
  * must be resident (tls_block_cache_update).  Same outputs and workspace as
- * tls_decode (which = 2); one fused launch chain. */
+ * tls_decode (which = 2); one fused launch chain.  guide_block_ids (M_{t-1},
+ * the lag mode of P:373) is required: TLS_ERR_INPUT when NULL, because the
+ * blocks of this step's M_t are not resident yet.  A selected token whose
+ * block is nevertheless not resident reads cache row 0 (no out-of-bounds
+ * access; use tls_block_cache_rows' `absent` count to detect it). */
 tls_status tls_decode_block_cache(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
                                   const int32_t* guide_block_ids, const tls_block_cache* cache, int32_t* block_ids,
                                   int32_t* token_ids, int32_t* num_tokens, float* token_scores, void* out,

@@ -140,9 +140,6 @@ int env_cluster() {
 tls_status plan_select(const tls_config* c, tls::SelectParams& p) {
   memset(&p, 0, sizeof(p));
   p.d = dims_of(c);
-  const char* cbe = getenv("TLS_CHUNK_BLOCKS");
-  p.cb_override = cbe ? atoi(cbe) : 0;
-  p.two_pass = getenv("TLS_K2_TWO_PASS") ? 1 : 0;
   tls::plan_select(p);
   if ((int)p.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "token-kernel shared-memory plan does not fit");
   return TLS_OK;
@@ -158,7 +155,6 @@ tls_status plan_attend(const tls_config* c, tls::AttendParams& p, int select, in
   p.mma = c->dtype == TLS_BF16 && c->layout == TLS_GQA && c->d_k == c->d_v && (c->d_k == 64 || c->d_k == 128) &&
           p.d.G <= 16;
   if (c->dtype == TLS_BF16 && c->layout == TLS_MLA && c->d_k == 576 && c->d_v == 512 && p.d.G <= 32) p.mma = 2;
-  p.heads_as_m = getenv("TLS_ATTN_HEADS_AS_M") ? 1 : 0;
   const long long pairs = (long long)c->batch * c->num_kv_heads;
   const int kt = tls::kt_effective(p.d);
   int cs = env_cluster();
@@ -392,12 +388,11 @@ tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int
   fp.ready = reinterpret_cast<unsigned*>(ws + c.w.ready_b);
   fp.epoch = epoch;
   fp.dbg = env_debug_buf();
-  fp.dbg_flags = getenv("TLS_TOPK_SAMPLE") ? 1 : 0;
   fp.qq = reinterpret_cast<float*>(ws + c.w.qq);
   // small query groups (GQA, G * d_k <= 512 elements): every tile CTA forms QQ itself (the same fp32 ops as
   // qq_kernel, so the same bits) and starts streaming without waiting for qq_kernel (A/B: C2 79.0 -> 77.2 us;
-  // at C3, G = 8, the per-tile work cost more than the wait: 127.4 -> 128.5); tuning: env TLS_QQ_WAIT
-  fp.qq_local = (cfg->layout == TLS_GQA && fp.d.G * cfg->d_k <= 512 && !getenv("TLS_QQ_WAIT")) ? 1 : 0;
+  // at C3, G = 8, the per-tile work cost more than the wait: 127.4 -> 128.5)
+  fp.qq_local = (cfg->layout == TLS_GQA && fp.d.G * cfg->d_k <= 512) ? 1 : 0;
   if (timed) g_timer.mark(st);
   cudaError_t e = tls::launch_qq(fp, st, lo_k1);
   if (e != cudaSuccess) return cuda_fail(e, "qq_kernel launch");
@@ -527,7 +522,7 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
   cudaError_t e = cudaEventRecord(pl->fork, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(fork)");
   tls::LaunchOpts lo_k1, lo_dep;
-  lo_k1.use_prio = lo_dep.use_prio = getenv("TLS_NOPRIO") ? 0 : 1;
+  lo_k1.use_prio = lo_dep.use_prio = 1;
   lo_k1.prio = pl->prio_lo;
   lo_dep.prio = pl->prio_hi;
   for (int i = 0; i < ns; ++i) {
@@ -704,6 +699,8 @@ tls_status tls_decode_block_cache(const tls_config* cfg, const void* q, const in
     return fail(TLS_ERR_INPUT, "block cache buffers must be non-NULL");
   if (cfg->layout == TLS_GQA && !cache->v_slots) return fail(TLS_ERR_INPUT, "GQA needs v_slots");
   if (cache->capacity < 1) return fail(TLS_ERR_CONFIG, "block cache capacity must be >= 1");
+  // only the lag-mode candidates M_{t-1} are guaranteed resident: M_t is fetched after this step
+  if (!guide_block_ids) return fail(TLS_ERR_INPUT, "tls_decode_block_cache needs guide_block_ids (M_{t-1}, P:373)");
   return run_step(cfg, q, cache->k_slots, cache->v_slots, seq_lens, idx, guide_block_ids, block_ids, token_ids,
                   num_tokens, token_scores, out, lse, workspace, workspace_bytes, 1, (cudaStream_t)stream,
                   cache->slot_of_block, (long long)cache->capacity * cfg->block_size);

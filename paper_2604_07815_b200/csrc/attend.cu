@@ -87,7 +87,12 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
       tout[pos] = tok;
       if (sout) sout[pos] = key2f(skeys[i]) * kLn2 - lnG;
     }
-    if (pos >= t0 && pos < t1) sel[pos - t0] = sob ? (sob[tok >> d.log2B] << d.log2B) + (tok & (d.B - 1)) : tok;
+    if (pos >= t0 && pos < t1) {
+      // block cache: row of the token's slot (a non-resident block -- a caller error, the guide must be resident --
+      // reads row 0 instead of out of bounds)
+      const int sl = sob ? sob[tok >> d.log2B] : 0;
+      sel[pos - t0] = sob ? (sl >= 0 ? (sl << d.log2B) + (tok & (d.B - 1)) : 0) : tok;
+    }
   };
   int* slist = reinterpret_cast<int*>(smem + p.off_slist);
   int K;
@@ -640,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const __grid_consta
   float* pml = p.part_ml + ((size_t)pair * cs + rank) * p.d.G * 2;
   if constexpr (MMA) {
     if constexpr (D == 128) {
-      if (p.d.G <= 8 && !p.heads_as_m) phase_attend_mma_t<D>(p, pair, b, g, sel, tloc, smem + p.off_akv, po, pml);
+      if (p.d.G <= 8) phase_attend_mma_t<D>(p, pair, b, g, sel, tloc, smem + p.off_akv, po, pml);
       else phase_attend_mma<D>(p, pair, b, g, sel, tloc, smem + p.off_akv, po, pml);
     } else {
       phase_attend_mma<D>(p, pair, b, g, sel, tloc, smem + p.off_akv, po, pml);

@@ -179,11 +179,6 @@ __device__ __forceinline__ void score_tile(const FusedParams& p, int pair, int b
   }
 }
 
-// Diagnostics: the sample-bracket select path of fast_topk is used when
-// FusedParams::dbg_flags bit 0 is set (env TLS_TOPK_SAMPLE); else the range
-// histogram select.
-__device__ __forceinline__ bool getenv_flag_sample(const FusedParams& p) { return p.dbg_flags & 1; }
-
 // Completion sentinel of the block-score buffer (all-ones bits: a NaN that no
 // arithmetic produces; set by tls_workspace_init, restored by every worker).
 constexpr uint32_t kScoreSentinel = 0xffffffffu;
@@ -215,11 +210,11 @@ __device__ __noinline__ void pair_worker(const FusedParams& p, int pair, int m, 
     // range-histogram select (the sample-bracket path measured 2x slower on 1.5k scores)
     bool done = false;
     constexpr int kBlkChunks = 2;  // <= 8 keys per thread (m <= 2048 blocks) within the kernel register budget
-    if (K < m && m <= 4 * kBlkChunks * kThreads && !getenv_flag_sample(p))
+    if (K < m && m <= 4 * kBlkChunks * kThreads)
       done = range_topk_select<kBlkChunks>(bkeys, m, K, scratch, fk, tk, hs, [&](int i, int pos) { bout[pos] = i; });
     TLS_STAMP(4)
     if (!done) {
-      const TopK t = fast_topk(bkeys, m, K, d.Kb >= m, fk, tk, getenv_flag_sample(p) ? scratch : nullptr);
+      const TopK t = fast_topk(bkeys, m, K, d.Kb >= m, fk, tk, nullptr);
       topk_emit(bkeys, m, t, tk, [&](int i, int pos) { bout[pos] = i; });
     }
     for (int pos = K + tid; pos < d.Kb; pos += kThreads) bout[pos] = -1;

@@ -54,7 +54,6 @@ struct FusedParams {
   unsigned* ready;         // workspace [pairs]: set to `epoch` when the pair's a2 outputs are written
   unsigned epoch;          // this call's hand-off value (host call counter, never 0)
   unsigned long long* dbg; // diagnostics only (env TLS_DEBUG_BUF): worker phase stamps
-  int dbg_flags;           // tuning: bit 0 = sample-bracket top-k_b (env TLS_TOPK_SAMPLE)
   unsigned off_bkeys, off_scratch, off_fk, smem_bytes;
 };
 
@@ -64,8 +63,6 @@ struct SelectParams {  // K2 (token_reg_kernel, or token_cluster_kernel when a c
   int kb_eff, kt_eff;  // min(Kb, M); min(Kt, kb_eff*B, S)
   int cb;              // candidate blocks per chunk CTA
   int tpw;             // > 0: token_reg_kernel with tpw 16-token tiles per warp; 0: token_cluster_kernel
-  int cb_override;     // tuning: env TLS_CHUNK_BLOCKS (0 = heuristic)
-  int two_pass;        // tuning: env TLS_K2_TWO_PASS forces token_cluster_kernel
   int nch;             // chunks per pair = ceil(kb_eff / cb)
   const void* q;
   const int* seq_lens;
@@ -94,7 +91,6 @@ struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally wit
   int cs;
   int mma;       // 1: bf16 mma.sync GQA path (d in {64,128}, G <= 16); 2: bf16 mma.sync MLA path (576/512)
   int tloc_max;  // ceil(kt_eff / cs)
-  int heads_as_m;  // tuning: env TLS_ATTN_HEADS_AS_M=1 keeps the heads-as-M mma form for G <= 8
   int mla_tc;      // MLA attention chunk tokens (64 or 32; see mla_stages)
   int select;    // 1: first select S_t = top-k_t from the keys (a4); 0: read token_ids / num_tokens
   int attend;    // 1: attention (a5); 0: selection only (tls_select)
@@ -187,8 +183,6 @@ static inline void plan_select(SelectParams& p) {
   } else {
     p.tpw = 0;
   }
-  if (p.two_pass) p.tpw = 0;  // tuning: env TLS_K2_TWO_PASS
-  if (p.cb_override > 0 && (p.tpw == 0 || p.cb_override <= cb_reg)) p.cb = p.cb_override;  // tuning
   if (p.cb > p.kb_eff) p.cb = p.kb_eff;
   p.nch = (p.kb_eff + p.cb - 1) / p.cb;
   size_t o = 0;
@@ -213,7 +207,9 @@ static inline void plan_select(SelectParams& p) {
 static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
   const Dims& d = p.d;
   p.kb_eff = kb_effective(d);
-  p.tloc_max = (kt_effective(d) + p.cs - 1) / p.cs;
+  // with the a4 prologue the list is |S_t| <= min(Kt, Kb*B, S); standalone attention takes any num_tokens <= min(Kt, S)
+  const int kmax = p.select ? kt_effective(d) : (d.Kt < d.S ? d.Kt : d.S);
+  p.tloc_max = (kmax + p.cs - 1) / p.cs;
   size_t o = 0;
   p.off_sel = (unsigned)o;
   o = align16(o + (size_t)(p.tloc_max + 1) * 4);

@@ -426,6 +426,7 @@ __device__ int hist_topk_select(const uint32_t* skeys, int nslots, const uint32_
     for (uint64_t m = bd; m; m &= m - 1) atomicAdd(&s_sub[sub_of(skeys[r0 + __ffsll((long long)m) - 1])], 1u);
     __syncthreads();
     const int c = (int)s_sub[kThreads - 1 - tid];
+    if (tid == 0) hs.bsel = -1;  // (ordered before the writer below by the scan's barriers)
     int tot_;
     const int ab = block_exclusive_scan(c, tk.scan, &tot_);
     if (ab < kr && kr <= ab + c) {
@@ -435,6 +436,11 @@ __device__ int hist_topk_select(const uint32_t* skeys, int nslots, const uint32_
     if (tid == 0) fk.bcount = 0;
     __syncthreads();
     const int sb = hs.bsel;
+    if (sb < 0) {  // the sub-bin counts do not bracket rank kr (cannot happen for an exact histogram): take
+                   // the generic select below instead of emitting a wrong set
+      nbk = 1 << 30;
+      goto generic_select;
+    }
     kr -= hs.above;
     uint64_t nbd = 0;
     for (uint64_t m = bd; m; m &= m - 1) {
@@ -455,6 +461,7 @@ __device__ int hist_topk_select(const uint32_t* skeys, int nslots, const uint32_
     __syncthreads();
     nbk = fk.bcount;
   }
+generic_select:
   if (nbk > 1024) {  // rare (e.g. thousands of equal keys): generic select into slist
     const TopK t = fast_topk(skeys, nslots, K, false, fk, tk, scratch);
     topk_emit(skeys, nslots, t, tk, [&](int i, int pos) { slist[pos] = i; });

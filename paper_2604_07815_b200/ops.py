@@ -533,12 +533,14 @@ class AsyncOffloadDecoder:
         next (the other layers of the model)."""
         cfg = self.cfg
         main = torch.cuda.current_stream(q.device)
-        if self.prev is None:  # first step: M_0 from a synchronous selection, fetched before the attention
-            bids0 = select(cfg, q, self.seq_lens, self.index)[0]
-            main.wait_event(self._update(bids0, None))
+        if self.prev is None:  # first step: M_0 from a synchronous selection, fetched before the attention, is
+            # the guide (candidates = this step's own M_t, the synchronous form P:137)
+            guide = select(cfg, q, self.seq_lens, self.index)[0]
+            main.wait_event(self._update(guide, None))
         else:
+            guide = self.prev
             main.wait_event(self.ready)  # M_{t-1} resident
-        res = decode_block_cache(cfg, q, self.seq_lens, self.index, self.cache, guide_block_ids=self.prev)
+        res = decode_block_cache(cfg, q, self.seq_lens, self.index, self.cache, guide_block_ids=guide)
         bids = res[2]
         # M_t's missing blocks go to free slots; M_{t-1} (read by this step) stays
         self.ready = self._update(bids, self.prev)

@@ -86,14 +86,22 @@ def bf16_half_ulp(x: np.ndarray) -> np.ndarray:
     return 0.5 * 2.0 ** (np.floor(np.log2(ax)) - 7)
 
 
+# Reading U19 applies only above this magnitude: below it half a bf16 ulp is <= 2^-6 = 0.0156 < 2e-2, so
+# the north star's flat 2e-2 max-abs bound leaves room for the output rounding and is used unchanged.
+U19_MIN_ABS = 5.12
+
+
 def compare_output(out_gpu: np.ndarray, out_ref: np.ndarray, dtype, what=""):
-    """North star (b).  Reading U19: for bf16 the max-abs bound
-    is taken on top of the unavoidable rounding of the reference to the bf16
-    output (|err| <= 2e-2 + half a bf16 ulp of the reference); for |ref| < 4
-    the extra term is below 2e-2 / 1.3, so it only matters for large outputs."""
+    """North star (b): max-abs 2e-2 and rel-L2 1e-2 for bf16, 1e-4 for fp32.
+    Reading U19: a bf16 output element whose reference exceeds
+    |5.12| is allowed half a bf16 ulp of the reference on top of 2e-2 (the
+    rounding of the result to the bf16 output format alone can exceed 2e-2 from
+    |ref| >= 8); every other element is held to the flat 2e-2."""
     mx, rl2 = attention_tol(dtype)
     diff = np.abs(out_gpu - out_ref)
-    allow = mx + (bf16_half_ulp(out_ref) if dtype == torch.bfloat16 else 0.0)
+    allow = mx
+    if dtype == torch.bfloat16:
+        allow = mx + np.where(np.abs(out_ref) > U19_MIN_ABS, bf16_half_ulp(out_ref), 0.0)
     i = np.unravel_index(np.argmax(diff - allow), diff.shape)
     err = diff.max()
     rel = np.linalg.norm(out_gpu - out_ref) / max(np.linalg.norm(out_ref), 1e-30)

@@ -285,15 +285,22 @@ def test_errors_are_reported():
 
 
 # ---- full BASELINE.json sizes, sampled pairs, bench launch configuration ----
-FULL_SAMPLES = {"c2": [(0, 0), (7, 3), (15, 7)], "c3": [(0, 0), (13, 5), (31, 7)], "c4": [(0, 0), (17, 0), (31, 0)]}
+N_FULL_PAIRS = 16
 
 
-@pytest.mark.slow
-@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
-def test_full_size_sampled_pairs(name):
-    w = W.CONFIGS[name]
-    inputs = W.make_inputs(w, seed=0, pattern="peaked", device=DEV)
-    q_cal, k_cal = W.calibration_sample(w, inputs, seed=0, pattern="peaked")
+def sampled_pairs(w, n, seed):
+    """n distinct (b, g) pairs: the first and the last pair plus a seeded sample of the rest."""
+    allp = [(b, g) for b in range(w.batch) for g in range(w.num_kv_heads)]
+    if len(allp) <= n:
+        return allp
+    rng = np.random.default_rng(seed)
+    mid = rng.choice(np.arange(1, len(allp) - 1), size=n - 2, replace=False)
+    return [allp[0]] + [allp[i] for i in sorted(mid)] + [allp[-1]]
+
+
+def run_full(w, pattern, seed=0, n_pairs=N_FULL_PAIRS):
+    inputs = W.make_inputs(w, seed=seed, pattern=pattern, device=DEV)
+    q_cal, k_cal = W.calibration_sample(w, inputs, seed=seed, pattern=pattern)
     channels = P.oracle_channels(w, q_cal, k_cal).to(DEV)
     cfg = tls.TLSConfig(**w.config_kwargs())
     idx = tls.alloc_index(cfg, channels)
@@ -301,11 +308,33 @@ def test_full_size_sampled_pairs(name):
     res = run_decode(cfg, inputs, idx)
     torch.cuda.synchronize()
     stats = {"block_near_ties": 0, "token_near_ties": 0}
-    for b, g in FULL_SAMPLES[name]:
+    pairs = sampled_pairs(w, n_pairs, seed + 101)
+    for b, g in pairs:
         check_pair(w, cfg, inputs, idx, res, b, g, stats)
-    print(f"{name}: near-ties {stats}")
+    print(f"{w.name} {pattern}: {len(pairs)} pairs, near-ties {stats}")
     del inputs, idx, res
     torch.cuda.empty_cache()
+    return stats
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("pattern", ["outlier", "uniform", "peaked"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_full_size_sampled_pairs(name, pattern):
+    """BASELINE.json's C2/C3/C4 at full size in the launch configuration bench.py times (one tls_decode over the
+    whole batch), 16 sampled pairs per case checked element by element against the oracle: the bench's own
+    `outlier` pattern, `uniform` (flat alpha~: the widest top-k_t boundary) and `peaked`."""
+    run_full(W.CONFIGS[name], pattern)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kb,kt", [(128, 512), (128, 2048), (256, 1024), (64, 1024)])
+def test_budgets_c3_shape(kb, kt):
+    """The paper's budgets (k_b = 128 blocks, k_t in {512, 1024, 2048}) and k_b in {64, 256} on the C3
+    per-pair shape (Qwen3-32B, 96k context; batch 2 = 16 pairs, every pair checked)."""
+    w = W.CONFIGS["c3"].with_(batch=2, top_blocks=kb, top_tokens=kt)
+    run_full(w, "outlier", seed=2, n_pairs=16)
+    run_full(w, "uniform", seed=3, n_pairs=16)
 
 
 @pytest.mark.parametrize("name", ["gqa4", "mla", "c1"])
