@@ -73,8 +73,8 @@ def kernel_bytes_per_pair(w, mode: int = 2) -> dict:
     a1 = m * 2 * w.d_k * s + q  # block summaries
     a3 = cand * (w.d_c // 2 + 8)  # INT4 codes + scale/zero of the candidate tokens
     a5 = kt * row + q + G * w.d_v * s  # selected K/V rows, o
-    if mode == 2:  # select_kernel: a1-a4; attend_kernel: a5
-        return {"select_kernel": a1 + a3, "token_cluster_kernel": 0.0, "attend_kernel": a5}
+    if mode == 3:  # the fused step kernel: a1-a5 in one launch
+        return {"step_kernel": a1 + a3 + a5}
     return {"select_kernel": a1, "token_cluster_kernel": a3 + q, "attend_kernel": a5}
 
 
@@ -345,8 +345,8 @@ def run_tls(args, w, rank, world, local_rank):
     # launch stream (events between launches also serialise them, so this pass runs without PDL overlap)
     n_k = max(10, min(args.steps, 200))
     tls.timing_enable(n_k + 3)
-    kern_step_times = time_steps(step, n_k, 3, flush, stream, on_timed_start=tls.timing_read)
-    kern_ms, kern_calls = tls.timing_read()
+    kern_step_times = time_steps(step, n_k, 3, flush, stream, on_timed_start=lambda: tls.timing_read(cfg))
+    kern_ms, kern_calls = tls.timing_read(cfg)
     tls.timing_enable(0)
     # e2e through the public API with HOST buffers: H2D q (pinned), decode, D2H out+lse
     q_host = queries.cpu().pin_memory()
@@ -365,7 +365,8 @@ def run_tls(args, w, rank, world, local_rank):
 
     ms = sum(times) / len(times)
     ms_e2e = sum(e2e_times) / len(e2e_times)
-    kavg = [kern_ms[k] / max(1, kern_calls) for k in tls.KERNELS]
+    names = tls.kernel_names(cfg)
+    kavg = [kern_ms[k] / max(1, kern_calls) for k in names]
     if world > 1:
         t = torch.tensor([ms, ms_e2e] + kavg, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -385,8 +386,8 @@ def run_tls(args, w, rank, world, local_rank):
     kernels = {k: {"avg_us": kavg[i] * 1e3, "share": kavg[i] / ms_ser,
                    "algorithmic_bytes_per_launch": kbytes[k] * pairs,
                    "gbs": kbytes[k] * pairs / (kavg[i] * 1e-3) / 1e9 if kavg[i] > 0 else None}
-               for i, k in enumerate(tls.KERNELS)}
-    dom = max(tls.KERNELS, key=lambda k: kernels[k]["avg_us"])
+               for i, k in enumerate(names)}
+    dom = max(names, key=lambda k: kernels[k]["avg_us"])
     dom_ach = kernels[dom]["gbs"]
     line = {
         "metric": METRIC,

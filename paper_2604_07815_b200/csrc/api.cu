@@ -29,6 +29,9 @@ cudaError_t launch_token_cluster(const SelectParams& p, cudaStream_t st, const L
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t st, const LaunchOpts& o);
 int score_cpl(int d_k, size_t elem_bytes);
 bool select_supported(int d_c, int G);
+bool step_supported(const Dims& d);
+bool plan_step(StepKParams& p, int nc);
+cudaError_t launch_step(const StepKParams& p, cudaStream_t st);
 }  // namespace tls
 
 namespace {
@@ -135,6 +138,25 @@ unsigned long long* env_debug_buf() {
 int env_cluster() {
   const char* env = getenv("TLS_CLUSTER");
   return (env && atoi(env) > 0) ? atoi(env) : 0;
+}
+
+// The fused step kernel (step.cu: a1-a5 of a pair in one thread-block cluster) for the configurations it
+// supports: nc = TLS_CLUSTER (tuning / tests) or 8 CTAs per pair, 16 when the pairs are too few to fill the
+// SMs three CTAs deep.  false: the kernel chain runs instead.
+bool step_plan(const tls_config* c, tls::StepKParams& sp) {
+  memset(&sp, 0, sizeof(sp));
+  sp.d = dims_of(c);
+  if (!tls::step_supported(sp.d)) return false;
+  const int env = env_cluster();
+  if (env) return env <= 16 && tls::plan_step(sp, env) && (int)sp.smem_bytes <= kMaxSmem;
+  const long long pairs = (long long)c->batch * c->num_kv_heads;
+  const int first = pairs * 8 < 3LL * num_sms() ? 16 : 8;
+  for (const int nc : {first, 16}) {
+    memset(&sp, 0, sizeof(sp));
+    sp.d = dims_of(c);
+    if (tls::plan_step(sp, nc) && (int)sp.smem_bytes <= kMaxSmem) return true;
+  }
+  return false;
 }
 
 tls_status plan_select(const tls_config* c, tls::SelectParams& p) {
@@ -300,6 +322,11 @@ tls_status chain_workspace(const tls_config* cfg, int do_attend, size_t* bytes) 
 }
 
 tls_status step_workspace(const tls_config* cfg, int do_attend, size_t* bytes) {
+  tls::StepKParams sk;
+  if (step_plan(cfg, sk)) {  // the fused step keeps every intermediate in shared memory
+    *bytes = 256;
+    return TLS_OK;
+  }
   const int ns = n_split(cfg);
   size_t tot = 0;
   for (int s = 0; s < ns; ++s) {
@@ -511,6 +538,32 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
   const StepPtrs all = {q, k_cache, v_cache, seq_lens, *idx, guide, block_ids, token_ids, num_tokens,
                         token_scores, out, lse, slot_of_block, kv_rows > 0 ? kv_rows : cfg->max_seq_len};
   if (g_timer.on && g_timer.used % kMarks != 0) g_timer.used -= g_timer.used % kMarks;  // drop a partial record
+  tls::StepKParams sk;
+  if (step_plan(cfg, sk)) {  // one launch: a1-a5 (a1-a4 for tls_select) of every pair, one cluster per pair
+    sk.attend = do_attend;
+    sk.q = q;
+    sk.seq_lens = seq_lens;
+    sk.block_minmax = idx->block_minmax;
+    sk.codes = idx->codes;
+    sk.scale_zero = idx->scale_zero;
+    sk.channels = idx->channels;
+    sk.guide = guide;
+    sk.k_cache = k_cache;
+    sk.v_cache = v_cache;
+    sk.kv_rows = kv_rows > 0 ? kv_rows : cfg->max_seq_len;
+    sk.slot_of_block = slot_of_block;
+    sk.block_ids = block_ids;
+    sk.token_ids = token_ids;
+    sk.num_tokens = num_tokens;
+    sk.token_scores = token_scores;
+    sk.out = out;
+    sk.lse = lse;
+    g_timer.mark(st);
+    cudaError_t e = tls::launch_step(sk, st);
+    if (e != cudaSuccess) return cuda_fail(e, "step_kernel launch");
+    for (int k = 1; k < kMarks; ++k) g_timer.mark(st);  // one launch: slot 0 holds the whole step
+    return TLS_OK;
+  }
   char* ws = static_cast<char*>(workspace);
   const int ns = n_split(cfg);
   if (ns == 1) return enqueue_chain(cfg, all, ws, do_attend, st, tls::LaunchOpts{}, tls::LaunchOpts{}, true);
@@ -725,7 +778,8 @@ tls_status tls_workspace_init(const tls_config* cfg, int32_t which, void* worksp
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(workspace, 0, need, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
-  if (which == 1) return TLS_OK;
+  tls::StepKParams sk;
+  if (which == 1 || step_plan(cfg, sk)) return TLS_OK;
   // every chain's block-score buffer starts as the completion sentinel (fused.cu kScoreSentinel)
   char* ws = static_cast<char*>(workspace);
   const int ns = n_split(cfg);
@@ -864,6 +918,8 @@ tls_status tls_block_cache_rows(const tls_config* cfg, const int32_t* token_ids,
 
 int32_t tls_launch_count(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK) return -1;
+  tls::StepKParams sk;
+  if ((which == 0 || which == 2) && step_plan(cfg, sk)) return 1;  // step_kernel
   const int mode = fused_mode(cfg), ns = n_split(cfg);
   switch (which) {
     case 0: return ns * (mode == 2 ? 1 : 4);  // qq, select, token and attend (selection prologue only) kernels
@@ -877,11 +933,15 @@ int32_t tls_launch_count(const tls_config* cfg, int32_t which) {
 
 int32_t tls_select_mode(const tls_config* cfg) {
   if (check_config(cfg) != TLS_OK) return -1;
+  tls::StepKParams sk;
+  if (step_plan(cfg, sk)) return 3;  // the fused step kernel
   return fused_mode(cfg);
 }
 
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK || which < 0 || which > 2) return -1;
+  tls::StepKParams sk;
+  if (which != 1 && step_plan(cfg, sk)) return sk.nc;
   tls::AttendParams ap;
   return plan_attend(cfg, ap, which != 1, which != 0) == TLS_OK ? ap.cs : -1;
 }

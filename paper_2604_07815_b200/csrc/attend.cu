@@ -706,8 +706,12 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem + p.off_akv);
   __nv_bfloat16* sKV = sQ + MT * 16 * DK;           // kMlaStages buffers of TC rows
   float* sS = reinterpret_cast<float*>(sKV + kMlaStages * TC * DK);
+  // P = exp2(S - m) as two bf16 pieces P_hi + P_lo (both exact sums of the fp32 value to ~2^-17): a single bf16 P
+  // costs up to 2^-9 |V| per selected token, which for peaked attention over the latent (outlier channels, |V| ~ 5)
+  // alone uses half the 2e-2 output tolerance; the second PV product removes it
   __nv_bfloat16* sP = reinterpret_cast<__nv_bfloat16*>(sS + MT * 16 * SST);
-  float* sAlpha = reinterpret_cast<float*>(sP + MT * 16 * PST);
+  __nv_bfloat16* sPl = sP + MT * 16 * PST;
+  float* sAlpha = reinterpret_cast<float*>(sPl + MT * 16 * PST);
   float* sM = sAlpha + MT * 16;
   float* sL = sM + MT * 16;
   const int t0 = (int)((long long)K * rank / cs), t1 = (int)((long long)K * (rank + 1) / cs);
@@ -829,7 +833,9 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
         for (int i = 0; i < NV; ++i) {
           const float e = fexp2(x[i] - mn);
           ps += e;
-          sP[h * PST + tq + i] = __float2bfloat16_rn(e);
+          const __nv_bfloat16 eh = __float2bfloat16_rn(e);
+          sP[h * PST + tq + i] = eh;
+          sPl[h * PST + tq + i] = __float2bfloat16_rn(e - __bfloat162float(eh));
         }
         ps += __shfl_xor_sync(0xffffffffu, ps, 1);
         ps += __shfl_xor_sync(0xffffffffu, ps, 2);
@@ -858,12 +864,13 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
     }
 #pragma unroll
     for (int kk = 0; kk < TC / 16; ++kk) {
-      uint32_t pa[MT][4];
+      uint32_t pa[MT][4], pl[MT][4];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const int prow = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
         const int pcol = kk * 16 + (lane >> 4) * 8;
         ldsm_x4(pa[mt], sP + prow * PST + pcol);
+        ldsm_x4(pl[mt], sPl + prow * PST + pcol);
       }
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
@@ -875,6 +882,8 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
         for (int mt = 0; mt < MT; ++mt) {
           mma_bf16_16816(o[mt][2 * jj], pa[mt], bv[0], bv[1]);
           mma_bf16_16816(o[mt][2 * jj + 1], pa[mt], bv[2], bv[3]);
+          mma_bf16_16816(o[mt][2 * jj], pl[mt], bv[0], bv[1]);
+          mma_bf16_16816(o[mt][2 * jj + 1], pl[mt], bv[2], bv[3]);
         }
       }
     }

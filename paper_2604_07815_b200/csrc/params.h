@@ -116,6 +116,35 @@ struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally wit
   unsigned off_sel, off_cblk, off_union, off_skeys, off_fk, off_slist, off_akv, off_aq, off_as, smem_bytes;
 };
 
+// Fused decode step (step.cu): a1-a5 of one pair in one thread-block cluster.
+struct StepKParams {
+  Dims d;
+  int nc;       // CTAs per pair (cluster size)
+  int mb;       // a1 block rows per CTA (multiple of 8)
+  int cb;       // a3 candidate blocks per CTA
+  int tok_max;  // a5 selected tokens per CTA, max
+  int attend;   // 0: selection only (tls_select)
+  const void* q;
+  const int* seq_lens;
+  const void* block_minmax;
+  const uint8_t* codes;
+  const float* scale_zero;
+  const int* channels;
+  const int* guide;          // lag mode: candidate blocks M_{t-1}, else NULL
+  const void* k_cache;
+  const void* v_cache;
+  long long kv_rows;         // rows per pair of k_cache / v_cache
+  const int* slot_of_block;  // block cache (offload engine), else NULL
+  int* block_ids;
+  int* token_ids;
+  int* num_tokens;
+  float* token_scores;
+  void* out;
+  float* lse;
+  // dynamic shared-memory plan
+  unsigned off_u, off_keys, off_hist, off_cand, off_sel, off_qq, off_qb, off_xs, off_part, smem_bytes;
+};
+
 // GPU token cache of the offload engine (offload.cu): make S_t resident.
 struct CacheFetchParams {
   Dims d;
@@ -235,7 +264,7 @@ static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
       p.off_akv = (unsigned)s2;
       const int tc = p.mla_tc == 32 ? 32 : 64;
       s2 += (size_t)mt16 * d.d_k * 2 + (size_t)mla_stages(tc) * tc * d.d_k * 2;
-      s2 += (size_t)mt16 * (tc + 4) * 4 + (size_t)mt16 * (tc + 8) * 2 + (size_t)3 * mt16 * 4;
+      s2 += (size_t)mt16 * (tc + 4) * 4 + (size_t)2 * mt16 * (tc + 8) * 2 + (size_t)3 * mt16 * 4;  // S, P_hi, P_lo
       s2 = align16(s2);
     } else if (p.mma) {
       p.off_akv = (unsigned)s2;  // 2 stages x (K chunk + V chunk); reused as the warp-partial scratch

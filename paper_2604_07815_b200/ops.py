@@ -30,6 +30,7 @@ __all__ = [
     "decode",
     "cluster_size",
     "select_mode",
+    "kernel_names",
     "KERNELS",
     "timing_enable",
     "TLSTokenCache",
@@ -309,13 +310,21 @@ def cluster_size(cfg: TLSConfig, which: int = 2) -> int:
     return int(_lib.load().tls_cluster_size(ctypes.byref(cc), which))
 
 
+# timing slots of the kernel chain (select mode 1) and of the fused step (mode 3, one launch)
 KERNELS = ("select_kernel", "token_cluster_kernel", "attend_kernel")
+STEP_KERNELS = ("step_kernel",)
 
 
 def select_mode(cfg: TLSConfig) -> int:
-    """2: select_kernel does a1-a4 (one launch); 1: a1-a2, then token_cluster_kernel + attend prologue."""
+    """3: the fused step kernel (a1-a5 of a pair in one thread-block cluster, one launch); 1: the kernel chain
+    (select_kernel a1-a2, token kernel a3, the attention kernel's prologue a4 + a5)."""
     cc = cfg.c()
     return int(_lib.load().tls_select_mode(ctypes.byref(cc)))
+
+
+def kernel_names(cfg: TLSConfig) -> tuple:
+    """Names of the launches one tls_decode call enqueues (the timing slots of timing_read)."""
+    return STEP_KERNELS if select_mode(cfg) == 3 else KERNELS
 
 
 def timing_enable(n_calls: int) -> None:
@@ -324,12 +333,14 @@ def timing_enable(n_calls: int) -> None:
     _lib.check(_lib.load().tls_timing_enable(int(n_calls)))
 
 
-def timing_read() -> tuple[dict, int]:
-    """(kernel name -> summed ms, number of calls) since the last read (tls_timing_read)."""
+def timing_read(cfg: TLSConfig | None = None) -> tuple[dict, int]:
+    """(kernel name -> summed ms, number of calls) since the last read (tls_timing_read); the names are those
+    of ``kernel_names(cfg)`` (the kernel chain's when cfg is None)."""
     ms = (ctypes.c_double * len(KERNELS))()
     calls = ctypes.c_int64(0)
     _lib.check(_lib.load().tls_timing_read(ms, ctypes.byref(calls)))
-    return {k: float(ms[i]) for i, k in enumerate(KERNELS)}, int(calls.value)
+    names = kernel_names(cfg) if cfg is not None else KERNELS
+    return {k: float(ms[i]) for i, k in enumerate(names)}, int(calls.value)
 
 
 # ------------------------------------------------------------------ KV offload (P:358-383)

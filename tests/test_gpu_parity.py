@@ -358,7 +358,11 @@ def test_block_scores_match_direct_form(name):
 def test_kernel_timing_hook_records_every_launch():
     """tls_timing_enable/read: one record per select/decode call, 4 slots, and
     recording does not change the results."""
-    w = SMALL["gqa8"]
+    for name in ("gqa8", "mla"):  # the fused step kernel (one slot) and the kernel chain (three slots)
+        check_timing_hook(SMALL[name])
+
+
+def check_timing_hook(w):
     cfg, inputs, idx = setup_case(w, seed=3)
     ref = run_decode(cfg, inputs, idx)
     tls.timing_enable(2)
@@ -366,10 +370,10 @@ def test_kernel_timing_hook_records_every_launch():
         res = run_decode(cfg, inputs, idx)
         tls.select(cfg, inputs["q"], inputs["seq_lens"], idx)
         run_decode(cfg, inputs, idx)  # more calls than reserved: events created on demand
-        ms, calls = tls.timing_read()
+        ms, calls = tls.timing_read(cfg)
         assert calls == 3
-        assert set(ms) == set(tls.KERNELS) and all(v > 0 for v in ms.values())
-        ms2, calls2 = tls.timing_read()
+        assert set(ms) == set(tls.kernel_names(cfg)) and all(v > 0 for v in ms.values())
+        ms2, calls2 = tls.timing_read(cfg)
         assert calls2 == 0 and all(v == 0 for v in ms2.values())
     finally:
         tls.timing_enable(0)
