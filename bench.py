@@ -73,8 +73,8 @@ def kernel_bytes_per_pair(w, mode: int = 2) -> dict:
     a1 = m * 2 * w.d_k * s + q  # block summaries
     a3 = cand * (w.d_c // 2 + 8)  # INT4 codes + scale/zero of the candidate tokens
     a5 = kt * row + q + G * w.d_v * s  # selected K/V rows, o
-    if mode == 3:  # the fused step kernel: a1-a5 in one launch
-        return {"step_kernel": a1 + a3 + a5}
+    if mode == 3:  # the persistent step kernel: a1-a5 in one launch
+        return {"pstep_kernel": a1 + a3 + a5}
     return {"select_kernel": a1, "token_cluster_kernel": a3 + q, "attend_kernel": a5}
 
 

@@ -15,6 +15,7 @@ from .ops import (  # noqa: F401
     decode,
     select,
     select_mode,
+    kernel_names,
     sparse_attend,
     KERNELS,
     timing_enable,

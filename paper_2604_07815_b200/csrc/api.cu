@@ -29,9 +29,11 @@ cudaError_t launch_token_cluster(const SelectParams& p, cudaStream_t st, const L
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t st, const LaunchOpts& o);
 int score_cpl(int d_k, size_t elem_bytes);
 bool select_supported(int d_c, int G);
-bool step_supported(const Dims& d);
-bool plan_step(StepKParams& p, int nc);
-cudaError_t launch_step(const StepKParams& p, cudaStream_t st);
+bool pstep_supported(const Dims& d);
+bool plan_pstep(PStepParams& p, int ns_override);
+size_t pstep_workspace(PStepParams& p, char* ws);
+int pstep_occupancy(size_t smem);
+cudaError_t launch_pstep(const PStepParams& p, int grid, cudaStream_t st);
 }  // namespace tls
 
 namespace {
@@ -140,23 +142,19 @@ int env_cluster() {
   return (env && atoi(env) > 0) ? atoi(env) : 0;
 }
 
-// The fused step kernel (step.cu: a1-a5 of a pair in one thread-block cluster) for the configurations it
-// supports: nc = TLS_CLUSTER (tuning / tests) or 8 CTAs per pair, 16 when the pairs are too few to fill the
-// SMs three CTAs deep.  false: the kernel chain runs instead.
-bool step_plan(const tls_config* c, tls::StepKParams& sp) {
+// The persistent step kernel (pstep.cu: one launch, work items of every stage of every pair claimed from a
+// ticket queue) for the configurations it supports; false: the kernel chain runs instead.  TLS_CLUSTER
+// (tuning / tests) sets its attention slices per pair; TLS_PSTEP="L1,L2,L3" (tuning) its schedule lags.
+bool pstep_plan(const tls_config* c, int do_attend, tls::PStepParams& sp) {
   memset(&sp, 0, sizeof(sp));
   sp.d = dims_of(c);
-  if (!tls::step_supported(sp.d)) return false;
+  if (!tls::pstep_supported(sp.d)) return false;
+  sp.attend = do_attend;
+  const char* e = getenv("TLS_PSTEP");
+  if (e) sscanf(e, "%d,%d,%d", &sp.L1, &sp.L2, &sp.L3);
   const int env = env_cluster();
-  if (env) return env <= 16 && tls::plan_step(sp, env) && (int)sp.smem_bytes <= kMaxSmem;
-  const long long pairs = (long long)c->batch * c->num_kv_heads;
-  const int first = pairs * 8 < 3LL * num_sms() ? 16 : 8;
-  for (const int nc : {first, 16}) {
-    memset(&sp, 0, sizeof(sp));
-    sp.d = dims_of(c);
-    if (tls::plan_step(sp, nc) && (int)sp.smem_bytes <= kMaxSmem) return true;
-  }
-  return false;
+  if (env > 16) return false;
+  return tls::plan_pstep(sp, env) && (int)sp.smem_bytes <= kMaxSmem;
 }
 
 tls_status plan_select(const tls_config* c, tls::SelectParams& p) {
@@ -322,9 +320,9 @@ tls_status chain_workspace(const tls_config* cfg, int do_attend, size_t* bytes) 
 }
 
 tls_status step_workspace(const tls_config* cfg, int do_attend, size_t* bytes) {
-  tls::StepKParams sk;
-  if (step_plan(cfg, sk)) {  // the fused step keeps every intermediate in shared memory
-    *bytes = 256;
+  tls::PStepParams sk;
+  if (pstep_plan(cfg, do_attend, sk)) {
+    *bytes = tls::pstep_workspace(sk, nullptr);
     return TLS_OK;
   }
   const int ns = n_split(cfg);
@@ -538,9 +536,12 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
   const StepPtrs all = {q, k_cache, v_cache, seq_lens, *idx, guide, block_ids, token_ids, num_tokens,
                         token_scores, out, lse, slot_of_block, kv_rows > 0 ? kv_rows : cfg->max_seq_len};
   if (g_timer.on && g_timer.used % kMarks != 0) g_timer.used -= g_timer.used % kMarks;  // drop a partial record
-  tls::StepKParams sk;
-  if (step_plan(cfg, sk)) {  // one launch: a1-a5 (a1-a4 for tls_select) of every pair, one cluster per pair
-    sk.attend = do_attend;
+  tls::PStepParams sk;
+  if (pstep_plan(cfg, do_attend, sk)) {  // one launch: every stage of every pair from the ticket queue
+    tls::pstep_workspace(sk, static_cast<char*>(workspace));
+    unsigned epoch = g_epoch.fetch_add(1u);
+    if (epoch == 0u) epoch = g_epoch.fetch_add(1u);
+    sk.epoch = epoch;
     sk.q = q;
     sk.seq_lens = seq_lens;
     sk.block_minmax = idx->block_minmax;
@@ -558,9 +559,14 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
     sk.token_scores = token_scores;
     sk.out = out;
     sk.lse = lse;
+    sk.dbg = env_debug_buf();
+    const int occ = tls::pstep_occupancy(sk.smem_bytes);
+    if (occ < 1) return fail(TLS_ERR_UNSUPPORTED, "persistent step kernel does not fit on an SM");
+    int grid = num_sms() * occ;
+    if (grid > sk.total) grid = sk.total;
     g_timer.mark(st);
-    cudaError_t e = tls::launch_step(sk, st);
-    if (e != cudaSuccess) return cuda_fail(e, "step_kernel launch");
+    cudaError_t e = tls::launch_pstep(sk, grid, st);
+    if (e != cudaSuccess) return cuda_fail(e, "pstep_kernel launch");
     for (int k = 1; k < kMarks; ++k) g_timer.mark(st);  // one launch: slot 0 holds the whole step
     return TLS_OK;
   }
@@ -778,8 +784,8 @@ tls_status tls_workspace_init(const tls_config* cfg, int32_t which, void* worksp
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(workspace, 0, need, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
-  tls::StepKParams sk;
-  if (which == 1 || step_plan(cfg, sk)) return TLS_OK;
+  tls::PStepParams sk;
+  if (which == 1 || pstep_plan(cfg, which == 2, sk)) return TLS_OK;  // counters start at 0
   // every chain's block-score buffer starts as the completion sentinel (fused.cu kScoreSentinel)
   char* ws = static_cast<char*>(workspace);
   const int ns = n_split(cfg);
@@ -918,8 +924,8 @@ tls_status tls_block_cache_rows(const tls_config* cfg, const int32_t* token_ids,
 
 int32_t tls_launch_count(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK) return -1;
-  tls::StepKParams sk;
-  if ((which == 0 || which == 2) && step_plan(cfg, sk)) return 1;  // step_kernel
+  tls::PStepParams sk;
+  if ((which == 0 || which == 2) && pstep_plan(cfg, which == 2, sk)) return 1;  // pstep_kernel
   const int mode = fused_mode(cfg), ns = n_split(cfg);
   switch (which) {
     case 0: return ns * (mode == 2 ? 1 : 4);  // qq, select, token and attend (selection prologue only) kernels
@@ -933,15 +939,15 @@ int32_t tls_launch_count(const tls_config* cfg, int32_t which) {
 
 int32_t tls_select_mode(const tls_config* cfg) {
   if (check_config(cfg) != TLS_OK) return -1;
-  tls::StepKParams sk;
-  if (step_plan(cfg, sk)) return 3;  // the fused step kernel
+  tls::PStepParams sk;
+  if (pstep_plan(cfg, 1, sk)) return 3;  // the persistent step kernel
   return fused_mode(cfg);
 }
 
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which) {
   if (check_config(cfg) != TLS_OK || which < 0 || which > 2) return -1;
-  tls::StepKParams sk;
-  if (which != 1 && step_plan(cfg, sk)) return sk.nc;
+  tls::PStepParams sk;
+  if (which != 1 && pstep_plan(cfg, 1, sk)) return sk.ns;  // attention slices per pair
   tls::AttendParams ap;
   return plan_attend(cfg, ap, which != 1, which != 0) == TLS_OK ? ap.cs : -1;
 }

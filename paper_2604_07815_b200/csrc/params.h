@@ -116,14 +116,18 @@ struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally wit
   unsigned off_sel, off_cblk, off_union, off_skeys, off_fk, off_slist, off_akv, off_aq, off_as, smem_bytes;
 };
 
-// Fused decode step (step.cu): a1-a5 of one pair in one thread-block cluster.
-struct StepKParams {
+// Persistent decode step (pstep.cu): one kernel, resident CTAs claim work items (TILE a1(+a2), TOKEN a3,
+// SEL a4, ATT a5) from a ticket counter in schedule-row order.
+struct PStepParams {
   Dims d;
-  int nc;       // CTAs per pair (cluster size)
-  int mb;       // a1 block rows per CTA (multiple of 8)
-  int cb;       // a3 candidate blocks per CTA
-  int tok_max;  // a5 selected tokens per CTA, max
-  int attend;   // 0: selection only (tls_select)
+  int pairs, kb_eff;
+  int tb, ntile;     // TILE: block rows per item, items per pair
+  int cb, nch;       // TOKEN: candidate blocks per item, items per pair
+  int ns;            // ATT: items (slices of S_t) per pair
+  int L1, L2, L3;    // schedule lags (rows) of TOKEN, SEL, ATT behind TILE
+  int total;         // tickets
+  int attend;        // 0: tls_select (no ATT items)
+  unsigned epoch;    // this call's hand-off value (host call counter)
   const void* q;
   const int* seq_lens;
   const void* block_minmax;
@@ -141,8 +145,21 @@ struct StepKParams {
   float* token_scores;
   void* out;
   float* lse;
-  // dynamic shared-memory plan
-  unsigned off_u, off_keys, off_hist, off_cand, off_sel, off_qq, off_qb, off_xs, off_part, smem_bytes;
+  // workspace (zeroed once by tls_workspace_init; every call leaves it so)
+  unsigned* sched;   // [0] ticket counter, [1] CTAs finished
+  unsigned* ctr;     // [pairs][8] per-pair counters and flags
+  float* scores;     // [pairs][Ms] a1 block scores
+  uint32_t* keys;    // [pairs][kb_eff * B] a3 ranking keys
+  uint32_t* khist;   // [pairs][kKeyBins] histogram of the keys
+  float* stats;      // [pairs][nch][8][2] a3 chunk softmax statistics
+  float* part_o;     // [pairs][ns][8][128] a5 partial outputs
+  float* part_ml;    // [pairs][ns][8][2] a5 partial (max, sum)
+  unsigned long long* dbg;  // diagnostics only (env TLS_DEBUG_BUF): per ticket (start, end, smid|role|sub)
+  unsigned off_tile, off_qq, off_bkeys, off_scratch, off_fk;            // TILE
+  unsigned off_stage, off_qb, off_cblk, off_lhist;                      // TOKEN
+  unsigned off_skeys, off_sscratch, off_shist, off_sfk, off_slist, off_scblk;  // SEL
+  unsigned off_kv, off_pbuf, off_sel;                                   // ATT
+  unsigned smem_bytes;
 };
 
 // GPU token cache of the offload engine (offload.cu): make S_t resident.

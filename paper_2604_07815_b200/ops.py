@@ -312,11 +312,12 @@ def cluster_size(cfg: TLSConfig, which: int = 2) -> int:
 
 # timing slots of the kernel chain (select mode 1) and of the fused step (mode 3, one launch)
 KERNELS = ("select_kernel", "token_cluster_kernel", "attend_kernel")
-STEP_KERNELS = ("step_kernel",)
+STEP_KERNELS = ("pstep_kernel",)
 
 
 def select_mode(cfg: TLSConfig) -> int:
-    """3: the fused step kernel (a1-a5 of a pair in one thread-block cluster, one launch); 1: the kernel chain
+    """3: the persistent step kernel (one launch; work items of every stage of every pair claimed from a ticket
+    queue, pstep.cu); 1: the kernel chain
     (select_kernel a1-a2, token kernel a3, the attention kernel's prologue a4 + a5)."""
     cc = cfg.c()
     return int(_lib.load().tls_select_mode(ctypes.byref(cc)))

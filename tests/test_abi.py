@@ -97,13 +97,13 @@ def test_null_and_misaligned_pointers(lib):
 
 
 def test_workspace_and_plan(lib):
-    # bf16 GQA, d 128, G <= 8, d_c 32, B 64: the fused step kernel (one launch, no workspace state)
+    # bf16 GQA, d 128, G <= 8, d_c 32, B 64: the persistent step kernel (one launch)
     c = cfg()
     assert lib.tls_select_mode(ctypes.byref(c)) == 3
     assert lib.tls_launch_count(ctypes.byref(c), 2) == 1
     assert lib.tls_launch_count(ctypes.byref(c), 0) == 1
-    assert lib.tls_workspace_bytes(ctypes.byref(c), 2) == 256
-    assert lib.tls_cluster_size(ctypes.byref(c), 2) in (8, 16)
+    assert lib.tls_workspace_bytes(ctypes.byref(c), 2) >= lib.tls_workspace_bytes(ctypes.byref(c), 0) > 0
+    assert lib.tls_cluster_size(ctypes.byref(c), 2) == 1  # 256 selected tokens: one attention slice
     # every other configuration runs the kernel chain
     c = cfg(dtype=_lib.TLS_FP32)
     assert lib.tls_workspace_bytes(ctypes.byref(c), 2) >= 2 * 2 * 64 * 4
@@ -116,7 +116,7 @@ def test_workspace_and_plan(lib):
     assert cs in (1, 2, 4, 8, 16)
     # headline shapes plan without error
     c3 = cfg(batch=32, num_q_heads=64, num_kv_heads=8, max_seq_len=98304, top_blocks=128, top_tokens=1024)
-    assert lib.tls_cluster_size(ctypes.byref(c3), 2) == 8 and lib.tls_select_mode(ctypes.byref(c3)) == 3
+    assert lib.tls_cluster_size(ctypes.byref(c3), 2) == 4 and lib.tls_select_mode(ctypes.byref(c3)) == 3
     c2 = cfg(batch=16, num_q_heads=32, num_kv_heads=8, max_seq_len=49152, top_blocks=128, top_tokens=1024)
     assert lib.tls_select_mode(ctypes.byref(c2)) == 3
     c4 = cfg(batch=32, num_q_heads=32, num_kv_heads=1, d_k=576, d_v=512, max_seq_len=65536, d_c=128,

@@ -253,8 +253,14 @@ def test_separate_calls_equal_fused(name):
     torch.cuda.synchronize()
     assert torch.equal(bids, fused[2]) and torch.equal(tids, fused[3]) and torch.equal(ntok, fused[4])
     assert torch.equal(tsc, fused[5])
-    torch.testing.assert_close(out.float(), fused[0].float(), rtol=0, atol=1e-6)
-    torch.testing.assert_close(lse, fused[1], rtol=0, atol=1e-6)
+    if tls.select_mode(cfg) == 3:
+        # the fused step attends in its own kernel (nc-way split, DSMEM merge), tls_sparse_attend in the
+        # attention kernel (its own split): the same sum in a different order
+        torch.testing.assert_close(out.float(), fused[0].float(), rtol=0, atol=2e-2)
+        torch.testing.assert_close(lse, fused[1], rtol=0, atol=1e-4)
+    else:
+        torch.testing.assert_close(out.float(), fused[0].float(), rtol=0, atol=1e-6)
+        torch.testing.assert_close(lse, fused[1], rtol=0, atol=1e-6)
 
 
 def test_edge_single_token_and_k1():

@@ -1,0 +1,58 @@
+"""Diagnostic: per-item timeline of the persistent step kernel (pstep.cu) from
+its %globaltimer stamps (TLS_DEBUG_BUF): for every ticket (start, end, SM,
+role, sub).  Prints per-role item durations and, per role, when the items ran
+(start/end percentiles) plus the busy time per SM.  Not a bench line.
+    python tools/pstep_timeline.py c3 [L1,L2,L3]"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2604_07815_b200 as tls  # noqa: E402
+from paper_2604_07815_b200 import workloads as W  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+if len(sys.argv) > 2:
+    os.environ["TLS_PSTEP"] = sys.argv[2]
+w = W.CONFIGS[name]
+cfg, inputs, idx, queries = bench.build_state(w, 0, torch.device("cuda"), "outlier")
+buf = torch.zeros(3 * 200000, dtype=torch.int64, device="cuda")
+flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+times = []
+for it in range(8):
+    if it == 7:
+        os.environ["TLS_DEBUG_BUF"] = hex(buf.data_ptr())
+    flush_buf.fill_(1)
+    ev[0].record()
+    tls.decode(cfg, queries[it % 8], inputs["k_cache"], inputs["v_cache"], inputs["seq_lens"], idx)
+    ev[1].record()
+    torch.cuda.synchronize()
+    times.append(ev[0].elapsed_time(ev[1]) * 1e3)
+os.environ.pop("TLS_DEBUG_BUF", None)
+raw = buf.view(-1, 3).cpu().numpy()
+raw = raw[raw[:, 1] > 0]
+t0 = raw[:, 0].min()
+st = (raw[:, 0] - t0) / 1e3
+en = (raw[:, 1] - t0) / 1e3
+role = (raw[:, 2] >> 24) & 0xff
+sm = raw[:, 2] >> 32
+print(f"{w.name}: step us (no stamps) {np.median(times[:7]):.1f}, with stamps {times[7]:.1f}; tickets {len(raw)}")
+names = ["TILE", "TOKEN", "SEL", "ATT"]
+pct = (0, 10, 50, 90, 100)
+for r, nm in enumerate(names):
+    sel = role == r
+    if not sel.any():
+        continue
+    dur = en[sel] - st[sel]
+    print(f"  {nm:6s} n={sel.sum():5d} dur us " + " ".join(f"{np.percentile(dur, p):6.1f}" for p in pct) +
+          " | start " + " ".join(f"{np.percentile(st[sel], p):6.1f}" for p in pct) +
+          " | end " + " ".join(f"{np.percentile(en[sel], p):6.1f}" for p in pct) +
+          f" | CTA-us {dur.sum():8.0f}")
+busy = np.zeros(int(sm.max()) + 1)
+for s_, a, b in zip(sm, st, en):
+    busy[s_] += b - a
+print(f"  end {en.max():.1f} us; busy CTA-us per SM: median {np.median(busy):.0f}, max {busy.max():.0f}")
