@@ -148,7 +148,7 @@ int env_cluster() {
 bool pstep_plan(const tls_config* c, int do_attend, tls::PStepParams& sp) {
   memset(&sp, 0, sizeof(sp));
   sp.d = dims_of(c);
-  if (!tls::pstep_supported(sp.d)) return false;
+  if (!tls::pstep_supported(sp.d) || getenv("TLS_NO_PSTEP")) return false;
   sp.attend = do_attend;
   const char* e = getenv("TLS_PSTEP");
   if (e) sscanf(e, "%d,%d,%d", &sp.L1, &sp.L2, &sp.L3);

@@ -86,18 +86,27 @@ __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
   return old;
 }
 
-// thread 0 spins (acquire) until *p >= v, then orders the async proxy after it
-__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned v) {
+// thread 0 spins until *p >= v (relaxed loads: an acquire load per spin would invalidate the SM's L1 each
+// time), then acquires and orders the async proxy after it.  A hand-off that never comes traps after
+// ~seconds; with the diagnostics buffer set (TLS_DEBUG_BUF, host-mapped memory works), a wait still pending
+// after ~2^18 spins is reported once at dbg[1 << 20 ..] (tag, observed << 32 | wanted) and keeps waiting.
+__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned v, unsigned long long* dbg = nullptr,
+                                         unsigned long long tag = 0) {
   unsigned spins = 0;
-  while (ld_acquire_gpu(p) < v) {
+  while (ld_relaxed_gpu(p) < v) {
     __nanosleep(64);
-    if (++spins > (1u << 26)) __trap();
+    if (++spins == (1u << 18) && dbg) {
+      const unsigned long long slot = atomicAdd(dbg + (1 << 20), 1ull);
+      if (slot < 4096) {
+        dbg[(1 << 20) + 1 + 2 * slot] = tag;
+        dbg[(1 << 20) + 2 + 2 * slot] = ((unsigned long long)ld_relaxed_gpu(p) << 32) | v;
+        __threadfence_system();
+      }
+    }
+    if (spins > (1u << 26)) __trap();
   }
+  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
-  asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
 struct ItemCtl {
@@ -160,28 +169,24 @@ __device__ __forceinline__ void decode_ticket(const PStepParams& p, int t, int& 
 // TILE: a1 over rows [i0, i0 + nb) of the pair's block summaries; the pair's
 // last finishing tile runs a2
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void run_tile(const PStepParams& p, int pair, int tile, uint8_t* smem, uint64_t* bars,
-                                      ItemCtl& ctl) {
+__device__ __noinline__ unsigned run_tile(const PStepParams& p, int pair, int tile, uint8_t* smem, uint64_t* bars,
+                                          unsigned bph, ItemCtl& ctl, unsigned long long* mark) {
   const Dims& d = p.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = pair / d.Hkv, g = pair - b * d.Hkv;
   const int n = min(max(__ldg(p.seq_lens + b), 0), d.S);
   const int m = (n + d.B - 1) >> d.log2B;  // reading U1
   const int ntiles = max(1, (m + p.tb - 1) / p.tb);
-  if (tile >= ntiles) return;  // past this pair's sequence: no work, not counted
+  if (tile >= ntiles) return 0u;  // past this pair's sequence: no work, not counted
   const int i0 = tile * p.tb;
   const int nb = max(0, min(p.tb, m - i0));
   const int ngrp = (nb + 7) >> 3;
   uint8_t* buf = smem + p.off_tile;
   float* QQ = reinterpret_cast<float*>(smem + p.off_qq);
   const uint8_t* src = reinterpret_cast<const uint8_t*>(p.block_minmax) + ((size_t)pair * d.M + i0) * kRowBytes;
+  const unsigned used = (1u << ngrp) - 1u;  // barriers this item completes once each
   if (tid == 0) {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes of earlier items first
-    for (int s = 0; s < ngrp; ++s) {
-      mbar_inval(&bars[s]);
-      mbar_init(&bars[s], 1);
-    }
-    mbar_fence_init();
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic accesses of earlier items first
     for (int s = 0; s < ngrp; ++s) {
       const int rows = min(8, nb - 8 * s);
       mbar_arrive_expect_tx(&bars[s], (uint32_t)(rows * kRowBytes));
@@ -201,13 +206,14 @@ __device__ __noinline__ void run_tile(const PStepParams& p, int pair, int tile, 
     QQ[kD + tid] = qn;
   }
   __syncthreads();
+  if (mark && tid == 0) *mark = 1;
   float* out = p.scores + (size_t)pair * d.Ms + i0;
   if (warp < ngrp) {
     float qreg[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) qreg[e] = QQ[lane * 8 + e];
     for (int gq = warp; gq < ngrp; gq += kWarps) {
-      mbar_wait(&bars[gq], 0);
+      mbar_wait(&bars[gq], (bph >> gq) & 1u);
       const int r8 = gq * 8;
       float acc[8];
 #pragma unroll
@@ -248,10 +254,11 @@ __device__ __noinline__ void run_tile(const PStepParams& p, int pair, int tile, 
     }
   }
   __syncthreads();  // this tile's scores stored
+  if (mark && tid == 0) *mark = 2;
   unsigned* ctr = p.ctr + (size_t)pair * 8;
   if (tid == 0) ctl.last = atom_add_acq_rel(ctr + kCtrTile, 1u) == (unsigned)(ntiles - 1);
   __syncthreads();
-  if (!ctl.last) return;
+  if (!ctl.last) return used;
   // ===== a2 (the pair's last finishing tile): M_t = top-k_b blocks, ties -> lower block id (U2) =====
   if (tid == 0) ctr[kCtrTile] = 0u;  // reset for the next call
   uint32_t* bkeys = reinterpret_cast<uint32_t*>(smem + p.off_bkeys);
@@ -260,6 +267,7 @@ __device__ __noinline__ void run_tile(const PStepParams& p, int pair, int tile, 
   const float* sc = p.scores + (size_t)pair * d.Ms;
   for (int i = tid; i < m; i += kThreads) bkeys[i] = f2key(__ldcg(sc + i));  // L2: the other tiles' stores
   __syncthreads();
+  if (mark && tid == 0) *mark = 3;
   const int K = min(d.Kb, m);
   int* bout = p.block_ids + (size_t)pair * d.Kb;
   bool done = false;
@@ -270,16 +278,18 @@ __device__ __noinline__ void run_tile(const PStepParams& p, int pair, int tile, 
     const TopK t = fast_topk(bkeys, m, K, d.Kb >= m, fk, ctl.tk, nullptr);
     topk_emit(bkeys, m, t, ctl.tk, [&](int i, int pos) { bout[pos] = i; });
   }
+  if (mark && tid == 0) *mark = 4;
   for (int q = K + tid; q < d.Kb; q += kThreads) bout[q] = -1;
   __syncthreads();
   if (tid == 0) st_release_gpu(ctr + kFlagBlocks, p.epoch);  // cumulative over the CTA barrier
+  return used;
 }
 
 // ---------------------------------------------------------------------------
 // TOKEN: a3 over candidate blocks [c cb, (c+1) cb) of the pair
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void run_token(const PStepParams& p, int pair, int chunk, uint8_t* smem, uint64_t* bars,
-                                       ItemCtl& ctl) {
+__device__ __noinline__ unsigned run_token(const PStepParams& p, int pair, int chunk, uint8_t* smem, uint64_t* bars,
+                                           unsigned bph, ItemCtl& ctl) {
   const Dims& d = p.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q4 = lane & 3, r0 = lane >> 2;
   const int b = pair / d.Hkv, g = pair - b * d.Hkv;
@@ -320,10 +330,7 @@ __device__ __noinline__ void run_token(const PStepParams& p, int pair, int chunk
   }
   if (tid == 0) {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    mbar_inval(&bars[0]);
-    mbar_init(&bars[0], 1);
-    mbar_fence_init();
-    wait_geq(ctr + kFlagBlocks, p.epoch);  // M_t of this pair (a2) published
+    wait_geq(ctr + kFlagBlocks, p.epoch, p.dbg, ((unsigned long long)pair << 32) | (1u << 16) | chunk);  // M_t (a2)
   }
   __syncthreads();
   // ---- this chunk's candidate blocks: M_t (ascending, -1 padded) or the lag-mode guide's valid ids ----
@@ -372,7 +379,7 @@ __device__ __noinline__ void run_token(const PStepParams& p, int pair, int chunk
       tma_bulk_g2s(stz + k * d.B, zbase + (size_t)blk * d.B, rows * 8, &bars[0]);
     }
   }
-  if (nbl > 0) mbar_wait(&bars[0], 0);
+  if (nbl > 0) mbar_wait(&bars[0], bph & 1u);
   const float sm2 = d.sm_scale * kLog2e;
   float sq[2];
 #pragma unroll
@@ -436,7 +443,7 @@ __device__ __noinline__ void run_token(const PStepParams& p, int pair, int chunk
   __syncthreads();
   if (tid == 0) {
     atom_add_acq_rel(ctr + kCtrStats, 1u);
-    wait_geq(ctr + kCtrStats, (unsigned)p.nch);  // every chunk of the pair published its statistics
+    wait_geq(ctr + kCtrStats, (unsigned)p.nch, p.dbg, ((unsigned long long)pair << 32) | (2u << 16) | chunk);  // all chunks' stats
   }
   __syncthreads();
   if (tid < 8) {  // lz_h = M_h + log2 Z_h over the nch chunks (chunk order: deterministic)
@@ -486,12 +493,14 @@ __device__ __noinline__ void run_token(const PStepParams& p, int pair, int chunk
     if (lhist[i]) atomicAdd(&gh[i], lhist[i]);
   __syncthreads();
   if (tid == 0) red_release_add_gpu(ctr + kCtrDone, 1u);  // keys + histogram counts of this chunk visible
+  return nbl > 0 ? 1u : 0u;
 }
 
 // ---------------------------------------------------------------------------
 // SEL: a4 over the pair's ranking keys
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void run_sel(const PStepParams& p, int pair, uint8_t* smem, uint64_t* bars, ItemCtl& ctl) {
+__device__ __noinline__ unsigned run_sel(const PStepParams& p, int pair, uint8_t* smem, uint64_t* bars, unsigned bph,
+                                         ItemCtl& ctl) {
   const Dims& d = p.d;
   const int tid = threadIdx.x;
   const int b = pair / d.Hkv;
@@ -507,16 +516,14 @@ __device__ __noinline__ void run_sel(const PStepParams& p, int pair, uint8_t* sm
   const uint32_t kbytes = (uint32_t)(p.kb_eff * d.B * 4);
   if (tid == 0) {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    mbar_inval(&bars[0]);
-    mbar_init(&bars[0], 1);
-    mbar_fence_init();
-    wait_geq(ctr + kCtrDone, (unsigned)p.nch);  // every chunk's keys and histogram counts
+    wait_geq(ctr + kCtrDone, (unsigned)p.nch, p.dbg, ((unsigned long long)pair << 32) | (3u << 16));  // every chunk's keys
     ctr[kCtrDone] = 0u;                          // reset for the next call (no other reader left)
     ctr[kCtrStats] = 0u;
     mbar_arrive_expect_tx(&bars[0], kbytes + kKeyBins * 4);
     tma_bulk_g2s(shist, p.khist + (size_t)pair * kKeyBins, kKeyBins * 4, &bars[0]);
     tma_bulk_g2s(skeys, p.keys + (size_t)pair * p.kb_eff * d.B, kbytes, &bars[0]);
   }
+  __syncthreads();  // the hand-off observed by thread 0 (and through it M_t) before anyone reads block_ids
   // candidate blocks in the order the TOKEN items used
   const int* cand = p.guide ? p.guide + (size_t)pair * d.Kb : p.block_ids + (size_t)pair * d.Kb;
   {
@@ -537,7 +544,7 @@ __device__ __noinline__ void run_sel(const PStepParams& p, int pair, uint8_t* sm
   }
   __syncthreads();
   const int nslots = ctl.kc << d.log2B;
-  mbar_wait(&bars[0], 0);
+  mbar_wait(&bars[0], bph & 1u);
   // the histogram is in shared memory now: zero the pair's global one for the next call
   for (int i = tid; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
   __shared__ HistSel hs;
@@ -564,6 +571,7 @@ __device__ __noinline__ void run_sel(const PStepParams& p, int pair, uint8_t* sm
   if (tid == 0) p.num_tokens[pair] = K;
   __syncthreads();
   if (tid == 0) st_release_gpu(ctr + kFlagTokens, p.epoch);  // S_t published (cumulative over the barrier)
+  return 1u;
 }
 
 // ---------------------------------------------------------------------------
@@ -577,7 +585,7 @@ __device__ __noinline__ void run_att(const PStepParams& p, int pair, int slice, 
   const int G = d.G;
   unsigned* ctr = p.ctr + (size_t)pair * 8;
   int* sel = reinterpret_cast<int*>(smem + p.off_sel);
-  if (tid == 0) wait_geq(ctr + kFlagTokens, p.epoch);  // (epochs only grow)
+  if (tid == 0) wait_geq(ctr + kFlagTokens, p.epoch, p.dbg, ((unsigned long long)pair << 32) | (4u << 16) | slice);
   __syncthreads();
   const int K = __ldcg(p.num_tokens + pair);
   const int t0 = (int)(((long long)K * slice) / p.ns);
@@ -807,10 +815,12 @@ __global__ void __launch_bounds__(kThreads, 3) pstep_kernel(const __grid_constan
   __shared__ __align__(8) uint64_t bars[8];
   __shared__ ItemCtl ctl;
   __shared__ int s_ticket;
+  __shared__ unsigned s_bph;  // parity of the current phase of each mbarrier (initialised once, never re-initialised)
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int s = 0; s < 8; ++s) mbar_init(&bars[s], 1);
     mbar_fence_init();
+    s_bph = 0u;
   }
   for (;;) {
     if (tid == 0) s_ticket = (int)atomicAdd(p.sched, 1u);
@@ -821,11 +831,21 @@ __global__ void __launch_bounds__(kThreads, 3) pstep_kernel(const __grid_constan
     int role, pair, sub;
     decode_ticket(p, t, role, pair, sub);
     unsigned long long t_start = p.dbg ? gtimer() : 0ull;
-    if (role == kTile) run_tile(p, pair, sub, smem, bars, ctl);
-    else if (role == kToken) run_token(p, pair, sub, smem, bars, ctl);
-    else if (role == kSel) run_sel(p, pair, smem, bars, ctl);
+    if (p.dbg && tid == 0) {
+      unsigned smid;
+      asm("mov.u32 %0, %%smid;" : "=r"(smid));
+      p.dbg[3 * (size_t)t] = t_start;
+      p.dbg[3 * (size_t)t + 2] = ((unsigned long long)smid << 32) | (unsigned)(role << 24 | sub) | (1ull << 31) |
+                                 ((unsigned long long)(pair & 0x7f) << 16);
+    }
+    const unsigned bph = s_bph;
+    unsigned used = 0u;  // mbarriers whose phase this item completed
+    if (role == kTile) used = run_tile(p, pair, sub, smem, bars, bph, ctl, p.dbg ? p.dbg + 3 * (size_t)t + 1 : nullptr);
+    else if (role == kToken) used = run_token(p, pair, sub, smem, bars, bph, ctl);
+    else if (role == kSel) used = run_sel(p, pair, smem, bars, bph, ctl);
     else run_att(p, pair, sub, smem, ctl);
-    __syncthreads();  // shared memory free for the next item
+    __syncthreads();  // shared memory free for the next item; every thread read s_bph
+    if (tid == 0) s_bph = bph ^ used;
     if (p.dbg && tid == 0) {  // diagnostics: per ticket (start, end, smid)
       unsigned smid;
       asm("mov.u32 %0, %%smid;" : "=r"(smid));

@@ -18,13 +18,17 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 if len(sys.argv) > 2:
     os.environ["TLS_PSTEP"] = sys.argv[2]
 w = W.CONFIGS[name]
+if len(sys.argv) > 3:
+    w = w.with_(batch=int(sys.argv[3]))
 cfg, inputs, idx, queries = bench.build_state(w, 0, torch.device("cuda"), "outlier")
-buf = torch.zeros(3 * 200000, dtype=torch.int64, device="cuda")
+buf = torch.zeros((1 << 20) + 1 + 8192, dtype=torch.int64, device="cuda")
 flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 times = []
+ALWAYS = os.environ.get("DBG_ALWAYS") == "1"
 for it in range(8):
-    if it == 7:
+    if it == 7 or ALWAYS:
+        buf.zero_()
         os.environ["TLS_DEBUG_BUF"] = hex(buf.data_ptr())
     flush_buf.fill_(1)
     ev[0].record()
@@ -33,7 +37,13 @@ for it in range(8):
     torch.cuda.synchronize()
     times.append(ev[0].elapsed_time(ev[1]) * 1e3)
 os.environ.pop("TLS_DEBUG_BUF", None)
-raw = buf.view(-1, 3).cpu().numpy()
+hung = int(buf[1 << 20].item())
+if hung:
+    info = buf[(1 << 20) + 1:(1 << 20) + 1 + 2 * min(hung, 4096)].view(-1, 2).cpu().numpy()
+    print(f"HUNG WAITS: {hung}")
+    for tag, val in info[:40]:
+        print(f"  pair {tag >> 32} kind {(tag >> 16) & 0xff} sub {tag & 0xffff}: observed {val >> 32} want {val & 0xffffffff}")
+raw = buf[: 3 * ((1 << 20) // 3)].view(-1, 3).cpu().numpy()
 raw = raw[raw[:, 1] > 0]
 t0 = raw[:, 0].min()
 st = (raw[:, 0] - t0) / 1e3
