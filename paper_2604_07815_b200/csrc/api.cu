@@ -148,10 +148,10 @@ int env_cluster() {
 bool pstep_plan(const tls_config* c, int do_attend, tls::PStepParams& sp) {
   memset(&sp, 0, sizeof(sp));
   sp.d = dims_of(c);
-  if (!tls::pstep_supported(sp.d) || getenv("TLS_NO_PSTEP")) return false;
+  const char* e = getenv("TLS_PSTEP");  // opt-in while it is slower than the chain
+  if (!tls::pstep_supported(sp.d) || e == nullptr) return false;
   sp.attend = do_attend;
-  const char* e = getenv("TLS_PSTEP");
-  if (e) sscanf(e, "%d,%d,%d", &sp.L1, &sp.L2, &sp.L3);
+  sscanf(e, "%d,%d,%d", &sp.L1, &sp.L2, &sp.L3);
   const int env = env_cluster();
   if (env > 16) return false;
   return tls::plan_pstep(sp, env) && (int)sp.smem_bytes <= kMaxSmem;

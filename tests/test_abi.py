@@ -96,14 +96,17 @@ def test_null_and_misaligned_pointers(lib):
     assert lib.tls_calibrate_channels(ctypes.byref(c), 16, 0, 16, 4, 0, 16, None, None) == _lib.TLS_ERR_INPUT
 
 
-def test_workspace_and_plan(lib):
-    # bf16 GQA, d 128, G <= 8, d_c 32, B 64: the persistent step kernel (one launch)
+def test_workspace_and_plan(lib, monkeypatch):
+    # bf16 GQA, d 128, G <= 8, d_c 32, B 64: the persistent step kernel (one launch) when opted in
     c = cfg()
+    monkeypatch.setenv("TLS_PSTEP", "0")
     assert lib.tls_select_mode(ctypes.byref(c)) == 3
     assert lib.tls_launch_count(ctypes.byref(c), 2) == 1
     assert lib.tls_launch_count(ctypes.byref(c), 0) == 1
     assert lib.tls_workspace_bytes(ctypes.byref(c), 2) >= lib.tls_workspace_bytes(ctypes.byref(c), 0) > 0
     assert lib.tls_cluster_size(ctypes.byref(c), 2) == 1  # 256 selected tokens: one attention slice
+    monkeypatch.delenv("TLS_PSTEP")
+    assert lib.tls_select_mode(ctypes.byref(c)) == 1
     # every other configuration runs the kernel chain
     c = cfg(dtype=_lib.TLS_FP32)
     assert lib.tls_workspace_bytes(ctypes.byref(c), 2) >= 2 * 2 * 64 * 4
@@ -116,9 +119,9 @@ def test_workspace_and_plan(lib):
     assert cs in (1, 2, 4, 8, 16)
     # headline shapes plan without error
     c3 = cfg(batch=32, num_q_heads=64, num_kv_heads=8, max_seq_len=98304, top_blocks=128, top_tokens=1024)
-    assert lib.tls_cluster_size(ctypes.byref(c3), 2) == 4 and lib.tls_select_mode(ctypes.byref(c3)) == 3
+    assert lib.tls_cluster_size(ctypes.byref(c3), 2) == 1 and lib.tls_select_mode(ctypes.byref(c3)) == 1
     c2 = cfg(batch=16, num_q_heads=32, num_kv_heads=8, max_seq_len=49152, top_blocks=128, top_tokens=1024)
-    assert lib.tls_select_mode(ctypes.byref(c2)) == 3
+    assert lib.tls_select_mode(ctypes.byref(c2)) == 1
     c4 = cfg(batch=32, num_q_heads=32, num_kv_heads=1, d_k=576, d_v=512, max_seq_len=65536, d_c=128,
              top_blocks=128, top_tokens=1024, layout=_lib.TLS_MLA)
     assert lib.tls_cluster_size(ctypes.byref(c4), 2) > 0
