@@ -38,7 +38,12 @@ def parse():
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--pattern", default="outlier", choices=["uniform", "outlier", "peaked"])
     ap.add_argument("--impl", default="tls", choices=["tls", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default, BASELINE.json configs[2]): the fixed problem sharded by KV head (GQA) "
+                         "or batch (MLA) over the ranks; weak: every rank a full copy")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="start the ranks, plan the shards, all_gather the plan, print one JSON line; no timing "
+                         "(runs on CPU with gloo: checks the launcher)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     return ap.parse_args()
@@ -184,8 +189,43 @@ def time_steps(fn, steps, warmup, flush, stream, on_timed_start=None):
     return [s.elapsed_time(e) for s, e in zip(starts, ends)]
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+_POOL_PAIRS: dict = {}
+
+
+def _pool_pair(key):
+    """One sampled pair in a forked worker (1 BLAS thread): the oracle's decode step O3-O11, timed."""
+    from oracle import tls_oracle as O
+
+    try:
+        from threadpoolctl import threadpool_limits
+        ctx = threadpool_limits(1)
+    except Exception:  # pragma: no cover
+        ctx = None
+    qg, keys, values, ch, index, prm = _POOL_PAIRS[key]
+    t0 = time.perf_counter()
+    O.tls_pair(qg, keys, values, ch, prm, index=index)
+    return time.perf_counter() - t0
+
+
 def cpu_baseline(w, inputs, idx_channels, budget_s, label):
-    """The fp64 oracle as it stands, timed on this host on a bounded sample of pairs."""
+    """The fp64 oracle as it stands (never tuned), timed on this host on a bounded sample of pairs:
+    (i) one process, 1 BLAS thread; (ii) a multiprocessing.Pool over every core this process may use,
+    each worker 1 BLAS thread, the sampled pairs spread over the workers (value = workers / mean per-pair
+    time under that concurrent load).  The prefill index build (O2, O5) is not part of a decode step and is
+    not timed."""
+    import multiprocessing as mp
+
     import numpy as np
 
     from oracle import tls_oracle as O
@@ -199,36 +239,62 @@ def cpu_baseline(w, inputs, idx_channels, budget_s, label):
     pairs = [(b, g) for b in range(w.batch) for g in range(w.num_kv_heads)]
     rng = np.random.default_rng(0)
     rng.shuffle(pairs)
+    cores = len(os.sched_getaffinity(0))
+
+    def pair_data(b, g):
+        n = int(inputs["seq_lens"][b])
+        qg = inputs["q"][b, g * G:(g + 1) * G].double().cpu().numpy()
+        if w.layout == "mla":
+            keys = inputs["k_cache"][b, :n].double().cpu().numpy()
+            values = keys[:, : w.d_v]
+        else:
+            keys = inputs["k_cache"][b, g, :n].double().cpu().numpy()
+            values = inputs["v_cache"][b, g, :n].double().cpu().numpy()
+        ch = idx_channels[g].cpu().numpy()
+        return qg, keys, values, ch, O.build_index_pair(keys, ch, w.block_size), prm
+
     done, spent = 0, 0.0
     ctx = threadpool_limits(1) if threadpool_limits else None
     if ctx:
         ctx.__enter__()
     try:
         for b, g in pairs:
-            n = int(inputs["seq_lens"][b])
-            qg = inputs["q"][b, g * G:(g + 1) * G].double().cpu().numpy()
-            if w.layout == "mla":
-                keys = inputs["k_cache"][b, :n].double().cpu().numpy()
-                values = keys[:, : w.d_v]
-            else:
-                keys = inputs["k_cache"][b, g, :n].double().cpu().numpy()
-                values = inputs["v_cache"][b, g, :n].double().cpu().numpy()
-            ch = idx_channels[g].cpu().numpy()
-            index = O.build_index_pair(keys, ch, w.block_size)  # prefill: not part of a decode step
+            qg, keys, values, ch, index, _ = pair_data(b, g)
             t0 = time.perf_counter()
             O.tls_pair(qg, keys, values, ch, prm, index=index)
             spent += time.perf_counter() - t0
             done += 1
-            if spent >= budget_s:
+            if spent >= budget_s or done >= 64:
                 break
     finally:
         if ctx:
             ctx.__exit__(None, None, None)
     per_pair = spent / done
     tokens_per_s = (1.0 / w.num_kv_heads) / per_pair  # a pair is 1/Hkv of one sequence's decode token
-    return {"value": tokens_per_s, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-            "sample": f"{done} of {len(pairs)} (batch, kv-head) pairs of {label}, O6-O11 per pair "
-                      f"({per_pair * 1e3:.1f} ms/pair, fp64 numpy, 1 BLAS thread), extrapolated to tokens/s"}
+    runs = [{"value": tokens_per_s, "cores": 1, "sample": f"{done} pairs, one process",
+             "ms_per_pair": per_pair * 1e3}]
+    value, used = tokens_per_s, 1
+    if cores > 1:  # (ii) every core: fork workers that inherit the sampled pairs (no pickling of the caches)
+        n_pool = min(len(pairs), 2 * cores, 64)
+        _POOL_PAIRS.clear()
+        for b, g in pairs[:n_pool]:
+            _POOL_PAIRS[(b, g)] = pair_data(b, g)
+        try:
+            with mp.get_context("fork").Pool(cores) as pool:
+                ts = pool.map(_pool_pair, list(_POOL_PAIRS.keys()), chunksize=1)
+            mean = sum(ts) / len(ts)
+            v = cores * (1.0 / w.num_kv_heads) / mean
+            runs.append({"value": v, "cores": cores, "sample": f"{len(ts)} pairs over a {cores}-process pool",
+                         "ms_per_pair": mean * 1e3})
+            value, used = v, cores
+        except Exception as e:  # pragma: no cover - reported, not fatal
+            runs.append({"error": repr(e)})
+        finally:
+            _POOL_PAIRS.clear()
+    return {"value": value, "unit": "tokens/s", "cores": used, "kind": "oracle", "cpu_model": cpu_model(),
+            "sample": f"(batch, kv-head) pairs of {label}: the oracle's decode step O3-O11 per pair (fp64 numpy, "
+                      f"1 BLAS thread per process; prefill index build untimed), extrapolated to tokens/s",
+            "runs": runs}
 
 
 # ---------------------------------------------------------------------- arms
@@ -294,7 +360,8 @@ def run_reference(args, w, rank, world):
         "config": {"workload": w.name, "step": "one (batch, kv-head) pair per step (bounded sample)",
                    "batch": w.batch, "context": w.context},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{args.steps} pairs of {w.name}, O6-O11 per pair, fp64 numpy, 1 BLAS thread"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{args.steps} pairs of {w.name}, O3-O11 per pair, fp64 numpy, 1 BLAS thread"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -305,9 +372,12 @@ def run_tls(args, w, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    w_full = w
+    plan = None
     if args.scaling == "strong" and world > 1:
-        # shard the fixed problem: KV heads (GQA) or batch (MLA) across ranks
-        from paper_2604_07815_b200.dist import shard_workload
+        # shard the fixed problem: KV heads (GQA) or batch (MLA) across ranks (dist.py; no collective in the step)
+        from paper_2604_07815_b200.dist import shard_plan, shard_workload
+        plan = shard_plan(w.batch, w.num_kv_heads, w.layout, world)
         w = shard_workload(w, rank, world)
     seed = rank if args.scaling == "weak" else 0
     cfg, inputs, idx, queries = build_state(w, seed, dev, args.pattern)
@@ -362,20 +432,36 @@ def run_tls(args, w, rank, world, local_rank):
         lse_host.copy_(lse, non_blocking=True)
 
     e2e_times = time_steps(e2e_step, max(10, args.steps // 4), 3, flush, stream)
+    assembly_us = None
+    if world > 1 and plan is not None:  # NCCL all_gather of the sharded outputs: verification only, timed apart
+        from paper_2604_07815_b200.dist import gather_outputs
+
+        torch.distributed.barrier()
+        ga = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        for _ in range(3):
+            gather_outputs(out, plan["axis"])
+        torch.cuda.synchronize()
+        ga[0].record(stream)
+        for _ in range(20):
+            gather_outputs(out, plan["axis"])
+        ga[1].record(stream)
+        torch.cuda.synchronize()
+        assembly_us = ga[0].elapsed_time(ga[1]) * 1e3 / 20
 
     ms = sum(times) / len(times)
     ms_e2e = sum(e2e_times) / len(e2e_times)
     names = tls.kernel_names(cfg)
     kavg = [kern_ms[k] / max(1, kern_calls) for k in names]
     if world > 1:
-        t = torch.tensor([ms, ms_e2e] + kavg, device=dev)
+        t = torch.tensor([ms, ms_e2e, assembly_us or 0.0] + kavg, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms, ms_e2e = float(t[0]), float(t[1])
-        kavg = [float(x) for x in t[2:]]
+        ms, ms_e2e, assembly_us = float(t[0]), float(t[1]), (float(t[2]) if assembly_us is not None else None)
+        kavg = [float(x) for x in t[3:]]
     if rank != 0:
         return
-    tokens_per_step = w.batch * world  # one decode token per sequence, every rank
-    bytes_step = algorithmic_bytes_per_pair(w) * w.batch * w.num_kv_heads
+    # one decode token per sequence: weak -> every rank its own batch; strong -> the one (sharded) batch
+    tokens_per_step = w.batch * world if args.scaling == "weak" else w_full.batch
+    bytes_step = algorithmic_bytes_per_pair(w) * w.batch * w.num_kv_heads * world  # all ranks' pairs
     peak, peak_src = hbm_peak()
     achieved = bytes_step / (ms * 1e-3) / 1e9
     clk = clocks.summary(t_wall0, t_wall1)
@@ -403,16 +489,21 @@ def run_tls(args, w, rank, world, local_rank):
         "dtype": "bf16" if w.dtype == torch.bfloat16 else "f32",
         "data": "synthetic",
         "config": {
-            "workload": w.name, "batch_per_gpu": w.batch, "global_batch": w.batch * (world if args.scaling == "weak" else 1),
+            "workload": w_full.name, "batch_per_gpu": w.batch, "kv_heads_per_gpu": w.num_kv_heads,
+            "global_batch": w.batch * world if args.scaling == "weak" else w_full.batch,
             "context": w.context, "num_q_heads": w.num_q_heads, "num_kv_heads": w.num_kv_heads, "d_k": w.d_k,
             "d_v": w.d_v, "layout": w.layout, "block_size": w.block_size, "d_c": w.d_c, "K_b": w.top_blocks,
             "K_t": w.top_tokens, "pattern": args.pattern, "cluster_size": tls.cluster_size(cfg, 2),
             "select_mode": mode,
             "l2": "flushed before every timed step (256 MiB write, untimed)",
-            "parallelism": f"{world} rank(s), (batch, kv-head) pairs independent, no collective in the step",
+            "parallelism": (f"{world} rank(s), " + (f"{plan['axis']} shard of the fixed problem" if plan else
+                            "each rank a full copy" if world > 1 else "one GPU") +
+                            "; (batch, kv-head) pairs independent, no collective in the step"),
             "layer": "one attention layer (tokens/s = batch / layer-step time)",
         },
         "us_per_step": ms * 1e3,
+        "per_gpu_us_per_step": ms * 1e3,
+        "assembly_allgather_us": assembly_us,
         "hbm_gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": dom_ach, "peak": peak, "unit": "GB/s", "frac": dom_ach / peak,
                      "traffic": ncu_traffic(w.name, dom), "peak_source": peak_src, "kernel": dom,
@@ -439,10 +530,52 @@ def run_tls(args, w, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args) -> int:
+    """`--gpus N` without a launcher: re-exec this command under torch.distributed.run, one rank per GPU."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+    return subprocess.call(cmd + sys.argv[1:])
+
+
+def dry_run(args, w, rank, world):
+    """Launcher check: every rank plans its shard, the plans are all_gathered, rank 0 prints one line."""
+    import torch.distributed as dist
+
+    from paper_2604_07815_b200.dist import shard_plan, shard_ranges
+
+    mine = [rank, 0, 0, 0, 0]
+    if world > 1 and args.scaling == "strong":
+        bsl, hsl = shard_ranges(w.batch, w.num_kv_heads, w.layout, rank, world)
+        mine = [rank, bsl.start, bsl.stop, hsl.start, hsl.stop]
+    t = torch.tensor(mine)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(parts, t)
+    else:
+        parts = [t]
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "scaling": args.scaling,
+                          "config": {"workload": w.name},
+                          "plan": shard_plan(w.batch, w.num_kv_heads, w.layout, world) if world > 1 else None,
+                          "ranks": [p.tolist() for p in parts]}), flush=True)
+
+
 def main():
     args = parse()
     from paper_2604_07815_b200 import workloads as W
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     w = W.CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -451,10 +584,16 @@ def main():
         run_reference(args, w, rank, world)
         return
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local_rank)
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            torch.distributed.init_process_group("gloo")
     try:
-        run_tls(args, w, rank, world, local_rank)
+        if args.dry_run:
+            dry_run(args, w, rank, world)
+        else:
+            run_tls(args, w, rank, world, local_rank)
     finally:
         if world > 1:
             torch.distributed.destroy_process_group()

@@ -286,6 +286,85 @@ tls_status tls_decode_block_cache(const tls_config* cfg, const void* q, const in
                                   int32_t* token_ids, int32_t* num_tokens, float* token_scores, void* out,
                                   float* lse, void* workspace, size_t workspace_bytes, tls_stream_t stream);
 
+/*
+ * ---- Sequence-split decode: one long sequence whose KV
+ * cache and index are split along the sequence over P ranks (rank r holds the
+ * block-aligned token range [t0_r, t0_r + n_r) of every sequence, its index
+ * built over that range).  The step stays exact: every global decision is
+ * taken from gathered local pieces that contain it (orchestrated, with the
+ * all_gathers, by paper_2604_07815_b200/seqsplit.py):
+ *   1. tls_block_scores on the local range; tls_block_topk -> local top-k_b
+ *      (score, global block id); all_gather; tls_topk_rows -> global M_t
+ *      (the global top-k_b is among the union of local top-k_b);
+ *   2. tls_select_range -> the local blocks of M_t; tls_token_stats -> this
+ *      rank's per-head softmax statistics over its candidates; all_gather;
+ *   3. tls_token_keys (merges the P statistics: alpha~ is a softmax over ALL
+ *      candidates J) -> ln alpha~ + global token id per local
+ *      candidate; tls_topk_rows -> local top-k_t; all_gather; tls_topk_rows ->
+ *      global S_t;
+ *   4. tls_select_range -> the local tokens of S_t; tls_sparse_attend_f32 ->
+ *      partial (out, lse); all_gather; tls_attn_merge (LSE identity) -> out
+ *      (P:142).
+ * All pointers are device memory; calls are asynchronous on `stream`.
+ */
+
+/* Exact top-k of each of `rows` rows of n (key, id) pairs (ids ascending per
+ * row, -1 = empty entry): the k largest keys, equal keys -> lower id (U2).
+ * keys/ids: [rows, n]; out_keys/out_ids: [rows, k] in ascending id order,
+ * padded with -inf / -1; out_count: [rows] (nullable) = min(k, #entries).
+ * TLS_ERR_INPUT for rows < 1, n < 1, k < 1 or a NULL pointer. */
+tls_status tls_topk_rows(int32_t rows, int32_t n, const float* keys, const int32_t* ids, int32_t k,
+                         float* out_keys, int32_t* out_ids, int32_t* out_count, tls_stream_t stream);
+
+/* A rank's local top-k_b with GLOBAL block ids: scores [batch, Hkv,
+ * ceil(max_seq_len / B)] from tls_block_scores on the local range; block i of
+ * pair (b, g) exists iff i < ceil(seq_lens[b] / B).  out_scores / out_block_ids
+ * [batch, Hkv, top_blocks]: the top_blocks largest scores (ties -> lower id),
+ * ids = i + block_offset in ascending order, -inf / -1 padded. */
+tls_status tls_block_topk(const tls_config* cfg, const float* scores, const int32_t* seq_lens, int32_t block_offset,
+                          float* out_scores, int32_t* out_block_ids, tls_stream_t stream);
+
+/* The ids of each row (ascending, -1 padded, k per row) that lie in [lo, hi),
+ * shifted by -lo, compacted in order and -1 padded: out_ids [rows, k];
+ * out_count [rows] (nullable).  TLS_ERR_INPUT for rows/k < 1, lo > hi, NULL. */
+tls_status tls_select_range(int32_t rows, int32_t k, const int32_t* ids, int32_t lo, int32_t hi,
+                            int32_t* out_ids, int32_t* out_count, tls_stream_t stream);
+
+/* This rank's part of a3's softmax normaliser over its candidate
+ * tokens: the tokens of block_ids [batch, Hkv, top_blocks] (local ids,
+ * ascending, -1 padded) below seq_lens[b].  For every pair and head h of the
+ * group, with L_hj = sm_scale log2(e) q~_h . k~_j (log2 units, q~_h = q_h[C]):
+ *   stats [batch, Hkv, G, 2] = (M_h = max_j L_hj, Z_h = sum_j 2^(L_hj - M_h)),
+ * (-inf, 0) when the rank has no candidate.  cfg describes the local range
+ * (max_seq_len = the local cache length).  GQA and MLA, bf16 and fp32. */
+tls_status tls_token_stats(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
+                           const int32_t* block_ids, float* stats, tls_stream_t stream);
+
+/* Ranking keys of this rank's candidates under the GLOBAL normaliser:
+ * stats_parts [n_parts, batch, Hkv, G, 2] are every rank's tls_token_stats
+ * (rank order); lz_h = M_h + log2 Z_h of their LSE merge.  For candidate slot
+ * s = k * B + r (block k of block_ids, row r):
+ *   keys [batch, Hkv, top_blocks * B] = ln alpha~_j = ln((1/G) sum_h 2^(L_hj - lz_h)),
+ *   token_ids (same shape) = j + token_offset (the global token id),
+ * (-inf, -1) for slots past the candidates or the sequence. */
+tls_status tls_token_keys(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
+                          const int32_t* block_ids, int32_t n_parts, const float* stats_parts,
+                          int32_t token_offset, float* keys, int32_t* token_ids, tls_stream_t stream);
+
+/* tls_sparse_attend with an fp32 output [batch, Hq, d_v] whatever the cache
+ * dtype (the partial results of the sequence split: rounded once, by the merge). */
+tls_status tls_sparse_attend_f32(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
+                                 const int32_t* token_ids, const int32_t* num_tokens, float* out, float* lse,
+                                 void* workspace, size_t workspace_bytes, tls_stream_t stream);
+
+/* LSE merge of n_parts partial attention results (split-K identity):
+ * parts_out [n_parts, batch, Hq, d_v] fp32 (tls_sparse_attend_f32), parts_lse [n_parts, batch,
+ * Hq] (natural log, -inf = no token in that part):
+ *   lse = log sum_p exp(lse_p);  out = sum_p exp(lse_p - lse) parts_out_p.
+ * out [batch, Hq, d_v] (cfg dtype); lse [batch, Hq] nullable. */
+tls_status tls_attn_merge(const tls_config* cfg, int32_t n_parts, const float* parts_out, const float* parts_lse,
+                          void* out, float* lse, tls_stream_t stream);
+
 /* Workspace bytes needed by: which = 0 tls_select, 1 tls_sparse_attend,
  * 2 tls_decode.  The select part holds the fp32 block scores of every pair,
  * per-chunk softmax statistics, the ranking key of every candidate token and a

@@ -24,6 +24,13 @@ EXPORTS = (
     "tls_select",
     "tls_sparse_attend",
     "tls_decode",
+    "tls_topk_rows",
+    "tls_block_topk",
+    "tls_select_range",
+    "tls_token_stats",
+    "tls_token_keys",
+    "tls_attn_merge",
+    "tls_sparse_attend_f32",
     "tls_workspace_bytes",
     "tls_launch_count",
     "tls_cluster_size",
@@ -120,6 +127,13 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "tls_calibrate_channels": (_I32, [_PCFG, _P, _I32, _P, _I32, ctypes.c_int64, _P, _P, _P]),
         "tls_build_index": (_I32, [_PCFG, _P, _P, _I32, _PIDX, _P]),
         "tls_block_scores": (_I32, [_PCFG, _P, _P, _P, _P, _P]),
+        "tls_topk_rows": (_I32, [_I32, _I32, _P, _P, _I32, _P, _P, _P, _P]),
+        "tls_block_topk": (_I32, [_PCFG, _P, _P, _I32, _P, _P, _P]),
+        "tls_select_range": (_I32, [_I32, _I32, _P, _I32, _I32, _P, _P, _P]),
+        "tls_token_stats": (_I32, [_PCFG, _P, _P, _PIDX, _P, _P, _P]),
+        "tls_token_keys": (_I32, [_PCFG, _P, _P, _PIDX, _P, _I32, _P, _I32, _P, _P, _P]),
+        "tls_attn_merge": (_I32, [_PCFG, _I32, _P, _P, _P, _P, _P]),
+        "tls_sparse_attend_f32": (_I32, [_PCFG, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_select": (_I32, [_PCFG, _P, _P, _PIDX, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_sparse_attend": (_I32, [_PCFG, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_cache_fetch": (_I32, [_PCFG, _P, _P, _P, _P, ctypes.POINTER(TLSTokenCacheC), _P, _P, _P]),

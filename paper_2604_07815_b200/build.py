@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libtls.so")
-SOURCES = ["api.cu", "fused.cu", "select.cu", "attend.cu", "index.cu", "offload.cu", "pstep.cu"]
+SOURCES = ["api.cu", "fused.cu", "select.cu", "attend.cu", "index.cu", "offload.cu", "pstep.cu", "seqsplit.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -34,6 +34,18 @@ bool plan_pstep(PStepParams& p, int ns_override);
 size_t pstep_workspace(PStepParams& p, char* ws);
 int pstep_occupancy(size_t smem);
 cudaError_t launch_pstep(const PStepParams& p, int grid, cudaStream_t st);
+cudaError_t launch_topk_rows(int rows, int n, const float* keys, const int* ids, int k, float* out_keys,
+                             int* out_ids, int* out_count, int id_base, const int* lens, int lens_div, int lens_unit,
+                             cudaStream_t st);
+cudaError_t launch_select_range(int rows, int k, const int* ids, int lo, int hi, int* out_ids, int* out_count,
+                                cudaStream_t st);
+size_t token_split_smem(const Dims& d);
+cudaError_t launch_token_split(const Dims& d, int mode, const void* q, const int* seq_lens, const uint8_t* codes,
+                               const float* scale_zero, const int* channels, const int* block_ids, int P,
+                               const float* stats_in, float* stats_out, float* keys_out, int* ids_out, int tok_off,
+                               cudaStream_t st);
+cudaError_t launch_attn_merge(bool bf16, int P, int rows, int dv, const float* parts_o, const float* parts_lse,
+                              void* out, float* lse, cudaStream_t st);
 }  // namespace tls
 
 namespace {
@@ -151,7 +163,6 @@ bool pstep_plan(const tls_config* c, int do_attend, tls::PStepParams& sp) {
   const char* e = getenv("TLS_PSTEP");  // opt-in while it is slower than the chain
   if (!tls::pstep_supported(sp.d) || e == nullptr) return false;
   sp.attend = do_attend;
-  sscanf(e, "%d,%d,%d", &sp.L1, &sp.L2, &sp.L3);
   const int env = env_cluster();
   if (env > 16) return false;
   return tls::plan_pstep(sp, env) && (int)sp.smem_bytes <= kMaxSmem;
@@ -537,7 +548,9 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
                         token_scores, out, lse, slot_of_block, kv_rows > 0 ? kv_rows : cfg->max_seq_len};
   if (g_timer.on && g_timer.used % kMarks != 0) g_timer.used -= g_timer.used % kMarks;  // drop a partial record
   tls::PStepParams sk;
-  if (pstep_plan(cfg, do_attend, sk)) {  // one launch: every stage of every pair from the ticket queue
+  if (pstep_plan(cfg, do_attend, sk)) {  // one launch: every stage of every pair (opt-in, TLS_PSTEP)
+    if (guide != nullptr || slot_of_block != nullptr)
+      return fail(TLS_ERR_UNSUPPORTED, "the persistent step kernel (TLS_PSTEP) has no lag / block-cache mode");
     tls::pstep_workspace(sk, static_cast<char*>(workspace));
     unsigned epoch = g_epoch.fetch_add(1u);
     if (epoch == 0u) epoch = g_epoch.fetch_add(1u);
@@ -562,8 +575,8 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
     sk.dbg = env_debug_buf();
     const int occ = tls::pstep_occupancy(sk.smem_bytes);
     if (occ < 1) return fail(TLS_ERR_UNSUPPORTED, "persistent step kernel does not fit on an SM");
-    int grid = num_sms() * occ;
-    if (grid > sk.total) grid = sk.total;
+    const int grid = num_sms() * occ;
+    sk.nstream = num_sms();  // one streamer per SM (the first wave places blockIdx 0..SMs-1 on distinct SMs)
     g_timer.mark(st);
     cudaError_t e = tls::launch_pstep(sk, grid, st);
     if (e != cudaSuccess) return cuda_fail(e, "pstep_kernel launch");
@@ -605,7 +618,7 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
 
 tls_status run_attend(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
                       const int32_t* token_ids, const int32_t* num_tokens, void* out, float* lse, void* workspace,
-                      size_t workspace_bytes, cudaStream_t st) {
+                      size_t workspace_bytes, cudaStream_t st, int out_f32 = 0) {
   tls_status s = check_config(cfg);
   if (s) return s;
   if (!q || !aligned16(q)) return fail(TLS_ERR_INPUT, "q must be a non-NULL 16-byte aligned device pointer");
@@ -627,6 +640,7 @@ tls_status run_attend(const tls_config* cfg, const void* q, const void* k_cache,
   ap.token_ids = const_cast<int32_t*>(token_ids);
   ap.num_tokens = const_cast<int32_t*>(num_tokens);
   ap.out = out;
+  ap.out_f32 = out_f32;
   ap.lse = lse;
   const size_t pairs = (size_t)cfg->batch * cfg->num_kv_heads;
   ap.part_o = static_cast<float*>(workspace);
@@ -726,6 +740,81 @@ tls_status tls_block_scores(const tls_config* cfg, const void* q, const int32_t*
   return TLS_OK;
 }
 
+// ---- sequence-split decode (seqsplit.cu)
+tls_status tls_topk_rows(int32_t rows, int32_t n, const float* keys, const int32_t* ids, int32_t k,
+                         float* out_keys, int32_t* out_ids, int32_t* out_count, tls_stream_t stream) {
+  if (rows < 1 || n < 1 || k < 1) return fail(TLS_ERR_INPUT, "rows, n and k must be >= 1");
+  if (!keys || !ids || !out_keys || !out_ids) return fail(TLS_ERR_INPUT, "keys, ids, out_keys, out_ids are required");
+  cudaError_t e = tls::launch_topk_rows(rows, n, keys, ids, k, out_keys, out_ids, out_count, 0, nullptr, 1, 1,
+                                        (cudaStream_t)stream);
+  return e == cudaSuccess ? TLS_OK : cuda_fail(e, "topk_rows_kernel launch");
+}
+
+tls_status tls_block_topk(const tls_config* cfg, const float* scores, const int32_t* seq_lens, int32_t block_offset,
+                          float* out_scores, int32_t* out_block_ids, tls_stream_t stream) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if (!scores || !seq_lens || !out_scores || !out_block_ids)
+    return fail(TLS_ERR_INPUT, "scores, seq_lens, out_scores and out_block_ids are required");
+  if (block_offset < 0) return fail(TLS_ERR_INPUT, "block_offset must be >= 0");
+  const tls::Dims d = dims_of(cfg);
+  cudaError_t e = tls::launch_topk_rows(cfg->batch * cfg->num_kv_heads, d.M, scores, nullptr, cfg->top_blocks,
+                                        out_scores, out_block_ids, nullptr, block_offset, seq_lens, cfg->num_kv_heads,
+                                        cfg->block_size, (cudaStream_t)stream);
+  return e == cudaSuccess ? TLS_OK : cuda_fail(e, "topk_rows_kernel launch");
+}
+
+tls_status tls_select_range(int32_t rows, int32_t k, const int32_t* ids, int32_t lo, int32_t hi,
+                            int32_t* out_ids, int32_t* out_count, tls_stream_t stream) {
+  if (rows < 1 || k < 1 || lo > hi) return fail(TLS_ERR_INPUT, "rows, k >= 1 and lo <= hi required");
+  if (!ids || !out_ids) return fail(TLS_ERR_INPUT, "ids and out_ids are required");
+  cudaError_t e = tls::launch_select_range(rows, k, ids, lo, hi, out_ids, out_count, (cudaStream_t)stream);
+  return e == cudaSuccess ? TLS_OK : cuda_fail(e, "select_range_kernel launch");
+}
+
+namespace {
+tls_status token_split(const tls_config* cfg, int mode, const void* q, const int32_t* seq_lens, const tls_index* idx,
+                       const int32_t* block_ids, int32_t n_parts, const float* stats_in, float* stats_out,
+                       float* keys, int32_t* token_ids, int32_t token_offset, cudaStream_t st) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if (!q || !seq_lens || !idx || !idx->codes || !idx->scale_zero || !idx->channels || !block_ids)
+    return fail(TLS_ERR_INPUT, "q, seq_lens, the token index and block_ids are required");
+  const tls::Dims d = dims_of(cfg);
+  if (tls::token_split_smem(d) > (size_t)kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "q~ of the group too large");
+  if (mode == 0 && !stats_out) return fail(TLS_ERR_INPUT, "stats is required");
+  if (mode == 1 && (n_parts < 1 || !stats_in || !keys || !token_ids))
+    return fail(TLS_ERR_INPUT, "n_parts >= 1, stats_parts, keys and token_ids are required");
+  cudaError_t e = tls::launch_token_split(d, mode, q, seq_lens, idx->codes, idx->scale_zero, idx->channels,
+                                          block_ids, n_parts, stats_in, stats_out, keys, token_ids, token_offset, st);
+  return e == cudaSuccess ? TLS_OK : cuda_fail(e, "token_split_kernel launch");
+}
+}  // namespace
+
+tls_status tls_token_stats(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
+                           const int32_t* block_ids, float* stats, tls_stream_t stream) {
+  return token_split(cfg, 0, q, seq_lens, idx, block_ids, 1, nullptr, stats, nullptr, nullptr, 0,
+                     (cudaStream_t)stream);
+}
+
+tls_status tls_token_keys(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
+                          const int32_t* block_ids, int32_t n_parts, const float* stats_parts,
+                          int32_t token_offset, float* keys, int32_t* token_ids, tls_stream_t stream) {
+  return token_split(cfg, 1, q, seq_lens, idx, block_ids, n_parts, stats_parts, nullptr, keys, token_ids,
+                     token_offset, (cudaStream_t)stream);
+}
+
+tls_status tls_attn_merge(const tls_config* cfg, int32_t n_parts, const float* parts_out, const float* parts_lse,
+                          void* out, float* lse, tls_stream_t stream) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if (n_parts < 1 || !parts_out || !parts_lse || !out)
+    return fail(TLS_ERR_INPUT, "n_parts >= 1, parts_out, parts_lse and out are required");
+  cudaError_t e = tls::launch_attn_merge(cfg->dtype == TLS_BF16, n_parts, cfg->batch * cfg->num_q_heads, cfg->d_v,
+                                         parts_out, parts_lse, out, lse, (cudaStream_t)stream);
+  return e == cudaSuccess ? TLS_OK : cuda_fail(e, "attn_merge_kernel launch");
+}
+
 tls_status tls_select(const tls_config* cfg, const void* q, const int32_t* seq_lens, const tls_index* idx,
                       const int32_t* guide_block_ids, int32_t* block_ids, int32_t* token_ids, int32_t* num_tokens,
                       float* token_scores, void* workspace, size_t workspace_bytes, tls_stream_t stream) {
@@ -738,6 +827,13 @@ tls_status tls_sparse_attend(const tls_config* cfg, const void* q, const void* k
                              void* workspace, size_t workspace_bytes, tls_stream_t stream) {
   return run_attend(cfg, q, k_cache, v_cache, token_ids, num_tokens, out, lse, workspace, workspace_bytes,
                     (cudaStream_t)stream);
+}
+
+tls_status tls_sparse_attend_f32(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
+                                 const int32_t* token_ids, const int32_t* num_tokens, float* out, float* lse,
+                                 void* workspace, size_t workspace_bytes, tls_stream_t stream) {
+  return run_attend(cfg, q, k_cache, v_cache, token_ids, num_tokens, out, lse, workspace, workspace_bytes,
+                    (cudaStream_t)stream, 1);
 }
 
 tls_status tls_decode(const tls_config* cfg, const void* q, const void* k_cache, const void* v_cache,
@@ -785,7 +881,12 @@ tls_status tls_workspace_init(const tls_config* cfg, int32_t which, void* worksp
   cudaError_t e = cudaMemsetAsync(workspace, 0, need, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   tls::PStepParams sk;
-  if (which == 1 || pstep_plan(cfg, which == 2, sk)) return TLS_OK;  // counters start at 0
+  if (which == 1) return TLS_OK;  // counters start at 0
+  if (pstep_plan(cfg, which == 2, sk)) {  // counters start at 0, block scores as the completion sentinel
+    tls::pstep_workspace(sk, static_cast<char*>(workspace));
+    e = cudaMemsetAsync(sk.scores, 0xff, (size_t)sk.pairs * sk.d.Ms * 4, st);
+    return e == cudaSuccess ? TLS_OK : cuda_fail(e, "cudaMemsetAsync");
+  }
   // every chain's block-score buffer starts as the completion sentinel (fused.cu kScoreSentinel)
   char* ws = static_cast<char*>(workspace);
   const int ns = n_split(cfg);

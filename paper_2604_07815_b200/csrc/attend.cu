@@ -119,6 +119,18 @@ static __device__ int select_tokens_prologue(const AttendParams& p, int pair, in
 }
 
 // --------------------------------------------------------------------------
+// Output element idx of the pair's [G, d_v] block: the cfg dtype, or fp32 when the caller asked for fp32
+// partials (tls_sparse_attend_f32: the sequence-split merge then rounds once).
+template <typename T>
+__device__ __forceinline__ void store_out(const AttendParams& p, T* outg, int idx, float v) {
+  if (p.out_f32) {
+    const size_t off = (size_t)(reinterpret_cast<const char*>(outg) - reinterpret_cast<const char*>(p.out)) / sizeof(T);
+    reinterpret_cast<float*>(p.out)[off + idx] = v;
+  } else {
+    outg[idx] = from_f32<T>(v);
+  }
+}
+
 // Phase E (generic CUDA-core path): partial attention of this CTA over its
 // tokens sel[0..tloc) for the G heads of the pair, log2 domain.
 // Leaves (am_h, al_h) in ctl and the unnormalised partial o in ao.
@@ -341,7 +353,7 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
       }
     }
     if (direct) {
-      outg[idx] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+      store_out(p, outg, idx, L > 0.f ? acc / L : 0.f);
       if (dcol == 0 && p.lse != nullptr)
         p.lse[(size_t)b * p.d.Hq + (size_t)g * p.d.G + h] = L > 0.f ? (M + flog2(L)) * kLn2 : -CUDART_INF_F;
     } else {
@@ -532,7 +544,7 @@ __device__ void phase_attend_mma_t(const AttendParams& p, int pair, int b, int g
       }
     }
     if (direct) {
-      outg[idx] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+      store_out(p, outg, idx, L > 0.f ? acc / L : 0.f);
       if (dcol == 0 && p.lse != nullptr)
         p.lse[(size_t)b * p.d.Hq + (size_t)g * p.d.G + h] = L > 0.f ? (M + flog2(L)) * kLn2 : -CUDART_INF_F;
     } else {
@@ -582,7 +594,7 @@ __device__ void phase_merge(const AttendParams& p, int pair, int b, int g, unsig
       float o = 0.f;
 #pragma unroll 4
       for (int rr = 0; rr < cs; ++rr) o = fmaf(__ldcg(po + (size_t)rr * tot + idx), s_w[rr][h], o);
-      outg[idx] = from_f32<T>(o * s_inv[h]);
+      store_out(p, outg, idx, o * s_inv[h]);
     }
   } else {
     for (int i0 = lo; i0 < hi; i0 += U * kThreads) {
@@ -602,7 +614,7 @@ __device__ void phase_merge(const AttendParams& p, int pair, int b, int g, unsig
 #pragma unroll
           for (int rr = 0; rr < 16; ++rr)
             if (rr < cs) o = fmaf(v[u][rr], s_w[rr][h], o);
-          outg[idx] = from_f32<T>(o * s_inv[h]);
+          store_out(p, outg, idx, o * s_inv[h]);
         }
       }
     }

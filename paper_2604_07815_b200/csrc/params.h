@@ -109,6 +109,7 @@ struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally wit
   int* num_tokens;
   float* token_scores;
   void* out;
+  int out_f32;     // 1: out is fp32 [batch, Hq, d_v] whatever the cache dtype (tls_sparse_attend_f32)
   float* lse;
   float* part_o;   // workspace [pairs, cs, G, d_v] fp32 partial outputs
   float* part_ml;  // workspace [pairs, cs, G, 2] fp32 partial (max, sum), log2 units
@@ -124,8 +125,9 @@ struct PStepParams {
   int tb, ntile;     // TILE: block rows per item, items per pair
   int cb, nch;       // TOKEN: candidate blocks per item, items per pair
   int ns;            // ATT: items (slices of S_t) per pair
-  int L1, L2, L3;    // schedule lags (rows) of TOKEN, SEL, ATT behind TILE
-  int total;         // tickets
+  int ntiles_total;  // TILE tickets (pairs * ntile, pair-major)
+  int nready;        // items that pass through the ready queue (pairs * (1 + nch + ns))
+  int nstream;       // streamer CTAs (blockIdx < nstream): a1 tiles, then ready items
   int attend;        // 0: tls_select (no ATT items)
   unsigned epoch;    // this call's hand-off value (host call counter)
   const void* q;
@@ -146,7 +148,8 @@ struct PStepParams {
   void* out;
   float* lse;
   // workspace (zeroed once by tls_workspace_init; every call leaves it so)
-  unsigned* sched;   // [0] ticket counter, [1] CTAs finished
+  unsigned* sched;   // [0] next TILE ticket, [1] CTAs finished, [2] ready-queue head, [3] ready-queue tail
+  unsigned long long* rq;  // [nready] ready queue: (epoch << 32) | item
   unsigned* ctr;     // [pairs][8] per-pair counters and flags
   float* scores;     // [pairs][Ms] a1 block scores
   uint32_t* keys;    // [pairs][kb_eff * B] a3 ranking keys
@@ -154,8 +157,8 @@ struct PStepParams {
   float* stats;      // [pairs][nch][8][2] a3 chunk softmax statistics
   float* part_o;     // [pairs][ns][8][128] a5 partial outputs
   float* part_ml;    // [pairs][ns][8][2] a5 partial (max, sum)
-  unsigned long long* dbg;  // diagnostics only (env TLS_DEBUG_BUF): per ticket (start, end, smid|role|sub)
-  unsigned off_tile, off_qq, off_bkeys, off_scratch, off_fk;            // TILE
+  unsigned long long* dbg;  // diagnostics only (env TLS_DEBUG_BUF): per item (start, end, smid|role|sub|pair)
+  unsigned off_tile, off_qq, off_bkeys, off_scratch, off_fk;            // TILE (two tile buffers from off_tile)
   unsigned off_stage, off_qb, off_cblk, off_lhist;                      // TOKEN
   unsigned off_skeys, off_sscratch, off_shist, off_sfk, off_slist, off_scblk;  // SEL
   unsigned off_kv, off_pbuf, off_sel;                                   // ATT

@@ -35,18 +35,23 @@
 //                    ns) of S_t (K/V rows by cp.async, tensor cores, split-P);
 //                    the pair's last finishing slice merges the ns partials
 //                    (LSE identity, T10) into out / lse.
-// Hand-offs are per-pair flags and counters in the workspace (release /
-// acquire at GPU scope); every counter is reset by its last user, so each call
-// leaves the workspace ready for the next one (tls_workspace_init once).
-//
-// Ticket order and forward progress: tickets are claimed in increasing order
-// by resident CTAs (the grid never exceeds one wave).  Row i of the schedule
-// holds ATT(i - L3), SEL(i - L2), TOKEN(i - L1), TILE(i), with 1 <= L1 < L2 <
-// L3, so every item waits only for items of earlier rows (already claimed by
-// running CTAs that never wait for later tickets) -- except the nch TOKEN
-// siblings of one pair, which exchange statistics; they are consecutive
-// tickets, so only the pair of the lowest unclaimed ticket can have unclaimed
-// siblings, and the other resident CTAs keep finishing items and claiming.
+// Scheduling: TILE tickets are claimed in pair-major order from one counter;
+// every other item enters a ready queue only once its inputs exist (the
+// pair's a2 pushes its nch TOKEN items, the last TOKEN runs a4 and pushes the
+// ns ATT items).  Each CTA holds at most one reserved queue slot (one
+// atomicAdd) and streams TILE items until that slot's entry is published,
+// then takes it at its next item boundary -- so no item waits for a producer
+// while holding its CTA, except the nch TOKEN siblings of one pair, which
+// exchange softmax statistics: a sibling's slot holder is never inside another
+// TOKEN item (one reservation per CTA), so it reaches the item after at most
+// one TILE.  A TILE item whose CTA has no ready item claims the next TILE
+// ticket and issues its TMA copies into the second tile buffer before
+// computing its own rows, so every CTA keeps two tiles of block summaries in
+// flight while it streams a1.
+// Per-pair counters in the workspace are reset by their last user and the
+// scheduler words by the last CTA out, so each call leaves the workspace ready
+// for the next one (tls_workspace_init once); queue entries carry the call's
+// epoch, so entries of an earlier call are never taken for this call's.
 //
 // Specialisation: bf16 GQA, d_k = d_v = 128, G <= 8, d_c = 32, B = 64 (the
 // BASELINE.json GQA configs).  Every other configuration runs the kernel chain
@@ -75,15 +80,26 @@ constexpr int kTC = 64;                     // a5 tokens per staged chunk
 constexpr int kStages = 2;                  // a5 cp.async stages
 constexpr float kKeyOff = 64.f;             // a3 ranking-key scale (reading U20)
 
-enum Role : int { kTile = 0, kToken = 1, kSel = 2, kAtt = 3 };
+enum Role : int { kTile = 0, kToken = 1, kSel = 2, kAtt = 3, kExit = 4, kA2 = 5 };
 
-// per-pair counters / flags (PStepParams::ctr, 8 words per pair)
-enum Ctr : int { kCtrTile = 0, kCtrStats = 1, kCtrDone = 2, kCtrAtt = 3, kFlagBlocks = 4, kFlagTokens = 5 };
+// per-pair counters (PStepParams::ctr, 8 words per pair)
+enum Ctr : int { kCtrTiles = 0, kCtrStats = 1, kCtrDone = 2, kCtrAtt = 3 };
+// scheduler words (PStepParams::sched)
+enum Sched : int { kTileNext = 0, kCtasOut = 1, kRqHead = 2, kRqTail = 3 };  // head: next slot to reserve
+constexpr int kBarsPerBuf = 8;  // TILE: one mbarrier per 8-row group of a tile buffer
 
 __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
   unsigned old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
 }
 
 // thread 0 spins until *p >= v (relaxed loads: an acquire load per spin would invalidate the SM's L1 each
@@ -94,7 +110,7 @@ __device__ __forceinline__ void wait_geq(const unsigned* p, unsigned v, unsigned
                                          unsigned long long tag = 0) {
   unsigned spins = 0;
   while (ld_relaxed_gpu(p) < v) {
-    __nanosleep(64);
+    __nanosleep(128);
     if (++spins == (1u << 18) && dbg) {
       const unsigned long long slot = atomicAdd(dbg + (1 << 20), 1ull);
       if (slot < 4096) {
@@ -118,156 +134,249 @@ struct ItemCtl {
 };
 
 // ---------------------------------------------------------------------------
-// schedule: row i = ATT(i - L3) x ns, SEL(i - L2), TOKEN(i - L1) x nch, TILE(i) x ntile
+// scheduler (thread 0 only)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ long long seg_count(long long i, long long a, long long P) {
-  // #j < i with a <= j < a + P
-  const long long lo = i < a ? a : i;
-  return (lo > a + P ? a + P : lo) - a;
+__device__ __forceinline__ unsigned pack_item(int role, int sub, int pair) {
+  return ((unsigned)role << 29) | ((unsigned)sub << 22) | (unsigned)pair;  // pair < 2^22, sub < 2^7
 }
-__device__ __forceinline__ long long row_start(const PStepParams& p, long long i) {
-  const long long P = p.pairs;
-  long long s = (long long)p.ntile * seg_count(i, 0, P) + (long long)p.nch * seg_count(i, p.L1, P) +
-                seg_count(i, p.L2, P);
-  if (p.attend) s += (long long)p.ns * seg_count(i, p.L3, P);
-  return s;
+__device__ __forceinline__ void unpack_item(unsigned it, int& role, int& sub, int& pair) {
+  role = (int)(it >> 29);
+  sub = (int)((it >> 22) & 0x7f);
+  pair = (int)(it & 0x3fffff);
 }
-__device__ __forceinline__ void decode_ticket(const PStepParams& p, int t, int& role, int& pair, int& sub) {
-  long long lo = 0, hi = (long long)p.pairs + (p.attend ? p.L3 : p.L2);  // row_start(lo) <= t < row_start(hi)
-  while (hi - lo > 1) {
-    const long long mid = (lo + hi) >> 1;
-    if (row_start(p, mid) <= t) lo = mid;
-    else hi = mid;
+// Items role x (sub 0 .. n-1) of `pair` enter the ready queue.  Called by thread 0 after a CTA barrier that
+// follows every store the items read: the release stores are cumulative over that barrier.
+__device__ __forceinline__ void push_items(const PStepParams& p, int role, int pair, int n) {
+  const unsigned base = atomicAdd(p.sched + kRqTail, (unsigned)n);
+  for (int i = 0; i < n; ++i)
+    st_release_u64(p.rq + base + i, ((unsigned long long)p.epoch << 32) | pack_item(role, i, pair));
+}
+// Ready-queue slots are reserved one at a time per CTA with one atomicAdd (a CAS pop by hundreds of idle CTAs
+// serialised every pop: 2.8 ms steps).  A CTA holding slot h streams TILE items until entry h is published
+// and takes it at its next item boundary.  Returns true (and the item) once the entry is there.
+__device__ __forceinline__ bool slot_ready(const PStepParams& p, int h, unsigned& item) {
+  // relaxed poll (an acquire load per poll invalidates the SM's L1 each time), one acquire fence on success
+  const unsigned long long e = *reinterpret_cast<volatile const unsigned long long*>(p.rq + h);
+  if ((unsigned)(e >> 32) != p.epoch) return false;
+  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");  // TMA reads of the producer's outputs
+  item = (unsigned)e;
+  return true;
+}
+// Claim the next TILE ticket (pair-major), -1 when they are all taken.
+__device__ __forceinline__ int claim_tile(const PStepParams& p) {
+  if (ld_relaxed_gpu(p.sched + kTileNext) >= (unsigned)p.ntiles_total) return -1;
+  const unsigned t = atomicAdd(p.sched + kTileNext, 1u);
+  return t < (unsigned)p.ntiles_total ? (int)t : -1;
+}
+
+// Rows of TILE ticket t: pair, tile, first row and row count (0: past the pair's sequence, reading U1).
+struct TileRef {
+  int pair, tile, i0, nb, ntiles, m;
+};
+__device__ __forceinline__ TileRef tile_ref(const PStepParams& p, int t) {
+  TileRef r;
+  r.pair = t / p.ntile;
+  r.tile = t - r.pair * p.ntile;
+  const int b = r.pair / p.d.Hkv;
+  const int n = min(max(__ldg(p.seq_lens + b), 0), p.d.S);
+  r.m = (n + p.d.B - 1) >> p.d.log2B;
+  r.ntiles = max(1, (r.m + p.tb - 1) / p.tb);
+  r.i0 = r.tile * p.tb;
+  r.nb = r.tile < r.ntiles ? max(0, min(p.tb, r.m - r.i0)) : -1;  // -1: no such tile for this pair
+  return r;
+}
+// Thread 0: TMA bulk copies of a tile's rows into tile buffer `buf` (one mbarrier per 8-row group).
+__device__ __forceinline__ void issue_tile(const PStepParams& p, const TileRef& r, uint8_t* smem, uint64_t* bars,
+                                           int buf) {
+  if (p.dbg) p.dbg[(1 << 19) + 3 * (r.pair * p.ntile + r.tile)] = gtimer();  // diagnostics: issue time
+  uint8_t* dst = smem + p.off_tile + (size_t)buf * p.tb * kRowBytes;
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(p.block_minmax) + ((size_t)r.pair * p.d.M + r.i0) * kRowBytes;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic accesses of earlier items first
+  for (int s = 0; s < (r.nb + 7) >> 3; ++s) {
+    const int rows = min(8, r.nb - 8 * s);
+    uint64_t* bar = &bars[buf * kBarsPerBuf + s];
+    mbar_arrive_expect_tx(bar, (uint32_t)(rows * kRowBytes));
+    tma_bulk_g2s(dst + (size_t)s * 8 * kRowBytes, src + (size_t)s * 8 * kRowBytes, (uint32_t)(rows * kRowBytes), bar);
   }
-  int off = (int)(t - row_start(p, lo));
-  const long long i = lo;
-  if (p.attend && i - p.L3 >= 0 && i - p.L3 < p.pairs) {
-    if (off < p.ns) {
-      role = kAtt, pair = (int)(i - p.L3), sub = off;
-      return;
-    }
-    off -= p.ns;
-  }
-  if (i - p.L2 >= 0 && i - p.L2 < p.pairs) {
-    if (off < 1) {
-      role = kSel, pair = (int)(i - p.L2), sub = 0;
-      return;
-    }
-    off -= 1;
-  }
-  if (i - p.L1 >= 0 && i - p.L1 < p.pairs) {
-    if (off < p.nch) {
-      role = kToken, pair = (int)(i - p.L1), sub = off;
-      return;
-    }
-    off -= p.nch;
-  }
-  role = kTile, pair = (int)i, sub = off;
 }
 
 // ---------------------------------------------------------------------------
-// TILE: a1 over rows [i0, i0 + nb) of the pair's block summaries; the pair's
-// last finishing tile runs a2
+// TILES (streamer CTAs, warp-specialised): warp 0 lane 0 produces, warps 1-7
+// consume.  The producer claims TILE tickets (each atomic's value is used one
+// tile later), waits until a tile buffer is empty, records the ticket and
+// issues the tile's TMA copies (one mbarrier per 8-row group); when a buffer
+// it refills held the pair's last tile (by index), the pair's A2 item enters
+// the ready queue.  Consumer warp w scores group w - 1 of each tile:
+// s_i = Q+ . k^max_i + Q- . k^min_i (P:99 via P:110 and linearity of sum_h),
+// then arrives on the buffer's empty barrier.  Barriers: full[b][g] = bars[8b + g],
+// empty[b] = bars[16 + b] (7 arrivals).  Used once per launch: their phases
+// start at 0 here.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ unsigned run_tile(const PStepParams& p, int pair, int tile, uint8_t* smem, uint64_t* bars,
-                                          unsigned bph, ItemCtl& ctl, unsigned long long* mark) {
+constexpr uint32_t kScoreSentinel = 0xffffffffu;  // all-ones: a NaN no arithmetic produces
+constexpr int kBarEmpty = 16, kBarTok = 18, kBarSel = 19, kNumBars = 20;
+constexpr int kConsumers = kWarps - 1;
+
+__device__ __noinline__ void run_tiles(const PStepParams& p, uint8_t* smem, uint64_t* bars, int* s_tick) {
   const Dims& d = p.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int b = pair / d.Hkv, g = pair - b * d.Hkv;
-  const int n = min(max(__ldg(p.seq_lens + b), 0), d.S);
-  const int m = (n + d.B - 1) >> d.log2B;  // reading U1
-  const int ntiles = max(1, (m + p.tb - 1) / p.tb);
-  if (tile >= ntiles) return 0u;  // past this pair's sequence: no work, not counted
-  const int i0 = tile * p.tb;
-  const int nb = max(0, min(p.tb, m - i0));
-  const int ngrp = (nb + 7) >> 3;
-  uint8_t* buf = smem + p.off_tile;
   float* QQ = reinterpret_cast<float*>(smem + p.off_qq);
-  const uint8_t* src = reinterpret_cast<const uint8_t*>(p.block_minmax) + ((size_t)pair * d.M + i0) * kRowBytes;
-  const unsigned used = (1u << ngrp) - 1u;  // barriers this item completes once each
-  if (tid == 0) {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic accesses of earlier items first
-    for (int s = 0; s < ngrp; ++s) {
-      const int rows = min(8, nb - 8 * s);
-      mbar_arrive_expect_tx(&bars[s], (uint32_t)(rows * kRowBytes));
-      tma_bulk_g2s(buf + (size_t)s * 8 * kRowBytes, src + (size_t)s * 8 * kRowBytes, (uint32_t)(rows * kRowBytes),
-                   &bars[s]);
-    }
-  }
-  if (tid < kD) {  // QQ = [Q+ | Q-] of the pair (fp32): the head-collapsed query
-    const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * kD;
-    float qp = 0.f, qn = 0.f;
-    for (int h = 0; h < d.G; ++h) {
-      const float v = __bfloat162float(qg[(size_t)h * kD + tid]);
-      qp += fmaxf(v, 0.f);
-      qn += fminf(v, 0.f);
-    }
-    QQ[tid] = qp;
-    QQ[kD + tid] = qn;
-  }
-  __syncthreads();
-  if (mark && tid == 0) *mark = 1;
-  float* out = p.scores + (size_t)pair * d.Ms + i0;
-  if (warp < ngrp) {
-    float qreg[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) qreg[e] = QQ[lane * 8 + e];
-    for (int gq = warp; gq < ngrp; gq += kWarps) {
-      mbar_wait(&bars[gq], (bph >> gq) & 1u);
-      const int r8 = gq * 8;
-      float acc[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        acc[u] = 0.f;
-        if (r8 + u < nb) {
-          float f[8];
-          unpack16<__nv_bfloat16>(reinterpret_cast<const uint4*>(buf + (size_t)(r8 + u) * kRowBytes)[lane], f);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[u] = fmaf(qreg[e], f[e], acc[u]);
+  if (warp == 0) {
+    if (lane == 0) {  // ---- producer
+      unsigned eph = 0u;         // parity of each empty barrier's current phase
+      int held[2] = {-1, -1};    // ticket whose tile sits in each buffer
+      unsigned next = atomicAdd(p.sched + kTileNext, 1u);
+      for (int k = 0;; ++k) {
+        const int b = k & 1;
+        if (k >= 2) {
+          mbar_wait(&bars[kBarEmpty + b], (eph >> b) & 1u);
+          eph ^= 1u << b;
+        }
+        const int t = next < (unsigned)p.ntiles_total ? (int)next : -1;
+        if (t >= 0) next = atomicAdd(p.sched + kTileNext, 1u);
+        s_tick[b] = t;
+        const TileRef r = tile_ref(p, t >= 0 ? t : 0);
+        if (t >= 0 && r.nb > 0) {
+          issue_tile(p, r, smem, bars, b);  // arms full[b][0 .. ngrp) with the rows' bytes
+        } else {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&bars[8 * b])) : "memory");
+        }
+        if (held[b] >= 0) {  // the tile this buffer held is scored: the pair's last tile hands a2 on
+          const TileRef rh = tile_ref(p, held[b]);
+          if (rh.nb >= 0 && rh.tile == rh.ntiles - 1) push_items(p, kA2, rh.pair, 1);
+        }
+        held[b] = t;
+        if (t < 0) {  // end posted into buffer b; the other buffer's tile, if any, completes last
+          const int o = b ^ 1;
+          if (held[o] >= 0) {
+            mbar_wait(&bars[kBarEmpty + o], (eph >> o) & 1u);
+            const TileRef rh = tile_ref(p, held[o]);
+            if (rh.nb >= 0 && rh.tile == rh.ntiles - 1) push_items(p, kA2, rh.pair, 1);
+          }
+          break;
         }
       }
-      // transposed butterfly: lanes 4u..4u+3 end with the dot product of row u
+    }
+  } else {  // ---- consumers: warp w scores row group w - 1 of each tile
+    unsigned cph = 0u;  // parity of each full barrier's current phase (uniform over the consumer warps)
+    int qq_pair = -1;
+    for (int k = 0;; ++k) {
+      const int b = k & 1;
+      mbar_wait(&bars[8 * b], (cph >> (8 * b)) & 1u);  // group 0: the ticket is posted (and its rows, if any)
+      const int t = s_tick[b];
+      if (t < 0) break;
+      const TileRef r = tile_ref(p, t);
+      const int nb = r.nb, pair = r.pair;
+      if (nb > 0 && pair != qq_pair) {  // QQ = [Q+ | Q-] of the pair (fp32): the head-collapsed query
+        asm volatile("bar.sync 1, %0;\n" ::"r"(kConsumers * 32) : "memory");  // every warp past the old QQ
+        const int b0 = pair / d.Hkv, g = pair - b0 * d.Hkv;
+        const int i = tid - 32;
+        if (i < kD) {
+          const __nv_bfloat16* qg =
+              reinterpret_cast<const __nv_bfloat16*>(p.q) + ((size_t)b0 * d.Hq + (size_t)g * d.G) * kD;
+          float qp = 0.f, qn = 0.f;
+          for (int h = 0; h < d.G; ++h) {
+            const float v = __bfloat162float(qg[(size_t)h * kD + i]);
+            qp += fmaxf(v, 0.f);
+            qn += fminf(v, 0.f);
+          }
+          QQ[i] = qp;
+          QQ[kD + i] = qn;
+        }
+        qq_pair = pair;
+        asm volatile("bar.sync 1, %0;\n" ::"r"(kConsumers * 32) : "memory");
+      }
+      const int ngrp = nb > 0 ? (nb + 7) >> 3 : 0;
+      const int gq = warp - 1;
+      if (gq < ngrp) {
+        const uint8_t* tbuf = smem + p.off_tile + (size_t)b * p.tb * kRowBytes;
+        float* out = p.scores + (size_t)pair * d.Ms + r.i0;
+        float qreg[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool up = lane & 16;
-        const float send = up ? acc[j] : acc[j + 4];
-        const float keep = up ? acc[j + 4] : acc[j];
-        acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-      }
+        for (int e = 0; e < 8; ++e) qreg[e] = QQ[lane * 8 + e];
+        if (gq > 0) mbar_wait(&bars[8 * b + gq], (cph >> (8 * b + gq)) & 1u);
+        if (p.dbg && gq == 0 && lane == 0) p.dbg[(1 << 19) + 3 * t + 1] = gtimer();  // diagnostics: rows landed
+        const int r8 = gq * 8;
+        float acc[8];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const bool up = lane & 8;
-        const float send = up ? acc[j] : acc[j + 2];
-        const float keep = up ? acc[j + 2] : acc[j];
-        acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        for (int u = 0; u < 8; ++u) {
+          acc[u] = 0.f;
+          if (r8 + u < nb) {
+            float f[8];
+            unpack16<__nv_bfloat16>(reinterpret_cast<const uint4*>(tbuf + (size_t)(r8 + u) * kRowBytes)[lane], f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[u] = fmaf(qreg[e], f[e], acc[u]);
+          }
+        }
+        // transposed butterfly: lanes 4u..4u+3 end with the dot product of row u
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool up = lane & 16;
+          const float send = up ? acc[j] : acc[j + 4];
+          const float keep = up ? acc[j + 4] : acc[j];
+          acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const bool up = lane & 8;
+          const float send = up ? acc[j] : acc[j + 2];
+          const float keep = up ? acc[j + 2] : acc[j];
+          acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+          const bool up = lane & 4;
+          const float send = up ? acc[0] : acc[1];
+          const float keep = up ? acc[1] : acc[0];
+          acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
+        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+        const int u = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        if ((lane & 3) == 0 && r8 + u < nb) out[r8 + u] = acc[0];
       }
-      {
-        const bool up = lane & 4;
-        const float send = up ? acc[0] : acc[1];
-        const float keep = up ? acc[1] : acc[0];
-        acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-      acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
-      acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
-      const int u = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-      if ((lane & 3) == 0 && r8 + u < nb) out[r8 + u] = acc[0];
+      cph ^= (ngrp > 0 ? (1u << ngrp) - 1u : 1u) << (8 * b);  // the armed groups (group 0 always) consumed
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&bars[kBarEmpty + b])) : "memory");
     }
   }
-  __syncthreads();  // this tile's scores stored
-  if (mark && tid == 0) *mark = 2;
-  unsigned* ctr = p.ctr + (size_t)pair * 8;
-  if (tid == 0) ctl.last = atom_add_acq_rel(ctr + kCtrTile, 1u) == (unsigned)(ntiles - 1);
   __syncthreads();
-  if (!ctl.last) return used;
-  // ===== a2 (the pair's last finishing tile): M_t = top-k_b blocks, ties -> lower block id (U2) =====
-  if (tid == 0) ctr[kCtrTile] = 0u;  // reset for the next call
+}
+
+// ---------------------------------------------------------------------------
+// A2 (worker): M_t = top-k_b blocks of the pair, ties -> lower block
+// id (U2).  The pair's tiles have lower tickets than the one that pushed this
+// item, so they are claimed by running streamers that never wait: the scores
+// still holding the sentinel arrive.  Restores the sentinel and pushes the
+// pair's TOKEN items.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void run_a2(const PStepParams& p, int pair, uint8_t* smem, ItemCtl& ctl) {
+  const Dims& d = p.d;
+  const int tid = threadIdx.x;
+  const int b = pair / d.Hkv;
+  const int n = min(max(__ldg(p.seq_lens + b), 0), d.S);
+  const int m = (n + d.B - 1) >> d.log2B;  // reading U1
   uint32_t* bkeys = reinterpret_cast<uint32_t*>(smem + p.off_bkeys);
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + p.off_scratch);
   FastTopKCtl& fk = *reinterpret_cast<FastTopKCtl*>(smem + p.off_fk);
-  const float* sc = p.scores + (size_t)pair * d.Ms;
-  for (int i = tid; i < m; i += kThreads) bkeys[i] = f2key(__ldcg(sc + i));  // L2: the other tiles' stores
+  uint32_t* sc = reinterpret_cast<uint32_t*>(p.scores + (size_t)pair * d.Ms);
+  if (tid < 32) {  // one warp waits until no score of the pair is the sentinel (relaxed polls, backing off)
+    unsigned spins = 0;
+    for (int i = tid; i < m;) {
+      if (ld_relaxed_gpu(sc + i) != kScoreSentinel) {
+        i += 32;
+        continue;
+      }
+      __nanosleep(256);
+      if (++spins > (1u << 24)) __trap();
+    }
+    __syncwarp();
+  }
   __syncthreads();
-  if (mark && tid == 0) *mark = 3;
+  for (int i = tid; i < m; i += kThreads) {
+    bkeys[i] = f2key(__uint_as_float(ld_relaxed_gpu(sc + i)));
+    sc[i] = kScoreSentinel;  // restored for the next call (no other reader of this score)
+  }
+  __syncthreads();
   const int K = min(d.Kb, m);
   int* bout = p.block_ids + (size_t)pair * d.Kb;
   bool done = false;
@@ -275,21 +384,24 @@ __device__ __noinline__ unsigned run_tile(const PStepParams& p, int pair, int ti
   if (K < m && m <= 4 * 2 * kThreads)
     done = range_topk_select<2>(bkeys, m, K, scratch, fk, ctl.tk, hs, [&](int i, int pos) { bout[pos] = i; });
   if (!done) {
-    const TopK t = fast_topk(bkeys, m, K, d.Kb >= m, fk, ctl.tk, nullptr);
-    topk_emit(bkeys, m, t, ctl.tk, [&](int i, int pos) { bout[pos] = i; });
+    const TopK tk = fast_topk(bkeys, m, K, d.Kb >= m, fk, ctl.tk, nullptr);
+    topk_emit(bkeys, m, tk, ctl.tk, [&](int i, int pos) { bout[pos] = i; });
   }
-  if (mark && tid == 0) *mark = 4;
   for (int q = K + tid; q < d.Kb; q += kThreads) bout[q] = -1;
   __syncthreads();
-  if (tid == 0) st_release_gpu(ctr + kFlagBlocks, p.epoch);  // cumulative over the CTA barrier
-  return used;
+  if (tid == 0) push_items(p, kToken, pair, p.nch);  // M_t published with the TOKEN items
 }
 
 // ---------------------------------------------------------------------------
-// TOKEN: a3 over candidate blocks [c cb, (c+1) cb) of the pair
+// TOKEN: a3 over candidate blocks [c cb, (c+1) cb) of the pair (M_t is
+// published: the item was pushed by the pair's a2); the pair's last finishing
+// TOKEN runs a4 (run_sel) and pushes the pair's ATT items
 // ---------------------------------------------------------------------------
+__device__ __noinline__ unsigned run_sel(const PStepParams& p, int pair, uint8_t* smem, uint64_t* bars, unsigned bph,
+                            ItemCtl& ctl);
+
 __device__ __noinline__ unsigned run_token(const PStepParams& p, int pair, int chunk, uint8_t* smem, uint64_t* bars,
-                                           unsigned bph, ItemCtl& ctl) {
+                                           unsigned bph, ItemCtl& ctl, int* ran_sel) {
   const Dims& d = p.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q4 = lane & 3, r0 = lane >> 2;
   const int b = pair / d.Hkv, g = pair - b * d.Hkv;
@@ -305,34 +417,7 @@ __device__ __noinline__ unsigned run_token(const PStepParams& p, int pair, int c
   const int rowb = d.d_c / 2;  // 16 B of codes per token
   float2* stz = reinterpret_cast<float2*>(stc + (size_t)p.cb * d.B * rowb);
   const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + ((size_t)b * d.Hq + (size_t)g * G) * kD;
-  // independent of M_t: q~ fragments and the zeroed local key histogram
-  {
-    const int* ch = p.channels + (size_t)g * d.d_c;
-    if (tid < kKS * 32) {  // lane ln, k-step s: head ln >> 2; channels cb, cb+4 | cb+1, cb+5 (token_tile_mma order)
-      const int ln = tid & 31, s = tid >> 5, h = ln >> 2;
-      const int c0 = 8 * (ln & 3) + 2 * s;
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
-      if (h < G) {
-        const int cc[4] = {c0, c0 + 4, c0 + 1, c0 + 5};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) v[e] = __bfloat162float(qg[(size_t)h * kD + __ldg(ch + cc[e])]);
-      }
-      qb[2 * tid] = pack_bf16x2(v[0], v[1]);
-      qb[2 * tid + 1] = pack_bf16x2(v[2], v[3]);
-    } else if (tid < kKS * 32 + 8) {  // sum_c q~_h[c]
-      const int h = tid - kKS * 32;
-      float s = 0.f;
-      if (h < G)
-        for (int c = 0; c < d.d_c; ++c) s += __bfloat162float(qg[(size_t)h * kD + __ldg(ch + c)]);
-      qsum[h] = s;
-    }
-    for (int i = tid; i < kKeyBins; i += kThreads) lhist[i] = 0u;
-  }
-  if (tid == 0) {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    wait_geq(ctr + kFlagBlocks, p.epoch, p.dbg, ((unsigned long long)pair << 32) | (1u << 16) | chunk);  // M_t (a2)
-  }
-  __syncthreads();
+  if (tid == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // before the stage's TMA writes
   // ---- this chunk's candidate blocks: M_t (ascending, -1 padded) or the lag-mode guide's valid ids ----
   const int c0 = chunk * p.cb;
   if (p.guide == nullptr) {
@@ -364,22 +449,47 @@ __device__ __noinline__ unsigned run_token(const PStepParams& p, int pair, int c
   }
   __syncthreads();
   const int nbl = ctl.kc;
-  if (warp == 0 && nbl > 0) {  // stage the chunk's INT4 codes and scale/zero rows (TMA bulk, one barrier)
-    const uint8_t* cbase = p.codes + (size_t)pair * d.S * rowb;
-    const float2* zbase = reinterpret_cast<const float2*>(p.scale_zero) + (size_t)pair * d.S;
-    uint32_t bytes = 0;
-    for (int k = lane; k < nbl; k += 32) bytes += (uint32_t)(min(d.B, d.S - cblk[k] * d.B) * (rowb + 8));
-    bytes = warp_sum_u32(bytes);
-    if (lane == 0) mbar_arrive_expect_tx(&bars[0], bytes);
-    __syncwarp();
-    for (int k = lane; k < nbl; k += 32) {
-      const int blk = cblk[k];
-      const int rows = min(d.B, d.S - blk * d.B);
-      tma_bulk_g2s(stc + (size_t)k * d.B * rowb, cbase + (size_t)blk * d.B * rowb, rows * rowb, &bars[0]);
-      tma_bulk_g2s(stz + k * d.B, zbase + (size_t)blk * d.B, rows * 8, &bars[0]);
+  if (warp == 0) {
+    if (nbl > 0) {  // stage the chunk's INT4 codes and scale/zero rows (TMA bulk, one barrier)
+      const uint8_t* cbase = p.codes + (size_t)pair * d.S * rowb;
+      const float2* zbase = reinterpret_cast<const float2*>(p.scale_zero) + (size_t)pair * d.S;
+      uint32_t bytes = 0;
+      for (int k = lane; k < nbl; k += 32) bytes += (uint32_t)(min(d.B, d.S - cblk[k] * d.B) * (rowb + 8));
+      bytes = warp_sum_u32(bytes);
+      if (lane == 0) mbar_arrive_expect_tx(&bars[kBarTok], bytes);
+      __syncwarp();
+      for (int k = lane; k < nbl; k += 32) {
+        const int blk = cblk[k];
+        const int rows = min(d.B, d.S - blk * d.B);
+        tma_bulk_g2s(stc + (size_t)k * d.B * rowb, cbase + (size_t)blk * d.B * rowb, rows * rowb, &bars[kBarTok]);
+        tma_bulk_g2s(stz + k * d.B, zbase + (size_t)blk * d.B, rows * 8, &bars[kBarTok]);
+      }
     }
+  } else {  // while the copies fly: q~ fragments and the zeroed local key histogram
+    const int* ch = p.channels + (size_t)g * d.d_c;
+    const int t = tid - 32;
+    if (t < kKS * 32) {  // lane ln, k-step s: head ln >> 2; channels cb, cb+4 | cb+1, cb+5 (token_tile_mma order)
+      const int ln = t & 31, s = t >> 5, h = ln >> 2;
+      const int cc0 = 8 * (ln & 3) + 2 * s;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (h < G) {
+        const int cc[4] = {cc0, cc0 + 4, cc0 + 1, cc0 + 5};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = __bfloat162float(qg[(size_t)h * kD + __ldg(ch + cc[e])]);
+      }
+      qb[2 * t] = pack_bf16x2(v[0], v[1]);
+      qb[2 * t + 1] = pack_bf16x2(v[2], v[3]);
+    } else if (t < kKS * 32 + 8) {  // sum_c q~_h[c]
+      const int h = t - kKS * 32;
+      float sum = 0.f;
+      if (h < G)
+        for (int c = 0; c < d.d_c; ++c) sum += __bfloat162float(qg[(size_t)h * kD + __ldg(ch + c)]);
+      qsum[h] = sum;
+    }
+    for (int i = t; i < kKeyBins; i += kThreads - 32) lhist[i] = 0u;
   }
-  if (nbl > 0) mbar_wait(&bars[0], bph & 1u);
+  __syncthreads();
+  if (nbl > 0) mbar_wait(&bars[kBarTok], (bph >> kBarTok) & 1u);
   const float sm2 = d.sm_scale * kLog2e;
   float sq[2];
 #pragma unroll
@@ -492,15 +602,23 @@ __device__ __noinline__ unsigned run_token(const PStepParams& p, int pair, int c
   for (int i = tid; i < kKeyBins; i += kThreads)
     if (lhist[i]) atomicAdd(&gh[i], lhist[i]);
   __syncthreads();
-  if (tid == 0) red_release_add_gpu(ctr + kCtrDone, 1u);  // keys + histogram counts of this chunk visible
-  return nbl > 0 ? 1u : 0u;
+  const unsigned used = nbl > 0 ? 1u << kBarTok : 0u;
+  // keys + histogram counts of this chunk visible (release); the last chunk acquires every chunk's
+  if (tid == 0) ctl.last = atom_add_acq_rel(ctr + kCtrDone, 1u) == (unsigned)(p.nch - 1);
+  __syncthreads();
+  if (!ctl.last) return used;
+  if (tid == 0) asm volatile("fence.proxy.async.global;\n" ::: "memory");  // TMA reads of the keys
+  *ran_sel = 1;
+  return used | run_sel(p, pair, smem, bars, bph, ctl);
 }
 
 // ---------------------------------------------------------------------------
-// SEL: a4 over the pair's ranking keys
+// SEL: a4 over the pair's ranking keys, run by the pair's last finishing
+// TOKEN item once every chunk's keys are visible; pushes the ATT items.
+// Uses mbarrier 1 (the TOKEN stage uses 0).
 // ---------------------------------------------------------------------------
 __device__ __noinline__ unsigned run_sel(const PStepParams& p, int pair, uint8_t* smem, uint64_t* bars, unsigned bph,
-                                         ItemCtl& ctl) {
+                            ItemCtl& ctl) {
   const Dims& d = p.d;
   const int tid = threadIdx.x;
   const int b = pair / d.Hkv;
@@ -515,15 +633,13 @@ __device__ __noinline__ unsigned run_sel(const PStepParams& p, int pair, uint8_t
   int* cblk = reinterpret_cast<int*>(smem + p.off_scblk);
   const uint32_t kbytes = (uint32_t)(p.kb_eff * d.B * 4);
   if (tid == 0) {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    wait_geq(ctr + kCtrDone, (unsigned)p.nch, p.dbg, ((unsigned long long)pair << 32) | (3u << 16));  // every chunk's keys
-    ctr[kCtrDone] = 0u;                          // reset for the next call (no other reader left)
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the TOKEN item's generic accesses first
+    ctr[kCtrDone] = 0u;                                                // reset for the next call (no reader left)
     ctr[kCtrStats] = 0u;
-    mbar_arrive_expect_tx(&bars[0], kbytes + kKeyBins * 4);
-    tma_bulk_g2s(shist, p.khist + (size_t)pair * kKeyBins, kKeyBins * 4, &bars[0]);
-    tma_bulk_g2s(skeys, p.keys + (size_t)pair * p.kb_eff * d.B, kbytes, &bars[0]);
+    mbar_arrive_expect_tx(&bars[kBarSel], kbytes + kKeyBins * 4);
+    tma_bulk_g2s(shist, p.khist + (size_t)pair * kKeyBins, kKeyBins * 4, &bars[kBarSel]);
+    tma_bulk_g2s(skeys, p.keys + (size_t)pair * p.kb_eff * d.B, kbytes, &bars[kBarSel]);
   }
-  __syncthreads();  // the hand-off observed by thread 0 (and through it M_t) before anyone reads block_ids
   // candidate blocks in the order the TOKEN items used
   const int* cand = p.guide ? p.guide + (size_t)pair * d.Kb : p.block_ids + (size_t)pair * d.Kb;
   {
@@ -544,7 +660,7 @@ __device__ __noinline__ unsigned run_sel(const PStepParams& p, int pair, uint8_t
   }
   __syncthreads();
   const int nslots = ctl.kc << d.log2B;
-  mbar_wait(&bars[0], bph & 1u);
+  mbar_wait(&bars[kBarSel], (bph >> kBarSel) & 1u);
   // the histogram is in shared memory now: zero the pair's global one for the next call
   for (int i = tid; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
   __shared__ HistSel hs;
@@ -570,8 +686,8 @@ __device__ __noinline__ unsigned run_sel(const PStepParams& p, int pair, uint8_t
   }
   if (tid == 0) p.num_tokens[pair] = K;
   __syncthreads();
-  if (tid == 0) st_release_gpu(ctr + kFlagTokens, p.epoch);  // S_t published (cumulative over the barrier)
-  return 1u;
+  if (tid == 0 && p.attend) push_items(p, kAtt, pair, p.ns);  // S_t published with the ATT items
+  return 1u << kBarSel;
 }
 
 // ---------------------------------------------------------------------------
@@ -585,9 +701,7 @@ __device__ __noinline__ void run_att(const PStepParams& p, int pair, int slice, 
   const int G = d.G;
   unsigned* ctr = p.ctr + (size_t)pair * 8;
   int* sel = reinterpret_cast<int*>(smem + p.off_sel);
-  if (tid == 0) wait_geq(ctr + kFlagTokens, p.epoch, p.dbg, ((unsigned long long)pair << 32) | (4u << 16) | slice);
-  __syncthreads();
-  const int K = __ldcg(p.num_tokens + pair);
+  const int K = __ldcg(p.num_tokens + pair);  // S_t is published: the item was pushed after it
   const int t0 = (int)(((long long)K * slice) / p.ns);
   const int tloc = (int)(((long long)K * (slice + 1)) / p.ns) - t0;
   {
@@ -812,51 +926,78 @@ __device__ __noinline__ void run_att(const PStepParams& p, int pair, int slice, 
 
 __global__ void __launch_bounds__(kThreads, 3) pstep_kernel(const __grid_constant__ PStepParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bars[8];
+  __shared__ __align__(8) uint64_t bars[kNumBars];
   __shared__ ItemCtl ctl;
-  __shared__ int s_ticket;
-  __shared__ unsigned s_bph;  // parity of the current phase of each mbarrier (initialised once, never re-initialised)
+  __shared__ unsigned s_item;
+  __shared__ int s_sel;          // the TOKEN item ran a4
+  __shared__ int s_tick[2];      // run_tiles: ticket in each tile buffer (-1: none)
+  __shared__ unsigned s_bph;     // parity of the current phase of each mbarrier (initialised once, never re-initialised)
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int s = 0; s < 8; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kNumBars; ++s) mbar_init(&bars[s], s == kBarEmpty || s == kBarEmpty + 1 ? kConsumers : 1);
     mbar_fence_init();
     s_bph = 0u;
   }
-  for (;;) {
-    if (tid == 0) s_ticket = (int)atomicAdd(p.sched, 1u);
-    __syncthreads();
-    const int t = s_ticket;
-    __syncthreads();  // every thread read the ticket
-    if (t >= p.total) break;
-    int role, pair, sub;
-    decode_ticket(p, t, role, pair, sub);
-    unsigned long long t_start = p.dbg ? gtimer() : 0ull;
-    if (p.dbg && tid == 0) {
-      unsigned smid;
-      asm("mov.u32 %0, %%smid;" : "=r"(smid));
-      p.dbg[3 * (size_t)t] = t_start;
-      p.dbg[3 * (size_t)t + 2] = ((unsigned long long)smid << 32) | (unsigned)(role << 24 | sub) | (1ull << 31) |
-                                 ((unsigned long long)(pair & 0x7f) << 16);
-    }
-    const unsigned bph = s_bph;
-    unsigned used = 0u;  // mbarriers whose phase this item completed
-    if (role == kTile) used = run_tile(p, pair, sub, smem, bars, bph, ctl, p.dbg ? p.dbg + 3 * (size_t)t + 1 : nullptr);
-    else if (role == kToken) used = run_token(p, pair, sub, smem, bars, bph, ctl);
-    else if (role == kSel) used = run_sel(p, pair, smem, bars, bph, ctl);
-    else run_att(p, pair, sub, smem, ctl);
-    __syncthreads();  // shared memory free for the next item; every thread read s_bph
-    if (tid == 0) s_bph = bph ^ used;
-    if (p.dbg && tid == 0) {  // diagnostics: per ticket (start, end, smid)
-      unsigned smid;
-      asm("mov.u32 %0, %%smid;" : "=r"(smid));
-      p.dbg[3 * (size_t)t] = t_start;
-      p.dbg[3 * (size_t)t + 1] = gtimer();
-      p.dbg[3 * (size_t)t + 2] = ((unsigned long long)smid << 32) | (unsigned)(role << 24 | sub);
+  __syncthreads();
+  if (blockIdx.x < (unsigned)p.nstream) {  // streamer: a1 until the tickets run out, then a worker
+    const unsigned long long t_start = p.dbg ? gtimer() : 0ull;
+    run_tiles(p, smem, bars, s_tick);
+    if (tid == 0) {
+      if (p.dbg) {
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        const unsigned long long slot = atomicAdd(p.dbg + (1 << 20) - 1, 1ull);
+        p.dbg[3 * slot] = t_start;
+        p.dbg[3 * slot + 1] = gtimer();
+        p.dbg[3 * slot + 2] = ((unsigned long long)smid << 32) | ((unsigned)kTile << 24);
+      }
     }
   }
-  if (tid == 0 && atom_add_acq_rel(p.sched + 1, 1u) == gridDim.x - 1) {  // the last CTA out resets the queue
-    p.sched[0] = 0u;
-    p.sched[1] = 0u;
+  for (;;) {  // worker: reserve the next ready-queue slot, wait for its item, run it
+    if (tid == 0) {
+      unsigned item = pack_item(kExit, 0, 0);
+      const unsigned h = atomicAdd(p.sched + kRqHead, 1u);
+      if (h < (unsigned)p.nready) {
+        unsigned spins = 0;
+        while (!slot_ready(p, (int)h, item)) {
+          __nanosleep(256);
+          if (++spins > (1u << 26)) __trap();
+        }
+      }
+      s_item = item;
+      s_sel = 0;
+    }
+    __syncthreads();
+    const unsigned item = s_item;
+    int role, sub, pair;
+    unpack_item(item, role, sub, pair);
+    if (role == kExit) break;
+    const unsigned long long t_start = p.dbg ? gtimer() : 0ull;
+    const unsigned bph = s_bph;
+    unsigned nbph = bph;
+    if (role == kA2) run_a2(p, pair, smem, ctl);
+    else if (role == kToken) nbph = bph ^ run_token(p, pair, sub, smem, bars, bph, ctl, &s_sel);
+    else run_att(p, pair, sub, smem, ctl);
+    __syncthreads();  // shared memory free for the next item; every thread read s_bph
+    if (tid == 0) s_bph = nbph;
+    if (p.dbg && tid == 0) {  // diagnostics: per item (start, end, smid | role | sub | pair)
+      unsigned smid;
+      asm("mov.u32 %0, %%smid;" : "=r"(smid));
+      const unsigned long long slot = atomicAdd(p.dbg + (1 << 20) - 1, 1ull);
+      if (slot < (1 << 20) / 3 - 1) {
+        const int r = (role == kToken && s_sel) ? kSel : (role == kA2 ? kTile : role);
+        p.dbg[3 * slot] = t_start;
+        p.dbg[3 * slot + 1] = gtimer();
+        p.dbg[3 * slot + 2] = ((unsigned long long)smid << 32) | ((unsigned)r << 24) | ((unsigned)(sub | (role == kA2 ? 0x80 : 0)) << 16) |
+                              (unsigned)(pair & 0xffff);
+      }
+    }
+  }
+  if (tid == 0 && atom_add_acq_rel(p.sched + kCtasOut, 1u) == gridDim.x - 1) {  // the last CTA out resets
+    p.sched[kTileNext] = 0u;
+    p.sched[kRqHead] = 0u;
+    p.sched[kRqTail] = 0u;
+    p.sched[kCtasOut] = 0u;
   }
 }
 
@@ -870,7 +1011,7 @@ bool plan_pstep(PStepParams& p, int ns_override) {
   const Dims& d = p.d;
   p.pairs = d.batch * d.Hkv;
   p.kb_eff = kb_effective(d);
-  p.tb = 64;  // 32 KB of block summaries per TILE
+  p.tb = 56;  // 28 KB of block summaries per TILE: 7 row groups, one per consumer warp
   p.ntile = (d.M + p.tb - 1) / p.tb;
   p.cb = 16;  // 1024 candidate tokens per TOKEN: 8 warps x kTPW tiles x 16
   if (p.cb > p.kb_eff) p.cb = p.kb_eff;
@@ -881,16 +1022,13 @@ bool plan_pstep(PStepParams& p, int ns_override) {
   if (p.ns < 1) p.ns = 1;
   const int tok_max = (kt + p.ns - 1) / p.ns;
   if ((size_t)p.kb_eff * d.B > (size_t)kSelRunMax * kThreads) return false;  // SEL: the one-pass register select
-  // lags (schedule rows): the TOKEN items of a pair come after roughly one wave of TILE items, SEL and ATT right
-  // behind them
-  if (p.L1 <= 0) p.L1 = 16;
-  if (p.L2 <= p.L1) p.L2 = p.L1 + 4;
-  if (p.L3 <= p.L2) p.L3 = p.L2 + 2;
-  p.total = (int)((long long)p.pairs * (p.ntile + p.nch + 1 + (p.attend ? p.ns : 0)));
+  p.ntiles_total = p.pairs * p.ntile;
+  p.nready = p.pairs * (1 + p.nch + (p.attend ? p.ns : 0));  // A2, TOKEN x nch, ATT x ns
+  if (p.pairs >= (1 << 22) || p.nch > 127 || p.ns > 127) return false;  // queue entry fields
   // shared memory: every role's regions start at 0 (one item at a time per CTA)
   size_t tile_end, tok_end, sel_end, att_end;
-  {  // TILE: the tile, QQ; the a2 regions alias the tile once it is scored
-    size_t o = (size_t)p.tb * kRowBytes;
+  {  // TILE: two tile buffers, QQ; the a2 regions alias the item's own buffer once it is scored
+    size_t o = 2 * (size_t)p.tb * kRowBytes;
     p.off_tile = 0;
     p.off_qq = (unsigned)o;
     o = align16(o + 2 * kD * 4);
@@ -901,7 +1039,7 @@ bool plan_pstep(PStepParams& p, int ns_override) {
     w = align16(w + (size_t)kBracketWords * 4);
     p.off_fk = (unsigned)w;
     w = align16(w + sizeof(FastTopKCtl));
-    if (w > (size_t)p.tb * kRowBytes) return false;  // a2 regions must fit inside the tile (QQ stays)
+    if (w > (size_t)p.tb * kRowBytes) return false;  // a2 regions must fit inside one tile buffer (QQ stays)
     tile_end = o;
   }
   {  // TOKEN: index stage, q~ fragments, candidate ids, local histogram
@@ -961,6 +1099,7 @@ size_t pstep_workspace(PStepParams& p, char* ws) {
     return at;
   };
   const size_t o_sched = take(256);
+  const size_t o_rq = take((size_t)p.nready * 8);
   const size_t o_ctr = take(P * 8 * 4);
   const size_t o_scores = take(P * d.Ms * 4);
   const size_t o_keys = take(P * p.kb_eff * d.B * 4);
@@ -970,6 +1109,7 @@ size_t pstep_workspace(PStepParams& p, char* ws) {
   const size_t o_pml = take(P * p.ns * 16 * 4);
   if (ws) {
     p.sched = reinterpret_cast<unsigned*>(ws + o_sched);
+    p.rq = reinterpret_cast<unsigned long long*>(ws + o_rq);
     p.ctr = reinterpret_cast<unsigned*>(ws + o_ctr);
     p.scores = reinterpret_cast<float*>(ws + o_scores);
     p.keys = reinterpret_cast<uint32_t*>(ws + o_keys);

@@ -114,8 +114,10 @@ def _workspace(cfg: TLSConfig, dev: torch.device, which: int):
         return None, 0
     # one zero-filled buffer per (device, stream, configuration): the pair completion words of
     # select_kernel carry state from call to call (tls_workspace_bytes in include/tls.h)
-    # (the sub-batch pipeline depth TLS_NSPLIT changes the workspace layout as well)
-    key = (dev, torch.cuda.current_stream(dev).cuda_stream, bytes(cc), which, os.environ.get("TLS_NSPLIT", ""))
+    # (the tuning variables that change the workspace layout -- sub-batch pipeline depth, attention split,
+    # the persistent step kernel -- are part of the key: a workspace is only reused with its own layout)
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream, bytes(cc), which, nbytes,
+           tuple(os.environ.get(v) for v in ("TLS_NSPLIT", "TLS_CLUSTER", "TLS_PSTEP", "TLS_TILE_KB")))
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
@@ -216,6 +218,103 @@ def block_scores(cfg: TLSConfig, q: torch.Tensor, seq_lens: torch.Tensor, index:
     return out
 
 
+# ---- sequence-split decode primitives (include/tls.h, seqsplit.cu; orchestration in seqsplit.py)
+def topk_rows(keys: torch.Tensor, ids: torch.Tensor, k: int):
+    """Exact top-k of each row of (key, id) pairs (ids ascending per row, -1 = empty): larger key first,
+    equal keys -> lower id.  Returns (keys [rows, k], ids [rows, k] ascending ids, count [rows])."""
+    lib = _lib.load()
+    dev = keys.device
+    rows, n = keys.reshape(-1, keys.shape[-1]).shape
+    _need(keys, "keys", tuple(keys.shape), torch.float32, dev)
+    _need(ids, "ids", tuple(keys.shape), torch.int32, dev)
+    ok = torch.empty(keys.shape[:-1] + (k,), dtype=torch.float32, device=dev)
+    oi = torch.empty(keys.shape[:-1] + (k,), dtype=torch.int32, device=dev)
+    cnt = torch.empty(keys.shape[:-1], dtype=torch.int32, device=dev)
+    _lib.check(lib.tls_topk_rows(rows, n, keys.data_ptr(), ids.data_ptr(), k, ok.data_ptr(), oi.data_ptr(),
+                                 cnt.data_ptr(), _stream(dev)))
+    return ok, oi, cnt
+
+
+def block_topk(cfg: TLSConfig, scores: torch.Tensor, seq_lens: torch.Tensor, block_offset: int):
+    """A rank's local top-k_b with global block ids.  Returns (scores, block_ids) [batch, Hkv, k_b]."""
+    lib = _lib.load()
+    dev = scores.device
+    _need(scores, "scores", (cfg.batch, cfg.num_kv_heads, cfg.num_blocks), torch.float32, dev)
+    _need(seq_lens, "seq_lens", (cfg.batch,), torch.int32, dev)
+    os_ = torch.empty((cfg.batch, cfg.num_kv_heads, cfg.top_blocks), dtype=torch.float32, device=dev)
+    ob = torch.empty((cfg.batch, cfg.num_kv_heads, cfg.top_blocks), dtype=torch.int32, device=dev)
+    cc = cfg.c()
+    _lib.check(lib.tls_block_topk(ctypes.byref(cc), scores.data_ptr(), seq_lens.data_ptr(), int(block_offset),
+                                  os_.data_ptr(), ob.data_ptr(), _stream(dev)))
+    return os_, ob
+
+
+def select_range(ids: torch.Tensor, lo: int, hi: int):
+    """The ids of each row (ascending, -1 padded) in [lo, hi), shifted by -lo, compacted, -1 padded.
+    Returns (ids, count)."""
+    lib = _lib.load()
+    dev = ids.device
+    _need(ids, "ids", tuple(ids.shape), torch.int32, dev)
+    k = ids.shape[-1]
+    rows = ids.numel() // k
+    out = torch.empty_like(ids)
+    cnt = torch.empty(ids.shape[:-1], dtype=torch.int32, device=dev)
+    _lib.check(lib.tls_select_range(rows, k, ids.data_ptr(), int(lo), int(hi), out.data_ptr(), cnt.data_ptr(),
+                                    _stream(dev)))
+    return out, cnt
+
+
+def token_stats(cfg: TLSConfig, q: torch.Tensor, seq_lens: torch.Tensor, index: TLSIndex, block_ids: torch.Tensor):
+    """This rank's per-head softmax statistics of a3 over its candidate blocks: [batch, Hkv, G, 2]
+    = (max_j L_hj, sum_j 2^(L_hj - max)), L in log2 units."""
+    lib = _lib.load()
+    dev = q.device
+    _need(q, "q", (cfg.batch, cfg.num_q_heads, cfg.d_k), cfg.dtype, dev)
+    _need(seq_lens, "seq_lens", (cfg.batch,), torch.int32, dev)
+    _need(block_ids, "block_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_blocks), torch.int32, dev)
+    st = torch.empty((cfg.batch, cfg.num_kv_heads, cfg.G, 2), dtype=torch.float32, device=dev)
+    cc, ic = cfg.c(), index.c()
+    _lib.check(lib.tls_token_stats(ctypes.byref(cc), q.data_ptr(), seq_lens.data_ptr(), ctypes.byref(ic),
+                                   block_ids.data_ptr(), st.data_ptr(), _stream(dev)))
+    return st
+
+
+def token_keys(cfg: TLSConfig, q: torch.Tensor, seq_lens: torch.Tensor, index: TLSIndex, block_ids: torch.Tensor,
+               stats_parts: torch.Tensor, token_offset: int):
+    """ln alpha~ of this rank's candidates under the normaliser merged from every rank's token_stats
+    (stats_parts [P, batch, Hkv, G, 2]) and their global token ids: ([batch, Hkv, k_b*B] x 2)."""
+    lib = _lib.load()
+    dev = q.device
+    _need(q, "q", (cfg.batch, cfg.num_q_heads, cfg.d_k), cfg.dtype, dev)
+    _need(block_ids, "block_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_blocks), torch.int32, dev)
+    P = stats_parts.shape[0]
+    _need(stats_parts, "stats_parts", (P, cfg.batch, cfg.num_kv_heads, cfg.G, 2), torch.float32, dev)
+    n = cfg.top_blocks * cfg.block_size
+    keys = torch.empty((cfg.batch, cfg.num_kv_heads, n), dtype=torch.float32, device=dev)
+    tids = torch.empty((cfg.batch, cfg.num_kv_heads, n), dtype=torch.int32, device=dev)
+    cc, ic = cfg.c(), index.c()
+    _lib.check(lib.tls_token_keys(ctypes.byref(cc), q.data_ptr(), seq_lens.data_ptr(), ctypes.byref(ic),
+                                  block_ids.data_ptr(), P, stats_parts.data_ptr(), int(token_offset), keys.data_ptr(),
+                                  tids.data_ptr(), _stream(dev)))
+    return keys, tids
+
+
+def attn_merge(cfg: TLSConfig, parts_out: torch.Tensor, parts_lse: torch.Tensor):
+    """LSE merge of P partial attention results: parts_out [P, batch, Hq, d_v], parts_lse [P, batch, Hq].
+    Returns (out, lse)."""
+    lib = _lib.load()
+    dev = parts_out.device
+    P = parts_out.shape[0]
+    _need(parts_out, "parts_out", (P, cfg.batch, cfg.num_q_heads, cfg.d_v), torch.float32, dev)
+    _need(parts_lse, "parts_lse", (P, cfg.batch, cfg.num_q_heads), torch.float32, dev)
+    out = torch.empty((cfg.batch, cfg.num_q_heads, cfg.d_v), dtype=cfg.dtype, device=dev)
+    lse = torch.empty((cfg.batch, cfg.num_q_heads), dtype=torch.float32, device=dev)
+    cc = cfg.c()
+    _lib.check(lib.tls_attn_merge(ctypes.byref(cc), P, parts_out.data_ptr(), parts_lse.data_ptr(), out.data_ptr(),
+                                  lse.data_ptr(), _stream(dev)))
+    return out, lse
+
+
 def _sel_outputs(cfg: TLSConfig, dev, out):
     if out is not None:
         return out
@@ -248,8 +347,9 @@ def select(cfg: TLSConfig, q: torch.Tensor, seq_lens: torch.Tensor, index: TLSIn
 
 
 def sparse_attend(cfg: TLSConfig, q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor | None,
-                  token_ids: torch.Tensor, num_tokens: torch.Tensor, out=None, lse=None):
-    """Attention over the selected tokens.  Returns (out, lse)."""
+                  token_ids: torch.Tensor, num_tokens: torch.Tensor, out=None, lse=None, out_f32: bool = False):
+    """Attention over the selected tokens.  Returns (out, lse); out in the cfg dtype, or
+    fp32 with out_f32 (tls_sparse_attend_f32: partial results that are merged later)."""
     lib = _lib.load()
     dev = q.device
     _need(q, "q", (cfg.batch, cfg.num_q_heads, cfg.d_k), cfg.dtype, dev)
@@ -259,12 +359,14 @@ def sparse_attend(cfg: TLSConfig, q: torch.Tensor, k_cache: torch.Tensor, v_cach
     _need(token_ids, "token_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_tokens), torch.int32, dev)
     _need(num_tokens, "num_tokens", (cfg.batch, cfg.num_kv_heads), torch.int32, dev)
     if out is None:
-        out = torch.empty((cfg.batch, cfg.num_q_heads, cfg.d_v), dtype=cfg.dtype, device=dev)
+        out = torch.empty((cfg.batch, cfg.num_q_heads, cfg.d_v), dtype=torch.float32 if out_f32 else cfg.dtype,
+                          device=dev)
     if lse is None:
         lse = torch.empty((cfg.batch, cfg.num_q_heads), dtype=torch.float32, device=dev)
     cc = cfg.c()
     ws, wsb = _workspace(cfg, dev, 1)
-    _lib.check(lib.tls_sparse_attend(ctypes.byref(cc), q.data_ptr(), k_cache.data_ptr(),
+    fn = lib.tls_sparse_attend_f32 if out_f32 else lib.tls_sparse_attend
+    _lib.check(fn(ctypes.byref(cc), q.data_ptr(), k_cache.data_ptr(),
                                      v_cache.data_ptr() if (v_cache is not None and cfg.layout == "gqa") else 0,
                                      token_ids.data_ptr(), num_tokens.data_ptr(), out.data_ptr(), lse.data_ptr(),
                                      ws, wsb, _stream(dev)))

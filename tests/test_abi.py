@@ -22,7 +22,7 @@ def lib():
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "tls.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(tls_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(tls_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(lib):

@@ -106,3 +106,24 @@ def test_shard_workload_strong_scaling():
     w4 = W.CONFIGS["c4"]
     parts = [D.shard_workload(w4, r, 4) for r in range(4)]
     assert sum(p.batch for p in parts) == w4.batch
+
+
+def test_bench_self_launches_n_ranks():
+    """`bench.py --gpus 2` without a launcher re-execs itself under torch.distributed.run (two ranks, gloo on
+    a CPU box): rank 0 prints n_gpus 2 and the strong-scaling KV-head shard plan of BASELINE.json configs[2]."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["plan"] == {"axis": "kv_head", "per_rank": 4}
+    assert sorted(tuple(x) for x in line["ranks"]) == [(0, 0, 32, 0, 4), (1, 0, 32, 4, 8)]

@@ -2,7 +2,7 @@
 its %globaltimer stamps (TLS_DEBUG_BUF): for every ticket (start, end, SM,
 role, sub).  Prints per-role item durations and, per role, when the items ran
 (start/end percentiles) plus the busy time per SM.  Not a bench line.
-    python tools/pstep_timeline.py c3 [L1,L2,L3]"""
+    python tools/pstep_timeline.py c3 [_ [batch]]"""
 import os
 import sys
 
@@ -15,8 +15,7 @@ import paper_2604_07815_b200 as tls  # noqa: E402
 from paper_2604_07815_b200 import workloads as W  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
-if len(sys.argv) > 2:
-    os.environ["TLS_PSTEP"] = sys.argv[2]
+os.environ.setdefault("TLS_PSTEP", "1")
 w = W.CONFIGS[name]
 if len(sys.argv) > 3:
     w = w.with_(batch=int(sys.argv[3]))
@@ -66,3 +65,13 @@ busy = np.zeros(int(sm.max()) + 1)
 for s_, a, b in zip(sm, st, en):
     busy[s_] += b - a
 print(f"  end {en.max():.1f} us; busy CTA-us per SM: median {np.median(busy):.0f}, max {busy.max():.0f}")
+# per-tile stamps of run_tiles (dbg[2^19 + 3 t]: issue, first rows landed, scored)
+ts = buf[(1 << 19):(1 << 19) + 3 * 20000].view(-1, 3).cpu().numpy().astype(np.int64)
+ts = ts[(ts[:, 0] > 0) & (ts[:, 2] > 0)]
+if len(ts):
+    lat = (ts[:, 1] - ts[:, 0]) / 1e3
+    cmp_ = (ts[:, 2] - ts[:, 1]) / 1e3
+    print(f"  tiles {len(ts)}: issue->landed us " + " ".join(f"{np.percentile(lat, p):6.2f}" for p in pct) +
+          " | landed->scored " + " ".join(f"{np.percentile(cmp_, p):6.2f}" for p in pct))
+    iss = np.sort((ts[:, 0] - t0) / 1e3)
+    print("  tile issue times us p0..p100: " + " ".join(f"{np.percentile(iss, p):6.1f}" for p in pct))
