@@ -247,7 +247,11 @@ tls_status tls_cache_fetch(const tls_config* cfg, const void* k_host, const void
  * of M_t that are not resident (in M_t order: the cache state is
  * deterministic), copies their B rows of K (and V) from pinned, device-mapped
  * host memory with a zero-copy gather, and writes the number of blocks fetched
- * per pair to miss_count (nullable): the transfer T_t = M_t \ C_t of P:378.
+ * per pair to miss_count (nullable): the transfer T_t = M_t \ C_t of P:378,
+ * where the resident set before the update is C_t = M_{t-2} u M_{t-1} (the
+ * previous update kept M_{t-2} and added M_{t-1}), a superset of the paper's
+ * C_t = M_{t-1} -- so |T_t| <= |M_t \ M_{t-1}| (tests/test_gpu_decode_loop.py
+ * checks the exact ledger on stationary, alternating and drifting queries).
  * keep_block_ids may be NULL (nothing pinned).  tls_block_cache_rows writes
  * the cache row slot_of_block[t / B] * B + t % B of every selected token
  * (0 past num_tokens or when the token's block is not resident, counted in
