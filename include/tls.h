@@ -412,8 +412,11 @@ int32_t tls_select_mode(const tls_config* cfg);
 
 /* CTAs per (batch, KV-head) pair -- the thread-block cluster size -- of the
  * token-select kernel (which = 0 or 2) or of the attention kernel (which = 1);
- * -1 for an invalid configuration.  The environment variable TLS_CLUSTER
- * overrides the heuristic for both (1, 2, 4, 8 or 16). */
+ * which = 3: the tokens per staged chunk of the MLA attention plan of
+ * tls_sparse_attend (64, or 32 when the selected-token list leaves no room for
+ * 64-token double buffering; 0 for GQA).  -1 for an invalid configuration.
+ * The environment variable TLS_CLUSTER overrides the heuristic for both
+ * cluster sizes (1, 2, 4, 8 or 16). */
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which);
 
 /* Live per-kernel device timing (diagnostics; used by bench.py for the

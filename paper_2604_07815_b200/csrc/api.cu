@@ -22,6 +22,8 @@
 namespace tls {
 cudaError_t launch_select_fused(const FusedParams& p, cudaStream_t st, const LaunchOpts& o);
 cudaError_t launch_qq(const FusedParams& p, cudaStream_t st, const LaunchOpts& o);
+cudaError_t launch_stream_select(const FusedParams& p, int grid, cudaStream_t st, const LaunchOpts& o);
+size_t stream_select_smem(int tb, size_t worker_bytes);
 cudaError_t launch_cache_fetch(const CacheFetchParams& p, cudaStream_t st);
 cudaError_t launch_block_cache_update(const BlockCacheParams& p, cudaStream_t st);
 cudaError_t launch_block_cache_rows(const BlockCacheParams& p, cudaStream_t st);
@@ -288,6 +290,7 @@ int score_tile_rows(int rowbytes) {
 
 struct ChainPlan {
   int mode;
+  int stream_sel;  // a1 + a2 by the persistent streaming kernel (one CTA per SM, TMA ring)
   tls::FusedParams fp;
   tls::SelectParams sp;  // mode 1
   tls::AttendParams ap;  // do_attend, or mode 1
@@ -305,6 +308,21 @@ tls_status plan_chain(const tls_config* cfg, int do_attend, ChainPlan& c) {
   if (c.fp.tb < 1) return fail(TLS_ERR_UNSUPPORTED, "block summary row larger than the K1 tile");
   tls::plan_fused(c.fp, sizeof(tls::FastTopKCtl));
   if ((int)c.fp.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "selection-kernel shared-memory plan does not fit");
+  {  // bf16 GQA with 512-byte summary rows: the streaming select kernel (fused.cu stream_select_kernel)
+    const char* e = getenv("TLS_STREAM_SEL");  // opt-in experiment ("1"): slower, DESIGN.md §5.1
+    c.stream_sel = c.mode == 1 && cfg->dtype == TLS_BF16 && cfg->layout == TLS_GQA && cfg->d_k == 128 &&
+                   e != nullptr && e[0] == '1';
+    if (c.stream_sel) {
+      const size_t worker = c.fp.off_fk + tls::align16(sizeof(tls::FastTopKCtl));
+      c.fp.tb = 56;  // 28 KB stages: 7 row groups (warps 0-6)
+      c.fp.smem_bytes = (unsigned)tls::stream_select_smem(c.fp.tb, worker);
+      if (c.fp.smem_bytes == 0) {  // the a2 worker regions (M-sized key list) do not fit one stage
+        c.stream_sel = 0;
+        c.fp.tb = score_tile_rows(2 * cfg->d_k * (int)elem_bytes(cfg));
+        tls::plan_fused(c.fp, sizeof(tls::FastTopKCtl));
+      }
+    }
+  }
   tls_status s = TLS_OK;
   if (c.mode == 1) {
     s = plan_select(cfg, c.sp);
@@ -422,6 +440,8 @@ tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int
   fp.qfrag = reinterpret_cast<uint8_t*>(ws + c.w.qfrag);
   fp.block_ids = a.block_ids;
   fp.ready = reinterpret_cast<unsigned*>(ws + c.w.ready_b);
+  fp.tcount = reinterpret_cast<unsigned*>(ws + c.w.tcount);
+  fp.sched = reinterpret_cast<unsigned*>(ws + c.w.sched);
   fp.epoch = epoch;
   fp.dbg = env_debug_buf();
   fp.qq = reinterpret_cast<float*>(ws + c.w.qq);
@@ -434,8 +454,16 @@ tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int
   if (e != cudaSuccess) return cuda_fail(e, "qq_kernel launch");
   tls::LaunchOpts lo_sel = lo_k1;
   lo_sel.pdl = lo_dep.pdl;  // select_kernel streams its tiles while qq_kernel finishes
-  e = tls::launch_select_fused(fp, st, lo_sel);
-  if (e != cudaSuccess) return cuda_fail(e, "select_kernel launch");
+  if (c.stream_sel) {
+    const int tiles = cfg->batch * cfg->num_kv_heads * ((fp.d.M + fp.tb - 1) / fp.tb);
+    // two CTAs per SM are launched; one per SM streams (the other exits at once: placement, fused.cu)
+    (void)tiles;
+    e = tls::launch_stream_select(fp, 2 * num_sms(), st, lo_sel);
+    if (e != cudaSuccess) return cuda_fail(e, "stream_select_kernel launch");
+  } else {
+    e = tls::launch_select_fused(fp, st, lo_sel);
+    if (e != cudaSuccess) return cuda_fail(e, "select_kernel launch");
+  }
   if (timed) g_timer.mark(st);
   tls::SelectParams& sp = c.sp;
   if (c.mode == 1) {
@@ -1046,7 +1074,12 @@ int32_t tls_select_mode(const tls_config* cfg) {
 }
 
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which) {
-  if (check_config(cfg) != TLS_OK || which < 0 || which > 2) return -1;
+  if (check_config(cfg) != TLS_OK || which < 0 || which > 3) return -1;
+  if (which == 3) {  // the MLA attention plan's tokens per staged chunk of tls_sparse_attend (64 or 32; 0: GQA)
+    tls::AttendParams ap;
+    if (plan_attend(cfg, ap, 0, 1) != TLS_OK) return -1;
+    return cfg->layout == TLS_MLA ? ap.mla_tc : 0;
+  }
   tls::PStepParams sk;
   if (which != 1 && pstep_plan(cfg, 1, sk)) return sk.ns;  // attention slices per pair
   tls::AttendParams ap;

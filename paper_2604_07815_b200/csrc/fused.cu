@@ -289,6 +289,306 @@ __global__ void __launch_bounds__(kThreads, CPL <= 2 ? 6 : 3) select_kernel(cons
   pair_worker(p, pair, m, smem, ctl.tk, dbg);
 }
 
+// ---------------------------------------------------------------------------
+// Streaming form of a1 + a2 (bf16 GQA, d_k = 128: 512-byte summary rows) -- OPT-IN (TLS_STREAM_SEL=1):
+// measured slower than the tile-per-CTA select_kernel (C3 serialised a1+a2 115 vs 58 us; overlapped step 180 vs
+// 128 us: one streamer CTA per SM sustains ~1.4 us per 28 KB stage, ~3 TB/s).
+// one persistent CTA per SM streams the block summaries through a ring of
+// kRing TMA stages (tb rows each), so that the HBM stream needs one CTA slot
+// per SM instead of six and the token kernel -- launched as this kernel's PDL
+// secondary, released at once because every streamer starts immediately --
+// runs on the other slots while a1 is still streaming.
+// Placement: 2 x #SM CTAs are launched (at most two fit an SM by shared
+// memory, so every SM receives two); the first to arrive on an SM (per-SM
+// word, the call's epoch) streams, the other exits at once and leaves its slot
+// to the token kernel.  (148 CTAs alone were packed two per SM onto 75 SMs.)
+// Warp specialisation: warp 7 lane 0 produces, warps 0-6 consume.  The
+// producer claims tiles from one counter (one claim ahead: each atomic's value
+// is read one tile later), waits until a stage is empty (mbarrier, one arrival
+// per consumer warp), records the ticket in the stage's slot and issues the
+// tile's copies (one TMA bulk copy + mbarrier per 8-row group).  Consumer warp
+// w scores row group w of each tile (s_i = Q+ . k^max_i + Q- . k^min_i, P:99
+// via P:110 and linearity of sum_h) and arrives on the stage's empty barrier;
+// it never waits for the producer's bookkeeping (a per-tile CTA barrier held
+// every tile behind it: 2.4 us per 28 KB tile).
+// Completion: when a stage comes back empty the producer counts its tile in
+// the pair's count of scored tiles (a hint; the scores themselves, against
+// the sentinel, are the data).  The CTA that claimed a pair's last tile (by
+// index) owns its a2; once the count is complete the producer posts an a2
+// marker into the next stage instead of a tile, and when the consumers reach
+// it (in ring order) all eight warps run pair_worker together while
+// the other stages' copies are in flight.  No CTA waits for another while
+// tiles remain, so the streams never fall into lockstep (a "last tile waits
+// for the others" rule: 331 us per a1 at C3) and the a2 work does not pile up
+// on the slowest CTA (a "last to count runs a2" rule: 412 us).
+constexpr int kRing = 4;
+constexpr int kPend = 16;          // pending a2 pairs per streamer
+constexpr int kEnd = -1;           // stage slot: no more tiles
+constexpr int kSkip = -0x7fffffff;  // stage slot: nothing (the producer waits for a2 counts without blocking)
+
+__device__ __forceinline__ void red_relaxed_add_gpu(unsigned* p, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 4) stream_select_kernel(const __grid_constant__ FusedParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];  // [kRing][tb rows][row] | the a2 worker regions
+  __shared__ __align__(8) uint64_t bars[kRing];      // full[stage]: the tile's rows and its pair's QQ landed
+  __shared__ __align__(16) float sqq[kRing][256];    // the tile's pair's [Q+ | Q-] per stage
+  __shared__ __align__(8) uint64_t empty[kRing];     // stage consumed (kConsumers arrivals)
+  __shared__ WorkerCtl ctl;
+  __shared__ int s_tick[kRing], s_role;
+  launch_dependents();  // the token kernel starts now, on the slots the streamers leave free
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kRow = 2 * 128 * (int)sizeof(T);
+  constexpr int kCons = kWarps - 1;  // consumer warps 0..6 (tb <= 56 rows: 7 row groups)
+  const int ntile = (d.M + p.tb - 1) / p.tb;
+  const int total = d.batch * d.Hkv * ntile;
+  unsigned* next = p.sched;           // tile ticket counter
+  unsigned* out_ctr = p.sched + 1;    // CTAs out
+  unsigned* sm_word = p.sched + 32;   // per SM: epoch of the call whose streamer it hosts
+  unsigned long long* dbg = p.dbg ? p.dbg + (size_t)blockIdx.x * 256 : nullptr;  // diagnostics (TLS_DEBUG_BUF)
+  struct Tile {
+    int pair, tile, i0, nb, ntl, m;
+  };
+  auto tile_of = [&](int t) {
+    Tile r;
+    r.pair = t / ntile;
+    r.tile = t - r.pair * ntile;
+    const int b = r.pair / d.Hkv;
+    const int n = min(max(p.seq_lens[b], 0), d.S);
+    r.m = (n + d.B - 1) >> d.log2B;  // reading U1
+    r.ntl = max(1, (r.m + p.tb - 1) / p.tb);
+    r.i0 = r.tile * p.tb;
+    r.nb = r.tile < r.ntl ? max(0, min(p.tb, r.m - r.i0)) : -1;  // -1: past the pair's sequence
+    return r;
+  };
+  auto worker = [&](int pair, uint8_t* a2) {  // a2 of a pair whose every tile is scored (all 256 threads);
+    // a2: the worker regions -- the stage of the a2 marker's slot, which holds no rows
+    const int b = pair / d.Hkv;
+    const int n = min(max(p.seq_lens[b], 0), d.S);
+    const int m = (n + d.B - 1) >> d.log2B;
+    uint32_t* bkeys = reinterpret_cast<uint32_t*>(a2 + p.off_bkeys);
+    const unsigned* sc = reinterpret_cast<const unsigned*>(p.scores + (size_t)pair * p.sstride);
+    // the scores are the data (a sentinel means not yet visible): 16-byte L2 loads, all issued before any is
+    // tested (the row stride is a multiple of 4 floats), then a per-vector re-poll where a sentinel remains
+    constexpr int kV = 4;  // vectors per thread per batch
+    for (int v0 = 0; v0 * 4 < m; v0 += kV * kThreads) {
+      uint4 v[kV];
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const int vi = v0 + u * kThreads + tid;
+        v[u] = vi * 4 < m ? __ldcg(reinterpret_cast<const uint4*>(sc) + vi) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const int vi = v0 + u * kThreads + tid;
+        if (vi * 4 >= m) continue;
+        unsigned spins = 0;
+        while ((v[u].x == kScoreSentinel && vi * 4 < m) || (v[u].y == kScoreSentinel && vi * 4 + 1 < m) ||
+               (v[u].z == kScoreSentinel && vi * 4 + 2 < m) || (v[u].w == kScoreSentinel && vi * 4 + 3 < m)) {
+          __nanosleep(64);
+          if (++spins > (1u << 24)) __trap();
+          v[u] = __ldcg(reinterpret_cast<const uint4*>(sc) + vi);
+        }
+        const unsigned w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (vi * 4 + e < m) bkeys[vi * 4 + e] = f2key(__uint_as_float(w[e]));
+      }
+    }
+    if (tid == 0) p.tcount[pair] = 0u;  // reset for the next call (no other user left)
+    __syncthreads();
+    pair_worker(p, pair, m, a2, ctl.tk, nullptr);
+    __syncthreads();  // the worker regions are reused by the next worker
+  };
+  if (tid == 0) {
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    s_role = atomicMax(sm_word + smid, p.epoch) < p.epoch;  // the first CTA of this call on this SM streams
+    if (s_role) {
+      for (int i = 0; i < kRing; ++i) mbar_init(&bars[i], 1);
+      for (int i = 0; i < kRing; ++i) mbar_init(&empty[i], kCons);
+      mbar_fence_init();
+    }
+  }
+  __syncthreads();
+  if (s_role) {
+    if (dbg && tid == 0) dbg[0] = gtimer();
+    const bool prod = tid == kCons * 32;  // warp 7 lane 0
+    // ---- producer state (meaningful in the producer thread only) ----
+    __shared__ int pend[kPend];  // pairs whose a2 this CTA owns, oldest first (producer only)
+    int npend = 0;
+    unsigned seen = 0u;          // the count of pend[0] as read one slot earlier (a hint)
+    unsigned eph = 0u;           // empty barriers' phase parities
+    unsigned ahead = 0u;         // the ticket claimed one slot ahead
+    bool tickets = true, ended = false;
+    if (prod) ahead = atomicAdd(next, 1u);
+    // post slot j into stage j % kRing: a tile ticket (>= 0), an a2 marker (-2 - pair) or the end (-1)
+    auto post_slot = [&](int j) {
+      const int st = j % kRing;
+      if (j >= kRing) {  // the stage's previous slot is consumed
+        mbar_wait(&empty[st], (eph >> st) & 1u);
+        eph ^= 1u << st;
+      }
+      if (ended) return;
+      // never block here: a pending pair's tiles may sit in this CTA's own ring, unconsumed
+      int post = kEnd;
+      for (;;) {
+        if (npend > 0) {
+          const int pair = pend[0];
+          const int m = (min(max(p.seq_lens[pair / d.Hkv], 0), d.S) + d.B - 1) >> d.log2B;
+          const unsigned need = (unsigned)max(1, (m + p.tb - 1) / p.tb);
+          if (seen >= need) {
+            post = -2 - pair;
+            for (int i = 1; i < npend; ++i) pend[i - 1] = pend[i];
+            --npend;
+            seen = 0u;
+            break;
+          }
+        }
+        if (tickets && npend < kPend && ahead < (unsigned)total) {
+          post = (int)ahead;
+          ahead = atomicAdd(next, 1u);
+          const Tile r = tile_of(post);
+          if (r.nb >= 0 && r.tile == r.ntl - 1) pend[npend++] = r.pair;  // this CTA owns the pair's a2
+          break;
+        }
+        if (ahead >= (unsigned)total) tickets = false;
+        if (npend > 0) {  // a count not complete yet: a skip slot (the consumers pass it) and look again
+          post = kSkip;
+          __nanosleep(200);
+        }
+        break;  // (npend == 0 and no tickets: the end)
+      }
+      s_tick[st] = post;
+      if (post >= 0) {
+        const Tile r = tile_of(post);
+        if (r.nb > 0) {  // one bulk copy of the rows and one of the pair's QQ (qq_kernel) per stage
+          const uint8_t* src =
+              reinterpret_cast<const uint8_t*>(p.block_minmax) + ((size_t)r.pair * d.M + r.i0) * kRow;
+          mbar_arrive_expect_tx(&bars[st], (uint32_t)(r.nb * kRow + 2 * 128 * 4));
+          tma_bulk_g2s(smem + (size_t)st * p.tb * kRow, src, (uint32_t)(r.nb * kRow), &bars[st]);
+          tma_bulk_g2s(sqq[st], p.qq + (size_t)r.pair * 2 * 128, 2 * 128 * 4, &bars[st]);
+        } else {
+          mbar_arrive(&bars[st]);  // no rows: the slot is posted
+        }
+      } else {
+        mbar_arrive(&bars[st]);  // an a2 marker, a skip or the end
+        if (post == kEnd) ended = true;
+      }
+      if (npend > 0) seen = ld_relaxed_gpu(p.tcount + pend[0]);  // look again at the next slot
+    };
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // QQ, q fragments, zeroed histograms (qq_kernel)
+    if (prod)
+      for (int j = 0; j < kRing - 1; ++j) post_slot(j);
+    unsigned cph = 0u;  // consumers: full barriers' phase parities (the same in every consumer thread)
+    for (int k = 0;; ++k) {
+      const int st = k % kRing;
+      if (warp == kCons) {  // the producer posts slot k + kRing - 1 (its stage held slot k - 1)
+        if (prod) post_slot(k + kRing - 1);
+        __syncwarp();
+      }
+      if (dbg && tid == 0 && k < 60) dbg[8 + 4 * k] = gtimer();
+      mbar_wait(&bars[st], (cph >> st) & 1u);  // slot k is posted (and its rows and QQ landed)
+      cph ^= 1u << st;
+      const int t = s_tick[st];
+      if (t == kEnd) break;
+      if (t < 0) {  // an a2 marker or a skip
+        if (warp < kCons) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);
+        }
+        if (t != kSkip) worker(-2 - t, smem + (size_t)st * p.tb * kRow);  // ===== a2: all eight warps =====
+        continue;
+      }
+      const Tile r = tile_of(t);
+      const int ngrp = r.nb > 0 ? (r.nb + 7) >> 3 : 0;
+      if (warp < ngrp) {
+        float qreg[8];
+        {
+          const float4 qa = reinterpret_cast<const float4*>(sqq[st])[lane * 2];
+          const float4 qb = reinterpret_cast<const float4*>(sqq[st])[lane * 2 + 1];
+          qreg[0] = qa.x, qreg[1] = qa.y, qreg[2] = qa.z, qreg[3] = qa.w;
+          qreg[4] = qb.x, qreg[5] = qb.y, qreg[6] = qb.z, qreg[7] = qb.w;
+        }
+        if (dbg && tid == 0 && k < 60) dbg[9 + 4 * k] = gtimer();
+        const uint8_t* tile = smem + (size_t)st * p.tb * kRow;
+        const int r8 = warp * 8;
+        float acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc[u] = 0.f;
+          if (r8 + u < r.nb) {
+            float f[8];
+            unpack16<T>(reinterpret_cast<const uint4*>(tile + (size_t)(r8 + u) * kRow)[lane], f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[u] = fmaf(qreg[e], f[e], acc[u]);
+          }
+        }
+        // transposed butterfly: lanes 4u..4u+3 end with the dot product of row u
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool up = lane & 16;
+          const float send = up ? acc[j] : acc[j + 4];
+          const float keep = up ? acc[j + 4] : acc[j];
+          acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const bool up = lane & 8;
+          const float send = up ? acc[j] : acc[j + 2];
+          const float keep = up ? acc[j + 2] : acc[j];
+          acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+          const bool up = lane & 4;
+          const float send = up ? acc[0] : acc[1];
+          const float keep = up ? acc[1] : acc[0];
+          acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
+        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+        const int u = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        if ((lane & 3) == 0 && r8 + u < r.nb) p.scores[(size_t)r.pair * p.sstride + r.i0 + r8 + u] = acc[0];
+      }
+      if (warp < kCons) {
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&empty[st]);  // this warp is done with the stage
+          if (warp == 0 && r.nb >= 0) red_relaxed_add_gpu(p.tcount + r.pair, 1u);  // count the tile (hint)
+        }
+      }
+    }
+    if (dbg && tid == 0) {
+      unsigned smid;
+      asm("mov.u32 %0, %%smid;" : "=r"(smid));
+      dbg[1] = gtimer();
+      dbg[2] = smid;
+    }
+  }
+  if (tid == 0 && atomicAdd(out_ctr, 1u) == gridDim.x - 1) {  // the last CTA out resets the counters
+    *next = 0u;
+    *out_ctr = 0u;
+  }
+}
+
+cudaError_t launch_stream_select(const FusedParams& p, int grid, cudaStream_t st, const LaunchOpts& o) {
+  auto kern = stream_select_kernel<__nv_bfloat16>;
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, false);
+  if (e != cudaSuccess) return e;
+  return launch_ex(kern, dim3((unsigned)grid), kThreads, p.smem_bytes, st, o, 0, p);
+}
+
+// The worker regions use the stage of the a2 marker's slot, so they must fit one stage.
+size_t stream_select_smem(int tb, size_t worker_bytes) {
+  return worker_bytes <= (size_t)tb * 512 ? (size_t)kRing * tb * 512 : 0;
+}
+
 // Per-pair query-side work once per call: QQ = [Q+ | Q-] (fp32, P:110 +
 // linearity of sum_h), so that the ceil(M / tb) tile CTAs of a pair do not each
 // re-read the pair's G query rows (MLA: 32 x 576 bf16 per tile), and the token

@@ -52,6 +52,8 @@ struct FusedParams {
   uint8_t* qfrag;          // workspace [pairs, qfrag_bytes(d)]: q~ fragment blobs for the token kernel
   int* block_ids;          // [pairs, Kb] out: M_t ascending, -1 padded
   unsigned* ready;         // workspace [pairs]: set to `epoch` when the pair's a2 outputs are written
+  unsigned* tcount;        // workspace [pairs]: scored tiles of the pair (stream_select_kernel; reset by a2)
+  unsigned* sched;         // workspace [256]: stream_select_kernel's ticket / exit counters, per-SM streamer epoch
   unsigned epoch;          // this call's hand-off value (host call counter, never 0)
   unsigned long long* dbg; // diagnostics only (env TLS_DEBUG_BUF): worker phase stamps
   unsigned off_bkeys, off_scratch, off_fk, smem_bytes;
@@ -335,7 +337,7 @@ static inline int qfrag_bytes(const Dims& d) {
 }
 
 struct SelectWs {
-  size_t scores, keys, khist, qfrag, ready_b, ready_t, qq, total;
+  size_t scores, keys, khist, qfrag, ready_b, ready_t, tcount, sched, qq, total;
 };
 static inline SelectWs select_workspace(const Dims& d) {
   SelectWs w;
@@ -347,7 +349,9 @@ static inline SelectWs select_workspace(const Dims& d) {
   w.qfrag = w.khist + a256(pairs * kKeyBins * 4);
   w.ready_b = w.qfrag + a256(pairs * (size_t)qfrag_bytes(d));
   w.ready_t = w.ready_b + a256(pairs * 4);
-  w.qq = w.ready_t + a256(pairs * 4);
+  w.tcount = w.ready_t + a256(pairs * 4);
+  w.sched = w.tcount + a256(pairs * 4);
+  w.qq = w.sched + a256(256 * 4);
   w.total = w.qq + a256(pairs * 2 * (size_t)d.d_k * 4);
   return w;
 }

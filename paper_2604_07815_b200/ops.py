@@ -117,7 +117,7 @@ def _workspace(cfg: TLSConfig, dev: torch.device, which: int):
     # (the tuning variables that change the workspace layout -- sub-batch pipeline depth, attention split,
     # the persistent step kernel -- are part of the key: a workspace is only reused with its own layout)
     key = (dev, torch.cuda.current_stream(dev).cuda_stream, bytes(cc), which, nbytes,
-           tuple(os.environ.get(v) for v in ("TLS_NSPLIT", "TLS_CLUSTER", "TLS_PSTEP", "TLS_TILE_KB")))
+           tuple(os.environ.get(v) for v in ("TLS_NSPLIT", "TLS_CLUSTER", "TLS_PSTEP", "TLS_TILE_KB", "TLS_STREAM_SEL")))
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)

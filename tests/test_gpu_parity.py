@@ -503,6 +503,8 @@ def test_mla_attention_large_selection_uses_small_chunks():
     w = W.Workload("mla-big", 1, 32, 1, 576, 512, 131072, d_c=128, top_blocks=2048, top_tokens=131072, layout="mla",
                    sm_scale=1.0 / math.sqrt(192.0))
     cfg = tls.TLSConfig(**w.config_kwargs())
+    assert tls.cluster_size(cfg, 3) == 32  # the 32-token fallback plan is the one that runs
+    assert tls.cluster_size(tls.TLSConfig(**SMALL["mla"].config_kwargs()), 3) == 64
     g = torch.Generator(device=DEV).manual_seed(11)
     q = torch.randn((1, 32, 576), generator=g, device=DEV).to(torch.bfloat16)
     k = torch.randn((1, w.context, 576), generator=g, device=DEV).to(torch.bfloat16)
@@ -514,3 +516,19 @@ def test_mla_attention_large_selection_uses_small_chunks():
     torch.cuda.synchronize()
     torch.testing.assert_close(out[0].float(), ref, rtol=0, atol=2e-2)
     torch.testing.assert_close(lse[0], torch.logsumexp(s, dim=-1), rtol=0, atol=1e-2)
+
+
+@pytest.mark.parametrize("name", ["gqa4", "gqa8"])
+def test_streaming_select_experiment(name, monkeypatch):
+    """The opt-in streaming a1 + a2 kernel (TLS_STREAM_SEL=1, fused.cu stream_select_kernel: one streamer CTA
+    per SM, warp-specialised TMA ring, a2 markers) selects the same blocks and tokens as the oracle."""
+    monkeypatch.setenv("TLS_STREAM_SEL", "1")
+    w = SMALL[name]
+    cfg, inputs, idx = setup_case(w, seed=6)
+    for _ in range(3):  # repeated calls: the ticket / exit counters and per-SM words reset themselves
+        res = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    stats = {"block_near_ties": 0, "token_near_ties": 0}
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            check_pair(w, cfg, inputs, idx, res, b, g, stats)
