@@ -369,6 +369,27 @@ tls_status tls_sparse_attend_f32(const tls_config* cfg, const void* q, const voi
 tls_status tls_attn_merge(const tls_config* cfg, int32_t n_parts, const float* parts_out, const float* parts_lse,
                           void* out, float* lse, tls_stream_t stream);
 
+/*
+ * ---- The paper's comparison operators,
+ * built from the calls above:
+ *   Quest (block level only): tls_block_scores -> tls_block_topk (offset 0) ->
+ *     tls_expand_blocks -> tls_sparse_attend over every token of M_t;
+ *   DS (token level only, every block a candidate): tls_block_iota ->
+ *     tls_token_stats -> tls_token_keys (one part) -> tls_topk_rows(k_t) ->
+ *     tls_sparse_attend;
+ * (paper_2604_07815_b200/ops.py quest_decode, ds_decode).
+ *
+ * tls_expand_blocks: token_ids [batch, Hkv, k_out] = the tokens below
+ * seq_lens[b] of block_ids [batch, Hkv, top_blocks] (ascending, -1 padded),
+ * ascending, truncated to k_out, -1 padded; num_tokens [batch, Hkv].
+ * TLS_ERR_UNSUPPORTED for top_blocks > 1024.
+ * tls_block_iota: block_ids [batch, Hkv, top_blocks] = 0 .. m-1 (m =
+ * ceil(seq_lens[b] / B)), -1 padded (top_blocks >= m selects every block).
+ */
+tls_status tls_expand_blocks(const tls_config* cfg, const int32_t* block_ids, const int32_t* seq_lens,
+                             int32_t k_out, int32_t* token_ids, int32_t* num_tokens, tls_stream_t stream);
+tls_status tls_block_iota(const tls_config* cfg, const int32_t* seq_lens, int32_t* block_ids, tls_stream_t stream);
+
 /* Workspace bytes needed by: which = 0 tls_select, 1 tls_sparse_attend,
  * 2 tls_decode.  The select part holds the fp32 block scores of every pair,
  * per-chunk softmax statistics, the ranking key of every candidate token and a

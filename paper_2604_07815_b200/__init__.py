@@ -31,6 +31,8 @@ from .ops import (  # noqa: F401
     block_cache_rows,
     decode_block_cache,
     AsyncOffloadDecoder,
+    quest_decode,
+    ds_decode,
 )
 from ._lib import TLSError, load  # noqa: F401
 

@@ -31,6 +31,8 @@ EXPORTS = (
     "tls_token_keys",
     "tls_attn_merge",
     "tls_sparse_attend_f32",
+    "tls_expand_blocks",
+    "tls_block_iota",
     "tls_workspace_bytes",
     "tls_launch_count",
     "tls_cluster_size",
@@ -134,6 +136,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "tls_token_keys": (_I32, [_PCFG, _P, _P, _PIDX, _P, _I32, _P, _I32, _P, _P, _P]),
         "tls_attn_merge": (_I32, [_PCFG, _I32, _P, _P, _P, _P, _P]),
         "tls_sparse_attend_f32": (_I32, [_PCFG, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+        "tls_expand_blocks": (_I32, [_PCFG, _P, _P, _I32, _P, _P, _P]),
+        "tls_block_iota": (_I32, [_PCFG, _P, _P, _P]),
         "tls_select": (_I32, [_PCFG, _P, _P, _PIDX, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_sparse_attend": (_I32, [_PCFG, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
         "tls_cache_fetch": (_I32, [_PCFG, _P, _P, _P, _P, ctypes.POINTER(TLSTokenCacheC), _P, _P, _P]),

@@ -42,6 +42,9 @@ cudaError_t launch_topk_rows(int rows, int n, const float* keys, const int* ids,
 cudaError_t launch_select_range(int rows, int k, const int* ids, int lo, int hi, int* out_ids, int* out_count,
                                 cudaStream_t st);
 size_t token_split_smem(const Dims& d);
+cudaError_t launch_expand_blocks(const Dims& d, const int* block_ids, const int* seq_lens, int k_out, int* token_ids,
+                                 int* num_tokens, cudaStream_t st);
+cudaError_t launch_block_iota(const Dims& d, const int* seq_lens, int* block_ids, cudaStream_t st);
 cudaError_t launch_token_split(const Dims& d, int mode, const void* q, const int* seq_lens, const uint8_t* codes,
                                const float* scale_zero, const int* channels, const int* block_ids, int P,
                                const float* stats_in, float* stats_out, float* keys_out, int* ids_out, int tok_off,
@@ -798,6 +801,26 @@ tls_status tls_select_range(int32_t rows, int32_t k, const int32_t* ids, int32_t
   if (!ids || !out_ids) return fail(TLS_ERR_INPUT, "ids and out_ids are required");
   cudaError_t e = tls::launch_select_range(rows, k, ids, lo, hi, out_ids, out_count, (cudaStream_t)stream);
   return e == cudaSuccess ? TLS_OK : cuda_fail(e, "select_range_kernel launch");
+}
+
+tls_status tls_expand_blocks(const tls_config* cfg, const int32_t* block_ids, const int32_t* seq_lens,
+                             int32_t k_out, int32_t* token_ids, int32_t* num_tokens, tls_stream_t stream) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if (!block_ids || !seq_lens || !token_ids || !num_tokens || k_out < 1)
+    return fail(TLS_ERR_INPUT, "block_ids, seq_lens, token_ids, num_tokens and k_out >= 1 are required");
+  if (cfg->top_blocks > 1024) return fail(TLS_ERR_UNSUPPORTED, "top_blocks > 1024");
+  cudaError_t e = tls::launch_expand_blocks(dims_of(cfg), block_ids, seq_lens, k_out, token_ids, num_tokens,
+                                            (cudaStream_t)stream);
+  return e == cudaSuccess ? TLS_OK : cuda_fail(e, "expand_blocks_kernel launch");
+}
+
+tls_status tls_block_iota(const tls_config* cfg, const int32_t* seq_lens, int32_t* block_ids, tls_stream_t stream) {
+  tls_status s = check_config(cfg);
+  if (s) return s;
+  if (!seq_lens || !block_ids) return fail(TLS_ERR_INPUT, "seq_lens and block_ids are required");
+  cudaError_t e = tls::launch_block_iota(dims_of(cfg), seq_lens, block_ids, (cudaStream_t)stream);
+  return e == cudaSuccess ? TLS_OK : cuda_fail(e, "block_iota_kernel launch");
 }
 
 namespace {

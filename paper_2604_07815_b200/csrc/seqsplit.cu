@@ -184,6 +184,53 @@ __global__ void __launch_bounds__(kT) select_range_kernel(int k, const int* __re
 }
 
 // ---------------------------------------------------------------------------
+// The comparison operators of the paper:
+// expand_blocks -- Quest's token set: every token (below the sequence length)
+//   of the selected blocks, ascending (block ids ascending, -1 padded).
+// block_iota -- DS's candidate blocks: every block of the sequence.
+// One CTA per pair.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) expand_blocks_kernel(Dims d, const int* __restrict__ block_ids,
+                                                           const int* __restrict__ seq_lens, int k_out,
+                                                           int* token_ids, int* num_tokens) {
+  __shared__ int sh[32];
+  __shared__ int s_pre[1024 + 1];
+  const int pair = blockIdx.x, b = pair / d.Hkv;
+  const int n = min(max(seq_lens[b], 0), d.S);
+  const int* bl = block_ids + (size_t)pair * d.Kb;
+  int* out = token_ids + (size_t)pair * k_out;
+  // tokens per selected block (ascending ids: the output is the concatenation in block order)
+  int total = 0;
+  for (int base = 0; base < d.Kb; base += kT) {
+    const int i = base + threadIdx.x;
+    const int blk = i < d.Kb ? bl[i] : -1;
+    const int cnt = blk >= 0 ? max(0, min(d.B, n - blk * d.B)) : 0;
+    int tot;
+    const int pos = cta_exclusive_scan(cnt, sh, &tot);
+    if (i < d.Kb && i < 1024) s_pre[i] = total + pos;
+    total += tot;
+  }
+  if (threadIdx.x == 0) s_pre[min(d.Kb, 1024)] = total;
+  __syncthreads();
+  const int kk = min(total, k_out);
+  for (int i = 0; i < min(d.Kb, 1024); ++i) {  // block i's tokens, one per thread
+    const int blk = bl[i];
+    if (blk < 0) break;
+    const int c = s_pre[i + 1] - s_pre[i];
+    for (int r = threadIdx.x; r < c; r += kT)
+      if (s_pre[i] + r < kk) out[s_pre[i] + r] = blk * d.B + r;
+  }
+  for (int q = kk + threadIdx.x; q < k_out; q += kT) out[q] = -1;
+  if (threadIdx.x == 0) num_tokens[pair] = kk;
+}
+
+__global__ void __launch_bounds__(kT) block_iota_kernel(Dims d, const int* __restrict__ seq_lens, int* block_ids) {
+  const int pair = blockIdx.x, b = pair / d.Hkv;
+  const int m = (min(max(seq_lens[b], 0), d.S) + d.B - 1) / d.B;  // reading U1
+  for (int i = threadIdx.x; i < d.Kb; i += kT) block_ids[(size_t)pair * d.Kb + i] = i < m ? i : -1;
+}
+
+// ---------------------------------------------------------------------------
 // a3 on a rank's candidate blocks (block_ids: local block ids, ascending, -1
 // padded, k_b per pair) -- one CTA per pair.  Logits in log2 units
 // (reading U10: sm_scale = 1/sqrt(d)):
@@ -351,6 +398,17 @@ cudaError_t launch_topk_rows(int rows, int n, const float* keys, const int* ids,
 cudaError_t launch_select_range(int rows, int k, const int* ids, int lo, int hi, int* out_ids, int* out_count,
                                 cudaStream_t st) {
   select_range_kernel<<<rows, kT, 0, st>>>(k, ids, lo, hi, out_ids, out_count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand_blocks(const Dims& d, const int* block_ids, const int* seq_lens, int k_out, int* token_ids,
+                                 int* num_tokens, cudaStream_t st) {
+  expand_blocks_kernel<<<d.batch * d.Hkv, kT, 0, st>>>(d, block_ids, seq_lens, k_out, token_ids, num_tokens);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_iota(const Dims& d, const int* seq_lens, int* block_ids, cudaStream_t st) {
+  block_iota_kernel<<<d.batch * d.Hkv, kT, 0, st>>>(d, seq_lens, block_ids);
   return cudaGetLastError();
 }
 

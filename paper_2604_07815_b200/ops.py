@@ -39,6 +39,8 @@ __all__ = [
     "cache_fetch",
     "offload_decode",
     "timing_read",
+    "quest_decode",
+    "ds_decode",
 ]
 
 _DT = {torch.bfloat16: _lib.TLS_BF16, torch.float32: _lib.TLS_FP32}
@@ -313,6 +315,63 @@ def attn_merge(cfg: TLSConfig, parts_out: torch.Tensor, parts_lse: torch.Tensor)
     _lib.check(lib.tls_attn_merge(ctypes.byref(cc), P, parts_out.data_ptr(), parts_lse.data_ptr(), out.data_ptr(),
                                   lse.data_ptr(), _stream(dev)))
     return out, lse
+
+
+# ---- the paper's comparison operators, from the calls above
+def expand_blocks(cfg: TLSConfig, block_ids: torch.Tensor, seq_lens: torch.Tensor, k_out: int):
+    """Every token (below the sequence length) of the selected blocks, ascending: (token_ids, num_tokens)."""
+    lib = _lib.load()
+    dev = block_ids.device
+    _need(block_ids, "block_ids", (cfg.batch, cfg.num_kv_heads, cfg.top_blocks), torch.int32, dev)
+    tids = torch.empty((cfg.batch, cfg.num_kv_heads, k_out), dtype=torch.int32, device=dev)
+    nt = torch.empty((cfg.batch, cfg.num_kv_heads), dtype=torch.int32, device=dev)
+    cc = cfg.c()
+    _lib.check(lib.tls_expand_blocks(ctypes.byref(cc), block_ids.data_ptr(), seq_lens.data_ptr(), int(k_out),
+                                     tids.data_ptr(), nt.data_ptr(), _stream(dev)))
+    return tids, nt
+
+
+def block_iota(cfg: TLSConfig, seq_lens: torch.Tensor):
+    """Every block of each sequence as the candidate set ([batch, Hkv, top_blocks], -1 padded)."""
+    lib = _lib.load()
+    dev = seq_lens.device
+    out = torch.empty((cfg.batch, cfg.num_kv_heads, cfg.top_blocks), dtype=torch.int32, device=dev)
+    cc = cfg.c()
+    _lib.check(lib.tls_block_iota(ctypes.byref(cc), seq_lens.data_ptr(), out.data_ptr(), _stream(dev)))
+    return out
+
+
+def _with(cfg: TLSConfig, **kw) -> TLSConfig:
+    import dataclasses
+
+    return dataclasses.replace(cfg, **kw)
+
+
+def quest_decode(cfg: TLSConfig, q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor | None,
+                 seq_lens: torch.Tensor, index: TLSIndex):
+    """Quest (the block-level baseline of P:395): the top-k_b blocks by the bound s_i and
+    attention over EVERY token of them -- no token-level stage.  Returns (out, lse, block_ids, token_ids,
+    num_tokens); k_t of the attention = k_b * B."""
+    scores = block_scores(cfg, q, seq_lens, index)
+    _, bids = block_topk(cfg, scores, seq_lens, 0)
+    kq = cfg.top_blocks * cfg.block_size
+    tids, nt = expand_blocks(cfg, bids, seq_lens, kq)
+    out, lse = sparse_attend(_with(cfg, top_tokens=kq), q, k_cache, v_cache, tids, nt)
+    return out, lse, bids, tids, nt
+
+
+def ds_decode(cfg: TLSConfig, q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor | None,
+              seq_lens: torch.Tensor, index: TLSIndex):
+    """DS (the token-level baseline of P:395: alpha~ over the channel-projected INT4 index of EVERY cached token,
+    P:127-134, then top-k_t) -- TLS with every block a candidate (k_b = m).  Returns (out, lse,
+    token_ids, num_tokens, ln_alpha)."""
+    cfg_all = _with(cfg, top_blocks=cfg.num_blocks)
+    cand = block_iota(cfg_all, seq_lens)
+    stats = token_stats(cfg_all, q, seq_lens, index, cand)
+    keys, ids = token_keys(cfg_all, q, seq_lens, index, cand, stats.unsqueeze(0), 0)
+    lk, tids, nt = topk_rows(keys, ids, cfg.top_tokens)
+    out, lse = sparse_attend(cfg, q, k_cache, v_cache, tids, nt)
+    return out, lse, tids, nt, lk
 
 
 def _sel_outputs(cfg: TLSConfig, dev, out):

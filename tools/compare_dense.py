@@ -2,13 +2,13 @@
 device time of one TLS decode step vs a dense decode over the full context, on the
 same synthetic workload, L2 flushed before each call.  Not a bench line.
 
-Comparison operators of the paper expressed as configurations of this
-operator, same kernels, same inputs:
-  quest -- block selection only: K_t = K_b * B, so every token of the K_b selected
-           blocks is attended (the token scoring still runs, so this is an upper
-           bound on a Quest kernel built from these parts);
-  ds    -- token selection only: K_b = m, every block is a candidate (the channel-
-           index scoring runs over the whole context).
+Comparison operators of the paper, same inputs (tests/test_gpu_compare_ops.py checks both
+against the oracle):
+  quest -- ops.quest_decode: block selection only (a1, a2 by tls_block_scores / tls_block_topk), attention over
+           every token of the K_b selected blocks (tls_expand_blocks, tls_sparse_attend);
+  ds    -- ops.ds_decode: token selection only, every block a candidate (tls_block_iota, tls_token_stats,
+           tls_token_keys, tls_topk_rows -- the CUDA-core kernels of the sequence split -- tls_sparse_attend).
+Every record carries the SM clock sampled during its timings.
 Dense baselines: GQA -- flash_attn.flash_attn_with_kvcache (the library's FA2 decode
 kernel; the KV cache is re-laid out to [B, S, Hkv, D] once, untimed); MLA (d_k 576,
 beyond flash_attn's head dims) -- this repo's attention kernel over every token.
@@ -43,19 +43,20 @@ def main():
     flush = lambda: flush_buf.fill_(1)  # noqa: E731
     st = torch.cuda.current_stream()
     res = []
+    clocks = bench.ClockSampler(0)
+    clocks.start()
     for name in names:
+        t_rec0 = __import__("time").time()
         w = EXTRA.get(name) or W.CONFIGS[name]
         cfg, inputs, idx, queries = bench.build_state(w, 0, dev, "outlier")
         q = queries[0]
         t_tls = med(bench.time_steps(lambda i: tls.decode(cfg, queries[i % 8], inputs["k_cache"], inputs["v_cache"],
                                                            inputs["seq_lens"], idx), 50, 5, flush, st))
         rec = {"workload": w.name, "tls_us": t_tls * 1e3, "context": w.context, "batch": w.batch, "layout": w.layout}
-        for tag, kw in (("quest", {"top_tokens": w.top_blocks * w.block_size}), ("ds", {"top_blocks": cfg.num_blocks})):
+        for tag, fn in (("quest", tls.quest_decode), ("ds", tls.ds_decode)):
             try:
-                vcfg = tls.TLSConfig(**{**w.config_kwargs(), **kw})
-                t_v = med(bench.time_steps(lambda i: tls.decode(vcfg, queries[i % 8], inputs["k_cache"],
-                                                                inputs["v_cache"], inputs["seq_lens"], idx),
-                                           20, 3, flush, st))
+                t_v = med(bench.time_steps(lambda i: fn(cfg, queries[i % 8], inputs["k_cache"], inputs["v_cache"],
+                                                        inputs["seq_lens"], idx), 20, 3, flush, st))
                 rec.update({f"{tag}_us": t_v * 1e3, f"tls_speedup_vs_{tag}": t_v / t_tls})
             except Exception as e:  # noqa: BLE001
                 rec[f"{tag}_error"] = f"{type(e).__name__}: {e}"[:200]
@@ -83,6 +84,7 @@ def main():
                 rec.update(dense="this repo's attention kernel over every token", dense_us=t_d * 1e3, speedup=t_d / t_tls)
             except Exception as e:  # noqa: BLE001
                 rec.update(dense_error=f"{type(e).__name__}: {e}"[:200])
+        rec["clocks"] = clocks.summary(t_rec0, __import__("time").time())
         print(json.dumps(rec), flush=True)
         res.append(rec)
         del inputs, idx, queries
@@ -91,3 +93,4 @@ def main():
 
 if __name__ == "__main__":
     main()
+    # (the clock sampler thread is a daemon; nvidia-smi exits with the process)
