@@ -435,7 +435,9 @@ int32_t tls_select_mode(const tls_config* cfg);
  * token-select kernel (which = 0 or 2) or of the attention kernel (which = 1);
  * which = 3: the tokens per staged chunk of the MLA attention plan of
  * tls_sparse_attend (64, or 32 when the selected-token list leaves no room for
- * 64-token double buffering; 0 for GQA).  -1 for an invalid configuration.
+ * 64-token double buffering; 0 for GQA); which = 4: that plan's engine (3 =
+ * tcgen05 tensor cores with TMEM accumulators, 2 = mma.sync, 1 = CUDA cores).
+ * -1 for an invalid configuration.
  * The environment variable TLS_CLUSTER overrides the heuristic for both
  * cluster sizes (1, 2, 4, 8 or 16). */
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which);

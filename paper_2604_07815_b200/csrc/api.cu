@@ -195,6 +195,23 @@ tls_status plan_attend(const tls_config* c, tls::AttendParams& p, int select, in
   const int kt = tls::kt_effective(p.d);
   int cs = env_cluster();
   if (!attend) cs = 1;  // selection only: one CTA per pair
+  if (p.mma == 2 && attend) {  // MLA on tcgen05 (attend.cu attend_mla_tc_kernel)
+    const char* e = getenv("TLS_MLA_TC");  // opt-in ("1"): slower than the mma.sync kernel so far
+    // one wave of CTAs (one per SM), each with >= 128 selected tokens
+    int c2 = cs;
+    if (!c2) {
+      c2 = 1;
+      while (c2 < 16 && pairs * c2 * 2 <= (long long)num_sms() && (kt + 2 * c2 - 1) / (2 * c2) >= 128) c2 *= 2;
+    }
+    if (e && e[0] == '1') {
+      p.mma = 3;
+      p.mla_tc = 64;
+      p.cs = c2;
+      tls::plan_attend(p, sizeof(tls::FastTopKCtl));
+      if ((int)p.smem_bytes <= kMaxSmem) return TLS_OK;
+      p.mma = 2;  // does not fit: the mma.sync kernel
+    }
+  }
   if (!cs) {
     // split a pair's tokens over more CTAs only while the whole grid stays one wave of
     // co-resident CTAs (MLA: one 117 KB CTA per SM; GQA mma: two) and each CTA keeps >= 64
@@ -1097,11 +1114,12 @@ int32_t tls_select_mode(const tls_config* cfg) {
 }
 
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which) {
-  if (check_config(cfg) != TLS_OK || which < 0 || which > 3) return -1;
-  if (which == 3) {  // the MLA attention plan's tokens per staged chunk of tls_sparse_attend (64 or 32; 0: GQA)
+  if (check_config(cfg) != TLS_OK || which < 0 || which > 4) return -1;
+  if (which == 3 || which == 4) {  // tls_sparse_attend's attention plan
     tls::AttendParams ap;
     if (plan_attend(cfg, ap, 0, 1) != TLS_OK) return -1;
-    return cfg->layout == TLS_MLA ? ap.mla_tc : 0;
+    if (which == 4) return ap.mma == 3 ? 3 : (ap.mma ? 2 : 1);  // tcgen05 | mma.sync | CUDA cores
+    return cfg->layout == TLS_MLA ? ap.mla_tc : 0;             // MLA tokens per staged chunk
   }
   tls::PStepParams sk;
   if (which != 1 && pstep_plan(cfg, 1, sk)) return sk.ns;  // attention slices per pair

@@ -925,6 +925,359 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_kernel(const __grid_co
   phase_merge<__nv_bfloat16, 4>(p, pair, b, 0, rank);
 }
 
+// --------------------------------------------------------------------------
+// MLA attention on the 5th-generation tensor cores (tcgen05 + TMEM), p.mma == 3.
+// Per CTA: chunks of 64 selected tokens, double-buffered (the gather of chunk
+// c + 2 is in flight while chunk c + 1 is computed).  A chunk's latent rows
+// (576 bf16) are gathered once into shared memory in the canonical
+// no-swizzle core-matrix layout (8 tokens x 16 B per 128-byte core matrix;
+// token groups SBO = 9216 B apart, 8-dim groups LBO = 128 B apart), which
+// serves BOTH products:
+//   S^T[64 tok x NH] = K_chunk . Q^T        (A = the chunk, K-major: M = 64)
+//   O^T[512 x NH]   += V^T . P^T            (A = the chunk's first 512 dims,
+//        MN-major: the same core matrices with the roles of LBO / SBO swapped)
+// Q (NH padded heads, K-major) and P^T (bf16 hi + lo pieces, MN-major over
+// heads) are the B operands.  Accumulators in TMEM: S^T double-buffered in
+// columns [0, 64), O^T in 4 M-blocks of NH columns from column 64.  One thread
+// issues the MMAs; tcgen05.commit -> mbarriers hand them to the softmax warps
+// (0-3: lanes 0-15 of each quarter hold one token each, the M = 64 layout)
+// and to the epilogue.  P = 2^(S - m_ref) against a per-head reference max set
+// by the first chunk and raised (with an O rescale through tcgen05.ld/st) only
+// when a chunk exceeds it by more than 2^8, so TMEM is rarely touched between
+// products.  The epilogue writes this CTA's partial (o, m_ref, l); the cluster
+// merge of attend_mla_kernel (phase_merge) finishes the pair.
+// P:73 (one shared latent head, V = the first d_v dims).
+// --------------------------------------------------------------------------
+namespace tc {
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | ((uint64_t)1 << 46);  // version 1, SWIZZLE_NONE
+}
+// kind::f16, D fp32, A/B bf16; a_mn / b_mn: MN-major operand
+__host__ __device__ constexpr uint32_t idesc(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          tmem),
+      "l"(da), "l"(db), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// 32 lanes x 32 columns (32-bit): thread t of the warp gets lane (32 * (warp % 4) + t), columns c0..c0+31
+__device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\n"
+                 : "=r"(done)
+                 : "r"(smem_u32(bar)), "r"(parity)
+                 : "memory");
+  } while (!done);
+}
+// transposed butterfly over the 32 lanes: on entry every lane holds 32 values (one per column); on exit lane l
+// holds op over the lanes of column l (31 shuffles)
+template <bool MAX>
+__device__ __forceinline__ float transpose_reduce(float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool up = lane & w;
+#pragma unroll
+    for (int j = 0; j < w; ++j) {
+      const float send = up ? v[j] : v[j + w];
+      const float keep = up ? v[j + w] : v[j];
+      const float got = __shfl_xor_sync(0xffffffffu, send, w);
+      v[j] = MAX ? fmaxf(keep, got) : keep + got;
+    }
+  }
+  return v[0];  // lane l: column l
+}
+}  // namespace tc
+
+constexpr int kTcTok = 64;            // tokens per chunk (the M of S^T; M = 64 puts row m in TMEM lane 32(m/16) + m%16)
+constexpr int kTcRowGrp = 576 / 8;    // 72 core matrices per token group
+constexpr uint32_t kTcSbo = kTcRowGrp * 128;  // 9216 B between token groups (and head groups of Q)
+constexpr float kTcLazy = 8.f;        // rescale O only when a chunk's max exceeds the reference by > 2^8
+
+template <int NH>
+__global__ void __launch_bounds__(kThreads, 1) attend_mla_tc_kernel(const __grid_constant__ AttendParams p) {
+  constexpr int DK = 576, DV = 512;
+  constexpr uint32_t kChunkBytes = (uint32_t)kTcTok * DK * 2;  // 73728
+  constexpr uint32_t kPBytes = (uint32_t)kTcTok * NH * 2;      // one bf16 piece of P^T
+  constexpr int kOcol = 64;                                     // O^T: 4 M-blocks x NH columns from column 64
+  constexpr uint32_t kTmemCols = 256;
+  static_assert(kOcol + (DV / 128) * NH <= (int)kTmemCols, "TMEM plan");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar_s[2], bar_o[2];
+  __shared__ uint32_t s_tmem;
+  __shared__ float s_red[4][NH];
+  __shared__ float s_mref[NH], s_l[NH], s_scale[NH];
+  __shared__ int s_rescale;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned rank = blockIdx.x;
+  const int cs = p.cs;
+  const int pair = blockIdx.y;
+  const int b = pair;  // MLA: one KV head
+  const int G = p.d.G;
+  int* sel = reinterpret_cast<int*>(smem + p.off_sel);
+  __shared__ TopKCtl tk;
+  unsigned long long* dbg = p.dbg ? p.dbg + ((size_t)pair * cs + rank) * 32 : nullptr;  // diagnostics
+#define TC_STAMP(i) \
+  if (dbg && tid == 0) dbg[i] = gtimer();
+  TC_STAMP(0)
+  if (p.ready_in != nullptr) {  // the token kernel's keys and histogram for this pair
+    if (tid == 0) {
+      wait_count(p.ready_in + pair, (unsigned)p.ready_count);
+      if (cs == 1) p.ready_in[pair] = 0u;
+    }
+    __syncthreads();
+  }
+  int K;
+  if (p.select) {
+    K = select_tokens_prologue(p, pair, b, rank, smem, sel, tk);
+    if (!p.attend) return;
+  } else {
+    K = min(min(max(p.num_tokens[pair], 0), p.d.Kt), p.tloc_max * cs);
+  }
+  const int t0 = (int)((long long)K * rank / cs), t1 = (int)((long long)K * (rank + 1) / cs);
+  const int tloc = t1 - t0;
+  TC_STAMP(1)
+  if (!p.select) {
+    const int* ids = p.token_ids + (size_t)pair * p.d.Kt;
+    for (int i = tid; i < tloc; i += kThreads) sel[i] = ids[t0 + i];
+  }
+  uint8_t* sKV = smem + p.off_akv;            // 2 chunk buffers: [8 token groups][72 dim groups][128 B]
+  uint8_t* sQ = sKV + 2 * kChunkBytes;        // [NH/8 head groups][72][128 B]
+  uint8_t* sP = sQ + (size_t)NH * DK * 2;     // [2 buffers][hi | lo][8 token groups][NH/8][128 B]
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&s_tmem)),
+                 "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_s[i], 1);
+      mbar_init(&bar_o[i], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();  // sel (gathers below)
+  // Q: NH padded heads -> K-major core matrices (head h, dims 8c..8c+7 at (h/8)*SBO + c*128 + (h%8)*16)
+  const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + (size_t)b * p.d.Hq * DK;
+  for (int i = tid; i < NH * kTcRowGrp; i += kThreads) {
+    const int h = i / kTcRowGrp, c = i - h * kTcRowGrp;
+    cp_async16(sQ + (h >> 3) * kTcSbo + c * 128 + (h & 7) * 16, qg + (size_t)(h < G ? h : 0) * DK + c * 8, h < G);
+  }
+  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.kv_rows * DK;
+  auto gather = [&](int c) {  // chunk c's latent rows (zero past tloc) into buffer c % 2; one cp.async group
+    uint8_t* dst = sKV + (c & 1) * kChunkBytes;
+    for (int i = tid; i < kTcTok * kTcRowGrp; i += kThreads) {
+      const int row = i / kTcRowGrp, ch = i - row * kTcRowGrp;
+      const int t = c * kTcTok + row;
+      const bool ok = t < tloc;
+      cp_async16(dst + (row >> 3) * kTcSbo + ch * 128 + (row & 7) * 16, kb + (size_t)(ok ? sel[t] : 0) * DK + ch * 8,
+                 ok);
+    }
+    cp_async_commit();
+  };
+  const int nchunks = (tloc + kTcTok - 1) / kTcTok;
+  if (nchunks > 0) gather(0);  // (with Q in the same group)
+  if (nchunks > 1) gather(1);
+  if (tid < NH) s_l[tid] = 0.f;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  const float sm2 = p.d.sm_scale * kLog2e;
+  for (int c = 0; c < nchunks; ++c) {
+    const int bf = c & 1;
+    if (c + 1 < nchunks) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the rows (and Q), for the tensor cores
+    __syncthreads();
+    if (c < 4) TC_STAMP(2 + 4 * c)
+    // ---- S^T = K Q^T: M = 64 tokens, N = NH, K = 576 (36 steps of 16 dims = 2 core matrices) ----
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      constexpr uint32_t id = tc::idesc(64, NH, 0, 0);
+      const uint32_t a0 = smem_u32(sKV + bf * kChunkBytes), b0 = smem_u32(sQ);
+      for (int ks = 0; ks < DK / 16; ++ks)
+        tc::mma(tmem + bf * 32, tc::sdesc(a0 + ks * 256, 128, kTcSbo), tc::sdesc(b0 + ks * 256, 128, kTcSbo), id, ks > 0);
+      tc::commit(&bar_s[bf]);
+    }
+    // ---- softmax (warps 0-3; lanes 0-15 of warp w hold tokens 16w .. 16w + 15) ----
+    if (warp < 4) {
+      tc::wait_bar(&bar_s[bf], (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (c < 4) TC_STAMP(3 + 4 * c)
+      float v[32];
+      tc::ld32(tmem + ((uint32_t)(warp * 32) << 16) + bf * 32, v);
+      const int tok = warp * 16 + lane;
+      const bool valid = lane < 16 && c * kTcTok + tok < tloc;
+#pragma unroll
+      for (int h = 0; h < 32; ++h) v[h] = (valid && h < NH) ? v[h] * sm2 : -CUDART_INF_F;
+      float w[32];
+#pragma unroll
+      for (int h = 0; h < 32; ++h) w[h] = v[h];
+      const float wm = tc::transpose_reduce<true>(w);  // lane h: this warp's max of head h
+      if (lane < NH) s_red[warp][lane] = wm;
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (tid < NH) {  // the reference max: the first chunk's, raised only by more than 2^kTcLazy
+        const float mc = fmaxf(fmaxf(s_red[0][tid], s_red[1][tid]), fmaxf(s_red[2][tid], s_red[3][tid]));
+        const float mo = c == 0 ? -CUDART_INF_F : s_mref[tid];
+        const bool up = mc > mo + kTcLazy;  // (first chunk: always)
+        s_scale[tid] = up ? (mo == -CUDART_INF_F ? 0.f : fexp2(mo - mc)) : 1.f;
+        if (up) s_mref[tid] = mc;
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (tid == 0) {
+        int any = 0;
+        for (int h = 0; h < NH; ++h) any |= (c > 0 && s_scale[h] != 1.f);
+        s_rescale = any;
+      }
+      float e[32];
+#pragma unroll
+      for (int h = 0; h < 32; ++h) {
+        const float m = h < NH ? s_mref[h] : 0.f;
+        e[h] = (h < NH && m != -CUDART_INF_F) ? fexp2(v[h] - m) : 0.f;
+      }
+      if (valid) {  // P = 2^(S - m_ref) as bf16 hi + lo pieces into the MN-major B layout of buffer bf:
+                    // token t, heads 8j..8j+7 at (t/8)*((NH/8)*128) + j*128 + (t%8)*16
+        uint8_t* phi = sP + bf * 2 * kPBytes + (tok >> 3) * ((NH / 8) * 128) + (tok & 7) * 16;
+        uint8_t* plo = phi + kPBytes;
+#pragma unroll
+        for (int j = 0; j < NH / 8; ++j) {
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float a = e[8 * j + 2 * u], bb = e[8 * j + 2 * u + 1];
+            const float ah = __bfloat162float(__float2bfloat16_rn(a)), bh = __bfloat162float(__float2bfloat16_rn(bb));
+            hi[u] = pack_bf16x2(ah, bh);
+            lo[u] = pack_bf16x2(a - ah, bb - bh);
+          }
+          *reinterpret_cast<uint4*>(phi + j * 128) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(plo + j * 128) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+      } else if (lane < 16) {  // a token slot past tloc: zero P (the zero-filled row must not contribute)
+        uint8_t* phi = sP + bf * 2 * kPBytes + (tok >> 3) * ((NH / 8) * 128) + (tok & 7) * 16;
+#pragma unroll
+        for (int j = 0; j < NH / 8; ++j) {
+          *reinterpret_cast<uint4*>(phi + j * 128) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(phi + kPBytes + j * 128) = make_uint4(0, 0, 0, 0);
+        }
+      }
+      const float ws = tc::transpose_reduce<false>(e);  // lane h: this warp's sum of head h
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");   // s_red (max) read by every thread before reuse
+      if (lane < NH) s_red[warp][lane] = ws;
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (tid < NH) s_l[tid] = s_l[tid] * s_scale[tid] + s_red[0][tid] + s_red[1][tid] + s_red[2][tid] + s_red[3][tid];
+      if (s_rescale) {  // O *= scale per head (column): the previous chunk's PV must be complete
+        tc::wait_bar(&bar_o[bf ^ 1], ((c - 1) >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        for (int mb = 0; mb < DV / 128; ++mb) {
+          const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + kOcol + mb * NH;
+          float o[32];
+          tc::ld32(ta, o);
+          uint32_t r[32];
+#pragma unroll
+          for (int h = 0; h < 32; ++h) r[h] = __float_as_uint(h < NH ? o[h] * s_scale[h] : o[h]);
+          asm volatile(
+              "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+              "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(ta),
+              "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+              "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+              "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+              "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P, for the tensor cores
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    }
+    __syncthreads();  // P written, S read, O rescaled
+    if (c < 4) TC_STAMP(4 + 4 * c)
+    // ---- O^T += V^T P^T: 4 M-blocks of 128 dims, N = NH, K = 64 tokens (4 steps of 2 token groups) ----
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      constexpr uint32_t id = tc::idesc(128, NH, 1, 1);
+      const uint32_t a0 = smem_u32(sKV + bf * kChunkBytes);
+      for (int part = 0; part < 2; ++part) {  // P_hi, then P_lo
+        const uint32_t pb = smem_u32(sP) + bf * 2 * kPBytes + part * kPBytes;
+        for (int mb = 0; mb < DV / 128; ++mb)
+          for (int ks = 0; ks < kTcTok / 16; ++ks)
+            tc::mma(tmem + kOcol + mb * NH, tc::sdesc(a0 + mb * 16 * 128 + ks * 2 * kTcSbo, kTcSbo, 128),
+                    tc::sdesc(pb + ks * 2 * ((NH / 8) * 128), (NH / 8) * 128, 128), id, c > 0 || part > 0 || ks > 0);
+      }
+      tc::commit(&bar_o[bf]);
+    }
+    if (c + 2 < nchunks) {  // buffer bf is read by this PV: refill it once the PV is done
+      tc::wait_bar(&bar_o[bf], (c >> 1) & 1);
+      gather(c + 2);
+    }
+    if (c < 4) TC_STAMP(5 + 4 * c)
+  }
+  if (nchunks > 0) {  // the last PV
+    tc::wait_bar(&bar_o[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  }
+  // ---- epilogue: this CTA's partial (unnormalised o, reference max, sum) ----
+  const int tot = G * DV;
+  float* po = p.part_o + ((size_t)pair * cs + rank) * tot;
+  float* pml = p.part_ml + ((size_t)pair * cs + rank) * G * 2;
+  if (tid < G) {
+    pml[2 * tid] = nchunks > 0 ? s_mref[tid] : -CUDART_INF_F;
+    pml[2 * tid + 1] = nchunks > 0 ? s_l[tid] : 0.f;
+  }
+  if (warp < 4 && nchunks > 0) {
+    for (int mb = 0; mb < DV / 128; ++mb) {
+      float v[32];
+      tc::ld32(tmem + ((uint32_t)(warp * 32) << 16) + kOcol + mb * NH, v);
+      const int dcol = mb * 128 + warp * 32 + lane;  // TMEM lane = output dim
+#pragma unroll
+      for (int h = 0; h < 32; ++h)
+        if (h < G) po[(size_t)h * DV + dcol] = v[h];
+    }
+  }
+  TC_STAMP(18)
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols));
+  if (cs > 1) cluster_sync_all();
+  if (cs > 1 && p.ready_in != nullptr && rank == 0 && tid == 0) p.ready_in[pair] = 0u;  // all CTAs passed the wait
+  __syncthreads();
+  TC_STAMP(19)
+  phase_merge<__nv_bfloat16, 4>(p, pair, b, 0, rank);
+  TC_STAMP(20)
+#undef TC_STAMP
+}
+
+template <int NH>
+static cudaError_t launch_mla_tc(const AttendParams& p, cudaStream_t st, const LaunchOpts& o) {
+  auto kern = attend_mla_tc_kernel<NH>;
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, p.cs > 8);
+  if (e != cudaSuccess) return e;
+  return launch_ex(kern, dim3((unsigned)p.cs, (unsigned)(p.d.batch * p.d.Hkv), 1), kThreads, p.smem_bytes, st, o,
+                   (unsigned)p.cs, p);
+}
+
 template <typename T, bool MMA, int D>
 static cudaError_t launch_k3(const AttendParams& p, cudaStream_t st, const LaunchOpts& o) {
   auto kern = attend_kernel<T, MMA, D>;
@@ -948,6 +1301,7 @@ cudaError_t launch_attend(const AttendParams& p, cudaStream_t st, const LaunchOp
     if (p.d.bf16) return launch_k3<__nv_bfloat16, false, 0>(p, st, o);
     return launch_k3<float, false, 0>(p, st, o);
   }
+  if (p.mma == 3) return p.d.G <= 16 ? launch_mla_tc<16>(p, st, o) : launch_mla_tc<32>(p, st, o);
   if (p.mma == 2) {
     if (p.mla_tc == 32) return p.d.G <= 16 ? launch_mla<1, 32>(p, st, o) : launch_mla<2, 32>(p, st, o);
     return p.d.G <= 16 ? launch_mla<1, 64>(p, st, o) : launch_mla<2, 64>(p, st, o);

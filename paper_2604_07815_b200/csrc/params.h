@@ -93,7 +93,7 @@ struct AttendParams {  // K3 (attend_kernel / attend_mla_kernel), optionally wit
   int cs;
   int mma;       // 1: bf16 mma.sync GQA path (d in {64,128}, G <= 16); 2: bf16 mma.sync MLA path (576/512)
   int tloc_max;  // ceil(kt_eff / cs)
-  int mla_tc;      // MLA attention chunk tokens (64 or 32; see mla_stages)
+  int mla_tc;      // MLA attention chunk tokens (64 or 32; see mla_stages); 128 on the tcgen05 path (mma 3)
   int select;    // 1: first select S_t = top-k_t from the keys (a4); 0: read token_ids / num_tokens
   int attend;    // 1: attention (a5); 0: selection only (tls_select)
   int kb_eff;
@@ -281,7 +281,11 @@ static inline void plan_attend(AttendParams& p, size_t fastctl_bytes) {
   }
   if (p.attend) {
     size_t s2 = o;
-    if (p.mma == 2) {  // MLA tensor-core path: Q, 2 latent-row chunks, S, P, alpha/m/l
+    if (p.mma == 3) {  // MLA tcgen05 path: two 64-token chunks (core-matrix layout), Q, 2 x P hi + lo
+      const int nh = d.G <= 16 ? 16 : 32;
+      p.off_akv = (unsigned)s2;
+      s2 = align16(s2 + (size_t)2 * 64 * d.d_k * 2 + (size_t)nh * d.d_k * 2 + (size_t)2 * 2 * 64 * nh * 2);
+    } else if (p.mma == 2) {  // MLA tensor-core path: Q, 2 latent-row chunks, S, P, alpha/m/l
       const int mt16 = d.G <= 16 ? 16 : 32;
       p.off_akv = (unsigned)s2;
       const int tc = p.mla_tc == 32 ? 32 : 64;

@@ -503,8 +503,9 @@ def test_mla_attention_large_selection_uses_small_chunks():
     w = W.Workload("mla-big", 1, 32, 1, 576, 512, 131072, d_c=128, top_blocks=2048, top_tokens=131072, layout="mla",
                    sm_scale=1.0 / math.sqrt(192.0))
     cfg = tls.TLSConfig(**w.config_kwargs())
-    assert tls.cluster_size(cfg, 3) == 32  # the 32-token fallback plan is the one that runs
-    assert tls.cluster_size(tls.TLSConfig(**SMALL["mla"].config_kwargs()), 3) == 64
+    assert tls.cluster_size(cfg, 3) == 32 and tls.cluster_size(cfg, 4) == 2  # the mma.sync 32-token fallback runs
+    small = tls.TLSConfig(**SMALL["mla"].config_kwargs())
+    assert tls.cluster_size(small, 4) == 2 and tls.cluster_size(small, 3) == 64  # MLA: mma.sync by default
     g = torch.Generator(device=DEV).manual_seed(11)
     q = torch.randn((1, 32, 576), generator=g, device=DEV).to(torch.bfloat16)
     k = torch.randn((1, w.context, 576), generator=g, device=DEV).to(torch.bfloat16)
@@ -527,6 +528,27 @@ def test_streaming_select_experiment(name, monkeypatch):
     cfg, inputs, idx = setup_case(w, seed=6)
     for _ in range(3):  # repeated calls: the ticket / exit counters and per-SM words reset themselves
         res = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    stats = {"block_near_ties": 0, "token_near_ties": 0}
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            check_pair(w, cfg, inputs, idx, res, b, g, stats)
+
+
+@pytest.mark.parametrize("case", ["small", "dense", "c4"])
+def test_mla_tcgen05_attention(case, monkeypatch):
+    """The MLA attention on the 5th-generation tensor cores (TLS_MLA_TC=1, attend.cu attend_mla_tc_kernel:
+    tcgen05.mma with TMEM accumulators, S^T = K Q^T and O^T += V^T P^T from one core-matrix copy of each 64-token
+    chunk) against the oracle: the decode of small MLA cases, the degenerate budget (= dense attention),
+    and BASELINE.json's C4 at full size on sampled pairs."""
+    monkeypatch.setenv("TLS_MLA_TC", "1")
+    if case == "c4":
+        run_full(W.CONFIGS["c4"], "outlier", seed=5, n_pairs=8)
+        return
+    w = SMALL["mla"] if case == "small" else SMALL["mla"].with_(top_blocks=10 ** 4, top_tokens=10 ** 5)
+    cfg, inputs, idx = setup_case(w, seed=8)
+    assert tls.cluster_size(cfg, 4) == 3  # the tcgen05 plan runs
+    res = run_decode(cfg, inputs, idx)
     torch.cuda.synchronize()
     stats = {"block_near_ties": 0, "token_near_ties": 0}
     for b in range(w.batch):
