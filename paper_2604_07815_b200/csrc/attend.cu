@@ -1030,7 +1030,6 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_tc_kernel(const __grid
   __shared__ uint32_t s_tmem;
   __shared__ float s_red[4][NH];
   __shared__ float s_mref[NH], s_l[NH], s_scale[NH];
-  __shared__ int s_rescale;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned rank = blockIdx.x;
   const int cs = p.cs;
@@ -1067,6 +1066,9 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_tc_kernel(const __grid
   uint8_t* sKV = smem + p.off_akv;            // 2 chunk buffers: [8 token groups][72 dim groups][128 B]
   uint8_t* sQ = sKV + 2 * kChunkBytes;        // [NH/8 head groups][72][128 B]
   uint8_t* sP = sQ + (size_t)NH * DK * 2;     // [2 buffers][hi | lo][8 token groups][NH/8][128 B]
+  // warp roles: 0-3 softmax (TMEM lane quarters), 4 lane 0 MMA issue, 5-7 gather (cp.async)
+  constexpr int kProd = 3 * 32;
+  __shared__ __align__(8) uint64_t bar_full[2], bar_pfull[2];
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&s_tmem)),
                  "n"(kTmemCols));
@@ -1074,62 +1076,86 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_tc_kernel(const __grid
   }
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar_s[i], 1);
-      mbar_init(&bar_o[i], 1);
+      mbar_init(&bar_s[i], 1);       // S(c) MMAs complete (tcgen05.commit)
+      mbar_init(&bar_o[i], 1);       // PV(c) MMAs complete: buffer c % 2 and P(c % 2) free (tcgen05.commit)
+      mbar_init(&bar_full[i], kProd);  // the chunk's rows landed (cp.async.mbarrier.arrive per producer thread)
+      mbar_init(&bar_pfull[i], 128);   // P(c) written, S(c) read, O rescaled (softmax threads)
     }
     mbar_fence_init();
   }
-  __syncthreads();  // sel (gathers below)
-  // Q: NH padded heads -> K-major core matrices (head h, dims 8c..8c+7 at (h/8)*SBO + c*128 + (h%8)*16)
-  const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + (size_t)b * p.d.Hq * DK;
-  for (int i = tid; i < NH * kTcRowGrp; i += kThreads) {
-    const int h = i / kTcRowGrp, c = i - h * kTcRowGrp;
-    cp_async16(sQ + (h >> 3) * kTcSbo + c * 128 + (h & 7) * 16, qg + (size_t)(h < G ? h : 0) * DK + c * 8, h < G);
-  }
-  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.kv_rows * DK;
-  auto gather = [&](int c) {  // chunk c's latent rows (zero past tloc) into buffer c % 2; one cp.async group
-    uint8_t* dst = sKV + (c & 1) * kChunkBytes;
-    for (int i = tid; i < kTcTok * kTcRowGrp; i += kThreads) {
-      const int row = i / kTcRowGrp, ch = i - row * kTcRowGrp;
-      const int t = c * kTcTok + row;
-      const bool ok = t < tloc;
-      cp_async16(dst + (row >> 3) * kTcSbo + ch * 128 + (row & 7) * 16, kb + (size_t)(ok ? sel[t] : 0) * DK + ch * 8,
-                 ok);
-    }
-    cp_async_commit();
-  };
-  const int nchunks = (tloc + kTcTok - 1) / kTcTok;
-  if (nchunks > 0) gather(0);  // (with Q in the same group)
-  if (nchunks > 1) gather(1);
   if (tid < NH) s_l[tid] = 0.f;
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  __syncthreads();  // sel, barriers, the TMEM address
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = s_tmem;
   const float sm2 = p.d.sm_scale * kLog2e;
-  for (int c = 0; c < nchunks; ++c) {
-    const int bf = c & 1;
-    if (c + 1 < nchunks) cp_async_wait<1>();
-    else cp_async_wait<0>();
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the rows (and Q), for the tensor cores
-    __syncthreads();
-    if (c < 4) TC_STAMP(2 + 4 * c)
-    // ---- S^T = K Q^T: M = 64 tokens, N = NH, K = 576 (36 steps of 16 dims = 2 core matrices) ----
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      constexpr uint32_t id = tc::idesc(64, NH, 0, 0);
-      const uint32_t a0 = smem_u32(sKV + bf * kChunkBytes), b0 = smem_u32(sQ);
-      for (int ks = 0; ks < DK / 16; ++ks)
-        tc::mma(tmem + bf * 32, tc::sdesc(a0 + ks * 256, 128, kTcSbo), tc::sdesc(b0 + ks * 256, 128, kTcSbo), id, ks > 0);
-      tc::commit(&bar_s[bf]);
+  const int nchunks = (tloc + kTcTok - 1) / kTcTok;
+  const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(p.q) + (size_t)b * p.d.Hq * DK;
+  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.kv_rows * DK;
+  if (warp >= 5) {  // ======================= gather =======================
+    for (int c = 0; c < nchunks; ++c) {
+      const int bf = c & 1;
+      if (c >= 2) tc::wait_bar(&bar_o[bf], ((c - 2) >> 1) & 1);  // PV(c - 2) read this buffer
+      // 16-byte pieces, 8 rows x 4 chunks per warp instruction: each quarter-warp writes one contiguous 128-byte
+      // core matrix (conflict-free) and the warp reads 64 contiguous bytes of each of its 8 rows (whole sectors)
+      // (one row per lane group of 72 chunks: 128-byte-strided shared writes, a 4.5x slower gather)
+      const int lr = lane & 7, lc = lane >> 3, wp = warp - 5;
+      if (c == 0)  // Q: NH padded heads, K-major core matrices (head h, dims 8c..8c+7 at (h/8)*SBO + c*128 + (h%8)*16)
+        for (int j = wp; j < (NH / 8) * (kTcRowGrp / 4); j += 3) {
+          const int h = (j % (NH / 8)) * 8 + lr, ch = (j / (NH / 8)) * 4 + lc;
+          cp_async16(sQ + (h >> 3) * kTcSbo + ch * 128 + (h & 7) * 16, qg + (size_t)(h < G ? h : 0) * DK + ch * 8, h < G);
+        }
+      uint8_t* dst = sKV + bf * kChunkBytes;
+      for (int j = wp; j < (kTcTok / 8) * (kTcRowGrp / 4); j += 3) {
+        const int row = (j % (kTcTok / 8)) * 8 + lr, ch = (j / (kTcTok / 8)) * 4 + lc;
+        const int t = c * kTcTok + row;
+        const bool ok = t < tloc;
+        cp_async16(dst + (row >> 3) * kTcSbo + ch * 128 + (row & 7) * 16, kb + (size_t)(ok ? sel[t] : 0) * DK + ch * 8,
+                   ok);
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&bar_full[bf])) : "memory");
     }
-    // ---- softmax (warps 0-3; lanes 0-15 of warp w hold tokens 16w .. 16w + 15) ----
-    if (warp < 4) {
+  } else if (warp == 4) {  // ======================= MMA issue =======================
+    if (lane == 0) {
+      constexpr uint32_t id_s = tc::idesc(64, NH, 0, 0), id_o = tc::idesc(128, NH, 1, 1);
+      auto issue_s = [&](int c) {  // S^T = K Q^T: M = 64 tokens, N = NH, K = 576 (36 steps of 2 core matrices)
+        const int bf = c & 1;
+        tc::wait_bar(&bar_full[bf], (c >> 1) & 1);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the gathered rows, for the tensor cores
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t a0 = smem_u32(sKV + bf * kChunkBytes), b0 = smem_u32(sQ);
+        for (int ks = 0; ks < DK / 16; ++ks)
+          tc::mma(tmem + bf * 32, tc::sdesc(a0 + ks * 256, 128, kTcSbo), tc::sdesc(b0 + ks * 256, 128, kTcSbo), id_s,
+                  ks > 0);
+        tc::commit(&bar_s[bf]);
+      };
+      if (nchunks > 0) issue_s(0);
+      for (int c = 0; c < nchunks; ++c) {
+        const int bf = c & 1;
+        if (c + 1 < nchunks) issue_s(c + 1);  // overlaps the softmax of chunk c (S is double-buffered)
+        tc::wait_bar(&bar_pfull[bf], (c >> 1) & 1);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P, for the tensor cores
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        // O^T += V^T P^T: 4 M-blocks of 128 dims, N = NH, K = 64 tokens (4 steps of 2 token groups)
+        const uint32_t a0 = smem_u32(sKV + bf * kChunkBytes);
+        for (int part = 0; part < 2; ++part) {  // P_hi, then P_lo
+          const uint32_t pb = smem_u32(sP) + bf * 2 * kPBytes + part * kPBytes;
+          for (int mb = 0; mb < DV / 128; ++mb)
+            for (int ks = 0; ks < kTcTok / 16; ++ks)
+              tc::mma(tmem + kOcol + mb * NH, tc::sdesc(a0 + mb * 16 * 128 + ks * 2 * kTcSbo, kTcSbo, 128),
+                      tc::sdesc(pb + ks * 2 * ((NH / 8) * 128), (NH / 8) * 128, 128), id_o, c > 0 || part > 0 || ks > 0);
+        }
+        tc::commit(&bar_o[bf]);
+      }
+    }
+  } else {  // ======================= softmax (warps 0-3) =======================
+    for (int c = 0; c < nchunks; ++c) {
+      const int bf = c & 1;
       tc::wait_bar(&bar_s[bf], (c >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       if (c < 4) TC_STAMP(3 + 4 * c)
       float v[32];
-      tc::ld32(tmem + ((uint32_t)(warp * 32) << 16) + bf * 32, v);
+      tc::ld32(tmem + ((uint32_t)(warp * 32) << 16) + bf * 32, v);  // lanes 0-15 of warp w: tokens 16w .. 16w+15
       const int tok = warp * 16 + lane;
       const bool valid = lane < 16 && c * kTcTok + tok < tloc;
 #pragma unroll
@@ -1148,19 +1174,18 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_tc_kernel(const __grid
         if (up) s_mref[tid] = mc;
       }
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (tid == 0) {
-        int any = 0;
-        for (int h = 0; h < NH; ++h) any |= (c > 0 && s_scale[h] != 1.f);
-        s_rescale = any;
-      }
+      int any = 0;
+#pragma unroll
+      for (int h = 0; h < NH; ++h) any |= (c > 0 && s_scale[h] != 1.f);
       float e[32];
 #pragma unroll
       for (int h = 0; h < 32; ++h) {
         const float m = h < NH ? s_mref[h] : 0.f;
         e[h] = (h < NH && m != -CUDART_INF_F) ? fexp2(v[h] - m) : 0.f;
       }
-      if (valid) {  // P = 2^(S - m_ref) as bf16 hi + lo pieces into the MN-major B layout of buffer bf:
-                    // token t, heads 8j..8j+7 at (t/8)*((NH/8)*128) + j*128 + (t%8)*16
+      if (c >= 2) tc::wait_bar(&bar_o[bf], ((c - 2) >> 1) & 1);  // PV(c - 2) read P(bf)
+      if (lane < 16) {  // P = 2^(S - m_ref) as bf16 hi + lo pieces into the MN-major B layout of buffer bf:
+                        // token t, heads 8j..8j+7 at (t/8)*((NH/8)*128) + j*128 + (t%8)*16 (0 past tloc)
         uint8_t* phi = sP + bf * 2 * kPBytes + (tok >> 3) * ((NH / 8) * 128) + (tok & 7) * 16;
         uint8_t* plo = phi + kPBytes;
 #pragma unroll
@@ -1168,7 +1193,7 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_tc_kernel(const __grid
           uint32_t hi[4], lo[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const float a = e[8 * j + 2 * u], bb = e[8 * j + 2 * u + 1];
+            const float a = valid ? e[8 * j + 2 * u] : 0.f, bb = valid ? e[8 * j + 2 * u + 1] : 0.f;
             const float ah = __bfloat162float(__float2bfloat16_rn(a)), bh = __bfloat162float(__float2bfloat16_rn(bb));
             hi[u] = pack_bf16x2(ah, bh);
             lo[u] = pack_bf16x2(a - ah, bb - bh);
@@ -1176,20 +1201,13 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_tc_kernel(const __grid
           *reinterpret_cast<uint4*>(phi + j * 128) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
           *reinterpret_cast<uint4*>(plo + j * 128) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
         }
-      } else if (lane < 16) {  // a token slot past tloc: zero P (the zero-filled row must not contribute)
-        uint8_t* phi = sP + bf * 2 * kPBytes + (tok >> 3) * ((NH / 8) * 128) + (tok & 7) * 16;
-#pragma unroll
-        for (int j = 0; j < NH / 8; ++j) {
-          *reinterpret_cast<uint4*>(phi + j * 128) = make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(phi + kPBytes + j * 128) = make_uint4(0, 0, 0, 0);
-        }
       }
       const float ws = tc::transpose_reduce<false>(e);  // lane h: this warp's sum of head h
       asm volatile("bar.sync 1, 128;\n" ::: "memory");   // s_red (max) read by every thread before reuse
       if (lane < NH) s_red[warp][lane] = ws;
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
       if (tid < NH) s_l[tid] = s_l[tid] * s_scale[tid] + s_red[0][tid] + s_red[1][tid] + s_red[2][tid] + s_red[3][tid];
-      if (s_rescale) {  // O *= scale per head (column): the previous chunk's PV must be complete
+      if (any) {  // O *= scale per head (column): PV(c - 1) must be complete
         tc::wait_bar(&bar_o[bf ^ 1], ((c - 1) >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         for (int mb = 0; mb < DV / 128; ++mb) {
@@ -1211,33 +1229,15 @@ __global__ void __launch_bounds__(kThreads, 1) attend_mla_tc_kernel(const __grid
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P, for the tensor cores
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      if (c < 4) TC_STAMP(4 + 4 * c)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&bar_pfull[bf])) : "memory");
     }
-    __syncthreads();  // P written, S read, O rescaled
-    if (c < 4) TC_STAMP(4 + 4 * c)
-    // ---- O^T += V^T P^T: 4 M-blocks of 128 dims, N = NH, K = 64 tokens (4 steps of 2 token groups) ----
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      constexpr uint32_t id = tc::idesc(128, NH, 1, 1);
-      const uint32_t a0 = smem_u32(sKV + bf * kChunkBytes);
-      for (int part = 0; part < 2; ++part) {  // P_hi, then P_lo
-        const uint32_t pb = smem_u32(sP) + bf * 2 * kPBytes + part * kPBytes;
-        for (int mb = 0; mb < DV / 128; ++mb)
-          for (int ks = 0; ks < kTcTok / 16; ++ks)
-            tc::mma(tmem + kOcol + mb * NH, tc::sdesc(a0 + mb * 16 * 128 + ks * 2 * kTcSbo, kTcSbo, 128),
-                    tc::sdesc(pb + ks * 2 * ((NH / 8) * 128), (NH / 8) * 128, 128), id, c > 0 || part > 0 || ks > 0);
-      }
-      tc::commit(&bar_o[bf]);
-    }
-    if (c + 2 < nchunks) {  // buffer bf is read by this PV: refill it once the PV is done
-      tc::wait_bar(&bar_o[bf], (c >> 1) & 1);
-      gather(c + 2);
-    }
-    if (c < 4) TC_STAMP(5 + 4 * c)
   }
-  if (nchunks > 0) {  // the last PV
+  if (nchunks > 0) {  // every thread: the last PV is complete
     tc::wait_bar(&bar_o[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   }
+  __syncthreads();  // s_l, s_mref final
   // ---- epilogue: this CTA's partial (unnormalised o, reference max, sum) ----
   const int tot = G * DV;
   float* po = p.part_o + ((size_t)pair * cs + rank) * tot;

@@ -11,6 +11,7 @@ import bench  # noqa: E402
 import paper_2604_07815_b200 as tls  # noqa: E402
 from paper_2604_07815_b200 import workloads as W  # noqa: E402
 
+os.environ.setdefault("TLS_MLA_TC", "1")
 w = W.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c4"]
 cfg, inputs, idx, queries = bench.build_state(w, 0, torch.device("cuda"), "outlier")
 buf = torch.zeros(65536 * 32, dtype=torch.int64, device="cuda")
@@ -26,8 +27,7 @@ d = d[d[:, 0] > 0]
 t0 = d[:, 0].min()
 names = {0: "start", 1: "prologue done", 18: "epilogue done", 19: "merge start", 20: "end"}
 for c in range(4):
-    names.update({2 + 4 * c: f"c{c} rows landed", 3 + 4 * c: f"c{c} S done", 4 + 4 * c: f"c{c} P written",
-                  5 + 4 * c: f"c{c} next issued"})
+    names.update({3 + 4 * c: f"c{c} S done", 4 + 4 * c: f"c{c} P written"})
 print(f"{len(d)} CTAs; us since the first CTA start: p10 / p50 / p90")
 for i in sorted(names):
     col = d[:, i]
