@@ -340,15 +340,15 @@ __global__ void __launch_bounds__(kThreads, (NT == 1 && KS * NSPLIT <= 2) ? 5 : 
 //   pass 1: L_hj for every staged tile (token_tile_mma, once); per-warp head
 //           max m_h^w; E_hj = exp2(L_hj - m_h^w) kept in registers; per-warp
 //           sums -> CTA -> cluster (DSMEM, chunk order) -> lz_h = M_h + log2 Z_h.
-//   pass 2: sum_h exp2(L_hj - lz_h) = sum_h E_hj * c_h^w with the per-(warp,
-//           head) factor c_h^w = exp2(m_h^w - lz_h) (scaled by 2^kKeyOff so
-//           that alpha~ down to ~2^-126 per head stays representable), reduced
-//           over the four lanes that hold a token's heads with a transposed
-//           butterfly (3 shuffles per 4 tokens); every lane emits one key.
-// Reading U20: a head's term below 2^-126 of the warp's largest
-// term for that head flushes to 0 (fp32 range); only tokens with alpha~ below
-// ~2^-126 are affected.
-constexpr float kKeyOff = 64.f;
+//   pass 2: sum_h exp2(L_hj - lz_h) = 2^r_w sum_h E_hj * c_h^w with the
+//           per-(warp, head) factor c_h^w = exp2(m_h^w - lz_h - r_w), r_w its
+//           max over heads, reduced over the four lanes that hold a token's
+//           heads with a transposed butterfly (3 shuffles per 4 tokens); every
+//           lane emits one key.  A warp whose logits of some head span more
+//           than kUnder (attention-sink-like keys) keeps L instead of E and
+//           forms its keys in the log domain (reading U20: exact for any logit
+//           span; test_sink_tokens_wide_logit_span).
+constexpr float kUnder = 100.f;
 
 // 4 CTAs / SM (64 registers) where the variant fits without spilling, else 3.
 template <int KS, int NT, int NSPLIT>
@@ -475,11 +475,12 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
   const uint2* qb2 = reinterpret_cast<const uint2*>(smem + p.off_qb);
   const int tshift = d.log2B - 4;
   const int ntiles = nbl << tshift;
-  // ---- pass 1: logits of every tile (tile = warp + t * kWarps), per-warp head max ----
+  // ---- pass 1: logits of every tile (tile = warp + t * kWarps), L = sm_scale log2(e) (zero sum q~ + scale q~.code)
+  // from the tensor-core product of token_tile_mma, -inf past the sequence; per-warp head max and min ----
   float ev[TPW][NT][4];
-  float hm[NT][2];
+  float hm[NT][2], hl[NT][2];
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) hm[nt][0] = hm[nt][1] = -CUDART_INF_F;
+  for (int nt = 0; nt < NT; ++nt) hm[nt][0] = hm[nt][1] = -CUDART_INF_F, hl[nt][0] = hl[nt][1] = CUDART_INF_F;
 #pragma unroll
   for (int t = 0; t < TPW; ++t) {
     const int tile = warp + t * kWarps;
@@ -496,8 +497,11 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          ev[t][nt][e] = v0 ? fmaf(s0, acc[nt][e], z0.y * sq[nt][e]) : -CUDART_INF_F;
-          ev[t][nt][2 + e] = v1 ? fmaf(s1, acc[nt][2 + e], z1.y * sq[nt][e]) : -CUDART_INF_F;
+          const float l0 = fmaf(s0, acc[nt][e], z0.y * sq[nt][e]), l1 = fmaf(s1, acc[nt][2 + e], z1.y * sq[nt][e]);
+          // the min also sees the rows past the sequence (stale staging; at worst a needless log-domain warp)
+          hl[nt][e] = fminf(hl[nt][e], fminf(l0, l1));
+          ev[t][nt][e] = v0 ? l0 : -CUDART_INF_F;
+          ev[t][nt][2 + e] = v1 ? l1 : -CUDART_INF_F;
           hm[nt][e] = fmaxf(hm[nt][e], fmaxf(ev[t][nt][e], ev[t][nt][2 + e]));
         }
     } else {
@@ -507,20 +511,38 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
         for (int e = 0; e < 4; ++e) ev[t][nt][e] = -CUDART_INF_F;
     }
   }
-  float hs[NT][2];
+  // A warp whose logits of some head span more than kUnder (attention-sink-like keys) keeps L in registers and
+  // forms its keys in the log domain (pass 2); every other warp keeps E_hj = 2^(L_hj - m_h^w) >= 2^-kUnder.
+  bool wide = false;
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
 #pragma unroll
-      for (int o = 4; o < 32; o <<= 1) hm[nt][e] = fmaxf(hm[nt][e], __shfl_xor_sync(0xffffffffu, hm[nt][e], o));
+      for (int o = 4; o < 32; o <<= 1) {
+        hm[nt][e] = fmaxf(hm[nt][e], __shfl_xor_sync(0xffffffffu, hm[nt][e], o));
+        hl[nt][e] = fminf(hl[nt][e], __shfl_xor_sync(0xffffffffu, hl[nt][e], o));
+      }
+      wide |= hm[nt][e] - hl[nt][e] > kUnder;  // NaN (stale rows) compares false; -inf min -> true
+    }
+  wide = __any_sync(0xffffffffu, wide);
+  float hs[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
       const float mref = hm[nt][e] == -CUDART_INF_F ? 0.f : hm[nt][e];
       float s = 0.f;
+      if (wide) {
 #pragma unroll
-      for (int t = 0; t < TPW; ++t) {
-        ev[t][nt][e] = fexp2(ev[t][nt][e] - mref);
-        ev[t][nt][2 + e] = fexp2(ev[t][nt][2 + e] - mref);
-        s += ev[t][nt][e] + ev[t][nt][2 + e];
+        for (int t = 0; t < TPW; ++t) s += fexp2(ev[t][nt][e] - mref) + fexp2(ev[t][nt][2 + e] - mref);
+      } else {
+#pragma unroll
+        for (int t = 0; t < TPW; ++t) {
+          ev[t][nt][e] = fexp2(ev[t][nt][e] - mref);
+          ev[t][nt][2 + e] = fexp2(ev[t][nt][2 + e] - mref);
+          s += ev[t][nt][e] + ev[t][nt][2 + e];
+        }
       }
 #pragma unroll
       for (int o = 4; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -576,43 +598,93 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
     }
   }
   __syncthreads();
-  // ---- pass 2: ranking keys log2 sum_h exp2(L_hj - lz_h) ----
-  float cf[NT][2];
+  // ---- pass 2: ranking keys log2 sum_h exp2(L_hj - lz_h) (the head sum reduced over the four lanes that hold a
+  // token's heads with a transposed butterfly, 3 shuffles per 4 tokens; every lane emits one key) ----
+  // Narrow warp: key = r_w + log2 sum_h E_hj c_h^w with c_h^w = 2^(m_h^w - lz_h - r_w), r_w = max_h (m_h^w - lz_h),
+  // so the largest factor is 1.  Every token's largest term x = L_hj - lz_h then has x - r_w >= min_h (min_j L_hj -
+  // m_h^w) >= -kUnder, and a head whose factor or E underflows contributes below 2^-26 of it: the keys are exact
+  // to fp32 rounding.
+  // Wide warp: key = mx + log2 sum_h 2^(L_hj - lz_h - mx) with mx = max_h (L_hj - lz_h), whose largest term is 1
+  // -- exact for any span (reading U20).
+  float cf[NT][2], hz[NT][2];
+  float rw = -CUDART_INF_F;
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int h = nt * 8 + 2 * q4 + e;
-      cf[nt][e] = (h < d.G && hm[nt][e] != -CUDART_INF_F) ? fexp2(hm[nt][e] - ctl.hlz[h] + kKeyOff) : 0.f;
+      hz[nt][e] = h < d.G ? ctl.hlz[h] : CUDART_INF_F;  // x = L - (+inf) = -inf: no term
+      if (h < d.G && hm[nt][e] != -CUDART_INF_F) rw = fmaxf(rw, hm[nt][e] - hz[nt][e]);
     }
+  rw = fmaxf(rw, __shfl_xor_sync(0xffffffffu, rw, 1));
+  rw = fmaxf(rw, __shfl_xor_sync(0xffffffffu, rw, 2));
+  if (rw == -CUDART_INF_F) rw = 0.f;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      cf[nt][e] = (nt * 8 + 2 * q4 + e < d.G && hm[nt][e] != -CUDART_INF_F) ? fexp2(hm[nt][e] - hz[nt][e] - rw) : 0.f;
   uint32_t* kout = p.keys + (size_t)pair * p.kb_eff * d.B + ((size_t)cb0 << d.log2B);
   const bool bit0 = q4 & 1, bit1 = q4 & 2;
 #pragma unroll
   for (int t = 0; t < TPW; t += 2) {
     if (warp + t * kWarps >= ntiles) break;  // warp-uniform
     float pa = 0.f, pb = 0.f, pc = 0.f, pd = 0.f;  // (tile t, r0), (t, r0+8), (t+1, r0), (t+1, r0+8)
+    float ra = rw, rb = rw, rc = rw, rd = rw;  // log2 of the factor the sums carry
+    if (!wide) {
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        pa = fmaf(ev[t][nt][e], cf[nt][e], pa);
-        pb = fmaf(ev[t][nt][2 + e], cf[nt][e], pb);
-        pc = fmaf(ev[t + 1][nt][e], cf[nt][e], pc);
-        pd = fmaf(ev[t + 1][nt][2 + e], cf[nt][e], pd);
+        for (int e = 0; e < 2; ++e) {
+          pa = fmaf(ev[t][nt][e], cf[nt][e], pa);
+          pb = fmaf(ev[t][nt][2 + e], cf[nt][e], pb);
+          pc = fmaf(ev[t + 1][nt][e], cf[nt][e], pc);
+          pd = fmaf(ev[t + 1][nt][2 + e], cf[nt][e], pd);
+        }
+    } else {
+      float ma = -CUDART_INF_F, mb = -CUDART_INF_F, mc = -CUDART_INF_F, md = -CUDART_INF_F;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          ma = fmaxf(ma, ev[t][nt][e] - hz[nt][e]);
+          mb = fmaxf(mb, ev[t][nt][2 + e] - hz[nt][e]);
+          mc = fmaxf(mc, ev[t + 1][nt][e] - hz[nt][e]);
+          md = fmaxf(md, ev[t + 1][nt][2 + e] - hz[nt][e]);
+        }
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+        mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+        md = fmaxf(md, __shfl_xor_sync(0xffffffffu, md, o));
       }
+      ra = ma == -CUDART_INF_F ? 0.f : ma, rb = mb == -CUDART_INF_F ? 0.f : mb;
+      rc = mc == -CUDART_INF_F ? 0.f : mc, rd = md == -CUDART_INF_F ? 0.f : md;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          pa += fexp2(ev[t][nt][e] - hz[nt][e] - ra);
+          pb += fexp2(ev[t][nt][2 + e] - hz[nt][e] - rb);
+          pc += fexp2(ev[t + 1][nt][e] - hz[nt][e] - rc);
+          pd += fexp2(ev[t + 1][nt][2 + e] - hz[nt][e] - rd);
+        }
+    }
     // transposed butterfly: lane q4 ends with the head-sum of token q4 of (pa, pb, pc, pd)
     float k1 = bit0 ? pb : pa, k2 = bit0 ? pd : pc;
     k1 += __shfl_xor_sync(0xffffffffu, bit0 ? pa : pb, 1);
     k2 += __shfl_xor_sync(0xffffffffu, bit0 ? pc : pd, 1);
     float mine = bit1 ? k2 : k1;
     mine += __shfl_xor_sync(0xffffffffu, bit1 ? k1 : k2, 2);
+    const float mx = bit1 ? (bit0 ? rd : rc) : (bit0 ? rb : ra);
     const int tile = warp + (t + (bit1 ? 1 : 0)) * kWarps;
     const int row = r0 + (bit0 ? 8 : 0);
     if (tile < ntiles) {
       const int blk = cblk[cb0 + (tile >> tshift)];
       const int tok = (blk << d.log2B) + ((tile & ((1 << tshift) - 1)) << 4) + row;
       const bool v = tok < n;
-      const float kf = flog2(mine) - kKeyOff;
+      const float kf = mx + flog2(mine);
       kout[tile * 16 + row] = v ? f2key(kf) : 0u;
       if (v) atomicAdd(&lhist[key_bin(kf)], 1u);
     }

@@ -554,3 +554,41 @@ def test_mla_tcgen05_attention(case, monkeypatch):
     for b in range(w.batch):
         for g in range(w.num_kv_heads):
             check_pair(w, cfg, inputs, idx, res, b, g, stats)
+
+
+@pytest.mark.parametrize("name,every", [("gqa8", 16), ("mla", 16), ("gqa8", 1000), ("mla", 700)])
+def test_sink_tokens_wide_logit_span(name, every):
+    """Reading U20: attention-sink-like keys (tokens aligned with the group's queries so strongly that the
+    logits of the pair span > 200 nats) must not collapse the other candidates' ranking keys: alpha~ of an ordinary
+    token is then ~e^-200 of a sink's, below fp32's range as a value, but its ln alpha~ is representable and the
+    top-k_t among the ordinary tokens must still follow the oracle's order."""
+    w = SMALL[name]
+    inputs = W.make_inputs(w, seed=17, pattern="uniform", device=DEV, ragged=False)
+    G = w.num_q_heads // w.num_kv_heads
+    g = torch.Generator(device="cpu").manual_seed(17)
+    for b in range(w.batch):
+        for kh in range(w.num_kv_heads):
+            qbar = inputs["q"][b, kh * G:(kh + 1) * G].float().mean(0)
+            u = qbar / qbar.norm()
+            # every=16: one sink in every 16-token tile, so that every warp of the token kernel holds sinks and
+            # ordinary tokens together (log-domain keys); every=700/1000: most warps hold no sink, their keys carry
+            # the ~200-nat offset to lz in the per-warp factor r_w.  k_t exceeds the number of candidate sinks, so
+            # the boundary falls among the others
+            n_b = int(inputs["seq_lens"][b])
+            for t in range(5, n_b, every):
+                # logit boost ~ 40 * |q_h . u| * sqrt(d) * sm_scale: >= ~200 nats above the rest
+                if w.layout == "mla":
+                    inputs["k_cache"][b, t] = (inputs["k_cache"][b, t].float() + 40.0 * u * math.sqrt(w.d_k)).to(w.dtype)
+                else:
+                    inputs["k_cache"][b, kh, t] = (inputs["k_cache"][b, kh, t].float() + 40.0 * u * math.sqrt(w.d_k)).to(w.dtype)
+    q_cal, k_cal = W.calibration_sample(w, inputs, seed=17)
+    channels = P.oracle_channels(w, q_cal, k_cal).to(DEV)
+    cfg = tls.TLSConfig(**w.config_kwargs())
+    idx = tls.alloc_index(cfg, channels)
+    tls.build_index(cfg, inputs["k_cache"], inputs["seq_lens"], idx)
+    res = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    stats = {"block_near_ties": 0, "token_near_ties": 0}
+    for b in range(w.batch):
+        for kh in range(w.num_kv_heads):
+            check_pair(w, cfg, inputs, idx, res, b, kh, stats)
