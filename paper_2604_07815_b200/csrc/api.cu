@@ -403,6 +403,7 @@ struct StepPtrs {
   float* lse;
   const int32_t* slot_of_block;  // block cache (tls_decode_block_cache): K/V rows via the slot map, else NULL
   long long kv_rows;             // rows per pair of k_cache / v_cache (max_seq_len, or capacity * block_size)
+  int pair0;                     // first pair of this (sub-)batch (diagnostic stamps only)
 };
 
 // The pointers of sub-batch [b0, b0 + n) (row-major layouts of tls.h).
@@ -429,6 +430,7 @@ StepPtrs offset_ptrs(const tls_config* c, const StepPtrs& a, int b0) {
   r.token_scores = a.token_scores ? a.token_scores + B0 * Hkv * c->top_tokens : nullptr;
   r.out = a.out ? const_cast<char*>(adv(a.out, B0 * c->num_q_heads * c->d_v * eb)) : nullptr;
   r.lse = a.lse ? a.lse + B0 * c->num_q_heads : nullptr;
+  r.pair0 = a.pair0 + b0 * c->num_kv_heads;
   return r;
 }
 
@@ -464,6 +466,8 @@ tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int
   fp.sched = reinterpret_cast<unsigned*>(ws + c.w.sched);
   fp.epoch = epoch;
   fp.dbg = env_debug_buf();
+  unsigned long long* dbg0 = fp.dbg;
+  if (fp.dbg) fp.dbg += (size_t)a.pair0 * 16;
   fp.qq = reinterpret_cast<float*>(ws + c.w.qq);
   // small query groups (GQA, G * d_k <= 512 elements): every tile CTA forms QQ itself (the same fp32 ops as
   // qq_kernel, so the same bits) and starts streaming without waiting for qq_kernel (A/B: C2 79.0 -> 77.2 us;
@@ -501,7 +505,7 @@ tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int
     sp.ready_in = fp.ready;
     sp.ready_out = reinterpret_cast<unsigned*>(ws + c.w.ready_t);
     sp.epoch = epoch;
-    sp.dbg = fp.dbg ? fp.dbg + 65536 * 16 : nullptr;
+    sp.dbg = dbg0 ? dbg0 + 65536 * 16 + (size_t)a.pair0 * 64 : nullptr;
     e = tls::launch_token_cluster(sp, st, lo_dep);
     if (e != cudaSuccess) return cuda_fail(e, "token_cluster_kernel launch");
   }
@@ -517,7 +521,7 @@ tls_status enqueue_chain(const tls_config* cfg, const StepPtrs& a, char* ws, int
     ap.cand = a.guide ? a.guide : a.block_ids;
     ap.keys = sp.keys;
     ap.khist = sp.khist;
-    ap.dbg = fp.dbg ? fp.dbg + 65536 * 24 : nullptr;
+    ap.dbg = dbg0 ? dbg0 + 65536 * 24 + (size_t)a.pair0 * 8 : nullptr;
     ap.ready_in = c.mode == 1 ? sp.ready_out : nullptr;
     ap.ready_count = sp.nch;
     ap.epoch = epoch;
@@ -593,7 +597,7 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
   if (!workspace || workspace_bytes < need || !aligned16(workspace))
     return fail(TLS_ERR_WORKSPACE, "workspace must be >= %zu bytes, 16-byte aligned (got %zu)", need, workspace_bytes);
   const StepPtrs all = {q, k_cache, v_cache, seq_lens, *idx, guide, block_ids, token_ids, num_tokens,
-                        token_scores, out, lse, slot_of_block, kv_rows > 0 ? kv_rows : cfg->max_seq_len};
+                        token_scores, out, lse, slot_of_block, kv_rows > 0 ? kv_rows : cfg->max_seq_len, 0};
   if (g_timer.on && g_timer.used % kMarks != 0) g_timer.used -= g_timer.used % kMarks;  // drop a partial record
   tls::PStepParams sk;
   if (pstep_plan(cfg, do_attend, sk)) {  // one launch: every stage of every pair (opt-in, TLS_PSTEP)
@@ -650,6 +654,9 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent(fork)");
     int b0;
     const tls_config sc = sub_config(cfg, ns, i, &b0);
+    if (getenv("TLS_PRIO_ORDER")) {  // experiment: sub-batch i's whole chain at the i-th highest priority
+      lo_k1.prio = lo_dep.prio = std::min(pl->prio_hi + i, pl->prio_lo);
+    }
     size_t w;
     s = chain_workspace(&sc, do_attend, &w);
     if (s) return s;

@@ -2,8 +2,10 @@
 // for sm_100a: K3 attend_kernel, one thread-block cluster of cs CTAs per
 // (batch, KV-head) pair, each CTA a 1/cs slice of the pair's k_t tokens
 // (split-K flash decoding); the cs partials go to an L2-resident workspace,
-// one cluster barrier, then every CTA merges a slice with the LSE identity (T10).  bf16 GQA with head dim 64/128 runs on tensor cores (mma.sync);
-// MLA and fp32 run the generic CUDA-core path (NEXT: tcgen05 for MLA).
+// one cluster barrier, then every CTA merges a slice with the LSE identity (T10).
+// bf16 GQA with head dim 64/128 runs on tensor cores (mma.sync), MLA on
+// attend_mla_kernel (mma.sync; tcgen05 + TMEM form opt-in, TLS_MLA_TC=1), fp32
+// on the generic CUDA-core path.
 #include <math_constants.h>
 
 #include <type_traits>

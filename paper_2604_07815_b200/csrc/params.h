@@ -1,8 +1,9 @@
 // params.h -- host/device parameter blocks and shared-memory plans of the
-// three decode-step kernels:
-//   K1 block_score_kernel   (select.cu)  a1: block scores -> workspace
-//   K2 token_select_kernel  (select.cu)  a2-a4: top-k_b, token scores, top-k_t
-//   K3 attend_kernel        (attend.cu)  a5: sparse attention + LSE merge
+// decode-step kernels:
+//   qq_kernel, select_kernel (fused.cu)          a1: block scores; a2: top-k_b
+//   token_reg_kernel / token_cluster_kernel (select.cu)  a3: ranking keys
+//   attend_kernel / attend_mla_kernel (attend.cu)        a4: top-k_t; a5: attention
+//   pstep_kernel (pstep.cu, opt-in)              a1-a5 in one persistent launch
 #pragma once
 
 #include <stddef.h>

@@ -1,18 +1,17 @@
-// select.cu -- two-level selection of AsyncTLS (arXiv 2604.07815) for sm_100a.
+// select.cu -- token scoring (a3) of AsyncTLS (arXiv 2604.07815) for sm_100a.
 //
-//   K1 block_score_kernel   a1  s_i = Q+ . k^max_i + Q- . k^min_i  (P:99 via the
-//                               P:110 identity and linearity of sum_h): an
-//                               HBM-streaming GEMV over every block of every
-//                               pair, fp32 scores -> workspace.
-//   K1b block_topk_kernel   a2  M_t = top-k_b blocks, one CTA per pair
-//   K2 token_cluster_kernel a3  alpha~_j over the candidate tokens:
-//                               a cluster of nch chunk CTAs per pair; softmax
-//                               statistics merged over DSMEM, ranking keys and
-//                               their histogram -> workspace
-//   (a4, S_t = top-k_t tokens, runs at the start of attend.cu's
-//   kernel, which reads the keys and the histogram.)
-//
-// Citation key: P:n = line n of PAPER.md.  Readings U1..U19: DESIGN.md §3.
+// The decode step's kernels: qq_kernel + select_kernel (fused.cu: a1 block
+// scores as an HBM-streaming GEMV, a2 top-k_b in each pair's last tile CTA),
+// then K2 here, then attend_kernel (attend.cu: a4 top-k_t prologue + a5).
+//   K2 token_reg_kernel     a3  alpha~_j over the candidate tokens:
+//                               a cluster of nch chunk CTAs per pair, logits on
+//                               the tensor cores (mma.sync, INT4 codes -> bf16)
+//                               kept in registers, softmax statistics merged
+//                               over DSMEM, ranking keys and their histogram ->
+//                               workspace
+//   K2 token_cluster_kernel a3  the same contract when a chunk exceeds the
+//                               registers (two tensor-core passes over smem)
+// Citation key: P:n = line n of PAPER.md.  Readings U1..U20: DESIGN.md §3.
 #include <math_constants.h>
 
 #include "common.cuh"
