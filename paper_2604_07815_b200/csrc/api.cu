@@ -654,9 +654,6 @@ tls_status run_step(const tls_config* cfg, const void* q, const void* k_cache, c
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent(fork)");
     int b0;
     const tls_config sc = sub_config(cfg, ns, i, &b0);
-    if (getenv("TLS_PRIO_ORDER")) {  // experiment: sub-batch i's whole chain at the i-th highest priority
-      lo_k1.prio = lo_dep.prio = std::min(pl->prio_hi + i, pl->prio_lo);
-    }
     size_t w;
     s = chain_workspace(&sc, do_attend, &w);
     if (s) return s;
