@@ -436,7 +436,13 @@ int32_t tls_select_mode(const tls_config* cfg);
  * which = 3: the tokens per staged chunk of the MLA attention plan of
  * tls_sparse_attend (64, or 32 when the selected-token list leaves no room for
  * 64-token double buffering; 0 for GQA); which = 4: that plan's engine (3 =
- * tcgen05 tensor cores with TMEM accumulators, 2 = mma.sync, 1 = CUDA cores).
+ * tcgen05 tensor cores with TMEM accumulators, 2 = mma.sync, 1 = CUDA cores);
+ * which = 5: the token-scoring (a3) kernel's form (1 = one 1024-thread CTA per
+ * pair holding the pair's whole candidate index in shared memory, 4 = a cluster
+ * of two 512-thread CTAs holding half each, 2 = a cluster of chunk CTAs with the
+ * logits in registers, 3 = a cluster of chunk CTAs with two passes over shared
+ * memory; TLS_K2_FORM=cluster excludes forms 1 and 4, TLS_K2_FORM=1 / 2 forces
+ * form 1 / 4 where it fits).
  * -1 for an invalid configuration.
  * The environment variable TLS_CLUSTER overrides the heuristic for both
  * cluster sizes (1, 2, 4, 8 or 16). */

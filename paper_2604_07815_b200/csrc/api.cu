@@ -176,7 +176,10 @@ bool pstep_plan(const tls_config* c, int do_attend, tls::PStepParams& sp) {
 tls_status plan_select(const tls_config* c, tls::SelectParams& p) {
   memset(&p, 0, sizeof(p));
   p.d = dims_of(c);
-  tls::plan_select(p);
+  // TLS_K2_FORM (A/B and tests): "cluster" = the cluster forms even where token_pair_kernel fits; "1" / "2" =
+  // token_pair_kernel with that many CTAs per pair
+  const char* e = getenv("TLS_K2_FORM");
+  tls::plan_select(p, !e ? 0 : (e[0] == 'c' ? -1 : (e[0] == '1' ? 1 : (e[0] == '2' ? 2 : 0))));
   if ((int)p.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "token-kernel shared-memory plan does not fit");
   return TLS_OK;
 }
@@ -1118,7 +1121,13 @@ int32_t tls_select_mode(const tls_config* cfg) {
 }
 
 int32_t tls_cluster_size(const tls_config* cfg, int32_t which) {
-  if (check_config(cfg) != TLS_OK || which < 0 || which > 4) return -1;
+  if (check_config(cfg) != TLS_OK || which < 0 || which > 5) return -1;
+  if (which == 5) {  // the token kernel's form: 1 / 4 token_pair_kernel with 1 / 2 CTAs per pair, 2 register
+                     // cluster, 3 two-pass cluster
+    tls::SelectParams sp;
+    if (fused_mode(cfg) != 1 || plan_select(cfg, sp) != TLS_OK) return -1;
+    return sp.pairk == 1 ? 1 : (sp.pairk == 2 ? 4 : (sp.tpw > 0 ? 2 : 3));
+  }
   if (which == 3 || which == 4) {  // tls_sparse_attend's attention plan
     tls::AttendParams ap;
     if (plan_attend(cfg, ap, 0, 1) != TLS_OK) return -1;

@@ -29,6 +29,9 @@ struct Dims {
 };
 
 constexpr int kBracketWords = 2048;  // fast_topk's bracket scratch (fasttopk.cuh kBracketCap)
+constexpr int kPairGroups = 8;      // token_pair_kernel: staging groups (one mbarrier each)
+constexpr int kPairSmemMax = 219 * 1024;  // token_pair_kernel: dynamic shared-memory budget (api.cu kMaxSmem)
+constexpr int kPairSmemHalf = 104 * 1024; // ... of its two-CTA form (two CTAs per SM with their static blocks)
 constexpr int kKeyBins = 1024;      // fixed binning of the ranking keys: 1/16 log2 unit below kKeyTop
 constexpr float kKeyTop = 6.0f;     // > log2(32) >= every key (key = log2 alpha~ + log2 G <= log2 G)
 
@@ -67,6 +70,9 @@ struct SelectParams {  // K2 (token_reg_kernel, or token_cluster_kernel when a c
   int cb;              // candidate blocks per chunk CTA
   int tpw;             // > 0: token_reg_kernel with tpw 16-token tiles per warp; 0: token_cluster_kernel
   int nch;             // chunks per pair = ceil(kb_eff / cb)
+  int pairk;           // 1 / 2: token_pair_kernel with pairk CTAs per pair (cb = candidate blocks per CTA)
+  int gsh;             // token_pair_kernel: staging group = 2^gsh candidate blocks (<= kPairGroups groups)
+  int tmtpw, tmcols;   // token_pair_kernel: 16-token tiles per warp (even), TMEM columns allocated per CTA
   const void* q;
   const int* seq_lens;
   const float* scores;  // workspace [pairs, M] (K1)
@@ -216,13 +222,50 @@ static inline int kt_effective(const Dims& d) {
   return d.Kt < cand ? d.Kt : (int)cand;
 }
 
-static inline void plan_select(SelectParams& p) {
+static inline void plan_select(SelectParams& p, int pair_form = 0) {
   const Dims& d = p.d;
   p.kb_eff = kb_effective(d);
   p.kt_eff = kt_effective(d);
   const int nt0 = (d.G + 7) / 8, nt = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);  // instantiated NT
   const int ks = d.d_c / 16, nsplit = d.bf16 ? 1 : 3;
   const int per_block = d.B * (d.d_c / 2 + 8);
+  // one or two CTAs per pair (token_pair_kernel) when G <= 8, every block's scale/zero rows are 16-byte aligned
+  // (S even) and the candidate index fits shared memory: two 512-thread CTAs (two per SM) when half of it fits
+  // ~100 KB, else one 1024-thread CTA.  pair_form: 0 automatic, 1 / 2 force that many CTAs, < 0 the cluster forms
+  p.pairk = 0;
+  if (pair_form >= 0 && nt == 1 && (d.S & 1) == 0 && d.Kb <= 512) {
+    for (int nch = (pair_form ? pair_form : 2); nch >= 1; --nch) {
+      const int cb = (p.kb_eff + nch - 1) / nch;
+      size_t o = 0;
+      p.off_cblk = 0;
+      o = align16((size_t)p.kb_eff * 4);
+      p.off_qb = (unsigned)o;
+      o = align16(o + (size_t)nsplit * ks * 64 * 4);
+      p.off_qsum = (unsigned)o;
+      o = align16(o + 8 * 4);
+      p.off_qc = p.off_qrows = (unsigned)o;
+      o = (o + 127) & ~(size_t)127;
+      p.off_stage = (unsigned)o;
+      o = align16(o + (size_t)cb * per_block);
+      // TMEM logit store: 4 columns per tile, tiles per warp rounded up to even (pass 2 reads tiles in pairs)
+      const int nw = 32 / nch, tpw = (((cb << d.log2B) / 16 + nw - 1) / nw + 1) & ~1;
+      int cols = 32;
+      while (cols < nw * tpw) cols <<= 1;
+      if (d.B >= 16 && cols <= 512 / nch && o <= (size_t)(nch == 2 ? kPairSmemHalf : kPairSmemMax)) {
+        p.tmtpw = tpw;
+        p.tmcols = cols;
+        p.pairk = nch;
+        p.nch = nch;
+        p.tpw = 0;
+        p.cb = cb;
+        p.gsh = 0;
+        while (((cb + (1 << p.gsh) - 1) >> p.gsh) > kPairGroups) ++p.gsh;
+        p.smem_bytes = (unsigned)o;
+        return;
+      }
+      if (pair_form) break;
+    }
+  }
   // a pair's candidate blocks split over a cluster of nch <= 8 CTAs, ~24 KB (or more) of index each
   p.cb = (24 * 1024) / per_block;
   if (p.cb < 1) p.cb = 1;

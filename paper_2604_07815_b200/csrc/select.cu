@@ -701,6 +701,398 @@ __global__ void __launch_bounds__(kThreads, k2_min_blocks<KS, NT, NSPLIT>()) tok
 #undef TLS_STAMP
 }
 
+// ----------------------------------------------------------------------------
+// K2, one or two CTAs per pair (token_pair_kernel; G <= 8 and the pair's
+// candidate index in shared memory -- C2/C3: 128 blocks x 64 tokens x 24 B =
+// 192 KB): NCH = 1 is one 1024-thread CTA holding all of it; NCH = 2 is a
+// cluster of two 512-thread CTAs holding half each (two CTAs per SM, so one
+// CTA's start-up latency hides under the other's work).  Either way the
+// per-CTA fixed costs (hand-off wait, block-id read, merges, histogram) are
+// paid once or twice per pair instead of once per 1024 candidates, and the
+// softmax statistics merge inside the CTA (plus one DSMEM exchange for NCH 2).
+// Staging: every thread copies 16-byte chunks with cp.async (a block = B rows
+// of codes + B scale/zero pairs; rows past the cache end zero-filled) and
+// arrives on its staging group's mbarrier, so pass 1 runs on the first groups
+// while the rest land.  Two tensor-core passes over the staged codes (the same
+// L_hj = sm_scale log2(e) (zero sum q~ + scale q~.code) as the other forms,
+// P:129-133):
+//   pass 1: per-lane sum of 2^(L_hj - r) against a per-lane reference r =
+//           (largest logit seen) + kPairSlack, raised (warp-uniform branch)
+//           only when a logit exceeds it -> lanes -> warps -> CTA (-> cluster),
+//           fixed order -> lz_h = M_h + log2 Z_h;
+//   pass 2: L_hj recomputed (two mma + dequantisation per 16-token tile is
+//           cheaper than holding 8192 x G logits), x = L_hj - lz_h, key =
+//           log2 sum_h 2^x (the head sum over the four lanes that hold a
+//           token's heads by a transposed butterfly, 3 shuffles per 2 tiles).
+//           A token whose sum falls below 2^-100 (terms near the bottom of
+//           fp32's range: attention-sink-like logit spans, reading U20) is
+//           re-keyed in the log domain, mx + log2 sum_h 2^(x - mx): exact to
+//           fp32 rounding for any span.
+// The key histogram is built in shared memory; one release add per CTA hands
+// the pair to the attention kernel (ready count = NCH).
+constexpr int kPairThreads = 1024;
+constexpr float kPairSlack = 48.f;  // log2 units above the largest logit seen: terms <= 2^-48, no overflow
+
+// TMEM as the pair kernel's logit store: lane i of a warp writes / reads TMEM lane 32 (warp % 4) + i,
+// 4 (x4) or 8 (x8) consecutive 32-bit columns
+__device__ __forceinline__ void tm_st4(uint32_t taddr, float a, float b, float c, float d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr), "r"(__float_as_uint(a)),
+               "r"(__float_as_uint(b)), "r"(__float_as_uint(c)), "r"(__float_as_uint(d))
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void cp_async16_u(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0));
+}
+
+// acc = codes(16-token tile) x q~ (B fragments preloaded in registers, or read from shared memory per tile)
+template <int KS, int NSPLIT, bool PRE>
+__device__ __forceinline__ void pair_tile(const uint8_t* codes, const uint2 (&qbr)[PRE ? NSPLIT : 1][PRE ? KS : 1],
+                                          const uint2* qb2, float (&acc)[4]) {
+  CodeWords<KS> cw;
+  load_code_words<KS>(codes, true, true, cw);
+  constexpr int WPT = KS / 2;
+  uint32_t a[KS][4];
+#pragma unroll
+  for (int u = 0; u < WPT; ++u) {
+    uint32_t x0[4], x1[4];
+    unpack_nibbles8(cw.w0[u], x0);
+    unpack_nibbles8(cw.w1[u], x1);
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      a[2 * u + v][0] = x0[2 * v];
+      a[2 * u + v][1] = x1[2 * v];
+      a[2 * u + v][2] = x0[2 * v + 1];
+      a[2 * u + v][3] = x1[2 * v + 1];
+    }
+  }
+  acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 0; s < KS; ++s)
+#pragma unroll
+    for (int sp = 0; sp < NSPLIT; ++sp) {
+      uint2 bb;
+      if constexpr (PRE) bb = qbr[sp][s];
+      else bb = qb2[(sp * KS + s) * 32 + lane];
+      mma_bf16_16816(acc, a[s], bb.x, bb.y);
+    }
+}
+
+template <typename T, int KS, int NSPLIT, int NCH>
+__global__ void __launch_bounds__(kPairThreads / NCH, NCH) token_pair_kernel(const __grid_constant__ SelectParams p) {
+  constexpr int NTH = kPairThreads / NCH, NW = NTH / 32;
+  constexpr int rowbytes = KS * 8, lcpr = KS == 2 ? 0 : (KS == 4 ? 1 : 2);  // 16-byte chunks per code row: 2^lcpr
+  constexpr bool PRE = NSPLIT * KS <= 4;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t gbar[kPairGroups];
+  __shared__ __align__(8) uint64_t qbar;
+  __shared__ uint32_t lhist[kKeyBins];
+  __shared__ float s_wm[NW][8], s_ws[NW][8], s_lz[8];
+  __shared__ float s_cm[NCH][8], s_cz[NCH][8];  // [chunk][head]: every chunk's statistics, pushed by that chunk
+  __shared__ int s_kc, s_pslot;
+  __shared__ uint32_t s_tmem;
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q4 = lane & 3, r0 = lane >> 2;
+  const int chunk = NCH > 1 ? (int)blockIdx.x : 0, pair = blockIdx.y;
+  unsigned long long* dbg = p.dbg ? p.dbg + ((size_t)pair * 8 + chunk) * 8 : nullptr;
+#define TLS_STAMP(i) \
+  if (dbg && tid == 0) dbg[i] = gtimer();
+  TLS_STAMP(0)
+  launch_dependents();
+#pragma unroll
+  for (int i = 0; i < kKeyBins / NTH; ++i) lhist[tid + i * NTH] = 0u;
+  if constexpr (NCH > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");  // started
+  const int b = pair / d.Hkv;
+  const int n = min(max(p.seq_lens[b], 0), d.S);
+  const int m = (n + d.B - 1) >> d.log2B;
+  int* cblk = reinterpret_cast<int*>(smem + p.off_cblk);
+  const float* qsum = reinterpret_cast<const float*>(smem + p.off_qsum);
+  const uint8_t* stc = smem + p.off_stage;
+  const float2* stz = reinterpret_cast<const float2*>(smem + p.off_stage + ((size_t)p.cb << d.log2B) * rowbytes);
+  if (warp == 0) {
+    // TMEM columns for the pass-1 logits (L_hj of every staged token, 4 columns per 16-token tile per warp)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&s_tmem)),
+                 "r"((uint32_t)p.tmcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    if (lane == 0) {
+      for (int i = 0; i < kPairGroups; ++i) mbar_init(&gbar[i], NTH);  // one cp.async arrival per thread
+      mbar_init(&qbar, 1);
+      mbar_fence_init();
+      s_pslot = -1;
+      wait_ready(p.ready_in + pair, p.epoch);  // select_kernel's a2 outputs for this pair
+      if (NCH == 1) p.ready_in[pair] = 0u;     // the hand-off's only consumer
+      const uint32_t qfb = (uint32_t)(NSPLIT * KS * 256 + 32);  // the pair's q-fragment blob (qq_kernel)
+      mbar_arrive_expect_tx(&qbar, qfb);
+      tma_bulk_g2s(smem + p.off_qb, p.qfrag + (size_t)pair * qfb, qfb, &qbar);
+    }
+    __syncwarp();  // lane 0's acquire orders the warp's reads of the candidate list below
+    // candidate blocks: a2's M_t (ascending, -1 padded) or the lag-mode guide, compacted in list order to
+    // the valid ids (< m), at most kb_eff -- the same slots the attention prologue maps back to tokens
+    const int* cand = (p.guide ? p.guide : p.block_ids) + (size_t)pair * d.Kb;
+    constexpr int kMaxIt = 16;  // Kb <= 512 (plan)
+    int cv[kMaxIt];
+#pragma unroll
+    for (int i = 0; i < kMaxIt; ++i) cv[i] = i * 32 + lane < d.Kb ? cand[i * 32 + lane] : -1;  // loads in flight
+    int base = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxIt; ++i) {
+      if (i * 32 >= d.Kb) break;
+      const int blk = cv[i];
+      const bool ok = blk >= 0 && blk < m;
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      const int pos = base + __popc(bal & ((1u << lane) - 1u));
+      if (ok && pos < p.kb_eff) {
+        cblk[pos] = blk;
+        if (blk == m - 1) s_pslot = pos;  // the sequence's last (possibly partial) block
+      }
+      base += __popc(bal);
+    }
+    if (lane == 0) s_kc = min(base, p.kb_eff);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();  // cblk, s_kc, s_pslot, lhist zeroed, barriers initialised, TMEM allocated
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  TLS_STAMP(7)
+  // this warp's TMEM region: lanes of its quarter, columns (warp / 4) * 4 * tiles-per-warp ..
+  const uint32_t tmw = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 4 * p.tmtpw);
+  const int c0 = chunk * p.cb;                           // this CTA's first candidate slot
+  const int nbl = max(0, min(p.cb, s_kc - c0));          // and its number of candidate blocks
+  const int gsh = p.gsh;                                 // staging group = 2^gsh candidate blocks
+  {  // staging (cp.async, 16-byte chunks): warp w copies candidate blocks w, w + NW, ... (B rows of codes, then
+     // B scale/zero pairs), group by group; every thread arrives on a group's barrier once its copies landed
+    const uint32_t stc_u = smem_u32(stc), stz_u = smem_u32(stz);
+    const int ccb = d.B << lcpr, zcb = d.B >> 1;  // 16-byte chunks per block: codes, scale/zero
+    const uint8_t* cdb = p.codes + (size_t)pair * d.S * rowbytes + (size_t)lane * 16;
+    const float2* szb = reinterpret_cast<const float2*>(p.scale_zero) + (size_t)pair * d.S + 2 * lane;
+    int k = warp;
+    for (int g = 0; g < kPairGroups; ++g) {
+      const int kend = min((g + 1) << gsh, nbl);
+      for (; k < kend; k += NW) {
+        const int blk = cblk[c0 + k], rows = d.S - (blk << d.log2B);
+        const uint8_t* cs = cdb + (size_t)blk * (d.B * rowbytes);
+        const uint32_t cd = stc_u + (uint32_t)(k * ccb + lane) * 16u;
+        for (int c = 0; c < ccb; c += 32)
+          cp_async16_u(cd + (uint32_t)c * 16u, cs + (size_t)c * 16, ((c + lane) >> lcpr) < rows);
+        const float2* zs = szb + ((size_t)blk << d.log2B);
+        const uint32_t zd = stz_u + (uint32_t)(k * zcb + lane) * 16u;
+        for (int c = 0; c < zcb; c += 32) cp_async16_u(zd + (uint32_t)c * 16u, zs + 2 * c, 2 * (c + lane) < rows);
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&gbar[g])) : "memory");
+    }
+  }
+  const int nvl = n - (m - 1) * d.B;  // valid tokens of block m - 1
+  const int tshift = d.log2B - 4;
+  const int ntl = nbl << tshift;      // this CTA's 16-token tiles
+  // tiles holding rows past the sequence end: [tp0, tp1), inside block m - 1 (if this CTA holds it)
+  const int lp = s_pslot - c0;
+  const bool hasp = s_pslot >= 0 && lp >= 0 && lp < nbl && nvl < d.B;
+  const int tp0 = hasp ? (lp << tshift) + (nvl >> 4) : 0, tpn = hasp ? ((lp + 1) << tshift) - tp0 : 0;
+  TLS_STAMP(1)
+  const float sm2 = d.sm_scale * kLog2e;
+  mbar_wait(&qbar, 0);
+  float sq[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) sq[e] = sm2 * qsum[2 * q4 + e];  // padded heads: q~ = 0, sum 0
+  const uint2* qb2 = reinterpret_cast<const uint2*>(smem + p.off_qb);
+  uint2 qbr[PRE ? NSPLIT : 1][PRE ? KS : 1];
+  if constexpr (PRE) {
+#pragma unroll
+    for (int sp = 0; sp < NSPLIT; ++sp)
+#pragma unroll
+      for (int s2 = 0; s2 < KS; ++s2) qbr[sp][s2] = qb2[(sp * KS + s2) * 32 + lane];
+  }
+  // ---- pass 1: per-lane sums of heads 2q4, 2q4 + 1 against the lane's reference rf (packed fp32x2 math:
+  // .x = head 2q4, .y = head 2q4 + 1) ----
+  const float2 sq2 = make_float2(sq[0], sq[1]);
+  // the reference starts at the lane's first finite logit + kPairSlack (fx / fy: none seen yet); the logits go
+  // to TMEM (pass 2 reads them back instead of recomputing them)
+  float2 rf2 = make_float2(0.f, 0.f), hs2 = make_float2(0.f, 0.f);
+  bool fx = true, fy = true;
+  int gdone = -1;
+  for (int i = 0, t = warp; t < ntl; ++i, t += NW) {
+    const int grp = t >> (tshift + gsh);
+    while (gdone < grp) mbar_wait(&gbar[++gdone], 0);
+    float acc[4];
+    pair_tile<KS, NSPLIT, PRE>(stc + (size_t)t * 16 * rowbytes, qbr, qb2, acc);
+    const float2 z0 = stz[t * 16 + r0], z1 = stz[t * 16 + r0 + 8];
+    const float s0 = sm2 * z0.x, s1 = sm2 * z1.x;
+    // L for rows r0 (la) and r0 + 8 (lb), heads (2q4, 2q4 + 1)
+    float2 la = __ffma2_rn(make_float2(s0, s0), make_float2(acc[0], acc[1]), __fmul2_rn(make_float2(z0.y, z0.y), sq2));
+    float2 lb = __ffma2_rn(make_float2(s1, s1), make_float2(acc[2], acc[3]), __fmul2_rn(make_float2(z1.y, z1.y), sq2));
+    if ((unsigned)(t - tp0) < (unsigned)tpn) {  // warp-uniform: the sequence's partial last block
+      const int o = (t & ((1 << tshift) - 1)) << 4;
+      if (o + r0 >= nvl) la = make_float2(-CUDART_INF_F, -CUDART_INF_F);
+      if (o + r0 + 8 >= nvl) lb = make_float2(-CUDART_INF_F, -CUDART_INF_F);
+    }
+    tm_st4(tmw + 4 * i, la.x, la.y, lb.x, lb.y);
+    const float2 mt = make_float2(fmaxf(la.x, lb.x), fmaxf(la.y, lb.y));
+    if (__any_sync(0xffffffffu, fx || fy || mt.x > rf2.x || mt.y > rf2.y)) {  // first tile, then rare
+      if (mt.x > rf2.x || (fx && mt.x != -CUDART_INF_F)) {
+        const float nr = mt.x + kPairSlack;
+        hs2.x *= fexp2(rf2.x - nr);
+        rf2.x = nr, fx = false;
+      }
+      if (mt.y > rf2.y || (fy && mt.y != -CUDART_INF_F)) {
+        const float nr = mt.y + kPairSlack;
+        hs2.y *= fexp2(rf2.y - nr);
+        rf2.y = nr, fy = false;
+      }
+    }
+    const float2 nrf = make_float2(-rf2.x, -rf2.y);
+    la = __fadd2_rn(la, nrf);
+    lb = __fadd2_rn(lb, nrf);
+    hs2 = __fadd2_rn(hs2, __fadd2_rn(make_float2(fexp2(la.x), fexp2(la.y)), make_float2(fexp2(lb.x), fexp2(lb.y))));
+  }
+  float rf[2] = {fx ? -1e30f : rf2.x, fy ? -1e30f : rf2.y}, hs[2] = {hs2.x, hs2.y};
+#pragma unroll
+  for (int e = 0; e < 2; ++e)
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, rf[e], o), os = __shfl_xor_sync(0xffffffffu, hs[e], o);
+      const float nm = fmaxf(rf[e], om);
+      hs[e] = hs[e] * fexp2(rf[e] - nm) + os * fexp2(om - nm);
+      rf[e] = nm;
+    }
+  if (r0 == 0) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      s_wm[warp][2 * q4 + e] = rf[e];
+      s_ws[warp][2 * q4 + e] = hs[e];
+    }
+  }
+  TLS_STAMP(2)
+  __syncthreads();
+  TLS_STAMP(3)
+  if (warp < 8) {  // head h = warp: the warps' (reference, sum) merged in a fixed order
+    const float mv = lane < NW ? s_wm[lane][warp] : -1e30f, sv = lane < NW ? s_ws[lane][warp] : 0.f;
+    const float M = warp_max(mv);
+    const float S = warp_sum(sv * fexp2(mv - M));
+    if constexpr (NCH == 1) {
+      if (lane == 0) s_lz[warp] = (warp < d.G && S > 0.f) ? M + flog2(S) : CUDART_INF_F;
+    } else {
+      asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");  // every chunk CTA has started (DSMEM rule)
+      if (lane < NCH) {
+        *dsmem(&s_cm[chunk][warp], (unsigned)lane) = M;
+        *dsmem(&s_cz[chunk][warp], (unsigned)lane) = S;
+      }
+    }
+  }
+  if constexpr (NCH > 1) {
+    if (warp >= 8) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+    cluster_sync_all();  // every chunk's statistics have landed in every CTA
+    if (chunk == 0 && tid == 0) p.ready_in[pair] = 0u;  // every CTA of the pair passed its wait
+    if (tid < 8) {
+      float M = -1e30f, S = 0.f;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) M = fmaxf(M, s_cm[c][tid]);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) S += s_cz[c][tid] * fexp2(s_cm[c][tid] - M);
+      s_lz[tid] = (tid < d.G && S > 0.f) ? M + flog2(S) : CUDART_INF_F;
+    }
+  }
+  __syncthreads();
+  TLS_STAMP(4)
+  // ---- pass 2: ranking keys, two tiles per step (every lane emits one key per step) ----
+  float nlz[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) nlz[e] = -s_lz[2 * q4 + e];  // padded heads: -inf -> no term
+  const float2 nlz2 = make_float2(nlz[0], nlz[1]);
+  uint32_t* kout = p.keys + (size_t)pair * p.kb_eff * d.B + ((size_t)c0 << d.log2B);
+  const bool bit0 = q4 & 1, bit1 = q4 & 2;
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");  // this warp's logits are in TMEM
+  for (int i = 0, ta = warp; ta < ntl; i += 2, ta += 2 * NW) {
+    float x[2][2][2];  // [tile a / b][head e][row r0, r0 + 8]: L_hj - lz_h (tile b past the end: unused)
+    {
+      float v[8];
+      tm_ld8(tmw + 4 * i, v);
+      const float2 xa0 = __fadd2_rn(make_float2(v[0], v[1]), nlz2), xb0 = __fadd2_rn(make_float2(v[2], v[3]), nlz2);
+      const float2 xa1 = __fadd2_rn(make_float2(v[4], v[5]), nlz2), xb1 = __fadd2_rn(make_float2(v[6], v[7]), nlz2);
+      x[0][0][0] = xa0.x, x[0][1][0] = xa0.y, x[0][0][1] = xb0.x, x[0][1][1] = xb0.y;
+      x[1][0][0] = xa1.x, x[1][1][0] = xa1.y, x[1][0][1] = xb1.x, x[1][1][1] = xb1.y;
+    }
+    float pa = fexp2(x[0][0][0]) + fexp2(x[0][1][0]), pb = fexp2(x[0][0][1]) + fexp2(x[0][1][1]);
+    float pc = fexp2(x[1][0][0]) + fexp2(x[1][1][0]), pd = fexp2(x[1][0][1]) + fexp2(x[1][1][1]);
+    // transposed butterfly: lane q4 ends with the head sum of (tile bit1, row r0 + 8 bit0)
+    float k1 = bit0 ? pb : pa, k2 = bit0 ? pd : pc;
+    k1 += __shfl_xor_sync(0xffffffffu, bit0 ? pa : pb, 1);
+    k2 += __shfl_xor_sync(0xffffffffu, bit0 ? pc : pd, 1);
+    float mine = bit1 ? k2 : k1;
+    mine += __shfl_xor_sync(0xffffffffu, bit1 ? k1 : k2, 2);
+    const int t = ta + (bit1 ? NW : 0);
+    const int row = r0 + (bit0 ? 8 : 0);
+    const bool v = t < ntl && !((unsigned)(t - tp0) < (unsigned)tpn && ((t & ((1 << tshift) - 1)) << 4) + row >= nvl);
+    float kf = flog2(mine);
+    if (__any_sync(0xffffffffu, v && !(mine >= 0x1p-100f))) {  // log domain for this step (reading U20)
+      float ma = fmaxf(x[0][0][0], x[0][1][0]), mb = fmaxf(x[0][0][1], x[0][1][1]);
+      float mc = fmaxf(x[1][0][0], x[1][1][0]), md = fmaxf(x[1][0][1], x[1][1][1]);
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+        mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+        md = fmaxf(md, __shfl_xor_sync(0xffffffffu, md, o));
+      }
+      ma = ma == -CUDART_INF_F ? 0.f : ma, mb = mb == -CUDART_INF_F ? 0.f : mb;
+      mc = mc == -CUDART_INF_F ? 0.f : mc, md = md == -CUDART_INF_F ? 0.f : md;
+      pa = fexp2(x[0][0][0] - ma) + fexp2(x[0][1][0] - ma), pb = fexp2(x[0][0][1] - mb) + fexp2(x[0][1][1] - mb);
+      pc = fexp2(x[1][0][0] - mc) + fexp2(x[1][1][0] - mc), pd = fexp2(x[1][0][1] - md) + fexp2(x[1][1][1] - md);
+      k1 = bit0 ? pb : pa, k2 = bit0 ? pd : pc;
+      k1 += __shfl_xor_sync(0xffffffffu, bit0 ? pa : pb, 1);
+      k2 += __shfl_xor_sync(0xffffffffu, bit0 ? pc : pd, 1);
+      mine = bit1 ? k2 : k1;
+      mine += __shfl_xor_sync(0xffffffffu, bit1 ? k1 : k2, 2);
+      kf = (bit1 ? (bit0 ? md : mc) : (bit0 ? mb : ma)) + flog2(mine);
+    }
+    if (t < ntl) {
+      kout[t * 16 + row] = v ? f2key(kf) : 0u;
+      if (v) atomicAdd(&lhist[key_bin(kf)], 1u);
+    }
+  }
+  __syncthreads();
+  uint32_t* gh = p.khist + (size_t)pair * kKeyBins;
+#pragma unroll
+  for (int i = 0; i < kKeyBins / NTH; ++i) {
+    const int j = tid + i * NTH;
+    if constexpr (NCH == 1) gh[j] = lhist[j];  // the pair's whole histogram
+    else if (lhist[j]) atomicAdd(&gh[j], lhist[j]);  // zeroed by qq_kernel
+  }
+  TLS_STAMP(5)
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem), "r"((uint32_t)p.tmcols));
+  if (tid == 0)  // hand-off: a release add (this CTA's keys and histogram, cumulative over the CTA barrier)
+    red_release_add_gpu(p.ready_out + pair, 1u);
+  TLS_STAMP(6)
+#undef TLS_STAMP
+}
+
+template <typename T, int KS, int NSPLIT>
+static cudaError_t launch_k2_pair(const SelectParams& p, cudaStream_t st, const LaunchOpts& o) {
+  const unsigned pairs = (unsigned)(p.d.batch * p.d.Hkv);
+  if (p.pairk == 2) {
+    auto kern = token_pair_kernel<T, KS, NSPLIT, 2>;
+    cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, false);
+    if (e != cudaSuccess) return e;
+    return launch_ex(kern, dim3(2u, pairs, 1), kPairThreads / 2, p.smem_bytes, st, o, 2u, p);
+  }
+  auto kern = token_pair_kernel<T, KS, NSPLIT, 1>;
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, false);
+  if (e != cudaSuccess) return e;
+  return launch_ex(kern, dim3(1u, pairs, 1), kPairThreads, p.smem_bytes, st, o, 0u, p);
+}
+
 // ============================================================== launchers
 template <typename T, int KS, int NT, int NSPLIT>
 static cudaError_t launch_k2(const SelectParams& p, cudaStream_t st, const LaunchOpts& o) {
@@ -720,6 +1112,12 @@ bool select_supported(int d_c, int G) {
 template <typename T, int NS>
 static cudaError_t dispatch_k2(const SelectParams& p, cudaStream_t st, const LaunchOpts& o) {
   const int ks = p.d.d_c / 16, nt = (p.d.G + 7) / 8;
+  if (p.pairk) {
+    if (ks == 2) return launch_k2_pair<T, 2, NS>(p, st, o);
+    if (ks == 4) return launch_k2_pair<T, 4, NS>(p, st, o);
+    if (ks == 8) return launch_k2_pair<T, 8, NS>(p, st, o);
+    return cudaErrorInvalidValue;
+  }
 #define TLS_K2(KS_, NT_) \
   if (ks == KS_ && nt <= NT_) return launch_k2<T, KS_, NT_, NS>(p, st, o);
   TLS_K2(2, 1) TLS_K2(2, 2) TLS_K2(2, 4)

@@ -126,6 +126,17 @@ def test_workspace_and_plan(lib, monkeypatch):
              top_blocks=128, top_tokens=1024, layout=_lib.TLS_MLA)
     assert lib.tls_cluster_size(ctypes.byref(c4), 2) > 0
     assert lib.tls_launch_count(ctypes.byref(c4), 2) == 4
+    # token-kernel form: one CTA per pair where G <= 8 and the pair's candidate index fits shared memory
+    assert lib.tls_cluster_size(ctypes.byref(c3), 5) == 4 and lib.tls_cluster_size(ctypes.byref(c2), 5) == 4
+    monkeypatch.setenv("TLS_K2_FORM", "1")
+    assert lib.tls_cluster_size(ctypes.byref(c3), 5) == 1
+    monkeypatch.delenv("TLS_K2_FORM")
+    assert lib.tls_cluster_size(ctypes.byref(c4), 5) in (2, 3)  # MLA, G = 32: the cluster forms
+    c3kb = cfg(batch=32, num_q_heads=64, num_kv_heads=8, max_seq_len=98304, top_blocks=256, top_tokens=1024)
+    assert lib.tls_cluster_size(ctypes.byref(c3kb), 5) in (2, 3)  # 384 KB of candidates: too large for one CTA
+    monkeypatch.setenv("TLS_K2_FORM", "cluster")
+    assert lib.tls_cluster_size(ctypes.byref(c3), 5) == 2
+    monkeypatch.delenv("TLS_K2_FORM")
 
 
 def test_cluster_override(lib, monkeypatch):

@@ -556,12 +556,34 @@ def test_mla_tcgen05_attention(case, monkeypatch):
             check_pair(w, cfg, inputs, idx, res, b, g, stats)
 
 
-@pytest.mark.parametrize("name,every", [("gqa8", 16), ("mla", 16), ("gqa8", 1000), ("mla", 700)])
-def test_sink_tokens_wide_logit_span(name, every):
+@pytest.mark.parametrize("name", ["gqa4", "gqa8", "c1", "fp32_dc64_g8", "b128", "mha"])
+@pytest.mark.parametrize("form", ["pair2", "pair1", "cluster"])
+def test_token_kernel_forms(name, form, monkeypatch):
+    """Both forms of the token-scoring kernel (a3) against the oracle: one 1024-thread CTA per pair holding the
+    whole candidate index (the default where G <= 8 and it fits shared memory), and the cluster of chunk CTAs
+    (TLS_K2_FORM=cluster; the only form for MLA / G > 8)."""
+    monkeypatch.setenv("TLS_K2_FORM", {"pair2": "2", "pair1": "1", "cluster": "cluster"}[form])
+    w = SMALL[name]
+    cfg, inputs, idx = setup_case(w, seed=5, pattern="uniform")
+    assert tls.cluster_size(cfg, 5) == {"pair2": 4, "pair1": 1}.get(form, 2)
+    res = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    stats = {"block_near_ties": 0, "token_near_ties": 0}
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            check_pair(w, cfg, inputs, idx, res, b, g, stats)
+
+
+@pytest.mark.parametrize("name,every,form", [("gqa8", 16, "auto"), ("mla", 16, "auto"), ("gqa8", 1000, "auto"),
+                                             ("mla", 700, "auto"), ("gqa8", 16, "cluster"), ("gqa8", 1000, "cluster"),
+                                             ("gqa8", 16, "1"), ("gqa8", 1000, "1")])
+def test_sink_tokens_wide_logit_span(name, every, form, monkeypatch):
     """Reading U20: attention-sink-like keys (tokens aligned with the group's queries so strongly that the
     logits of the pair span > 200 nats) must not collapse the other candidates' ranking keys: alpha~ of an ordinary
     token is then ~e^-200 of a sink's, below fp32's range as a value, but its ln alpha~ is representable and the
     top-k_t among the ordinary tokens must still follow the oracle's order."""
+    if form != "auto":
+        monkeypatch.setenv("TLS_K2_FORM", form)
     w = SMALL[name]
     inputs = W.make_inputs(w, seed=17, pattern="uniform", device=DEV, ragged=False)
     G = w.num_q_heads // w.num_kv_heads
