@@ -179,7 +179,7 @@ tls_status plan_select(const tls_config* c, tls::SelectParams& p) {
   // TLS_K2_FORM (A/B and tests): "cluster" = the cluster forms even where token_pair_kernel fits; "1" / "2" =
   // token_pair_kernel with that many CTAs per pair
   const char* e = getenv("TLS_K2_FORM");
-  tls::plan_select(p, !e ? 0 : (e[0] == 'c' ? -1 : (e[0] == '1' ? 1 : (e[0] == '2' ? 2 : 0))));
+  tls::plan_select(p, !e ? 0 : (e[0] == 'c' ? -1 : (e[0] == '1' ? 1 : (e[0] == '2' ? 2 : (e[0] == '4' ? 4 : 0)))));
   if ((int)p.smem_bytes > kMaxSmem) return fail(TLS_ERR_UNSUPPORTED, "token-kernel shared-memory plan does not fit");
   return TLS_OK;
 }
@@ -1126,7 +1126,7 @@ int32_t tls_cluster_size(const tls_config* cfg, int32_t which) {
                      // cluster, 3 two-pass cluster
     tls::SelectParams sp;
     if (fused_mode(cfg) != 1 || plan_select(cfg, sp) != TLS_OK) return -1;
-    return sp.pairk == 1 ? 1 : (sp.pairk == 2 ? 4 : (sp.tpw > 0 ? 2 : 3));
+    return sp.pairk == 1 ? 1 : (sp.pairk == 2 ? 4 : (sp.pairk == 4 ? 5 : (sp.tpw > 0 ? 2 : 3)));
   }
   if (which == 3 || which == 4) {  // tls_sparse_attend's attention plan
     tls::AttendParams ap;

@@ -32,6 +32,7 @@ constexpr int kBracketWords = 2048;  // fast_topk's bracket scratch (fasttopk.cu
 constexpr int kPairGroups = 8;      // token_pair_kernel: staging groups (one mbarrier each)
 constexpr int kPairSmemMax = 219 * 1024;  // token_pair_kernel: dynamic shared-memory budget (api.cu kMaxSmem)
 constexpr int kPairSmemHalf = 104 * 1024; // ... of its two-CTA form (two CTAs per SM with their static blocks)
+constexpr int kPairSmemQuarter = 50 * 1024;  // ... of its four-CTA form (four CTAs per SM)
 constexpr int kKeyBins = 1024;      // fixed binning of the ranking keys: 1/16 log2 unit below kKeyTop
 constexpr float kKeyTop = 6.0f;     // > log2(32) >= every key (key = log2 alpha~ + log2 G <= log2 G)
 
@@ -234,7 +235,7 @@ static inline void plan_select(SelectParams& p, int pair_form = 0) {
   // ~100 KB, else one 1024-thread CTA.  pair_form: 0 automatic, 1 / 2 force that many CTAs, < 0 the cluster forms
   p.pairk = 0;
   if (pair_form >= 0 && nt == 1 && (d.S & 1) == 0 && d.Kb <= 512) {
-    for (int nch = (pair_form ? pair_form : 2); nch >= 1; --nch) {
+    for (int nch = (pair_form ? pair_form : 2); nch >= 1; nch = nch == 4 ? 2 : nch - 1) {
       const int cb = (p.kb_eff + nch - 1) / nch;
       size_t o = 0;
       p.off_cblk = 0;
@@ -251,7 +252,8 @@ static inline void plan_select(SelectParams& p, int pair_form = 0) {
       const int nw = 32 / nch, tpw = (((cb << d.log2B) / 16 + nw - 1) / nw + 1) & ~1;
       int cols = 32;
       while (cols < nw * tpw) cols <<= 1;
-      if (d.B >= 16 && cols <= 512 / nch && o <= (size_t)(nch == 2 ? kPairSmemHalf : kPairSmemMax)) {
+      if (d.B >= 16 && cols <= 512 / nch &&
+          o <= (size_t)(nch == 4 ? kPairSmemQuarter : (nch == 2 ? kPairSmemHalf : kPairSmemMax))) {
         p.tmtpw = tpw;
         p.tmcols = cols;
         p.pairk = nch;

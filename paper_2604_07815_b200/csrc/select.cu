@@ -1081,6 +1081,12 @@ __global__ void __launch_bounds__(kPairThreads / NCH, NCH) token_pair_kernel(con
 template <typename T, int KS, int NSPLIT>
 static cudaError_t launch_k2_pair(const SelectParams& p, cudaStream_t st, const LaunchOpts& o) {
   const unsigned pairs = (unsigned)(p.d.batch * p.d.Hkv);
+  if (p.pairk == 4) {
+    auto kern = token_pair_kernel<T, KS, NSPLIT, 4>;
+    cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, false);
+    if (e != cudaSuccess) return e;
+    return launch_ex(kern, dim3(4u, pairs, 1), kPairThreads / 4, p.smem_bytes, st, o, 4u, p);
+  }
   if (p.pairk == 2) {
     auto kern = token_pair_kernel<T, KS, NSPLIT, 2>;
     cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, false);

@@ -557,15 +557,15 @@ def test_mla_tcgen05_attention(case, monkeypatch):
 
 
 @pytest.mark.parametrize("name", ["gqa4", "gqa8", "c1", "fp32_dc64_g8", "b128", "mha"])
-@pytest.mark.parametrize("form", ["pair2", "pair1", "cluster"])
+@pytest.mark.parametrize("form", ["pair4", "pair2", "pair1", "cluster"])
 def test_token_kernel_forms(name, form, monkeypatch):
     """Both forms of the token-scoring kernel (a3) against the oracle: one 1024-thread CTA per pair holding the
     whole candidate index (the default where G <= 8 and it fits shared memory), and the cluster of chunk CTAs
     (TLS_K2_FORM=cluster; the only form for MLA / G > 8)."""
-    monkeypatch.setenv("TLS_K2_FORM", {"pair2": "2", "pair1": "1", "cluster": "cluster"}[form])
+    monkeypatch.setenv("TLS_K2_FORM", {"pair4": "4", "pair2": "2", "pair1": "1", "cluster": "cluster"}[form])
     w = SMALL[name]
     cfg, inputs, idx = setup_case(w, seed=5, pattern="uniform")
-    assert tls.cluster_size(cfg, 5) == {"pair2": 4, "pair1": 1}.get(form, 2)
+    assert tls.cluster_size(cfg, 5) == {"pair4": 5, "pair2": 4, "pair1": 1}.get(form, 2)
     res = run_decode(cfg, inputs, idx)
     torch.cuda.synchronize()
     stats = {"block_near_ties": 0, "token_near_ties": 0}

@@ -27,7 +27,7 @@ pairs = w.batch * w.num_kv_heads
 k2 = buf[65536 * 16: 65536 * 16 + pairs * 64].view(pairs * 8, 8).cpu().double() / 1e3
 k2 = k2[k2[:, 0] > 0]
 form = tls.cluster_size(cfg, 5)
-names = (["wait+issue", "pass1 (warp 0)", "pass1 all warps", "lz merge", "pass2 keys+hist", "end"] if form in (1, 4) else
+names = (["wait+issue", "pass1 (warp 0)", "pass1 all warps", "lz merge", "pass2 keys+hist", "end"] if form in (1, 4, 5) else
          ["wait+issue", "landed", "pass1+CTA merge", "cluster sync", "pass2 keys+hist", "end"])
 print(f"{w.name}: form {form}, {k2.shape[0]} token CTAs, per-phase us:      min    p10    med    p90    max")
 for i in range(6):
