@@ -62,7 +62,7 @@ def algorithmic_bytes_per_pair(w) -> float:
     return m * 2 * w.d_k * s + cand * (w.d_c // 2 + 8) + kt * row + G * (w.d_k + w.d_v) * s
 
 
-def kernel_bytes_per_pair(w, mode: int = 2) -> dict:
+def kernel_bytes_per_pair(w, mode: int = 2, token_kernel: str = "token_cluster_kernel") -> dict:
     """Algorithmic bytes per (batch, kv-head) pair of each launch of the step
     (the terms of algorithmic_bytes_per_pair split by the kernel that moves
     them; q is read by every kernel that uses it; intermediates -- scores,
@@ -80,7 +80,7 @@ def kernel_bytes_per_pair(w, mode: int = 2) -> dict:
     a5 = kt * row + q + G * w.d_v * s  # selected K/V rows, o
     if mode == 3:  # the persistent step kernel: a1-a5 in one launch
         return {"pstep_kernel": a1 + a3 + a5}
-    return {"select_kernel": a1, "token_cluster_kernel": a3 + q, "attend_kernel": a5}
+    return {"select_kernel": a1, token_kernel: a3 + q, "attend_kernel": a5}
 
 
 def hbm_peak():
@@ -467,7 +467,7 @@ def run_tls(args, w, rank, world, local_rank):
     clk = clocks.summary(t_wall0, t_wall1)
     pairs = w.batch * w.num_kv_heads
     mode = tls.select_mode(cfg)
-    kbytes = kernel_bytes_per_pair(w, mode)
+    kbytes = kernel_bytes_per_pair(w, mode, names[1] if len(names) > 1 else "token_cluster_kernel")
     ms_ser = sum(kern_step_times) / len(kern_step_times)
     kernels = {k: {"avg_us": kavg[i] * 1e3, "share": kavg[i] / ms_ser,
                    "algorithmic_bytes_per_launch": kbytes[k] * pairs,

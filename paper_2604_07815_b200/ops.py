@@ -485,8 +485,12 @@ def select_mode(cfg: TLSConfig) -> int:
 
 
 def kernel_names(cfg: TLSConfig) -> tuple:
-    """Names of the launches one tls_decode call enqueues (the timing slots of timing_read)."""
-    return STEP_KERNELS if select_mode(cfg) == 3 else KERNELS
+    """Names of the launches one tls_decode call enqueues (the timing slots of timing_read); the token kernel is
+    token_pair_kernel (one, two or four CTAs per pair) or token_cluster_kernel (token_reg_kernel /
+    token_cluster_kernel: a cluster of chunk CTAs), per ``cluster_size(cfg, 5)``."""
+    if select_mode(cfg) == 3:
+        return STEP_KERNELS
+    return (KERNELS[0], "token_pair_kernel", KERNELS[2]) if cluster_size(cfg, 5) in (1, 4, 5) else KERNELS
 
 
 def timing_enable(n_calls: int) -> None:

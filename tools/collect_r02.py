@@ -13,9 +13,9 @@ import sys
 
 V = sys.argv[1]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
+G, P = os.path.join(ROOT, "gpurun_out"), os.environ.get("TLS_PROFILES_OUT", os.path.join(ROOT, "profiles"))
 WL = {"c3": "c3-qwen3-32b-96k-b32", "c2": "c2-qwen3-8b-48k-b16", "c4": "c4-glm47flash-mla-64k-b32"}
-SLOT = {"select_kernel": "select_kernel", "token_reg_kernel": "token_cluster_kernel",
+SLOT = {"select_kernel": "select_kernel", "token_reg_kernel": "token_cluster_kernel", "token_pair_kernel": "token_pair_kernel",
         "token_cluster_kernel": "token_cluster_kernel", "attend_kernel": "attend_kernel",
         "attend_mla_kernel": "attend_kernel", "qq_kernel": "qq_kernel"}
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -100,7 +100,8 @@ for c in ("c3", "c2", "c4"):
     f = os.path.join(G, f"r02bench_{c}_{V}.json")
     if os.path.exists(f):
         shutil.copy(f, os.path.join(P, f"r02_bench_{c}_{V}.json"))
-for src, dst in ((f"r02smoke_{V}.log", f"r02_smoke_{V}.log"), (f"r02timeline_{V}.txt", f"r02_timeline_{V}.txt")):
+for src, dst in ((f"r02smoke_{V}.log", f"r02_smoke_{V}.log"), (f"r02timeline_{V}.txt", f"r02_timeline_{V}.txt"),
+                 (f"r02k2stamps_{V}.txt", f"r02_k2stamps_{V}.txt")):
     if os.path.exists(os.path.join(G, src)):
         shutil.copy(os.path.join(G, src), os.path.join(P, dst))
 print("collected", V)

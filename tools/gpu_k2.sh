@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 V=${1:-x}
 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "forms or small or sink or separate or repeated or lag or edge" > gpurun_out/k2_tests_${V}.log 2>&1
 tail -3 gpurun_out/k2_tests_${V}.log
-for f in auto 4 1; do
+for f in auto 1 cluster; do
 for c in c3 c2; do
   if [ $f = auto ]; then unset TLS_K2_FORM; else export TLS_K2_FORM=$f; fi
   timeout 300 python bench.py --config $c --no-cpu-baseline --steps 300 --warmup 20 > gpurun_out/k2_bench_${c}_${f}_${V}.json 2> gpurun_out/k2_bench_${c}_${f}_${V}.err
