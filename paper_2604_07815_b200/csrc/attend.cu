@@ -432,10 +432,12 @@ __device__ void phase_attend_mma_t(const AttendParams& p, int pair, int b, int g
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
   for (int c = 0; c < nchunks; ++c) {
+    cp_async_wait<kAttnStages - 2>();
+    // one barrier per chunk: chunk c landed for every thread's copies, and every warp finished chunk c - 1, whose
+    // stage the refill below overwrites
+    __syncthreads();
     if (c + kAttnStages - 1 < nchunks) load_chunk(c + kAttnStages - 1, (c + kAttnStages - 1) % kAttnStages);
     else cp_async_commit();
-    cp_async_wait<kAttnStages - 1>();
-    __syncthreads();  // chunk c landed for every thread's copies
     const __nv_bfloat16* sK = sbuf + (size_t)(c % kAttnStages) * 2 * TC * D;
     const __nv_bfloat16* sV = sK + TC * D;
     const int nt = min(TC, tloc - c * TC);
@@ -506,9 +508,9 @@ __device__ void phase_attend_mma_t(const AttendParams& p, int pair, int b, int g
         mma_bf16_16816(o[mt], a, pb0, pb1);
       }
     }
-    __syncthreads();  // stage c % kAttnStages consumed before it is refilled
   }
   cp_async_wait<0>();
+  __syncthreads();  // every warp done with the last stage
   // ---- merge the 4 token groups (the staging buffers become scratch) ----
   constexpr int WS = D + 4;
   float* wo = reinterpret_cast<float*>(kvbuf);  // [tg][8 heads][WS]
