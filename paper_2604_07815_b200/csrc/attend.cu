@@ -205,19 +205,25 @@ __device__ void phase_attend_mma(const AttendParams& p, int pair, int b, int g, 
   const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + (size_t)pair * p.kv_rows * D;
   const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(p.v_cache) + (size_t)pair * p.kv_rows * D;
   const int nchunks = (tloc + TC - 1) / TC;
+  // thread tid copies 16-byte chunk tid % CPR of rows tid / CPR + (kThreads / CPR) * it: a fixed column and
+  // swizzle (row & 7 is the same for every it), so per row only the token id and two addresses change
+  static_assert(kThreads % CPR == 0 && (kThreads / CPR) % 8 == 0, "fixed swizzle per thread");
+  const int lch = tid % CPR, lrow = tid / CPR;
+  const uint32_t sdst = smem_u32(sbuf) + (uint32_t)(lrow * D + ((lch ^ (lrow & 7)) << 3)) * 2u;
+  const __nv_bfloat16* kcol = kb + lch * 8;
+  const __nv_bfloat16* vcol = vb + lch * 8;
   auto load_chunk = [&](int c, int stage) {
-    __nv_bfloat16* sK = sbuf + (size_t)stage * 2 * TC * D;
-    __nv_bfloat16* sV = sK + TC * D;
+    const uint32_t dK = sdst + (uint32_t)stage * (2 * TC * D * 2), dV = dK + TC * D * 2;
     const int nt = min(TC, tloc - c * TC);
+    const int* sc = sel + c * TC + lrow;
 #pragma unroll
     for (int it = 0; it < (TC * CPR) / kThreads; ++it) {
-      const int i = tid + it * kThreads;
-      const int row = i / CPR, ch = i - row * CPR;
+      const int row = lrow + it * (kThreads / CPR);
       const bool ok = row < nt;
-      const int tok = ok ? sel[c * TC + row] : 0;
-      const int dst = row * D + ((ch ^ (row & 7)) << 3);
-      cp_async16(sK + dst, kb + (size_t)tok * D + ch * 8, ok);
-      cp_async16(sV + dst, vb + (size_t)tok * D + ch * 8, ok);
+      const size_t tok = (size_t)(ok ? sc[it * (kThreads / CPR)] : 0) * D;
+      const uint32_t o = (uint32_t)(it * (kThreads / CPR) * D * 2);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dK + o), "l"(kcol + tok), "r"(ok ? 16 : 0));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dV + o), "l"(vcol + tok), "r"(ok ? 16 : 0));
     }
     cp_async_commit();
   };

@@ -26,6 +26,8 @@ def test_sanitizer_clean(tool):
     r = subprocess.run(cmd + [sys.executable, os.path.join(ROOT, "tools", "sanitize_case.py")], capture_output=True,
                        text=True, timeout=1500, cwd=ROOT)
     out = r.stdout + r.stderr
+    if "compute-sanitizer is closed" in out:  # the GPU pool's wrapper refuses the tool (not this library's result)
+        pytest.skip("compute-sanitizer is disabled on this GPU pool: " + out.strip().splitlines()[-1][:200])
     assert r.returncode == 0 and "sanitize cases done" in out, out[-4000:]
     summary = "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" if tool == "racecheck" else \
         "ERROR SUMMARY: 0 errors"
