@@ -1126,7 +1126,7 @@ int32_t tls_cluster_size(const tls_config* cfg, int32_t which) {
                      // cluster, 3 two-pass cluster
     tls::SelectParams sp;
     if (fused_mode(cfg) != 1 || plan_select(cfg, sp) != TLS_OK) return -1;
-    return sp.pairk == 1 ? 1 : (sp.pairk == 2 ? 4 : (sp.pairk == 4 ? 5 : (sp.tpw > 0 ? 2 : 3)));
+    return sp.pairk == 1 ? 1 : (sp.pairk == 2 ? 4 : (sp.pairk == 4 ? 5 : (sp.pairk >= 8 ? 6 : (sp.tpw > 0 ? 2 : 3))));
   }
   if (which == 3 || which == 4) {  // tls_sparse_attend's attention plan
     tls::AttendParams ap;

@@ -272,6 +272,42 @@ static inline void plan_select(SelectParams& p, int pair_form = 0) {
   p.cb = (24 * 1024) / per_block;
   if (p.cb < 1) p.cb = 1;
   if (p.cb * 8 < p.kb_eff) p.cb = (p.kb_eff + 7) / 8;
+  // G > 8 (MLA): token_pair_nt_kernel, a cluster of 16 (else 8) 256-thread CTAs per pair holding the candidate
+  // index in shared memory and the logits in TMEM (bf16, d_c in {32, 128})
+  if (pair_form >= 0 && nt > 1 && d.bf16 && (d.S & 1) == 0 && d.Kb <= 512 && (ks == 2 || ks == 8) && d.B >= 16) {
+    for (int nch = 16; nch >= 8; nch /= 2) {
+      const int cb = (p.kb_eff + nch - 1) / nch;
+      size_t o = 0;
+      p.off_cblk = 0;
+      o = align16((size_t)p.kb_eff * 4);
+      p.off_qb = (unsigned)o;
+      o = align16(o + (size_t)nsplit * nt * ks * 64 * 4);
+      p.off_qsum = (unsigned)o;
+      o = align16(o + (size_t)nt * 8 * 4);
+      p.off_qc = p.off_qrows = (unsigned)o;
+      o = (o + 127) & ~(size_t)127;
+      p.off_stage = (unsigned)o;
+      o = align16(o + (size_t)cb * per_block);
+      const size_t stat = 4096 + 8 * nt * 8 * 4 + 2 * nt * 8 * 4 + 2 * (size_t)nch * nt * 8 * 4 + 256;
+      int per_sm = (int)((228 * 1024) / (o + stat + 1024));
+      if (per_sm > 4) per_sm = 4;
+      const int tpw = ((cb << d.log2B) / 16 + 7) / 8;
+      int cols = 32;
+      while (cols < 2 * 4 * nt * tpw) cols <<= 1;
+      if (per_sm >= 1 && cols * per_sm <= 512 && o <= (size_t)kPairSmemMax) {
+        p.tmtpw = tpw;
+        p.tmcols = cols;
+        p.pairk = nch;
+        p.nch = nch;
+        p.tpw = 0;
+        p.cb = cb;
+        p.gsh = 0;
+        while (((cb + (1 << p.gsh) - 1) >> p.gsh) > kPairGroups) ++p.gsh;
+        p.smem_bytes = (unsigned)o;
+        return;
+      }
+    }
+  }
   // register-resident K2: a CTA holds at most 8 warps x tpw tiles x 16 tokens, in a cluster of <= 16
   p.tpw = 8 / nt;
   const int cb_reg = (8 * p.tpw * 16) / d.B;  // 8 warps (kThreads = 256)

@@ -1099,6 +1099,379 @@ static cudaError_t launch_k2_pair(const SelectParams& p, cudaStream_t st, const 
   return launch_ex(kern, dim3(1u, pairs, 1), kPairThreads, p.smem_bytes, st, o, 0u, p);
 }
 
+// ----------------------------------------------------------------------------
+// K2 for G > 8 (MLA: G = 32, d_c = 128): token_pair_nt_kernel -- the token_pair_kernel design for NT = ceil(G/8)
+// n-tiles of 8 heads: a cluster of NCH 256-thread CTAs per pair, each holding cb candidate blocks in shared memory
+// (C4: 8 blocks x 64 tokens x 72 B), the logits of every tile in TMEM (NT x 4 columns per tile per warp).  With
+// 2 NT heads per lane a per-lane running (reference, sum) for each head would not fit the 64-register budget of
+// four CTAs per SM, so the softmax statistics take one more pass over TMEM:
+//   pass 1:  dequantised codes x q~ (NT x KS mma per tile), L -> TMEM, per-lane maxima;
+//   CTA max M_h (lanes -> warps, fixed order);
+//   pass 1b: TMEM -> per-lane sums of 2^(L - M_h) -> CTA sums (fixed order);
+//   cluster: every chunk's (M, S) pushed over DSMEM, merged in chunk order -> lz_h (identical in every CTA);
+//   pass 2:  TMEM -> key = log2 sum_h 2^(L - lz_h) (a lane's 2 NT heads, then the transposed butterfly over the
+//            four lanes holding a token's heads), the log-domain recomputation below 2^-100 (reading U20),
+//            keys + histogram, one release add per CTA.
+constexpr int kNtThreads = 256, kNtWarps = kNtThreads / 32;
+__device__ __forceinline__ int i_count(int ntl, int warp, int nw) { return warp < ntl ? (ntl - warp + nw - 1) / nw : 0; }
+
+template <typename T, int KS, int NSPLIT, int NCH, int NT>
+__global__ void __launch_bounds__(kNtThreads, 4) token_pair_nt_kernel(const __grid_constant__ SelectParams p) {
+  constexpr int NW = kNtWarps, NH = NT * 8;
+  constexpr int rowbytes = KS * 8, lcpr = KS == 2 ? 0 : (KS == 4 ? 1 : 2);
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t gbar[kPairGroups];
+  __shared__ __align__(8) uint64_t qbar;
+  __shared__ uint32_t lhist[kKeyBins];
+  __shared__ float s_w[NW][NH], s_mx[NH], s_lz[NH];
+  __shared__ float s_cm[NCH][NH], s_cz[NCH][NH];  // [chunk][head]: every chunk's statistics, pushed by that chunk
+  __shared__ int s_kc, s_pslot;
+  __shared__ uint32_t s_tmem;
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q4 = lane & 3, r0 = lane >> 2;
+  const int chunk = (int)blockIdx.x, pair = blockIdx.y;
+  unsigned long long* dbg = p.dbg && chunk < 8 ? p.dbg + ((size_t)pair * 8 + chunk) * 8 : nullptr;
+#define TLS_STAMP(i) \
+  if (dbg && tid == 0) dbg[i] = gtimer();
+  TLS_STAMP(0)
+  launch_dependents();
+#pragma unroll
+  for (int i = 0; i < kKeyBins / kNtThreads; ++i) lhist[tid + i * kNtThreads] = 0u;
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");  // started (matched before the DSMEM push)
+  const int b = pair / d.Hkv;
+  const int n = min(max(p.seq_lens[b], 0), d.S);
+  const int m = (n + d.B - 1) >> d.log2B;
+  int* cblk = reinterpret_cast<int*>(smem + p.off_cblk);
+  const float* qsum = reinterpret_cast<const float*>(smem + p.off_qsum);
+  const uint8_t* stc = smem + p.off_stage;
+  const float2* stz = reinterpret_cast<const float2*>(smem + p.off_stage + ((size_t)p.cb << d.log2B) * rowbytes);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&s_tmem)),
+                 "r"((uint32_t)p.tmcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    if (lane == 0) {
+      for (int i = 0; i < kPairGroups; ++i) mbar_init(&gbar[i], kNtThreads);
+      mbar_init(&qbar, 1);
+      mbar_fence_init();
+      s_pslot = -1;
+      wait_ready(p.ready_in + pair, p.epoch);  // select_kernel's a2 outputs for this pair
+      const uint32_t qfb = (uint32_t)(NSPLIT * NT * KS * 256 + NT * 32);  // the pair's q-fragment blob (qq_kernel)
+      mbar_arrive_expect_tx(&qbar, qfb);
+      tma_bulk_g2s(smem + p.off_qb, p.qfrag + (size_t)pair * qfb, qfb, &qbar);
+    }
+    __syncwarp();
+    const int* cand = (p.guide ? p.guide : p.block_ids) + (size_t)pair * d.Kb;
+    constexpr int kMaxIt = 16;  // Kb <= 512 (plan)
+    int cv[kMaxIt];
+#pragma unroll
+    for (int i = 0; i < kMaxIt; ++i) cv[i] = i * 32 + lane < d.Kb ? cand[i * 32 + lane] : -1;
+    int base = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxIt; ++i) {
+      if (i * 32 >= d.Kb) break;
+      const int blk = cv[i];
+      const bool ok = blk >= 0 && blk < m;
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      const int pos = base + __popc(bal & ((1u << lane) - 1u));
+      if (ok && pos < p.kb_eff) {
+        cblk[pos] = blk;
+        if (blk == m - 1) s_pslot = pos;
+      }
+      base += __popc(bal);
+    }
+    if (lane == 0) s_kc = min(base, p.kb_eff);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  TLS_STAMP(7)
+  const int c0 = chunk * p.cb;
+  const int nbl = max(0, min(p.cb, s_kc - c0));
+  const int gsh = p.gsh;
+  // TMEM: warp w -> lanes of quarter w % 4, columns (w / 4) * 4 NT * tiles-per-warp ..
+  const uint32_t tmw = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 4 * NT * p.tmtpw);
+  {  // staging: warp w copies candidate blocks w, w + NW, ... (cp.async), group by group
+    const uint32_t stc_u = smem_u32(stc), stz_u = smem_u32(stz);
+    const int ccb = d.B << lcpr, zcb = d.B >> 1;
+    const uint8_t* cdb = p.codes + (size_t)pair * d.S * rowbytes + (size_t)lane * 16;
+    const float2* szb = reinterpret_cast<const float2*>(p.scale_zero) + (size_t)pair * d.S + 2 * lane;
+    int k = warp;
+    for (int g = 0; g < kPairGroups; ++g) {
+      const int kend = min((g + 1) << gsh, nbl);
+      for (; k < kend; k += NW) {
+        const int blk = cblk[c0 + k], rows = d.S - (blk << d.log2B);
+        const uint8_t* cs = cdb + (size_t)blk * (d.B * rowbytes);
+        const uint32_t cd = stc_u + (uint32_t)(k * ccb + lane) * 16u;
+        for (int c = 0; c < ccb; c += 32)
+          cp_async16_u(cd + (uint32_t)c * 16u, cs + (size_t)c * 16, ((c + lane) >> lcpr) < rows);
+        const float2* zs = szb + ((size_t)blk << d.log2B);
+        const uint32_t zd = stz_u + (uint32_t)(k * zcb + lane) * 16u;
+        for (int c = 0; c < zcb; c += 32) cp_async16_u(zd + (uint32_t)c * 16u, zs + 2 * c, 2 * (c + lane) < rows);
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&gbar[g])) : "memory");
+    }
+  }
+  const int nvl = n - (m - 1) * d.B;
+  const int tshift = d.log2B - 4;
+  const int ntl = nbl << tshift;
+  const int lp = s_pslot - c0;
+  const bool hasp = s_pslot >= 0 && lp >= 0 && lp < nbl && nvl < d.B;
+  const int tp0 = hasp ? (lp << tshift) + (nvl >> 4) : 0, tpn = hasp ? ((lp + 1) << tshift) - tp0 : 0;
+  TLS_STAMP(1)
+  const float sm2 = d.sm_scale * kLog2e;
+  mbar_wait(&qbar, 0);
+  const uint2* qb2 = reinterpret_cast<const uint2*>(smem + p.off_qb);
+  const float2* qs2 = reinterpret_cast<const float2*>(qsum);  // [nt * 4 + q4]: heads nt*8 + 2q4, +1
+  // ---- pass 1: L -> TMEM, per-lane maxima of heads nt*8 + 2q4 + e ----
+  float2 mx[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) mx[nt] = make_float2(-CUDART_INF_F, -CUDART_INF_F);
+  int gdone = -1;
+  for (int i = 0, t = warp; t < ntl; ++i, t += NW) {
+    const int grp = t >> (tshift + gsh);
+    while (gdone < grp) mbar_wait(&gbar[++gdone], 0);
+    CodeWords<KS> cw;
+    load_code_words<KS>(stc + (size_t)t * 16 * rowbytes, true, true, cw);
+    uint32_t a[KS][4];
+#pragma unroll
+    for (int u = 0; u < KS / 2; ++u) {
+      uint32_t x0[4], x1[4];
+      unpack_nibbles8(cw.w0[u], x0);
+      unpack_nibbles8(cw.w1[u], x1);
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        a[2 * u + v][0] = x0[2 * v];
+        a[2 * u + v][1] = x1[2 * v];
+        a[2 * u + v][2] = x0[2 * v + 1];
+        a[2 * u + v][3] = x1[2 * v + 1];
+      }
+    }
+    const float2 z0 = stz[t * 16 + r0], z1 = stz[t * 16 + r0 + 8];
+    const float s0 = sm2 * z0.x, s1 = sm2 * z1.x;
+    const bool part = (unsigned)(t - tp0) < (unsigned)tpn;  // warp-uniform: the sequence's partial last block
+    const int o = (t & ((1 << tshift) - 1)) << 4;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int s2 = 0; s2 < KS; ++s2)
+#pragma unroll
+        for (int sp = 0; sp < NSPLIT; ++sp) {
+          const uint2 bb = qb2[((sp * NT + nt) * KS + s2) * 32 + lane];
+          mma_bf16_16816(acc, a[s2], bb.x, bb.y);
+        }
+      const float2 sq2 = __fmul2_rn(make_float2(sm2, sm2), qs2[nt * 4 + q4]);
+      float2 la = __ffma2_rn(make_float2(s0, s0), make_float2(acc[0], acc[1]), __fmul2_rn(make_float2(z0.y, z0.y), sq2));
+      float2 lb = __ffma2_rn(make_float2(s1, s1), make_float2(acc[2], acc[3]), __fmul2_rn(make_float2(z1.y, z1.y), sq2));
+      if (part) {
+        if (o + r0 >= nvl) la = make_float2(-CUDART_INF_F, -CUDART_INF_F);
+        if (o + r0 + 8 >= nvl) lb = make_float2(-CUDART_INF_F, -CUDART_INF_F);
+      }
+      tm_st4(tmw + (uint32_t)((i * NT + nt) * 4), la.x, la.y, lb.x, lb.y);
+      mx[nt] = make_float2(fmaxf(mx[nt].x, fmaxf(la.x, lb.x)), fmaxf(mx[nt].y, fmaxf(la.y, lb.y)));
+    }
+  }
+  const int ntw = i_count(ntl, warp, NW);
+  // CTA maxima per head (lanes -> warps -> CTA)
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int o2 = 4; o2 < 32; o2 <<= 1) {
+      mx[nt].x = fmaxf(mx[nt].x, __shfl_xor_sync(0xffffffffu, mx[nt].x, o2));
+      mx[nt].y = fmaxf(mx[nt].y, __shfl_xor_sync(0xffffffffu, mx[nt].y, o2));
+    }
+  if (r0 == 0) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      s_w[warp][nt * 8 + 2 * q4] = mx[nt].x;
+      s_w[warp][nt * 8 + 2 * q4 + 1] = mx[nt].y;
+    }
+  }
+  TLS_STAMP(2)
+  __syncthreads();
+  if (tid < NH) {
+    float M = -CUDART_INF_F;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, s_w[w][tid]);
+    s_mx[tid] = M;
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");  // this warp's logits are in TMEM
+  __syncthreads();
+  // ---- pass 1b: per-lane sums of 2^(L - M_h) from TMEM ----
+  float2 hs[NT], nm[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    hs[nt] = make_float2(0.f, 0.f);
+    const float a0 = s_mx[nt * 8 + 2 * q4], a1 = s_mx[nt * 8 + 2 * q4 + 1];
+    nm[nt] = make_float2(a0 == -CUDART_INF_F ? 0.f : -a0, a1 == -CUDART_INF_F ? 0.f : -a1);
+  }
+  for (int i = 0; i < ntw; ++i) {
+#pragma unroll
+    for (int h2 = 0; h2 < NT; h2 += 2) {  // 8 columns = two n-tiles per load
+      float v[8];
+      tm_ld8(tmw + (uint32_t)((i * NT + h2) * 4), v);
+#pragma unroll
+      for (int u = 0; u < 2 && h2 + u < NT; ++u) {
+        const float2 xa = __fadd2_rn(make_float2(v[4 * u], v[4 * u + 1]), nm[h2 + u]);
+        const float2 xb = __fadd2_rn(make_float2(v[4 * u + 2], v[4 * u + 3]), nm[h2 + u]);
+        hs[h2 + u] = __fadd2_rn(hs[h2 + u], __fadd2_rn(make_float2(fexp2(xa.x), fexp2(xa.y)),
+                                                       make_float2(fexp2(xb.x), fexp2(xb.y))));
+      }
+    }
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int o2 = 4; o2 < 32; o2 <<= 1) {
+      hs[nt].x += __shfl_xor_sync(0xffffffffu, hs[nt].x, o2);
+      hs[nt].y += __shfl_xor_sync(0xffffffffu, hs[nt].y, o2);
+    }
+  if (r0 == 0) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      s_w[warp][nt * 8 + 2 * q4] = hs[nt].x;
+      s_w[warp][nt * 8 + 2 * q4 + 1] = hs[nt].y;
+    }
+  }
+  __syncthreads();
+  TLS_STAMP(3)
+  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");  // every chunk CTA has started (DSMEM rule)
+  if (tid < NH) {  // this CTA's (M_h, S_h) to every chunk CTA
+    float S = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) S += s_w[w][tid];
+    const float M = s_mx[tid];
+    for (int rr = 0; rr < NCH; ++rr) {
+      *dsmem(&s_cm[chunk][tid], (unsigned)rr) = M;
+      *dsmem(&s_cz[chunk][tid], (unsigned)rr) = S;
+    }
+  }
+  cluster_sync_all();  // every chunk's statistics have landed in every CTA
+  if (chunk == 0 && tid == 0) p.ready_in[pair] = 0u;  // every CTA of the pair passed its wait
+  if (tid < NH) {
+    float M = -CUDART_INF_F;
+    for (int c = 0; c < NCH; ++c) M = fmaxf(M, s_cm[c][tid]);
+    float S = 0.f;
+    if (M != -CUDART_INF_F)
+      for (int c = 0; c < NCH; ++c)
+        if (s_cm[c][tid] != -CUDART_INF_F) S += s_cz[c][tid] * fexp2(s_cm[c][tid] - M);
+    s_lz[tid] = (tid < d.G && S > 0.f) ? M + flog2(S) : CUDART_INF_F;
+  }
+  __syncthreads();
+  TLS_STAMP(4)
+  // ---- pass 2: ranking keys, two tiles per step ----
+  float2 nlz[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) nlz[nt] = make_float2(-s_lz[nt * 8 + 2 * q4], -s_lz[nt * 8 + 2 * q4 + 1]);
+  uint32_t* kout = p.keys + (size_t)pair * p.kb_eff * d.B + ((size_t)c0 << d.log2B);
+  const bool bit0 = q4 & 1, bit1 = q4 & 2;
+  for (int i = 0, ta = warp; ta < ntl; i += 2, ta += 2 * NW) {
+    // p[u][r]: the lane's 2 NT heads of (tile u, row r); mxx[u][r]: their maximum (log domain)
+    float pr[2][2], mxx[2][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      pr[u][0] = pr[u][1] = 0.f;
+      mxx[u][0] = mxx[u][1] = -CUDART_INF_F;
+      if (u == 1 && ta + NW >= ntl) continue;  // warp-uniform
+#pragma unroll
+      for (int h2 = 0; h2 < NT; h2 += 2) {
+        float v[8];
+        tm_ld8(tmw + (uint32_t)(((i + u) * NT + h2) * 4), v);
+#pragma unroll
+        for (int w2 = 0; w2 < 2 && h2 + w2 < NT; ++w2) {
+          const float2 xa = __fadd2_rn(make_float2(v[4 * w2], v[4 * w2 + 1]), nlz[h2 + w2]);
+          const float2 xb = __fadd2_rn(make_float2(v[4 * w2 + 2], v[4 * w2 + 3]), nlz[h2 + w2]);
+          pr[u][0] += fexp2(xa.x) + fexp2(xa.y);
+          pr[u][1] += fexp2(xb.x) + fexp2(xb.y);
+          mxx[u][0] = fmaxf(mxx[u][0], fmaxf(xa.x, xa.y));
+          mxx[u][1] = fmaxf(mxx[u][1], fmaxf(xb.x, xb.y));
+        }
+      }
+    }
+    float pa = pr[0][0], pb = pr[0][1], pc = pr[1][0], pd = pr[1][1];
+    float k1 = bit0 ? pb : pa, k2 = bit0 ? pd : pc;
+    k1 += __shfl_xor_sync(0xffffffffu, bit0 ? pa : pb, 1);
+    k2 += __shfl_xor_sync(0xffffffffu, bit0 ? pc : pd, 1);
+    float mine = bit1 ? k2 : k1;
+    mine += __shfl_xor_sync(0xffffffffu, bit1 ? k1 : k2, 2);
+    const int t = ta + (bit1 ? NW : 0);
+    const int row = r0 + (bit0 ? 8 : 0);
+    const bool v = t < ntl && !((unsigned)(t - tp0) < (unsigned)tpn && ((t & ((1 << tshift) - 1)) << 4) + row >= nvl);
+    float kf = flog2(mine);
+    if (__any_sync(0xffffffffu, v && !(mine >= 0x1p-100f))) {  // log domain for this step (reading U20)
+      float ma = mxx[0][0], mb = mxx[0][1], mc = mxx[1][0], md = mxx[1][1];
+#pragma unroll
+      for (int o2 = 1; o2 < 4; o2 <<= 1) {
+        ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, o2));
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o2));
+        mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o2));
+        md = fmaxf(md, __shfl_xor_sync(0xffffffffu, md, o2));
+      }
+      ma = ma == -CUDART_INF_F ? 0.f : ma, mb = mb == -CUDART_INF_F ? 0.f : mb;
+      mc = mc == -CUDART_INF_F ? 0.f : mc, md = md == -CUDART_INF_F ? 0.f : md;
+      const float mm[2][2] = {{ma, mb}, {mc, md}};
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        pr[u][0] = pr[u][1] = 0.f;
+        if (u == 1 && ta + NW >= ntl) continue;
+#pragma unroll
+        for (int h2 = 0; h2 < NT; h2 += 2) {
+          float vv[8];
+          tm_ld8(tmw + (uint32_t)(((i + u) * NT + h2) * 4), vv);
+#pragma unroll
+          for (int w2 = 0; w2 < 2 && h2 + w2 < NT; ++w2) {
+            const float2 xa = __fadd2_rn(make_float2(vv[4 * w2], vv[4 * w2 + 1]), nlz[h2 + w2]);
+            const float2 xb = __fadd2_rn(make_float2(vv[4 * w2 + 2], vv[4 * w2 + 3]), nlz[h2 + w2]);
+            pr[u][0] += fexp2(xa.x - mm[u][0]) + fexp2(xa.y - mm[u][0]);
+            pr[u][1] += fexp2(xb.x - mm[u][1]) + fexp2(xb.y - mm[u][1]);
+          }
+        }
+      }
+      pa = pr[0][0], pb = pr[0][1], pc = pr[1][0], pd = pr[1][1];
+      k1 = bit0 ? pb : pa, k2 = bit0 ? pd : pc;
+      k1 += __shfl_xor_sync(0xffffffffu, bit0 ? pa : pb, 1);
+      k2 += __shfl_xor_sync(0xffffffffu, bit0 ? pc : pd, 1);
+      mine = bit1 ? k2 : k1;
+      mine += __shfl_xor_sync(0xffffffffu, bit1 ? k1 : k2, 2);
+      kf = (bit1 ? (bit0 ? md : mc) : (bit0 ? mb : ma)) + flog2(mine);
+    }
+    if (t < ntl) {
+      kout[t * 16 + row] = v ? f2key(kf) : 0u;
+      if (v) atomicAdd(&lhist[key_bin(kf)], 1u);
+    }
+  }
+  __syncthreads();
+  uint32_t* gh = p.khist + (size_t)pair * kKeyBins;
+#pragma unroll
+  for (int i = 0; i < kKeyBins / kNtThreads; ++i) {
+    const int j = tid + i * kNtThreads;
+    if (lhist[j]) atomicAdd(&gh[j], lhist[j]);  // zeroed by qq_kernel
+  }
+  TLS_STAMP(5)
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem), "r"((uint32_t)p.tmcols));
+  if (tid == 0) red_release_add_gpu(p.ready_out + pair, 1u);
+  TLS_STAMP(6)
+#undef TLS_STAMP
+}
+
+template <typename T, int KS, int NSPLIT, int NT>
+static cudaError_t launch_k2_nt(const SelectParams& p, cudaStream_t st, const LaunchOpts& o) {
+  const unsigned pairs = (unsigned)(p.d.batch * p.d.Hkv);
+  if (p.pairk == 16) {
+    auto kern = token_pair_nt_kernel<T, KS, NSPLIT, 16, NT>;
+    cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, true);
+    if (e != cudaSuccess) return e;
+    return launch_ex(kern, dim3(16u, pairs, 1), kNtThreads, p.smem_bytes, st, o, 16u, p);
+  }
+  auto kern = token_pair_nt_kernel<T, KS, NSPLIT, 8, NT>;
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), p.smem_bytes, false);
+  if (e != cudaSuccess) return e;
+  return launch_ex(kern, dim3(8u, pairs, 1), kNtThreads, p.smem_bytes, st, o, 8u, p);
+}
+
 // ============================================================== launchers
 template <typename T, int KS, int NT, int NSPLIT>
 static cudaError_t launch_k2(const SelectParams& p, cudaStream_t st, const LaunchOpts& o) {
@@ -1118,6 +1491,16 @@ bool select_supported(int d_c, int G) {
 template <typename T, int NS>
 static cudaError_t dispatch_k2(const SelectParams& p, cudaStream_t st, const LaunchOpts& o) {
   const int ks = p.d.d_c / 16, nt = (p.d.G + 7) / 8;
+  if (p.pairk >= 8) {  // token_pair_nt_kernel (G > 8; the q-fragment blob's n-tiles: 2 or 4)
+    if constexpr (NS == 1) {
+      const int ntb = nt <= 2 ? 2 : 4;
+      if (ks == 8 && ntb == 4) return launch_k2_nt<T, 8, NS, 4>(p, st, o);
+      if (ks == 8 && ntb == 2) return launch_k2_nt<T, 8, NS, 2>(p, st, o);
+      if (ks == 2 && ntb == 2) return launch_k2_nt<T, 2, NS, 2>(p, st, o);
+      if (ks == 2 && ntb == 4) return launch_k2_nt<T, 2, NS, 4>(p, st, o);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (p.pairk) {
     if (ks == 2) return launch_k2_pair<T, 2, NS>(p, st, o);
     if (ks == 4) return launch_k2_pair<T, 4, NS>(p, st, o);

@@ -33,6 +33,9 @@ SMALL = {
     "mha": W.Workload("t-mha", 2, 4, 4, 64, 64, 3000, top_blocks=8, top_tokens=128),
     "mla": W.Workload("t-mla", 2, 16, 1, 576, 512, 4133, d_c=128, top_blocks=16, top_tokens=256, layout="mla",
                       sm_scale=1.0 / math.sqrt(192.0)),
+    # even max_seq_len: the token kernel's one-cluster-per-pair form (token_pair_nt_kernel) applies
+    "mla_even": W.Workload("t-mla-even", 2, 16, 1, 576, 512, 4133, max_seq_len=4134, d_c=128, top_blocks=16,
+                           top_tokens=256, layout="mla", sm_scale=1.0 / math.sqrt(192.0)),
     "fp32_dc64_g8": W.Workload("t-fp32-dc64", 2, 16, 2, 128, 128, 3100, d_c=64, top_blocks=12, top_tokens=200,
                                dtype=torch.float32),
     "b128": W.Workload("t-b128", 2, 8, 2, 128, 128, 6000, block_size=128, top_blocks=10, top_tokens=300),
@@ -574,9 +577,30 @@ def test_token_kernel_forms(name, form, monkeypatch):
             check_pair(w, cfg, inputs, idx, res, b, g, stats)
 
 
+@pytest.mark.parametrize("name", ["mla", "g16", "g12"])
+@pytest.mark.parametrize("form", ["auto", "cluster"])
+def test_token_kernel_nt_forms(name, form, monkeypatch):
+    """G > 8 (MLA's 32 heads, GQA groups of 16 / 12): token_pair_nt_kernel (a cluster of 256-thread CTAs per pair,
+    logits in TMEM, softmax statistics by a second TMEM pass) against the oracle, and the cluster form."""
+    if form == "cluster":
+        monkeypatch.setenv("TLS_K2_FORM", "cluster")
+    w = {"mla": SMALL["mla_even"],  # even S: the pair form's 16-byte scale/zero rows
+         "g16": W.Workload("t-g16", 2, 32, 2, 128, 128, 6000, top_blocks=24, top_tokens=400),
+         "g12": W.Workload("t-g12", 2, 24, 2, 128, 128, 5000, top_blocks=16, top_tokens=300)}[name]
+    cfg, inputs, idx = setup_case(w, seed=7, pattern="outlier")
+    assert (tls.cluster_size(cfg, 5) == 6) == (form == "auto")
+    res = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    stats = {"block_near_ties": 0, "token_near_ties": 0}
+    for b in range(w.batch):
+        for g in range(w.num_kv_heads):
+            check_pair(w, cfg, inputs, idx, res, b, g, stats)
+
+
 @pytest.mark.parametrize("name,every,form", [("gqa8", 16, "auto"), ("mla", 16, "auto"), ("gqa8", 1000, "auto"),
                                              ("mla", 700, "auto"), ("gqa8", 16, "cluster"), ("gqa8", 1000, "cluster"),
-                                             ("gqa8", 16, "1"), ("gqa8", 1000, "1")])
+                                             ("gqa8", 16, "1"), ("gqa8", 1000, "1"), ("mla_even", 16, "auto"),
+                                             ("mla_even", 700, "auto")])
 def test_sink_tokens_wide_logit_span(name, every, form, monkeypatch):
     """Reading U20: attention-sink-like keys (tokens aligned with the group's queries so strongly that the
     logits of the pair span > 200 nats) must not collapse the other candidates' ranking keys: alpha~ of an ordinary
