@@ -595,29 +595,62 @@ size_t stream_select_smem(int tb, size_t worker_bytes) {
 // kernel's q~ fragment blob and zeroed key histogram, off the selection
 // worker's critical path.  select_kernel, launched as its PDL secondary, issues
 // its tile copies before waiting for it.
-template <typename T>
+// WIDE (G > 16, e.g. MLA's 32 heads): every head's loads in flight at once; the narrow form keeps 40 registers,
+// because qq_kernel co-runs with the select tiles (PDL) and its registers come out of theirs.
+template <typename T, bool WIDE>
 __global__ void __launch_bounds__(kThreads) qq_kernel(const __grid_constant__ FusedParams p) {
   launch_dependents();
   const Dims& d = p.d;
   const int pair = blockIdx.x, b = pair / d.Hkv, g = pair - b * d.Hkv;
   const T* qg = reinterpret_cast<const T*>(p.q) + ((size_t)b * d.Hq + (size_t)g * d.G) * d.d_k;
   float* qq = p.qq + (size_t)pair * 2 * d.d_k;
-  for (int c = threadIdx.x; c < d.d_k; c += kThreads) {
-    float qp = 0.f, qn = 0.f;
-#pragma unroll 8
-    for (int h = 0; h < d.G; ++h) {  // read-only loads: batched ahead of the stores below
-      const float v = to_f32<T>(__ldg(qg + (size_t)h * d.d_k + c));
-      qp += fmaxf(v, 0.f);
-      qn += fminf(v, 0.f);
+  if (WIDE && sizeof(T) == 2 && (d.d_k & 1) == 0) {
+    // bf16: two columns per thread, the loads of up to 32 heads in flight at once (one round trip per 32 heads;
+    // a per-head loop of dependent batches cost ~12 round trips at G = 32: MLA qq_kernel 18 us)
+    const uint32_t* q2 = reinterpret_cast<const uint32_t*>(qg);
+    const int half = d.d_k >> 1;
+    for (int c = threadIdx.x; c < half; c += kThreads) {
+      float qp0 = 0.f, qn0 = 0.f, qp1 = 0.f, qn1 = 0.f;
+      for (int h0 = 0; h0 < d.G; h0 += 32) {
+        uint32_t v[32];
+#pragma unroll
+        for (int h = 0; h < 32; ++h) v[h] = h0 + h < d.G ? __ldg(q2 + (size_t)(h0 + h) * half + c) : 0u;
+#pragma unroll
+        for (int h = 0; h < 32; ++h) {  // in head order: the same fp32 sums as the per-column loop
+          if (h0 + h < d.G) {
+            const float a = __uint_as_float(v[h] << 16), b2 = __uint_as_float(v[h] & 0xffff0000u);
+            qp0 += fmaxf(a, 0.f);
+            qn0 += fminf(a, 0.f);
+            qp1 += fmaxf(b2, 0.f);
+            qn1 += fminf(b2, 0.f);
+          }
+        }
+      }
+      qq[2 * c] = qp0;
+      qq[2 * c + 1] = qp1;
+      qq[d.d_k + 2 * c] = qn0;
+      qq[d.d_k + 2 * c + 1] = qn1;
     }
-    qq[c] = qp;
-    qq[d.d_k + c] = qn;
+  } else {
+    for (int c = threadIdx.x; c < d.d_k; c += kThreads) {
+      float qp = 0.f, qn = 0.f;
+#pragma unroll 8
+      for (int h = 0; h < d.G; ++h) {  // read-only loads: batched ahead of the stores below
+        const float v = to_f32<T>(__ldg(qg + (size_t)h * d.d_k + c));
+        qp += fmaxf(v, 0.f);
+        qn += fminf(v, 0.f);
+      }
+      qq[c] = qp;
+      qq[d.d_k + c] = qn;
+    }
   }
   // the token kernel's inputs that do not depend on the scores: the pair's q~ fragments
   // and a zeroed key histogram
   __shared__ float qc[4 * 8 * 128];  // NT * 8 * d_c <= 4096
-  const int* ch = p.channels + (size_t)g * d.d_c;
-  build_qfrag(d, qg, ch, p.qfrag, pair, qc);
+  __shared__ int s_ch[128];          // the channel ids staged once (the q~ gathers below index by them)
+  for (int c = threadIdx.x; c < d.d_c; c += kThreads) s_ch[c] = p.channels[(size_t)g * d.d_c + c];
+  __syncthreads();
+  build_qfrag<WIDE ? 16 : 8>(d, qg, s_ch, p.qfrag, pair, qc);
   for (int i = threadIdx.x; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
 }
 
@@ -646,7 +679,9 @@ static cudaError_t dispatch_sel(const FusedParams& p, cudaStream_t st, const Lau
 }
 
 cudaError_t launch_qq(const FusedParams& p, cudaStream_t st, const LaunchOpts& o) {
-  auto kern = p.d.bf16 ? qq_kernel<__nv_bfloat16> : qq_kernel<float>;
+  const bool wide = p.d.G > 16;
+  auto kern = p.d.bf16 ? (wide ? qq_kernel<__nv_bfloat16, true> : qq_kernel<__nv_bfloat16, false>)
+                       : (wide ? qq_kernel<float, true> : qq_kernel<float, false>);
   return launch_ex(kern, dim3((unsigned)(p.d.batch * p.d.Hkv)), kThreads, 0, st, o, 0, p);
 }
 

@@ -27,15 +27,16 @@ __device__ __forceinline__ float split_piece(float x, int sp) {
 // floats of shared scratch.  Called by all threads of K1b.
 // qrows: the pair's G query rows [G][d_k] (global or shared memory); ch: the
 // pair's d_c channel ids (global or shared memory).
+template <int NB>  // gathers in flight per thread
 __device__ inline void build_qfrag(const Dims& d, const void* qrows, const int* ch, uint8_t* qfrag, int pair,
                                    float* qc) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt0 = (d.G + 7) / 8, NT = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);
   const int DC = d.d_c, KS = DC / 16, WPT = KS / 2, NSPLIT = d.bf16 ? 1 : 3;
-  for (int i0 = 0; i0 < NT * 8 * DC; i0 += 8 * kThreads) {  // 8 independent loads in flight per thread
-    float v[8];
+  for (int i0 = 0; i0 < NT * 8 * DC; i0 += NB * kThreads) {  // NB independent loads in flight per thread
+    float v[NB];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < NB; ++u) {
       const int i = i0 + u * kThreads + tid;
       const int h = i / DC, c = i - h * DC;
       v[u] = 0.f;
@@ -46,7 +47,7 @@ __device__ inline void build_qfrag(const Dims& d, const void* qrows, const int* 
       }
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < NB; ++u) {
       const int i = i0 + u * kThreads + tid;
       if (i < NT * 8 * DC) qc[i] = v[u];
     }
