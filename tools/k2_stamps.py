@@ -41,3 +41,12 @@ if form in (1, 4):
 x = (k2[:, 6] - k2[:, 0]).sort().values
 n = len(x)
 print(f"  {'total':22s}" + " ".join(f"{float(x[min(n - 1, int(f * n))]):6.2f}" for f in (0, .1, .5, .9, 1)))
+# the attention kernel's a4 prologue (K3 stamps at 65536*24 + pair*8: 0 start, 2 keys landed, 3 selected,
+# 4 prologue end, 5 attention end)
+k3 = buf[65536 * 24: 65536 * 24 + pairs * 8].view(pairs, 8).cpu().double() / 1e3
+k3 = k3[k3[:, 0] > 0]
+print(f"{w.name}: {k3.shape[0]} attention CTAs (rank 0), per-phase us:   min    p10    med    p90    max")
+for nm, a, b in (("hand-off+keys landed", 0, 2), ("top-k_t select", 2, 3), ("emit", 3, 4), ("attention", 4, 5)):
+    x = (k3[:, b] - k3[:, a]).sort().values
+    n = len(x)
+    print(f"  {nm:22s}" + " ".join(f"{float(x[min(n - 1, int(f * n))]):6.2f}" for f in (0, .1, .5, .9, 1)))
