@@ -486,11 +486,14 @@ def select_mode(cfg: TLSConfig) -> int:
 
 def kernel_names(cfg: TLSConfig) -> tuple:
     """Names of the launches one tls_decode call enqueues (the timing slots of timing_read); the token kernel is
-    token_pair_kernel (one, two or four CTAs per pair) or token_cluster_kernel (token_reg_kernel /
+    token_pair_kernel (one, two or four CTAs per pair), token_pair_nt_kernel (G > 8) or token_cluster_kernel (token_reg_kernel /
     token_cluster_kernel: a cluster of chunk CTAs), per ``cluster_size(cfg, 5)``."""
     if select_mode(cfg) == 3:
         return STEP_KERNELS
-    return (KERNELS[0], "token_pair_kernel", KERNELS[2]) if cluster_size(cfg, 5) in (1, 4, 5) else KERNELS
+    form = cluster_size(cfg, 5)
+    if form == 6:
+        return (KERNELS[0], "token_pair_nt_kernel", KERNELS[2])
+    return (KERNELS[0], "token_pair_kernel", KERNELS[2]) if form in (1, 4, 5) else KERNELS
 
 
 def timing_enable(n_calls: int) -> None:

@@ -15,7 +15,7 @@ V = sys.argv[1]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G, P = os.path.join(ROOT, "gpurun_out"), os.environ.get("TLS_PROFILES_OUT", os.path.join(ROOT, "profiles"))
 WL = {"c3": "c3-qwen3-32b-96k-b32", "c2": "c2-qwen3-8b-48k-b16", "c4": "c4-glm47flash-mla-64k-b32"}
-SLOT = {"select_kernel": "select_kernel", "token_reg_kernel": "token_cluster_kernel", "token_pair_kernel": "token_pair_kernel",
+SLOT = {"select_kernel": "select_kernel", "token_reg_kernel": "token_cluster_kernel", "token_pair_kernel": "token_pair_kernel", "token_pair_nt_kernel": "token_pair_nt_kernel",
         "token_cluster_kernel": "token_cluster_kernel", "attend_kernel": "attend_kernel",
         "attend_mla_kernel": "attend_kernel", "qq_kernel": "qq_kernel"}
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",

@@ -17,7 +17,7 @@ for k in token_pair_kernel attend_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^${k}" -s 3 -c 1 \
     -o gpurun_out/r02full_${k}_c2_${V} python tools/profile_step.py --config c2 --steps 3 > /dev/null 2>&1
 done
-for k in token_cluster_kernel attend_mla_kernel select_kernel; do
+for k in token_pair_nt_kernel attend_mla_kernel select_kernel qq_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^${k}" -s 3 -c 1 \
     -o gpurun_out/r02full_${k}_c4_${V} python tools/profile_step.py --config c4 --steps 3 > /dev/null 2>&1
 done
@@ -26,7 +26,7 @@ for c in c3 c2 c4; do
 done
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02smoke_${V}.log 2>&1
 for c in c3 c2 c4; do timeout 200 python tools/timeline.py $c; done > gpurun_out/r02timeline_${V}.txt 2>&1
-timeout 200 python tools/k2_stamps.py c3 > gpurun_out/r02k2stamps_${V}.txt 2>&1
+timeout 200 python tools/k2_stamps.py c3 > gpurun_out/r02k2stamps_${V}.txt 2>&1; timeout 200 python tools/k2_stamps.py c4 >> gpurun_out/r02k2stamps_${V}.txt 2>&1
 ls gpurun_out/ | grep ${V} | wc -l
 # summarise on the box (the .ncu-rep files exceed gpurun's 64 MiB return limit); keep the C3 token-kernel report
 mkdir -p gpurun_out/prof_${V}
