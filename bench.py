@@ -494,6 +494,7 @@ def run_tls(args, w, rank, world, local_rank):
             "context": w.context, "num_q_heads": w.num_q_heads, "num_kv_heads": w.num_kv_heads, "d_k": w.d_k,
             "d_v": w.d_v, "layout": w.layout, "block_size": w.block_size, "d_c": w.d_c, "K_b": w.top_blocks,
             "K_t": w.top_tokens, "pattern": args.pattern, "cluster_size": tls.cluster_size(cfg, 2),
+            "token_kernel": tls.kernel_names(cfg)[1] if mode != 3 else None,
             "select_mode": mode,
             "l2": "flushed before every timed step (256 MiB write, untimed)",
             "parallelism": (f"{world} rank(s), " + (f"{plan['axis']} shard of the fixed problem" if plan else

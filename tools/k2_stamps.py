@@ -50,3 +50,7 @@ for nm, a, b in (("hand-off+keys landed", 0, 2), ("top-k_t select", 2, 3), ("emi
     x = (k3[:, b] - k3[:, a]).sort().values
     n = len(x)
     print(f"  {nm:22s}" + " ".join(f"{float(x[min(n - 1, int(f * n))]):6.2f}" for f in (0, .1, .5, .9, 1)))
+# inside hist_topk_select (the last CTA to write wins): clock64 cycles since the function's start at its checkpoints
+cyc = buf[65536 * 4: 65536 * 4 + 6].cpu().tolist()
+print(f"{w.name}: hist_topk_select cycles at checkpoints (boundary bin found, interval, boundary keys gathered, "
+      f"threshold, positions, emitted): {cyc}")
