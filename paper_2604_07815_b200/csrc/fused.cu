@@ -607,9 +607,12 @@ __global__ void __launch_bounds__(kThreads) qq_kernel(const __grid_constant__ Fu
   if (WIDE && sizeof(T) == 2 && (d.d_k & 1) == 0) {
     // bf16: two columns per thread, the loads of up to 32 heads in flight at once (one round trip per 32 heads;
     // a per-head loop of dependent batches cost ~12 round trips at G = 32: MLA qq_kernel 18 us)
+    // grid.y CTAs per pair (one per n-tile of 8 heads): CTA y takes QQ column slice y and the q~ fragments of
+    // n-tile y, so the latency-bound per-pair work is split four ways (the select tiles wait for the whole grid)
     const uint32_t* q2 = reinterpret_cast<const uint32_t*>(qg);
-    const int half = d.d_k >> 1;
-    for (int c = threadIdx.x; c < half; c += kThreads) {
+    const int half = d.d_k >> 1, per = (half + (int)gridDim.y - 1) / (int)gridDim.y;
+    const int cend = min(half, per * ((int)blockIdx.y + 1));
+    for (int c = per * (int)blockIdx.y + threadIdx.x; c < cend; c += kThreads) {
       float qp0 = 0.f, qn0 = 0.f, qp1 = 0.f, qn1 = 0.f;
       for (int h0 = 0; h0 < d.G; h0 += 32) {
         uint32_t v[32];
@@ -650,8 +653,9 @@ __global__ void __launch_bounds__(kThreads) qq_kernel(const __grid_constant__ Fu
   __shared__ int s_ch[128];          // the channel ids staged once (the q~ gathers below index by them)
   for (int c = threadIdx.x; c < d.d_c; c += kThreads) s_ch[c] = p.channels[(size_t)g * d.d_c + c];
   __syncthreads();
-  build_qfrag<WIDE ? 16 : 8>(d, qg, s_ch, p.qfrag, pair, qc);
-  for (int i = threadIdx.x; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
+  build_qfrag<WIDE ? 16 : 8>(d, qg, s_ch, p.qfrag, pair, qc, (int)blockIdx.y, gridDim.y > 1 ? (int)blockIdx.y + 1 : 4);
+  if (blockIdx.y == 0)
+    for (int i = threadIdx.x; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
 }
 
 // ============================================================== launchers
@@ -682,7 +686,9 @@ cudaError_t launch_qq(const FusedParams& p, cudaStream_t st, const LaunchOpts& o
   const bool wide = p.d.G > 16;
   auto kern = p.d.bf16 ? (wide ? qq_kernel<__nv_bfloat16, true> : qq_kernel<__nv_bfloat16, false>)
                        : (wide ? qq_kernel<float, true> : qq_kernel<float, false>);
-  return launch_ex(kern, dim3((unsigned)(p.d.batch * p.d.Hkv)), kThreads, 0, st, o, 0, p);
+  // wide bf16: one CTA per n-tile of 8 heads (the fp32 / narrow forms: one CTA per pair)
+  const unsigned ny = (wide && p.d.bf16 && (p.d.d_k & 1) == 0) ? (unsigned)((p.d.G + 7) / 8 <= 2 ? 2 : 4) : 1u;
+  return launch_ex(kern, dim3((unsigned)(p.d.batch * p.d.Hkv), ny), kThreads, 0, st, o, 0, p);
 }
 
 cudaError_t launch_select_fused(const FusedParams& p, cudaStream_t st, const LaunchOpts& o) {

@@ -27,20 +27,23 @@ __device__ __forceinline__ float split_piece(float x, int sp) {
 // floats of shared scratch.  Called by all threads of K1b.
 // qrows: the pair's G query rows [G][d_k] (global or shared memory); ch: the
 // pair's d_c channel ids (global or shared memory).
+// [ntlo, nthi): the n-tiles (groups of 8 heads) this CTA builds (a split qq_kernel builds one per CTA).
 template <int NB>  // gathers in flight per thread
 __device__ inline void build_qfrag(const Dims& d, const void* qrows, const int* ch, uint8_t* qfrag, int pair,
-                                   float* qc) {
+                                   float* qc, int ntlo = 0, int nthi = 4) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt0 = (d.G + 7) / 8, NT = nt0 <= 1 ? 1 : (nt0 <= 2 ? 2 : 4);
   const int DC = d.d_c, KS = DC / 16, WPT = KS / 2, NSPLIT = d.bf16 ? 1 : 3;
-  for (int i0 = 0; i0 < NT * 8 * DC; i0 += NB * kThreads) {  // NB independent loads in flight per thread
+  nthi = min(nthi, NT);
+  const int ilo = ntlo * 8 * DC, ihi = nthi * 8 * DC;
+  for (int i0 = ilo; i0 < ihi; i0 += NB * kThreads) {  // NB independent loads in flight per thread
     float v[NB];
 #pragma unroll
     for (int u = 0; u < NB; ++u) {
       const int i = i0 + u * kThreads + tid;
       const int h = i / DC, c = i - h * DC;
       v[u] = 0.f;
-      if (i < NT * 8 * DC && h < d.G) {
+      if (i < ihi && h < d.G) {
         const size_t o = (size_t)h * d.d_k + ch[c];
         v[u] = d.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(qrows)[o])
                       : reinterpret_cast<const float*>(qrows)[o];
@@ -49,7 +52,7 @@ __device__ inline void build_qfrag(const Dims& d, const void* qrows, const int* 
 #pragma unroll
     for (int u = 0; u < NB; ++u) {
       const int i = i0 + u * kThreads + tid;
-      if (i < NT * 8 * DC) qc[i] = v[u];
+      if (i < ihi) qc[i] = v[u];
     }
   }
   __syncthreads();
@@ -58,6 +61,7 @@ __device__ inline void build_qfrag(const Dims& d, const void* qrows, const int* 
   for (int idx = tid; idx < NSPLIT * NT * KS * 32; idx += kThreads) {
     const int ln = idx & 31, rest = idx >> 5;
     const int s = rest % KS, nt = (rest / KS) % NT, sp = rest / (KS * NT);
+    if (nt < ntlo || nt >= nthi) continue;
     const float* qh = qc + (nt * 8 + (ln >> 2)) * DC;
     const int cb = 8 * ((ln & 3) * WPT + (s >> 1)) + 2 * (s & 1);
     uint2 v;
@@ -66,7 +70,7 @@ __device__ inline void build_qfrag(const Dims& d, const void* qrows, const int* 
     reinterpret_cast<uint2*>(qb)[idx] = v;
   }
   float* qsum = reinterpret_cast<float*>(qb + 2 * NSPLIT * NT * KS * 32);
-  for (int h = warp; h < NT * 8; h += kWarps) {
+  for (int h = ntlo * 8 + warp; h < nthi * 8; h += kWarps) {
     float sum = 0.f;
     for (int c = lane; c < DC; c += 32) sum += qc[h * DC + c];
     sum = warp_sum(sum);
