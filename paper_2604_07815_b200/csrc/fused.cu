@@ -610,8 +610,9 @@ __global__ void __launch_bounds__(kThreads) qq_kernel(const __grid_constant__ Fu
     // grid.y CTAs per pair (one per n-tile of 8 heads): CTA y takes QQ column slice y and the q~ fragments of
     // n-tile y, so the latency-bound per-pair work is split four ways (the select tiles wait for the whole grid)
     const uint32_t* q2 = reinterpret_cast<const uint32_t*>(qg);
-    const int half = d.d_k >> 1, per = (half + (int)gridDim.y - 1) / (int)gridDim.y;
-    const int cend = min(half, per * ((int)blockIdx.y + 1));
+    const int nq = (int)gridDim.y / 2;  // CTAs y < nq: QQ column slices; y >= nq: the q~ fragments of n-tile y - nq
+    const int half = d.d_k >> 1, per = (half + nq - 1) / nq;
+    const int cend = (int)blockIdx.y < nq ? min(half, per * ((int)blockIdx.y + 1)) : 0;
     for (int c = per * (int)blockIdx.y + threadIdx.x; c < cend; c += kThreads) {
       float qp0 = 0.f, qn0 = 0.f, qp1 = 0.f, qn1 = 0.f;
       for (int h0 = 0; h0 < d.G; h0 += 32) {
@@ -649,12 +650,14 @@ __global__ void __launch_bounds__(kThreads) qq_kernel(const __grid_constant__ Fu
   }
   // the token kernel's inputs that do not depend on the scores: the pair's q~ fragments
   // and a zeroed key histogram
+  const int ntl = gridDim.y > 1 ? (int)blockIdx.y - (int)gridDim.y / 2 : 0;  // this CTA's n-tile (split form)
+  if (gridDim.y > 1 && ntl < 0) return;  // a QQ slice CTA
   __shared__ float qc[4 * 8 * 128];  // NT * 8 * d_c <= 4096
   __shared__ int s_ch[128];          // the channel ids staged once (the q~ gathers below index by them)
   for (int c = threadIdx.x; c < d.d_c; c += kThreads) s_ch[c] = p.channels[(size_t)g * d.d_c + c];
   __syncthreads();
-  build_qfrag<WIDE ? 16 : 8>(d, qg, s_ch, p.qfrag, pair, qc, (int)blockIdx.y, gridDim.y > 1 ? (int)blockIdx.y + 1 : 4);
-  if (blockIdx.y == 0)
+  build_qfrag<WIDE ? 16 : 8>(d, qg, s_ch, p.qfrag, pair, qc, ntl, gridDim.y > 1 ? ntl + 1 : 4);
+  if (ntl == 0)
     for (int i = threadIdx.x; i < kKeyBins; i += kThreads) p.khist[(size_t)pair * kKeyBins + i] = 0u;
 }
 
@@ -687,7 +690,7 @@ cudaError_t launch_qq(const FusedParams& p, cudaStream_t st, const LaunchOpts& o
   auto kern = p.d.bf16 ? (wide ? qq_kernel<__nv_bfloat16, true> : qq_kernel<__nv_bfloat16, false>)
                        : (wide ? qq_kernel<float, true> : qq_kernel<float, false>);
   // wide bf16: one CTA per n-tile of 8 heads (the fp32 / narrow forms: one CTA per pair)
-  const unsigned ny = (wide && p.d.bf16 && (p.d.d_k & 1) == 0) ? (unsigned)((p.d.G + 7) / 8 <= 2 ? 2 : 4) : 1u;
+  const unsigned ny = (wide && p.d.bf16 && (p.d.d_k & 1) == 0) ? 2u * ((p.d.G + 7) / 8 <= 2 ? 2u : 4u) : 1u;
   return launch_ex(kern, dim3((unsigned)(p.d.batch * p.d.Hkv), ny), kThreads, 0, st, o, 0, p);
 }
 
