@@ -50,7 +50,14 @@ for nm, a, b in (("hand-off+keys landed", 0, 2), ("top-k_t select", 2, 3), ("emi
     x = (k3[:, b] - k3[:, a]).sort().values
     n = len(x)
     print(f"  {nm:22s}" + " ".join(f"{float(x[min(n - 1, int(f * n))]):6.2f}" for f in (0, .1, .5, .9, 1)))
-# inside hist_topk_select (the last CTA to write wins): clock64 cycles since the function's start at its checkpoints
-cyc = buf[65536 * 4: 65536 * 4 + 6].cpu().tolist()
-print(f"{w.name}: hist_topk_select cycles at checkpoints (boundary bin found, interval, boundary keys gathered, "
-      f"threshold, positions, emitted): {cyc}")
+# inside hist_topk_select: clock64 cycles since the function's start at its checkpoints (per pair, rank-0 CTA:
+# dbg + 65536*4 of the K3 base), and the boundary-bin size (K3 stamp slot 7)
+cyc = buf[65536 * 24 + 65536 * 4: 65536 * 24 + 65536 * 4 + pairs * 8].view(pairs, 8)[:, :6].cpu().double()
+cyc = cyc[cyc[:, 5] > 0]
+if cyc.shape[0]:
+    med = cyc.median(0).values.tolist()
+    print(f"{w.name}: hist_topk_select median cycles at (boundary bin, interval, boundary keys gathered, threshold, "
+          f"positions, emitted): {[int(x) for x in med]}")
+nbk = buf[65536 * 24: 65536 * 24 + pairs * 8].view(pairs, 8)[:, 7].cpu().double()
+nbk = nbk.sort().values
+print(f"{w.name}: boundary-bin keys per pair: min {int(nbk[0])} median {int(nbk[len(nbk) // 2])} max {int(nbk[-1])}")
