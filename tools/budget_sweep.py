@@ -16,6 +16,8 @@ names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["c3", "c2"]
 dev = torch.device("cuda")
 flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 st = torch.cuda.current_stream()
+clocks = bench.ClockSampler(0)  # SM clock / throttle reasons during each record's timed region
+clocks.start()
 for name in names:
     base = W.CONFIGS[name]
     for pattern in ("outlier", "uniform", "peaked"):
@@ -24,6 +26,7 @@ for name in names:
             if pattern != "outlier" and (kb, kt) != (128, 1024):
                 continue
             cfg = tls.TLSConfig(**{**base.config_kwargs(), "top_blocks": kb, "top_tokens": kt})
+            t_rec0 = __import__("time").time()
             try:
                 ts = bench.time_steps(lambda i: tls.decode(cfg, queries[i % 8], inputs["k_cache"], inputs["v_cache"],
                                                            inputs["seq_lens"], idx), 50, 5, lambda: flush_buf.fill_(1), st)
@@ -33,6 +36,7 @@ for name in names:
             except Exception as e:  # noqa: BLE001
                 rec = {"workload": base.name, "pattern": pattern, "top_blocks": kb, "top_tokens": kt,
                        "error": f"{type(e).__name__}: {e}"[:160]}
+            rec["clocks"] = clocks.summary(t_rec0, __import__("time").time())
             print(json.dumps(rec), flush=True)
         del inputs, idx, queries
         torch.cuda.empty_cache()

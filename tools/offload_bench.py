@@ -47,6 +47,9 @@ for _ in range(args.steps + 1):
     qs.append(q.clone())
     q = (q.float() + args.eps * torch.randn(q.shape, generator=g, device=dev)).to(q.dtype)
 st = torch.cuda.current_stream()
+clocks = bench.ClockSampler(0)  # SM clock / throttle reasons during the timed region (recorded with the numbers)
+clocks.start()
+t_rec0 = time.time()
 ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
 misses = []
 row = 2 * w.d_k * 2  # K + V bytes per token (bf16)
@@ -103,5 +106,6 @@ else:
            "block_hit_rate": 1.0 - mean_miss / w.top_blocks,
            "fetched_bytes_per_layer_step": mean_miss * pairs * w.block_size * row,
            "gpu_cache_bytes_per_layer": int(engs[0].cache.k_slots.numel() * 2 * 2)}
-rec.update(host_kv_bytes=int(k_host.numel() * 2 + v_host.numel() * 2), pin_seconds=pin_s)
+rec.update(host_kv_bytes=int(k_host.numel() * 2 + v_host.numel() * 2), pin_seconds=pin_s,
+           clocks=clocks.summary(t_rec0, time.time()))
 print(json.dumps(rec), flush=True)
