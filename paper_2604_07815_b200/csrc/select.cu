@@ -3,6 +3,14 @@
 // The decode step's kernels: qq_kernel + select_kernel (fused.cu: a1 block
 // scores as an HBM-streaming GEMV, a2 top-k_b in each pair's last tile CTA),
 // then K2 here, then attend_kernel (attend.cu: a4 top-k_t prologue + a5).
+//   K2 token_pair_kernel    a3  (default, G <= 8) one cluster of 1 / 2 / 4 CTAs
+//                               per pair holding the pair's whole candidate
+//                               index in shared memory (cp.async staging in
+//                               mbarrier groups), logits on the tensor cores
+//                               (mma.sync) kept in TMEM between the two passes
+//   K2 token_pair_nt_kernel a3  (G > 8, MLA) the same with NT n-tiles of 8
+//                               heads: a cluster of 8 / 16 CTAs, statistics by
+//                               a second pass over TMEM
 //   K2 token_reg_kernel     a3  alpha~_j over the candidate tokens:
 //                               a cluster of nch chunk CTAs per pair, logits on
 //                               the tensor cores (mma.sync, INT4 codes -> bf16)
