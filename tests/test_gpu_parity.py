@@ -282,6 +282,30 @@ def test_edge_single_token_and_k1():
             check_pair(w, cfg, inputs, idx, res, b, g, stats)
 
 
+@pytest.mark.parametrize("form", ["2", "1", "4", "cluster"])
+def test_empty_and_partial_sequences_every_token_form(form, monkeypatch):
+    """A batch with an empty sequence (n = 0: no candidate, no selected token, output 0 / lse -inf), one shorter than a
+    block and one ending mid-block, through every token-kernel form (the pair forms mask the partial last block's
+    rows; the empty pair stages nothing)."""
+    monkeypatch.setenv("TLS_K2_FORM", form)
+    w = W.Workload("t-empty", 4, 16, 2, 128, 128, 2000, top_blocks=8, top_tokens=200)
+    inputs = W.make_inputs(w, seed=13, device=DEV, seq_lens=[1999, 0, 40, 1217])  # (calibration reads sequence 0)
+    q_cal, k_cal = W.calibration_sample(w, inputs, seed=13)
+    channels = P.oracle_channels(w, q_cal, k_cal).to(DEV)
+    cfg = tls.TLSConfig(**w.config_kwargs())
+    idx = tls.alloc_index(cfg, channels)
+    tls.build_index(cfg, inputs["k_cache"], inputs["seq_lens"], idx)
+    res = run_decode(cfg, inputs, idx)
+    torch.cuda.synchronize()
+    out, lse, bids, tids, ntok, tsc = res
+    assert int(ntok[1].max()) == 0 and bool((tids[1] == -1).all()) and bool((bids[1] == -1).all())
+    assert bool(torch.isfinite(out[1].float()).all()) and float(out[1].float().abs().max()) == 0.0
+    stats = {"block_near_ties": 0, "token_near_ties": 0}
+    for b in (0, 2, 3):
+        for g in range(w.num_kv_heads):
+            check_pair(w, cfg, inputs, idx, res, b, g, stats)
+
+
 def test_errors_are_reported():
     w = SMALL["gqa4"]
     cfg, inputs, idx = setup_case(w)
