@@ -1,7 +1,7 @@
 // params.h -- host/device parameter blocks and shared-memory plans of the
 // decode-step kernels:
 //   qq_kernel, select_kernel (fused.cu)          a1: block scores; a2: top-k_b
-//   token_reg_kernel / token_cluster_kernel (select.cu)  a3: ranking keys
+//   token_pair_kernel / token_pair_nt_kernel / token_reg_kernel / token_cluster_kernel (select.cu)  a3: ranking keys
 //   attend_kernel / attend_mla_kernel (attend.cu)        a4: top-k_t; a5: attention
 //   pstep_kernel (pstep.cu, opt-in)              a1-a5 in one persistent launch
 #pragma once
